@@ -1,0 +1,398 @@
+#!/usr/bin/env python3
+"""ABCS hot-path benchmark (contract: one JSON line from rank 0).
+
+Headline (BASELINE.json metric, workload = configs[1], "cfg2"): megapixels/s of
+sense + reconstruct (DD-ABCS, B=16, fp32 DCTs, inverse-DCT reconstruction) over a
+batch of 1024 synthetic 512x512 uint8 images per GPU, one step = the subrate
+sweep {0.1, 0.3, 0.5} (3 x 1024 images). Inputs are resident in HBM (generated
+on device) and larger than L2 (268 MB u8 per subrate + ~1.4 GB of outputs).
+Secondary object "ida": cfg4 (64 x 512^2, BBV 0.3, 10 IDA iterations), image-
+iterations/s. Multi-GPU: one process per GPU, each rank senses its own 1024
+images (disjoint global image indices), no collective on the data path
+("scaling": "weak"); timing is the max over ranks of CUDA-event time.
+
+--impl reference runs the reference's own CPU implementation (oracle/_ref, the
+unmodified reference library, else the C port) on the host cores on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SUBRATES = ((1, 10), (3, 10), (1, 2))
+CFG2 = dict(H=512, W=512, B=16, n=1024, ellipses=20, sigma=5.0, seed=2)
+CFG4 = dict(H=512, W=512, B=16, n=64, ellipses=20, sigma=5.0, seed=4, num=3, den=10, iters=10)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def max_over_ranks(v, world, device=None):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU (reference) arm
+def cpu_sample(checker, imgs, threads):
+    """sense + reconstruct(idct) of every image at every subrate; returns (seconds, pixels)."""
+    t0 = time.perf_counter()
+    px = 0
+    for num, den in SUBRATES:
+        if hasattr(checker, "sense_reconstruct_batch"):
+            checker.sense_reconstruct_batch(imgs, CFG2["B"], num, den, 2, method=0, iters=1, threads=threads)
+        else:  # C port: per image, threaded
+            from concurrent.futures import ThreadPoolExecutor
+
+            def one(i):
+                ms = checker.sense(imgs[i], CFG2["B"], num, den, 2)
+                checker.decode(ms["rows"], ms["cols"], CFG2["B"], ms["counts"], ms["coeffs"])
+
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(len(imgs))))
+        px += imgs.shape[0] * imgs.shape[1] * imgs.shape[2]
+    return time.perf_counter() - t0, px
+
+
+def sample_images(n):
+    import paper_2001_09632_b200 as p
+    return p.synth_images_host(p.SynthSpec(CFG2["H"], CFG2["W"], CFG2["ellipses"], CFG2["sigma"], CFG2["seed"]), 0, n)
+
+
+def get_checker():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as o
+    if o.Reference.available():
+        return o.Reference(), "reference"
+    return o.CPort(), "port"
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    checker, kind = get_checker()
+    threads = host_cores()
+    n = max(2 * threads, 8)
+    imgs = sample_images(n)
+    for _ in range(args.warmup):
+        cpu_sample(checker, imgs[: min(n, threads)], threads)
+    times, px = [], 0
+    for _ in range(args.steps):
+        t, p_ = cpu_sample(checker, imgs, threads)
+        times.append(t)
+        px = p_
+    sec = float(np.mean(times))
+    value = px / sec / 1e6
+    sample = f"{n} cfg2 images (512x512, seed {CFG2['seed']}) x subrates {{0.1,0.3,0.5}} per step"
+    line = {
+        "impl": "reference", "metric": "megapixels/s for ABCS sense+reconstruct", "value": round(value, 3),
+        "unit": "MP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: DD-ABCS B=16 subrate sweep {0.1,0.3,0.5}, IDCT reconstruction, 512x512 u8",
+                   "images_per_step": n, "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "MP/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2001_09632_b200 as p
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    ctx = p.Context.get(local)
+    hbm, peak_src = peaks()
+    n = CFG2["n"]
+    spec = p.SynthSpec(CFG2["H"], CFG2["W"], CFG2["ellipses"], CFG2["sigma"], CFG2["seed"])
+    imgs = p.synth_images(spec, rank * n, n, device=local)  # disjoint global indices per rank
+    cfgs = [p.SensingConfig(CFG2["B"], num, den, p.Algorithm.DD) for num, den in SUBRATES]
+    plans = [p.sense_plan(c, CFG2["H"], CFG2["W"]) for c in cfgs]
+    batches = [p.sense_batch(imgs, c, pl) for c, pl in zip(cfgs, plans)]  # allocates outputs once
+    outs = [p.decode_batch(b) for b in batches]
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(len(SUBRATES))]
+          for _ in range(args.steps)]
+    sense_ms = [0.0] * len(SUBRATES)
+    decode_ms = [0.0] * len(SUBRATES)
+
+    def step(evs):
+        for j, (c, pl, b) in enumerate(zip(cfgs, plans, batches)):
+            if evs:
+                evs[j][0].record(stream)
+            p.sense_batch(imgs, c, pl, out=b)
+            if evs:
+                evs[j][1].record(stream)
+            p.decode_batch(b, out=outs[j])
+            if evs:
+                evs[j][2].record(stream)
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    launches0 = ctx.launches()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k in range(args.steps):
+        step(ev[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        for j in range(len(SUBRATES)):
+            sense_ms[j] += ev[k][j][0].elapsed_time(ev[k][j][1])
+            decode_ms[j] += ev[k][j][1].elapsed_time(ev[k][j][2])
+    launches = ctx.launches() - launches0
+    clk = clocks.stop() if clocks else None
+    barrier(world)
+    ms = start.elapsed_time(end)
+    ms_max = max_over_ranks(ms, world, dev)
+    ms_step = ms_max / args.steps
+    px_step = len(SUBRATES) * n * CFG2["H"] * CFG2["W"]
+    value = world * px_step * args.steps / (ms_max / 1e3) / 1e6
+
+    # algorithmic bytes: sense = N + 4K + 2nB ; decode = 4K + 2nB + 4N  (per image)
+    N = CFG2["H"] * CFG2["W"]
+    per_j = []
+    for j, pl in enumerate(plans):
+        K, nB = pl.coeffs_per_image, pl.n_blocks
+        sense_b = n * (N + 4 * K + 2 * nB)
+        dec_b = n * (4 * K + 2 * nB + 4 * N)
+        per_j.append(dict(subrate=f"{SUBRATES[j][0]}/{SUBRATES[j][1]}", K=K,
+                          sense_ms=sense_ms[j] / args.steps, decode_ms=decode_ms[j] / args.steps,
+                          sense_bytes=sense_b, decode_bytes=dec_b))
+    dec_bytes = sum(x["decode_bytes"] for x in per_j)
+    dec_ms = sum(x["decode_ms"] for x in per_j)
+    sen_bytes = sum(x["sense_bytes"] for x in per_j)
+    sen_ms = sum(x["sense_ms"] for x in per_j)
+    dominant = "decode_kernel" if dec_ms >= sen_ms else "sense (dd_weights+alloc+gather)"
+    if dec_ms >= sen_ms:
+        ach = dec_bytes / (dec_ms / 1e3) / 1e9
+        traffic_alg = dec_bytes / len(SUBRATES)
+    else:
+        ach = sen_bytes / (sen_ms / 1e3) / 1e9
+        traffic_alg = sen_bytes / len(SUBRATES)
+    pipe_ach = (dec_bytes + sen_bytes) / ((dec_ms + sen_ms) / 1e3) / 1e9
+
+    # e2e through the C ABI with host buffers (pinned), H2D + kernels + D2H in the timed region
+    import ctypes as C
+    lib = p._lib.load()
+    h_in = torch.empty((n, CFG2["H"], CFG2["W"]), dtype=torch.uint8, pin_memory=True)
+    h_in.copy_(imgs.cpu())
+    h_out = torch.empty((n, CFG2["H"], CFG2["W"]), dtype=torch.float32, pin_memory=True)
+    e2e_times = []
+    for it in range(1 + max(1, min(args.steps, 3))):
+        barrier(world)
+        t0 = time.perf_counter()
+        for pl in plans:
+            st = lib.abcs_sense_decode_host(ctx.handle, C.byref(pl), h_in.data_ptr(), n, h_out.data_ptr(),
+                                            None, None, 64)
+            if st != 0:
+                raise RuntimeError(p._lib.last_error())
+        dt = time.perf_counter() - t0
+        if it > 0:
+            e2e_times.append(dt)
+    e2e_s = max_over_ranks(float(np.mean(e2e_times)), world, dev)
+    e2e_value = world * px_step / e2e_s / 1e6
+    h2d = len(SUBRATES) * n * N
+    d2h = len(SUBRATES) * n * N * 4
+
+    # secondary: cfg4 IDA (64 x 512^2, BBV 0.3, 10 iterations)
+    ida = run_ida(p, torch, local, rank, hbm, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        checker, kind = get_checker()
+        threads = host_cores()
+        ns = max(threads, 8)
+        himgs = imgs[:ns].cpu().numpy()
+        cpu_sample(checker, himgs[: min(ns, threads)], threads)  # warm
+        sec, pxs = cpu_sample(checker, himgs, threads)
+        cpu = {"value": round(pxs / sec / 1e6, 3), "unit": "MP/s", "cores": threads, "kind": kind,
+               "sample": f"{ns} of this rank's cfg2 images x subrates {{0.1,0.3,0.5}} ({sec:.2f} s wall)"}
+
+    if rank == 0:
+        line = {
+            "metric": "megapixels/s for ABCS sense+reconstruct", "value": round(value, 1), "unit": "MP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg2: 1024 x 512x512 u8 per GPU, DD-ABCS B=16, subrate sweep {0.1,0.3,0.5}, "
+                                   "IDCT reconstruction (BASELINE configs[1])",
+                       "global_batch": world * n, "l2": "inputs+outputs >> L2 (no flush needed)",
+                       "parallelism": f"dp{world} (independent images, no collective)"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": hbm,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                         "algorithmic_bytes_per_launch": int(traffic_alg), "traffic": None},
+            "pipeline_roofline": {"achieved": round(pipe_ach, 1), "frac": round(pipe_ach / hbm, 4),
+                                  "phases": per_j},
+            "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
+            "ida": ida,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ida(p, torch, local, rank, hbm, world, dev):
+    c = CFG4
+    spec = p.SynthSpec(c["H"], c["W"], c["ellipses"], c["sigma"], c["seed"])
+    imgs = p.synth_images(spec, rank * c["n"], c["n"], device=local)
+    cfg = p.SensingConfig(c["B"], c["num"], c["den"], p.Algorithm.BBV)
+    b = p.sense_batch(imgs, cfg)
+    rc = p.ReconConfig(p.ReconMethod.Ida, iterations=c["iters"])
+    out = torch.empty((c["n"], c["H"], c["W"]), dtype=torch.float32, device=dev)
+    for _ in range(3):
+        p.ida_batch(b, rc, out=out, trace=False, check=False)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    s.record()
+    for _ in range(reps):
+        p.ida_batch(b, rc, out=out, trace=False, check=False)
+    e.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(s.elapsed_time(e) / reps, world, dev)
+    N, K = c["H"] * c["W"], b.plan.coeffs_per_image
+    per_iter = c["n"] * (8 * N + 12 * K)
+    init = c["n"] * (8 * K + 4 * N)
+    alg = per_iter * c["iters"] + init
+    ach = alg / (ms / 1e3) / 1e9
+    return {"metric": "IDA image-iterations/s (cfg4: 64 x 512^2, BBV 0.3, 10 it, dct_threshold)",
+            "value": round(world * c["n"] * c["iters"] / (ms / 1e3), 1), "unit": "it/s",
+            "mp_it_per_s": round(world * c["n"] * c["iters"] * N / (ms / 1e3) / 1e6, 1),
+            "ms_per_batch": round(ms, 3),
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "algorithmic_bytes": int(alg)}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank)
+        return run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,221 @@
+/* abcs_b200.h — C ABI of the B200-native ABCS hot path (libabcs_b200.so).
+ *
+ * Drop-in boundary for the reference's C++ API in /root/reference/proj/core
+ * (headers proj/core/include/abcs/<name>.hpp). The reference exposes no C ABI or
+ * plugin registry; its public surface is the abcs:: C++ functions below. This
+ * header is the thin, batched, device-pointer, stream-ordered C layer those
+ * functions are re-implemented over (paper_2001_09632_b200/cpp/ is the C++
+ * shim that restores the exact abcs:: signatures; INTEGRATION.md shows the
+ * bindings). Plain pointers and sizes only: device buffers are caller-owned,
+ * `stream` is a cudaStream_t passed as void*, no CUDA or torch types appear.
+ *
+ * Every call returns an abcs_status; on failure abcs_last_error() returns a
+ * thread-local message. The status codes map to the reference's exceptions:
+ *   ABCS_ERR_INVALID_ARGUMENT -> std::invalid_argument
+ *   ABCS_ERR_FORMAT           -> abcs::FormatError        (image.hpp:12-15)
+ *   ABCS_ERR_DIVERGENCE       -> abcs::DivergenceError    (recon.hpp:22-30)
+ *   ABCS_ERR_LOGIC            -> std::logic_error
+ * and ABCS_ERR_CUDA / ABCS_ERR_UNSUPPORTED have no reference counterpart
+ * (device failure; a configuration the device path does not implement — it
+ * never silently falls back to a CPU path).
+ */
+#ifndef ABCS_B200_H
+#define ABCS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ABCS_B200_ABI_VERSION 1
+
+typedef enum {
+  ABCS_OK = 0,
+  ABCS_ERR_INVALID_ARGUMENT = 1,
+  ABCS_ERR_FORMAT = 2,
+  ABCS_ERR_DIVERGENCE = 3,
+  ABCS_ERR_CUDA = 4,
+  ABCS_ERR_LOGIC = 5,
+  ABCS_ERR_UNSUPPORTED = 6
+} abcs_status;
+
+/* abcs::Algorithm (sensing.hpp:12) */
+typedef enum { ABCS_ALGO_ZZ = 0, ABCS_ALGO_BBV = 1, ABCS_ALGO_DD = 2 } abcs_algorithm;
+
+/* fallback reasons of abcs::sense (sensing.cpp:445-465) */
+typedef enum {
+  ABCS_FALLBACK_NONE = 0,
+  ABCS_FALLBACK_BBV_FULL_RATE = 1, /* C_R == 1 */
+  ABCS_FALLBACK_BBV_CF_EXCEEDS_BLOCK = 2,
+  ABCS_FALLBACK_DD_PHASE1_ZERO = 3
+} abcs_fallback;
+
+typedef struct abcs_ctx abcs_ctx;
+
+/* abcs::SensingConfig (sensing.hpp:20-40). cr_num/cr_den need not be reduced. */
+typedef struct {
+  int32_t block;
+  uint32_t cr_num;
+  uint32_t cr_den;
+  int32_t algorithm;     /* abcs_algorithm */
+  int32_t has_threshold; /* SensingConfig::threshold engaged (DD override) */
+  int32_t reserved;
+  double threshold;
+} abcs_sensing_config;
+
+/* Everything abcs::sense derives from (config, image size) before touching a
+ * pixel: grid (image.cpp:106-116), M (sensing.cpp:41-44), fallbacks
+ * (sensing.cpp:445-465), BBV L/X0/n_S/M_BBV (sensing.cpp:243-256), allocate_bbv
+ * cap/budget (sensing.cpp:303-319), DD phase1/T/cap (sensing.cpp:328-330,360),
+ * measurement_budget (sensing.cpp:472-487). Computed on the host by
+ * abcs_sense_plan_init; the same plan serves every image of that size. */
+typedef struct {
+  int32_t height, width, block;
+  int32_t rows, cols, n_blocks;
+  int32_t algorithm;       /* requested */
+  int32_t algorithm_used;  /* MeasurementSet::algorithm after fallbacks */
+  int32_t fallback;        /* abcs_fallback */
+  int32_t zz_last_zero;    /* sense()'s "some blocks receive zero" warning */
+  uint32_t cr_num, cr_den; /* as stored in the MeasurementSet */
+  double threshold;        /* MeasurementSet::threshold */
+  int64_t target;          /* M = floor(C_R * N) over the cropped grid */
+  int64_t coeffs_per_image;/* K = sum(counts), identical for every image */
+  int64_t side_per_image;  /* BBV side-data length */
+  int64_t budget_actual;   /* measurement_budget().actual */
+  int64_t bbv_stride;      /* L */
+  int32_t bbv_offset;      /* X0 */
+  int32_t bbv_per_side;    /* n_S */
+  int64_t bbv_phase1_total;/* M_BBV */
+  int32_t bbv_valid_probes;/* probes per side that stay inside the block */
+  int32_t dd_phase1;       /* floor(B^2 C_R / 2) */
+  int32_t cap;             /* per-block allocator cap */
+  int32_t count_base;      /* added to each allocation (DD phase 1) */
+  int64_t alloc_budget;    /* budget handed to largest_remainder_allocate */
+  int64_t zz_per_block;    /* balanced_counts: floor(M / n_B) */
+  int64_t zz_extra;        /* balanced_counts: M mod n_B */
+} abcs_sense_plan;
+
+/* abcs::ReconConfig for method Ida with the dct_threshold denoiser (recon.hpp:32-41,
+ * denoise.hpp:19-27). */
+typedef struct {
+  int32_t iterations;      /* >= 1 */
+  int32_t denoiser_block;  /* DenoiserSpec param "block" (8 supported on device) */
+  double damping;          /* D_F >= 1 */
+  double k;                /* DenoiserSpec param "k" (2.7) */
+} abcs_ida_config;
+
+/* Seeded synthetic scene generator; mirrors csrc/synth_gen.h sg_spec. */
+typedef struct {
+  int32_t height, width;
+  int32_t n_ellipses;
+  int32_t video;
+  int32_t max_shift;
+  int32_t reserved;
+  double noise_sigma;
+  uint64_t seed;
+} abcs_synth_spec;
+
+/* ---- library / context --------------------------------------------------- */
+int abcs_abi_version(void);
+const char* abcs_last_error(void);
+int abcs_ctx_create(int device, abcs_ctx** out);
+int abcs_ctx_destroy(abcs_ctx* ctx);
+/* number of kernels this ctx has launched (for bench's gpu_launches claim) */
+int64_t abcs_ctx_launch_count(const abcs_ctx* ctx);
+
+/* ---- host-side logic (no GPU needed) -------------------------------------- */
+/* SensingConfig::parse_ratio (sensing.cpp:46-80) */
+int abcs_parse_ratio(const char* text, uint32_t* num, uint32_t* den);
+/* dd_threshold (sensing.cpp:405-416) */
+double abcs_dd_threshold(int32_t image_height, uint32_t cr_num, uint32_t cr_den);
+/* zigzag_order (zigzag.cpp:8-26): index[k] = row*B + col */
+int abcs_zigzag_order(int32_t block, int32_t* index);
+/* config validation + every derivation of sense() for one image size */
+int abcs_sense_plan_init(const abcs_sensing_config* cfg, int32_t height, int32_t width,
+                         abcs_sense_plan* plan);
+/* host generator (identical bytes to abcs_synth_generate) */
+int abcs_synth_generate_host(const abcs_synth_spec* spec, int64_t first_index, int32_t n_images,
+                             uint8_t* out);
+
+/* ---- device hot path ------------------------------------------------------ */
+
+/* abcs::sense (sensing.hpp:98-99) on n images of the plan's size. images: u8,
+ * image i at d_images + i*image_stride, rows `pitch` bytes apart.
+ * Outputs per image i: counts[i*n_blocks ..] (u16, row-major blocks),
+ * offsets[i*n_blocks ..] (exclusive prefix sums of counts; nullable),
+ * payload[i*K ..] (f32 zigzag prefixes, block-major), side[i*S ..] (f32 BBV
+ * boundary differences; nullable when S == 0). */
+int abcs_sense_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_images,
+                     int64_t image_stride, int32_t pitch, int32_t n_images, uint16_t* d_counts,
+                     int32_t* d_offsets, float* d_payload, float* d_side, void* stream);
+
+/* Phase-1 weights only (bbv_measure variation / DD significance counts n_i),
+ * u32 per block — exposes the pre-measurement of sensing.cpp:266-294 / :341-358. */
+int abcs_sense_weights_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_images,
+                             int64_t image_stride, int32_t pitch, int32_t n_images,
+                             uint32_t* d_weights, float* d_side, void* stream);
+
+/* largest_remainder_allocate (sensing.cpp:110-177) for n independent weight
+ * vectors of n_blocks integer weights; caps per block (nullable -> uniform
+ * `cap`). counts = base + allocation (u16), offsets = exclusive scan (nullable).
+ * d_status[i] (nullable) receives an abcs_status per vector. */
+int abcs_allocate_batch(abcs_ctx* ctx, const uint32_t* d_weights, int32_t n_blocks,
+                        int32_t n_vectors, int64_t budget, const int32_t* d_caps, int32_t cap,
+                        int32_t base, uint16_t* d_counts, int32_t* d_offsets, int32_t* d_status,
+                        void* stream);
+
+/* decode_idct (recon.cpp:109-117) = SensingOperator::adjoint (operators.cpp:50-76):
+ * out image i (cropped rows*B x cols*B, f32, `out_pitch` floats per row) from
+ * counts/payload. offsets nullable (computed). d_format_error (nullable, per
+ * image) receives ABCS_ERR_FORMAT when sum(counts) != d_payload_len[i]
+ * (nullable) or ABCS_ERR_INVALID_ARGUMENT when a count exceeds B^2. */
+int abcs_decode_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                      const uint16_t* d_counts, const int32_t* d_offsets, const float* d_payload,
+                      int64_t payload_stride, int32_t n_images, float* d_out, int64_t out_stride,
+                      int32_t out_pitch, const int64_t* d_payload_len, int32_t* d_error,
+                      void* stream);
+
+/* SensingOperator::forward (operators.cpp:23-48) on f32 fields. */
+int abcs_forward_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                       const uint16_t* d_counts, const int32_t* d_offsets, const float* d_field,
+                       int64_t field_stride, int32_t field_pitch, int32_t n_images, float* d_y,
+                       int64_t y_stride, void* stream);
+
+/* denoise(dct_threshold) (denoise.cpp:52-92,96-109) on f32 fields; sigma per image (host array). */
+int abcs_denoise_dct_batch(abcs_ctx* ctx, const float* d_field, int32_t height, int32_t width,
+                           int64_t field_stride, int32_t n_images, const double* sigma, double k,
+                           int32_t block, float* d_out, void* stream);
+
+/* reconstruct() with method Ida (recon.cpp:199-259): warm start, `iterations`
+ * damp_step(Ida) steps with the dct_threshold denoiser, final clamp to [0,255].
+ * d_ref (nullable): u8 reference images for the per-iteration PSNR trace.
+ * d_trace (nullable): n*(iterations+1) rows of {iteration, ||z||, sigma, psnr}.
+ * d_diverged (nullable): per image {first diverged iteration or 0, kind}
+ * (kind 1 non-finite estimate, 2 |x| > 1e6, 3 non-finite residual). Async;
+ * abcs_ida_check() turns the device record into a status after the stream syncs. */
+int abcs_ida_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                   const uint16_t* d_counts, const int32_t* d_offsets, const float* d_y,
+                   int64_t y_stride, int32_t n_images, const abcs_ida_config* cfg,
+                   const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, float* d_out,
+                   int64_t out_stride, int32_t out_pitch, double* d_trace, int32_t* d_diverged,
+                   void* stream);
+int abcs_ida_check(const int32_t* h_diverged, int32_t n_images, int32_t* first_image);
+
+/* Synthetic inputs on the device (same bytes as abcs_synth_generate_host). */
+int abcs_synth_generate(abcs_ctx* ctx, const abcs_synth_spec* spec, int64_t first_index,
+                        int32_t n_images, uint8_t* d_out, int64_t image_stride, void* stream);
+
+/* End-to-end host-buffer pipeline: u8 host images in -> sense -> decode_idct ->
+ * f32 host pixels out (cropped), with H2D / kernels / D2H overlapped in chunks
+ * on the ctx's streams. h_images/h_out should be pinned for full PCIe rate.
+ * Optional host outputs: counts (n*n_blocks) and payload (n*K). Blocks until done. */
+int abcs_sense_decode_host(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* h_images,
+                           int32_t n_images, float* h_out, uint16_t* h_counts, float* h_payload,
+                           int32_t chunk_images);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABCS_B200_H */

@@ -1,0 +1,409 @@
+// extern "C" entry points of libabcs_b200.so (declared in include/abcs_b200.h).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "synth_gen.h"
+
+namespace abcs_b200 {
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ABCS_OK;
+  return set_error(ABCS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* ctx_scratch(Ctx* ctx, size_t bytes, cudaStream_t stream, int* status) {
+  *status = ABCS_OK;
+  if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+  if (ctx->scratch) {
+    // growth is rare (first call of a bigger batch): drain users of the old buffer
+    cudaError_t e = cudaStreamSynchronize(stream);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      *status = cuda_status(e, "scratch sync");
+      return nullptr;
+    }
+    cudaFree(ctx->scratch);
+    ctx->scratch = nullptr;
+    ctx->scratch_bytes = 0;
+  }
+  const size_t want = bytes + bytes / 4 + (1u << 20);
+  cudaError_t e = cudaMalloc(&ctx->scratch, want);
+  if (e != cudaSuccess) {
+    ctx->scratch = nullptr;
+    *status = cuda_status(e, "scratch alloc");
+    return nullptr;
+  }
+  ctx->scratch_bytes = want;
+  return ctx->scratch;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static bool block_supported(int B) { return B == 8 || B == 16 || B == 32; }
+
+}  // namespace abcs_b200
+
+using namespace abcs_b200;
+
+#define CHECK_CTX(ctx) \
+  if (!(ctx)) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null context")
+
+extern "C" {
+
+int abcs_ctx_create(int device, abcs_ctx** out) {
+  if (!out) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null output");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_error(ABCS_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= n) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad device index");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceProperties");
+  if (prop.major != 10) return set_error(ABCS_ERR_UNSUPPORTED, "libabcs_b200 is built for sm_100a (B200) only");
+  auto* ctx = new Ctx;
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  for (auto& st : ctx->pipe) {
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      return cuda_status(e, "stream create");
+    }
+  }
+  *out = reinterpret_cast<abcs_ctx*>(ctx);
+  return ABCS_OK;
+}
+
+int abcs_ctx_destroy(abcs_ctx* c) {
+  if (!c) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+  for (auto& st : ctx->pipe)
+    if (st) cudaStreamDestroy(st);
+  delete ctx;
+  return ABCS_OK;
+}
+
+int64_t abcs_ctx_launch_count(const abcs_ctx* c) {
+  return c ? reinterpret_cast<const Ctx*>(c)->launches : 0;
+}
+
+int abcs_sense_weights_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
+                             int32_t pitch, int32_t n, uint32_t* d_weights, float* d_side, void* stream) {
+  CHECK_CTX(c);
+  if (!p || (!d_images && n > 0) || !d_weights || n < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, d_weights, d_side,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace abcs_b200 {
+
+static size_t sense_scratch_bytes(const abcs_sense_plan* p, int32_t n, bool have_offsets) {
+  const int64_t nbt = (int64_t)n * p->n_blocks;
+  const size_t off_bytes = have_offsets ? 0 : align_up(nbt * 4, 256);
+  const size_t w_bytes = align_up(nbt * 4, 256);
+  const size_t a_bytes = align_up(allocate_scratch_bytes(p->n_blocks, n), 256);
+  return off_bytes + w_bytes + a_bytes;
+}
+
+static int sense_validate(const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride, int32_t pitch,
+                          int32_t n, uint16_t* d_counts, float* d_payload, float* d_side) {
+  if (!p || n < 0 || (n > 0 && (!d_images || !d_counts || !d_payload)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(p->block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (pitch < p->width || image_stride < (int64_t)pitch * (p->height - 1) + p->width)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "image pitch/stride smaller than the image");
+  if (p->algorithm_used == ABCS_ALGO_BBV && p->side_per_image > 0 && !d_side && n > 0)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bbv sensing needs a side-data buffer");
+  return ABCS_OK;
+}
+
+// sense() on n images with caller-provided scratch (sense_scratch_bytes).
+static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride, int32_t pitch,
+                      int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload, float* d_side, char* scr,
+                      cudaStream_t s) {
+  if (n == 0) return ABCS_OK;
+  const int64_t nbt = (int64_t)n * p->n_blocks;
+  const size_t off_bytes = d_offsets ? 0 : align_up(nbt * 4, 256);
+  const size_t w_bytes = align_up(nbt * 4, 256);
+  int32_t* offsets = d_offsets ? d_offsets : reinterpret_cast<int32_t*>(scr);
+  uint32_t* weights = reinterpret_cast<uint32_t*>(scr + off_bytes);
+  void* ascr = scr + off_bytes + w_bytes;
+  int st;
+  if (p->algorithm_used == ABCS_ALGO_ZZ) {
+    st = launch_zz_counts(ctx, *p, n, d_counts, offsets, s);
+    if (st) return st;
+  } else {
+    st = launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, weights, d_side, s);
+    if (st) return st;
+    st = launch_allocate(ctx, weights, p->n_blocks, n, p->alloc_budget, nullptr, p->cap, p->count_base, d_counts,
+                         offsets, nullptr, ascr, s);
+    if (st) return st;
+  }
+  return launch_gather(ctx, p->rows, p->cols, p->block, d_images, nullptr, image_stride, pitch, n, d_counts, offsets,
+                       d_payload, p->coeffs_per_image, s);
+}
+
+}  // namespace abcs_b200
+
+extern "C" {
+
+int abcs_sense_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
+                     int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
+                     float* d_side, void* stream) {
+  CHECK_CTX(c);
+  int st = sense_validate(p, d_images, image_stride, pitch, n, d_counts, d_payload, d_side);
+  if (st || n == 0) return st;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
+  if (st) return st;
+  return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s);
+}
+
+int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
+                        const int32_t* d_caps, int32_t cap, int32_t base, uint16_t* d_counts, int32_t* d_offsets,
+                        int32_t* d_status, void* stream) {
+  CHECK_CTX(c);
+  if (n_blocks < 0 || n_vectors < 0 || (n_blocks * (int64_t)n_vectors > 0 && (!d_weights || !d_counts)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  void* scr = ctx_scratch(ctx, allocate_scratch_bytes(n_blocks, n_vectors), s, &st);
+  if (st) return st;
+  return launch_allocate(ctx, d_weights, n_blocks, n_vectors, budget, d_caps, cap, base, d_counts, d_offsets, d_status,
+                         scr, s);
+}
+
+int abcs_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                      const int32_t* d_offsets, const float* d_payload, int64_t payload_stride, int32_t n,
+                      float* d_out, int64_t out_stride, int32_t out_pitch, const int64_t* d_payload_len,
+                      int32_t* d_error, void* stream) {
+  CHECK_CTX(c);
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_out)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (out_pitch < cols * block || out_stride < (int64_t)out_pitch * (rows * block - 1) + cols * block)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch/stride smaller than the image");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  const int32_t* offsets = d_offsets;
+  if (!offsets || d_error) {
+    int32_t* tmp = nullptr;
+    if (!d_offsets) {
+      tmp = static_cast<int32_t*>(ctx_scratch(ctx, (size_t)n * rows * cols * 4, s, &st));
+      if (st) return st;
+      offsets = tmp;
+    }
+    st = launch_offsets(ctx, rows * cols, n, block, d_counts, tmp, d_payload_len, d_error, s);
+    if (st) return st;
+  }
+  return launch_decode(ctx, rows, cols, block, d_counts, offsets, d_payload, payload_stride, n, d_out, out_stride,
+                       out_pitch, s);
+}
+
+int abcs_forward_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                       const int32_t* d_offsets, const float* d_field, int64_t field_stride, int32_t field_pitch,
+                       int32_t n, float* d_y, int64_t y_stride, void* stream) {
+  CHECK_CTX(c);
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_field || !d_y)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  const int32_t* offsets = d_offsets;
+  if (!offsets) {
+    int32_t* tmp = static_cast<int32_t*>(ctx_scratch(ctx, (size_t)n * rows * cols * 4, s, &st));
+    if (st) return st;
+    st = launch_offsets(ctx, rows * cols, n, block, d_counts, tmp, nullptr, nullptr, s);
+    if (st) return st;
+    offsets = tmp;
+  }
+  return launch_gather(ctx, rows, cols, block, nullptr, d_field, field_stride, field_pitch, n, d_counts, offsets, d_y,
+                       y_stride, s);
+}
+
+int abcs_denoise_dct_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int64_t field_stride,
+                           int32_t n, const double* sigma, double k, int32_t block, float* d_out, void* stream) {
+  CHECK_CTX(c);
+  if (height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_out || !sigma)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (sigma[i] < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "denoise: sigma must be >= 0");
+  const int b = std::max(1, std::min(block, std::min(height, width)));
+  if (b != 8 || height % 4 != 0 || width % 4 != 0)
+    return set_error(ABCS_ERR_UNSUPPORTED, "device dct_threshold supports 8x8 tiles on dims divisible by 4");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  double* thr = static_cast<double*>(ctx_scratch(ctx, (size_t)n * 8, s, &st));
+  if (st) return st;
+  std::vector<double> h(n);
+  for (int i = 0; i < n; ++i) h[i] = k * sigma[i];
+  cudaError_t e = cudaMemcpyAsync(thr, h.data(), n * 8, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "threshold upload");
+  e = cudaStreamSynchronize(s);  // h goes out of scope
+  if (e != cudaSuccess) return cuda_status(e, "threshold upload");
+  return launch_denoise(ctx, d_field, height, width, field_stride, n, thr, d_out, s);
+}
+
+int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                   const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n, const abcs_ida_config* cfg,
+                   const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, float* d_out, int64_t out_stride,
+                   int32_t out_pitch, double* d_trace, int32_t* d_diverged, void* stream) {
+  CHECK_CTX(c);
+  if (!cfg) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null config");
+  // ReconConfig::validate (recon.cpp:39-43)
+  if (cfg->iterations < 1) return set_error(ABCS_ERR_INVALID_ARGUMENT, "iterations must be >= 1");
+  if (cfg->damping < 1.0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "damping factor D_F must be >= 1");
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_out)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  const int Hc = rows * block, Wc = cols * block;
+  const int b = std::max(1, std::min(cfg->denoiser_block, std::min(Hc, Wc)));
+  if (b != 8) return set_error(ABCS_ERR_UNSUPPORTED, "device IDA supports the 8x8 dct_threshold denoiser");
+  if (out_pitch < Wc) return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch smaller than the image");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  const size_t off_bytes = d_offsets ? 0 : align_up((size_t)n * rows * cols * 4, 256);
+  const size_t need = off_bytes + ida_scratch_bytes(rows, cols, block, y_stride, n, *cfg);
+  char* scr = static_cast<char*>(ctx_scratch(ctx, need, s, &st));
+  if (st) return st;
+  const int32_t* offsets = d_offsets;
+  if (!offsets) {
+    st = launch_offsets(ctx, rows * cols, n, block, d_counts, reinterpret_cast<int32_t*>(scr), nullptr, nullptr, s);
+    if (st) return st;
+    offsets = reinterpret_cast<int32_t*>(scr);
+  }
+  return launch_ida(ctx, rows, cols, block, d_counts, offsets, d_y, y_stride, n, *cfg, d_ref, ref_stride, ref_pitch,
+                    d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, s);
+}
+
+int abcs_ida_check(const int32_t* h_diverged, int32_t n, int32_t* first_image) {
+  if (first_image) *first_image = -1;
+  if (!h_diverged) return ABCS_OK;
+  for (int i = 0; i < n; ++i) {
+    const int it = h_diverged[2 * i], kind = h_diverged[2 * i + 1];
+    if (it > 0) {
+      if (first_image) *first_image = i;
+      const char* what = kind == 1 ? "non-finite estimate" : (kind == 2 ? "|x| > 1e6" : "non-finite residual");
+      return set_error(ABCS_ERR_DIVERGENCE,
+                       std::string("solver diverged (") + what + ") at iteration " + std::to_string(it));
+    }
+  }
+  return ABCS_OK;
+}
+
+int abcs_synth_generate(abcs_ctx* c, const abcs_synth_spec* spec, int64_t first_index, int32_t n, uint8_t* d_out,
+                        int64_t image_stride, void* stream) {
+  CHECK_CTX(c);
+  if (!spec || n < 0 || (n > 0 && !d_out)) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (spec->height < 1 || spec->width < 1 || spec->n_ellipses < 0 || spec->n_ellipses > SG_MAX_ELLIPSES)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad synth spec");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  void* scr = ctx_scratch(ctx, (size_t)n * sizeof(sg_scene), s, &st);
+  if (st) return st;
+  return launch_synth(ctx, *spec, first_index, n, d_out, image_stride, scr, s);
+}
+
+// Chunked H2D -> sense -> decode -> D2H over the ctx's three streams: each
+// stream owns one slot of device buffers, so chunk i's copies overlap the other
+// streams' kernels. Inputs/outputs are host buffers (pinned for full PCIe
+// rate); the slot buffers are cached in the ctx across calls.
+int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* h_images, int32_t n, float* h_out,
+                           uint16_t* h_counts, float* h_payload, int32_t chunk) {
+  CHECK_CTX(c);
+  if (!p || n < 0 || (n > 0 && (!h_images || !h_out))) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(p->block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  if (chunk <= 0) chunk = 16;
+  if (chunk > n) chunk = n;
+  constexpr int kSlots = 3;
+  const int64_t px_in = (int64_t)p->height * p->width;
+  const int64_t px_out = (int64_t)p->rows * p->block * p->cols * p->block;
+  const int64_t K = p->coeffs_per_image, S = p->side_per_image, NB = p->n_blocks;
+  const size_t b_img = align_up(chunk * px_in, 256), b_cnt = align_up(chunk * NB * 2, 256),
+               b_off = align_up(chunk * NB * 4, 256), b_pay = align_up(chunk * K * 4 + 4, 256),
+               b_side = align_up(chunk * S * 4 + 4, 256), b_out = align_up(chunk * px_out * 4, 256),
+               b_scr = align_up(sense_scratch_bytes(p, chunk, true), 256);
+  const size_t per_slot = b_img + b_cnt + b_off + b_pay + b_side + b_out + b_scr;
+  if (per_slot * kSlots > ctx->pipe_bytes) {
+    cudaDeviceSynchronize();
+    if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+    ctx->pipe_buf = nullptr;
+    ctx->pipe_bytes = 0;
+    cudaError_t e = cudaMalloc(&ctx->pipe_buf, per_slot * kSlots);
+    if (e != cudaSuccess) return cuda_status(e, "pipeline alloc");
+    ctx->pipe_bytes = per_slot * kSlots;
+  }
+  int st = ABCS_OK;
+  const int nchunks = (n + chunk - 1) / chunk;
+  for (int ci = 0; ci < nchunks && st == ABCS_OK; ++ci) {
+    const int k = ci % kSlots;
+    char* base = static_cast<char*>(ctx->pipe_buf) + per_slot * k;
+    uint8_t* img = reinterpret_cast<uint8_t*>(base);
+    uint16_t* counts = reinterpret_cast<uint16_t*>(base + b_img);
+    int32_t* offsets = reinterpret_cast<int32_t*>(base + b_img + b_cnt);
+    float* payload = reinterpret_cast<float*>(base + b_img + b_cnt + b_off);
+    float* side = reinterpret_cast<float*>(base + b_img + b_cnt + b_off + b_pay);
+    float* out = reinterpret_cast<float*>(base + b_img + b_cnt + b_off + b_pay + b_side);
+    char* scr = base + b_img + b_cnt + b_off + b_pay + b_side + b_out;
+    const int first = ci * chunk;
+    const int cnt = std::min(chunk, n - first);
+    cudaStream_t s = ctx->pipe[k];
+    cudaError_t e = cudaMemcpyAsync(img, h_images + first * px_in, cnt * px_in, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { st = cuda_status(e, "h2d"); break; }
+    st = sense_impl(ctx, p, img, px_in, p->width, cnt, counts, offsets, payload, side, scr, s);
+    if (st) break;
+    st = launch_decode(ctx, p->rows, p->cols, p->block, counts, offsets, payload, K, cnt, out, px_out,
+                       p->cols * p->block, s);
+    if (st) break;
+    e = cudaMemcpyAsync(h_out + first * px_out, out, cnt * px_out * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && h_counts)
+      e = cudaMemcpyAsync(h_counts + first * NB, counts, cnt * NB * 2, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && h_payload)
+      e = cudaMemcpyAsync(h_payload + first * K, payload, cnt * K * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { st = cuda_status(e, "d2h"); break; }
+  }
+  for (auto& s : ctx->pipe) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (st == ABCS_OK && e != cudaSuccess) st = cuda_status(e, "pipeline sync");
+  }
+  return st;
+}
+
+}  // extern "C"

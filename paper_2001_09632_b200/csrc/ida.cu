@@ -1,0 +1,571 @@
+// IDA refinement (reconstruct() with ReconMethod::Ida, recon.cpp:199-259) and
+// the dct_threshold denoiser (denoise.cpp:52-92).
+//
+// State carried between launches is pseudo_t = x_t + A* z_t (recon.cpp:75-79)
+// plus z_t, so one launch per iteration does everything blockwise-local:
+//   x_{t+1} = D_{sigma_t}(pseudo_t)          (8x8 tiles, stride 4, 4-px halo)
+//   z_{t+1} = y - A x_{t+1} + z_t / D_F      (finish_step, recon.cpp:81-93)
+//   pseudo_{t+1} = x_{t+1} + A* z_{t+1}      (next iteration's pseudo_data)
+// and reduces ||z_{t+1}||^2, the trace PSNR error and the divergence checks
+// (check_finite, recon.cpp:53-73) per image; the last CTA of each image turns
+// the partials into sigma_{t+1} = ||z||/sqrt(M) for the next launch (the only
+// cross-block dependency, hence the kernel boundary). The warm start
+// (init_state, recon.cpp:119-131: x0 = A*y, z0 = y - A x0, sigma0 = ||y||/sqrt(M))
+// is the same block phase fed by a decode. The last iteration writes the
+// clamped estimate instead of pseudo (recon.cpp:255-257).
+#include <cfloat>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace abcs_b200 {
+
+constexpr int kIdaThreads = 256;
+constexpr int kRegion = 32;             // output pixels per CTA side
+constexpr int kHalo = 4;                // denoiser tile overlap
+constexpr int kIn = kRegion + 2 * kHalo;  // 40
+constexpr int kInPitch = kIn + 1;
+constexpr int kAccPitch = kRegion + 1;
+constexpr int kTileSlots = kIdaThreads / 8;  // 32 concurrent 8x8 tiles
+constexpr int kTileFloats = 8 * 9;
+
+struct IdaParams {
+  int rows, cols, n;
+  int Hc, Wc;
+  int regions_x, regions_y, regions_per_img;
+  const uint16_t* counts;
+  const int32_t* offsets;
+  const float* y;
+  int64_t y_stride;
+  float* z;                // in place
+  const float* pseudo_in;  // step: pseudo_t
+  float* pseudo_out;       // pseudo_{t+1} (nullptr on the last step)
+  float* x_out;            // clamped estimate on the last step
+  int64_t out_stride;
+  int out_pitch;
+  const uint8_t* ref;
+  int64_t ref_stride;
+  int ref_pitch;
+  float onsager;           // 1/D_F (0 for the warm start)
+  double k;                // threshold multiplier
+  const double* sigma_in;  // sigma_t per image (step); unused for init
+  double* sigma_out;       // sigma_{t+1} per image
+  double* msize;           // M per image (written by init, read by steps)
+  double* partials;        // [n][regions_per_img][4]
+  unsigned int* counters;  // [n]
+  double* trace;           // [n][iters+1][4] or nullptr
+  int trace_row;
+  int trace_rows;
+  int32_t* diverged;       // [n][2] or nullptr
+  unsigned long long* badx;  // [n] min (index*2 + kind) for x, ~0 = none
+  unsigned long long* badz;  // [n] min index for z
+  int iteration;           // iteration number after this launch (0 for init)
+  int is_init;
+};
+
+// ---------------------------------------------------------------------------
+// dct_soft_threshold over one 32x32 output region: s_in holds the field on
+// [R0-4, R0+36) x [C0-4, C0+36) (zeros outside the image). Tiles with origins
+// in {R0-4, ..., R0+28} intersected with the valid origin set {0,4,..,H-8} are
+// processed in 4 parity phases so overlapping tiles never race, which also
+// fixes the summation order. s_acc receives sum/weight (denoise.cpp:90).
+__device__ void denoise_region(const float* s_in, float* s_acc, float* s_tile, int R0, int C0, int H, int W,
+                               float thr) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kRegion * kAccPitch; i += kIdaThreads) s_acc[i] = 0.f;
+  __syncthreads();
+  const int slot = tid / 8, t = tid % 8;
+  const unsigned gmask = 0xffu << ((tid & 31) & ~7);
+  float* T = s_tile + slot * kTileFloats;
+  for (int phase = 0; phase < 4; ++phase) {
+    const int pa = phase >> 1, pb = phase & 1;
+    // tiles of this phase: ti in {pa, pa+2, ..}, tj in {pb, pb+2, ..} (ti,tj in 0..8)
+    const int nti = (9 - pa + 1) / 2, ntj = (9 - pb + 1) / 2;
+    const int ntiles = nti * ntj;
+    for (int base = 0; base < ntiles; base += kTileSlots) {
+      const int idx = base + slot;
+      bool active = idx < ntiles;
+      int orr = 0, oc = 0;
+      if (active) {
+        const int ti = pa + 2 * (idx / ntj), tj = pb + 2 * (idx % ntj);
+        orr = R0 - kHalo + 4 * ti;
+        oc = C0 - kHalo + 4 * tj;
+        active = orr >= 0 && orr <= H - 8 && oc >= 0 && oc <= W - 8;
+      }
+      if (active) {
+        const int lr = orr - (R0 - kHalo), lc = oc - (C0 - kHalo);
+        float x[8], y[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = s_in[(lr + t) * kInPitch + lc + c];
+        Dct<8>::fwd(x, y);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) T[t * 9 + v] = y[v];
+        __syncwarp(gmask);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = T[u * 9 + t];
+        Dct<8>::fwd(x, y);  // y[u] = coefficient (u, t)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u == 0 && t == 0) continue;  // DC passes through (denoise.cpp:76)
+          const float c = y[u];
+          const float mag = fabsf(c) - thr;
+          y[u] = mag > 0.f ? copysignf(mag, c) : 0.f;
+        }
+        Dct<8>::inv(y, x);  // x[r] = column t of C^T Y
+#pragma unroll
+        for (int r = 0; r < 8; ++r) T[r * 9 + t] = x[r];
+        __syncwarp(gmask);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) y[v] = T[t * 9 + v];
+        Dct<8>::inv(y, x);  // row t of the tile
+        const int ar = orr + t - R0;
+        if (ar >= 0 && ar < kRegion) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int ac = oc + c - C0;
+            if (ac >= 0 && ac < kRegion) s_acc[ar * kAccPitch + ac] += x[c];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // weights: number of valid tile origins covering the pixel, per axis
+  for (int i = tid; i < kRegion * kRegion; i += kIdaThreads) {
+    const int r = i / kRegion, c = i % kRegion;
+    const int gr = R0 + r, gc = C0 + c;
+    if (gr >= H || gc >= W) continue;
+    const int br = 4 * (gr / 4), bc = 4 * (gc / 4);
+    const int wr = (br - 4 >= 0 ? 1 : 0) + (br <= H - 8 ? 1 : 0);
+    const int wc = (bc - 4 >= 0 ? 1 : 0) + (bc <= W - 8 ? 1 : 0);
+    s_acc[r * kAccPitch + c] = s_acc[r * kAccPitch + c] / (float)(wr * wc);
+  }
+  __syncthreads();
+}
+
+// Load field[R0-4 .. R0+36) x [C0-4 .. C0+36) into s_in (zeros outside).
+__device__ void load_halo(const float* __restrict__ f, int64_t pitch, int R0, int C0, int H, int W, float* s_in) {
+  for (int i = threadIdx.x; i < kIn * kIn; i += kIdaThreads) {
+    const int r = i / kIn, c = i % kIn;
+    const int gr = R0 - kHalo + r, gc = C0 - kHalo + c;
+    float v = 0.f;
+    if (gr >= 0 && gr < H && gc >= 0 && gc < W) v = __ldg(f + (int64_t)gr * pitch + gc);
+    s_in[r * kInPitch + c] = v;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Block phase over the sensing blocks of the region, with x in s_x:
+//   z_new = (y - A x) + onsager * z_old   (init: z_old = 0)
+//   out   = x + A* z_new                  (last step: clamp(x) instead)
+// red[0] = sum z_new^2, red[1] = sum (ref - x)^2, red[2] = sum y^2, red[3] = sum counts.
+template <int B>
+__device__ void block_phase(const IdaParams& P, int img, int R0, int C0, const float* s_x, float* s_tile,
+                            const unsigned short* s_zz, double* red) {
+  constexpr int BPR = kRegion / B;  // blocks per region side
+  constexpr int NG = BPR * BPR;     // groups needed
+  constexpr int TF = Tile<B>::kFloats;
+  __shared__ double s_red[4][kIdaThreads / 32];
+  __shared__ unsigned long long s_bad[2];
+  const int tid = threadIdx.x;
+  const int g = tid / B, lane = tid % B;
+  double zsum = 0.0, sse = 0.0, ysum = 0.0, csum = 0.0;
+  unsigned long long badx = ~0ull, badz = ~0ull;
+  if (tid == 0) {
+    s_bad[0] = ~0ull;
+    s_bad[1] = ~0ull;
+  }
+  if (g < NG) {
+    const int gbr = R0 / B + g / BPR, gbc = C0 / B + g % BPR;
+    if (gbr < P.rows && gbc < P.cols) {
+      const int64_t nb = (int64_t)P.rows * P.cols;
+      const int64_t bidx = (int64_t)img * nb + (int64_t)gbr * P.cols + gbc;
+      const int cnt = P.counts[bidx];
+      const int64_t off = (int64_t)img * P.y_stride + P.offsets[bidx];
+      if (lane == 0) csum = (double)cnt;
+      Tile<B> ta{s_tile + g * 2 * TF}, tb{s_tile + g * 2 * TF + TF};
+      const int lr = (g / BPR) * B + lane, lc0 = (g % BPR) * B;
+      float xr[B], y[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) xr[c] = s_x[lr * kAccPitch + lc0 + c];
+      // A x (operators.cpp:23-48): forward DCT of the block, rows then columns
+      Dct<B>::fwd(xr, y);
+#pragma unroll
+      for (int v = 0; v < B; ++v) ta.at(lane, v) = y[v];
+#pragma unroll
+      for (int v = 0; v < B; ++v) tb.at(lane, v) = 0.f;
+      __syncwarp(group_mask<B>());
+      {
+        float col[B], cy[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) col[u] = ta.at(u, lane);
+        Dct<B>::fwd(col, cy);
+#pragma unroll
+        for (int u = 0; u < B; ++u) ta.at(u, lane) = cy[u];
+      }
+      __syncwarp(group_mask<B>());
+      // finish_step z update (recon.cpp:86-88)
+      for (int k = lane; k < cnt; k += B) {
+        const int flat = s_zz[k];
+        const float ax = ta.zz(flat);
+        const float yv = P.y[off + k];
+        const float zo = P.is_init ? 0.f : P.z[off + k];
+        const float zn = (yv - ax) + P.onsager * zo;
+        P.z[off + k] = zn;
+        tb.zz(flat) = zn;
+        zsum += (double)zn * (double)zn;
+        ysum += (double)yv * (double)yv;
+        if (!isfinite(zn)) {
+          const unsigned long long gi = (unsigned long long)(P.offsets[bidx] + k);
+          badz = gi < badz ? gi : badz;
+        }
+      }
+      __syncwarp(group_mask<B>());
+      // A* z_new (operators.cpp:50-76): columns then rows
+      {
+        float col[B], cx[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) col[u] = tb.at(u, lane);
+        Dct<B>::inv(col, cx);
+#pragma unroll
+        for (int r = 0; r < B; ++r) tb.at(r, lane) = cx[r];
+      }
+      __syncwarp(group_mask<B>());
+      float az[B];
+      {
+        float rw[B];
+#pragma unroll
+        for (int v = 0; v < B; ++v) rw[v] = tb.at(lane, v);
+        Dct<B>::inv(rw, az);
+      }
+      const int gr = gbr * B + lane, gc0 = gbc * B;
+      const uint8_t* refrow =
+          P.ref ? P.ref + (int64_t)img * P.ref_stride + (int64_t)gr * P.ref_pitch + gc0 : nullptr;
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const float xv = xr[c];
+        if (!isfinite(xv) || fabsf(xv) > 1e6f) {  // check_finite (recon.cpp:56-65)
+          const unsigned long long gi =
+              ((unsigned long long)((int64_t)gr * P.Wc + gc0 + c) << 1) | (isfinite(xv) ? 1ull : 0ull);
+          badx = gi < badx ? gi : badx;
+        }
+        if (refrow) {
+          const double d = (double)refrow[c] - (double)xv;
+          sse += d * d;
+        }
+      }
+      float o[B];
+      float* dst;
+      if (P.pseudo_out) {
+        dst = P.pseudo_out + (int64_t)img * P.Hc * P.Wc + (int64_t)gr * P.Wc + gc0;
+#pragma unroll
+        for (int c = 0; c < B; ++c) o[c] = xr[c] + az[c];
+        store_row_f32<B>(dst, o, true);
+      } else {
+        dst = P.x_out + (int64_t)img * P.out_stride + (int64_t)gr * P.out_pitch + gc0;
+#pragma unroll
+        for (int c = 0; c < B; ++c) o[c] = fminf(fmaxf(xr[c], 0.f), 255.f);  // recon.cpp:255-257
+        store_row_f32<B>(dst, o, (P.out_pitch % 4 == 0) && (P.out_stride % 4 == 0));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zsum += __shfl_xor_sync(0xffffffffu, zsum, o);
+    sse += __shfl_xor_sync(0xffffffffu, sse, o);
+    ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
+    csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    s_red[0][tid >> 5] = zsum;
+    s_red[1][tid >> 5] = sse;
+    s_red[2][tid >> 5] = ysum;
+    s_red[3][tid >> 5] = csum;
+  }
+  if (badx != ~0ull) atomicMin(&s_bad[0], badx);
+  if (badz != ~0ull) atomicMin(&s_bad[1], badz);
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) {
+      double a = 0.0;
+      for (int w = 0; w < kIdaThreads / 32; ++w) a += s_red[q][w];
+      red[q] = a;
+    }
+    if (s_bad[0] != ~0ull) atomicMin(P.badx + img, s_bad[0]);
+    if (s_bad[1] != ~0ull) atomicMin(P.badz + img, s_bad[1]);
+  }
+}
+
+// Last CTA of an image folds the region partials (fixed order, so the result
+// is deterministic) into sigma, the trace row and the divergence record.
+__device__ void finish_image(const IdaParams& P, int img, int region, const double* mine) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
+    for (int q = 0; q < 4; ++q) part[q] = mine[q];
+    __threadfence();
+    const unsigned prev = atomicAdd(P.counters + img, 1u);
+    s_last = (prev == (unsigned)P.regions_per_img - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  const volatile double* pp = P.partials + (int64_t)img * P.regions_per_img * 4;
+  for (int r = 0; r < P.regions_per_img; ++r)
+    for (int q = 0; q < 4; ++q) a[q] += pp[4 * r + q];
+  P.counters[img] = 0;  // ready for the next launch
+  double M;
+  if (P.is_init) {
+    M = a[3];
+    P.msize[img] = M;
+  } else {
+    M = P.msize[img];
+  }
+  const double znorm = sqrt(a[0]);
+  // init_state: sigma0 = ||y|| / sqrt(M) (recon.cpp:129); finish_step: ||z|| / sqrt(M) (:91)
+  const double sigma = (P.is_init ? sqrt(a[2]) : znorm) / sqrt(M);
+  P.sigma_out[img] = sigma;
+  if (P.trace) {
+    double* row = P.trace + ((int64_t)img * P.trace_rows + P.trace_row) * 4;
+    row[0] = (double)P.iteration;
+    row[1] = znorm;
+    row[2] = sigma;
+    double psnr = __longlong_as_double(0x7ff8000000000000ll);  // NaN without a reference
+    if (P.ref) {
+      const double mse = a[1] / ((double)P.Hc * (double)P.Wc);  // metrics.cpp:63-77
+      psnr = (mse == 0.0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(255.0 * 255.0 / mse);
+    }
+    row[3] = psnr;
+  }
+  if (!P.is_init) {
+    const unsigned long long bx = P.badx[img], bz = P.badz[img];
+    if ((bx != ~0ull || bz != ~0ull) && P.diverged && P.diverged[2 * img] == 0) {
+      P.diverged[2 * img] = P.iteration;
+      P.diverged[2 * img + 1] = (bx != ~0ull) ? ((bx & 1ull) ? 2 : 1) : 3;
+    }
+  }
+  P.badx[img] = ~0ull;
+  P.badz[img] = ~0ull;
+}
+
+// Warm start: x0 = A* y (decode into smem), then the block phase with onsager 0.
+template <int B>
+__global__ void __launch_bounds__(kIdaThreads) ida_init_kernel(IdaParams P) {
+  __shared__ float s_x[kRegion * kAccPitch];
+  __shared__ float s_tile[2 * (kRegion / B) * (kRegion / B) * Tile<B>::kFloats];
+  __shared__ unsigned short s_zz[B * B];
+  __shared__ double s_mine[4];
+  load_zigzag<B>(s_zz);
+  const int img = blockIdx.y;
+  const int region = blockIdx.x;
+  const int R0 = (region / P.regions_x) * kRegion, C0 = (region % P.regions_x) * kRegion;
+  __syncthreads();
+  constexpr int BPR = kRegion / B;
+  const int g = threadIdx.x / B, lane = threadIdx.x % B;
+  if (g < BPR * BPR) {
+    const int gbr = R0 / B + g / BPR, gbc = C0 / B + g % BPR;
+    if (gbr < P.rows && gbc < P.cols) {
+      const int64_t bidx = (int64_t)img * P.rows * P.cols + (int64_t)gbr * P.cols + gbc;
+      const int cnt = P.counts[bidx];
+      const float* src = P.y + (int64_t)img * P.y_stride + P.offsets[bidx];
+      Tile<B> t{s_tile + g * Tile<B>::kFloats};
+#pragma unroll
+      for (int v = 0; v < B; ++v) t.at(lane, v) = 0.f;
+      __syncwarp(group_mask<B>());
+      for (int k = lane; k < cnt; k += B) t.zz(s_zz[k]) = src[k];
+      __syncwarp(group_mask<B>());
+      float col[B], cx[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) col[u] = t.at(u, lane);
+      Dct<B>::inv(col, cx);
+#pragma unroll
+      for (int r = 0; r < B; ++r) t.at(r, lane) = cx[r];
+      __syncwarp(group_mask<B>());
+#pragma unroll
+      for (int v = 0; v < B; ++v) col[v] = t.at(lane, v);
+      Dct<B>::inv(col, cx);
+      const int lr = (g / BPR) * B + lane, lc0 = (g % BPR) * B;
+#pragma unroll
+      for (int c = 0; c < B; ++c) s_x[lr * kAccPitch + lc0 + c] = cnt ? cx[c] : 0.f;
+    }
+  }
+  __syncthreads();
+  block_phase<B>(P, img, R0, C0, s_x, s_tile, s_zz, s_mine);
+  finish_image(P, img, region, s_mine);
+}
+
+// One IDA iteration: denoise pseudo_t over the region (+4 px halo), then the block phase.
+template <int B>
+__global__ void __launch_bounds__(kIdaThreads) ida_step_kernel(IdaParams P) {
+  __shared__ float s_in[kIn * kInPitch];
+  __shared__ float s_x[kRegion * kAccPitch];
+  __shared__ float s_tile[kTileSlots * kTileFloats];
+  __shared__ unsigned short s_zz[B * B];
+  __shared__ double s_mine[4];
+  static_assert(2 * (kRegion / B) * (kRegion / B) * Tile<B>::kFloats <= kTileSlots * kTileFloats, "tile smem");
+  load_zigzag<B>(s_zz);
+  const int img = blockIdx.y;
+  const int region = blockIdx.x;
+  const int R0 = (region / P.regions_x) * kRegion, C0 = (region % P.regions_x) * kRegion;
+  const float thr = (float)(P.k * P.sigma_in[img]);
+  load_halo(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s_in);
+  denoise_region(s_in, s_x, s_tile, R0, C0, P.Hc, P.Wc, thr);
+  block_phase<B>(P, img, R0, C0, s_x, s_tile, s_zz, s_mine);
+  finish_image(P, img, region, s_mine);
+}
+
+// Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109).
+__global__ void __launch_bounds__(kIdaThreads)
+denoise_kernel(const float* __restrict__ field, int H, int W, int64_t stride, const double* __restrict__ thr,
+               float* __restrict__ out, int regions_x) {
+  __shared__ float s_in[kIn * kInPitch];
+  __shared__ float s_x[kRegion * kAccPitch];
+  __shared__ float s_tile[kTileSlots * kTileFloats];
+  const int img = blockIdx.y, region = blockIdx.x;
+  const int R0 = (region / regions_x) * kRegion, C0 = (region % regions_x) * kRegion;
+  load_halo(field + (int64_t)img * stride, W, R0, C0, H, W, s_in);
+  denoise_region(s_in, s_x, s_tile, R0, C0, H, W, (float)thr[img]);
+  for (int i = threadIdx.x; i < kRegion * kRegion; i += kIdaThreads) {
+    const int r = i / kRegion, c = i % kRegion;
+    if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s_x[r * kAccPitch + c];
+  }
+}
+
+int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t stride, int32_t n,
+                   const double* thresholds_dev, float* out, cudaStream_t s) {
+  const int rx = (w + kRegion - 1) / kRegion, ry = (h + kRegion - 1) / kRegion;
+  for (int done = 0; done < n;) {
+    const int cnt = std::min(n - done, 65535);
+    denoise_kernel<<<dim3(rx * ry, cnt), kIdaThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
+                                                              thresholds_dev + done, out + (int64_t)done * stride, rx);
+    ctx->launches++;
+    done += cnt;
+  }
+  return cuda_status(cudaGetLastError(), "denoise launch");
+}
+
+static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
+
+size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
+                         const abcs_ida_config& cfg) {
+  const int64_t Hc = (int64_t)rows * block, Wc = (int64_t)cols * block;
+  const int64_t regions = ((Hc + kRegion - 1) / kRegion) * ((Wc + kRegion - 1) / kRegion);
+  size_t b = 0;
+  b += 2 * align256((size_t)n * Hc * Wc * 4);               // pseudo ping-pong
+  b += align256((size_t)n * y_stride * 4);                  // z
+  b += align256((size_t)n * (cfg.iterations + 1) * 8);      // sigma per step
+  b += align256((size_t)n * 8);                             // M
+  b += align256((size_t)n * regions * 4 * 8);               // partials
+  b += align256((size_t)n * 4);                             // counters
+  b += 2 * align256((size_t)n * 8);                         // badx, badz
+  return b;
+}
+
+int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts, const int32_t* offsets,
+               const float* y, int64_t y_stride, int32_t n, const abcs_ida_config& cfg, const uint8_t* ref,
+               int64_t ref_stride, int32_t ref_pitch, float* out, int64_t out_stride, int32_t out_pitch,
+               double* trace, int32_t* diverged, void* scratch, cudaStream_t s) {
+  const int64_t Hc = (int64_t)rows * block, Wc = (int64_t)cols * block;
+  const int rx = (int)((Wc + kRegion - 1) / kRegion), ry = (int)((Hc + kRegion - 1) / kRegion);
+  const int64_t regions = (int64_t)rx * ry;
+  char* p = static_cast<char*>(scratch);
+  float* pseudo[2];
+  pseudo[0] = reinterpret_cast<float*>(p);
+  p += align256((size_t)n * Hc * Wc * 4);
+  pseudo[1] = reinterpret_cast<float*>(p);
+  p += align256((size_t)n * Hc * Wc * 4);
+  float* z = reinterpret_cast<float*>(p);
+  p += align256((size_t)n * y_stride * 4);
+  double* sigma = reinterpret_cast<double*>(p);
+  p += align256((size_t)n * (cfg.iterations + 1) * 8);
+  double* msize = reinterpret_cast<double*>(p);
+  p += align256((size_t)n * 8);
+  double* partials = reinterpret_cast<double*>(p);
+  p += align256((size_t)n * regions * 4 * 8);
+  unsigned int* counters = reinterpret_cast<unsigned int*>(p);
+  p += align256((size_t)n * 4);
+  unsigned long long* badx = reinterpret_cast<unsigned long long*>(p);
+  p += align256((size_t)n * 8);
+  unsigned long long* badz = reinterpret_cast<unsigned long long*>(p);
+  cudaError_t e = cudaMemsetAsync(counters, 0, (size_t)n * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(badx, 0xff, (size_t)n * 8, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(badz, 0xff, (size_t)n * 8, s);
+  if (e == cudaSuccess && diverged) e = cudaMemsetAsync(diverged, 0, (size_t)n * 2 * 4, s);
+  if (e != cudaSuccess) return cuda_status(e, "ida scratch init");
+
+  IdaParams P{};
+  P.rows = rows;
+  P.cols = cols;
+  P.n = n;
+  P.Hc = (int)Hc;
+  P.Wc = (int)Wc;
+  P.regions_x = rx;
+  P.regions_y = ry;
+  P.regions_per_img = (int)regions;
+  P.counts = counts;
+  P.offsets = offsets;
+  P.y = y;
+  P.y_stride = y_stride;
+  P.z = z;
+  P.out_stride = out_stride;
+  P.out_pitch = out_pitch;
+  P.ref = ref;
+  P.ref_stride = ref_stride;
+  P.ref_pitch = ref_pitch;
+  P.k = cfg.k;
+  P.msize = msize;
+  P.partials = partials;
+  P.counters = counters;
+  P.trace = trace;
+  P.trace_rows = cfg.iterations + 1;
+  P.diverged = diverged;
+  P.badx = badx;
+  P.badz = badz;
+  const dim3 grid((unsigned)regions, (unsigned)n);
+  if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "IDA batch limited to 65535 images per call");
+  auto init = [&](auto kern) {
+    P.is_init = 1;
+    P.onsager = 0.f;
+    P.pseudo_in = nullptr;
+    P.pseudo_out = pseudo[0];
+    P.x_out = nullptr;
+    P.sigma_in = nullptr;
+    P.sigma_out = sigma;
+    P.trace_row = 0;
+    P.iteration = 0;
+    kern<<<grid, kIdaThreads, 0, s>>>(P);
+    ctx->launches++;
+  };
+  auto step = [&](auto kern, int t) {
+    P.is_init = 0;
+    P.onsager = (float)(1.0 / cfg.damping);  // IDA: onsager = 1/D_F (recon.cpp:183-184)
+    P.pseudo_in = pseudo[t & 1];
+    const bool last = (t + 1 == cfg.iterations);
+    P.pseudo_out = last ? nullptr : pseudo[(t + 1) & 1];
+    P.x_out = last ? out : nullptr;
+    P.sigma_in = sigma + (int64_t)t * n;
+    P.sigma_out = sigma + (int64_t)(t + 1) * n;
+    P.trace_row = t + 1;
+    P.iteration = t + 1;
+    kern<<<grid, kIdaThreads, 0, s>>>(P);
+    ctx->launches++;
+  };
+  if (block == 8) {
+    init(ida_init_kernel<8>);
+    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<8>, t);
+  } else if (block == 16) {
+    init(ida_init_kernel<16>);
+    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<16>, t);
+  } else if (block == 32) {
+    init(ida_init_kernel<32>);
+    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<32>, t);
+  } else {
+    return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  }
+  return cuda_status(cudaGetLastError(), "ida launch");
+}
+
+}  // namespace abcs_b200

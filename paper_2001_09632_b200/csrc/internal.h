@@ -1,0 +1,69 @@
+// Internal declarations shared by the host entry points (capi.cu, plan.cpp)
+// and the kernel translation units.
+#pragma once
+#include <cstdint>
+#include <string>
+
+#include "../../include/abcs_b200.h"
+
+#if defined(__CUDACC__) || defined(ABCS_WITH_CUDA_RUNTIME)
+#include <cuda_runtime.h>
+#endif
+
+namespace abcs_b200 {
+
+int set_error(int code, const std::string& msg);
+void clear_error();
+
+#if defined(__CUDACC__) || defined(ABCS_WITH_CUDA_RUNTIME)
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // e2e pipeline streams
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int64_t launches = 0;
+  void* pipe_buf = nullptr;  // abcs_sense_decode_host slot buffers
+  size_t pipe_bytes = 0;
+  // pinned staging for abcs_sense_decode_host is caller-provided; nothing here
+};
+
+// Stream-ordered scratch owned by the ctx (grows; never shrinks).
+void* ctx_scratch(Ctx* ctx, size_t bytes, cudaStream_t stream, int* status);
+
+int cuda_status(cudaError_t e, const char* what);
+
+// Kernel launchers (return abcs_status).
+int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs, int64_t img_stride,
+                         int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s);
+int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors,
+                    int64_t budget, const int32_t* caps, int32_t cap, int32_t base, uint16_t* counts,
+                    int32_t* offsets, int32_t* status, void* scratch, cudaStream_t s);
+size_t allocate_scratch_bytes(int32_t n_blocks, int32_t n_vectors);
+int launch_zz_counts(Ctx* ctx, const abcs_sense_plan& p, int32_t n, uint16_t* counts, int32_t* offsets,
+                     cudaStream_t s);
+int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint8_t* imgs,
+                  const float* fimgs, int64_t img_stride, int32_t pitch, int32_t n,
+                  const uint16_t* counts, const int32_t* offsets, float* payload, int64_t payload_stride,
+                  cudaStream_t s);
+int launch_offsets(Ctx* ctx, int32_t n_blocks, int32_t n, int32_t block, const uint16_t* counts,
+                   int32_t* offsets, const int64_t* payload_len, int32_t* error, cudaStream_t s);
+int launch_decode(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
+                  const int32_t* offsets, const float* payload, int64_t payload_stride, int32_t n,
+                  float* out, int64_t out_stride, int32_t out_pitch, cudaStream_t s);
+int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t stride, int32_t n,
+                   const double* thresholds_dev, float* out, cudaStream_t s);
+int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
+               const int32_t* offsets, const float* y, int64_t y_stride, int32_t n,
+               const abcs_ida_config& cfg, const uint8_t* ref, int64_t ref_stride, int32_t ref_pitch,
+               float* out, int64_t out_stride, int32_t out_pitch, double* trace, int32_t* diverged,
+               void* scratch, cudaStream_t s);
+size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
+                         const abcs_ida_config& cfg);
+int launch_synth(Ctx* ctx, const abcs_synth_spec& spec, int64_t first, int32_t n, uint8_t* out,
+                 int64_t stride, void* scratch, cudaStream_t s);
+
+#endif
+
+}  // namespace abcs_b200

@@ -1,0 +1,83 @@
+#!/usr/bin/env python3
+"""Regenerates tests/golden/* from the REFERENCE library itself (oracle/_ref,
+compiled from /root/reference/proj/core/src by oracle/Makefile). Run in the
+build container (the reference is not on the GPU box):
+
+    make -C oracle && python tests/golden/make_golden.py
+
+Inputs are stored in the fixtures, so they do not depend on our generator.
+"""
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import oracle as o  # noqa: E402
+import paper_2001_09632_b200 as p  # noqa: E402
+
+SENSE_CASES = [  # (H, W, B, num, den, algo, seed)
+    (256, 256, 16, 1, 4, 1, 1),    # cfg1 shape
+    (64, 64, 16, 1, 10, 2, 2), (64, 64, 16, 3, 10, 2, 2), (64, 64, 16, 1, 2, 2, 2),  # cfg2 shapes
+    (72, 96, 8, 1, 5, 1, 3),       # cfg3 shape (B=8, L=5)
+    (64, 64, 16, 3, 10, 1, 4),     # cfg4 shape
+    (64, 64, 16, 1, 4, 2, 5),      # cfg5 shape
+    (64, 64, 16, 1, 4, 0, 6),      # zz
+    (64, 64, 16, 1, 1, 1, 7),      # bbv full-rate fallback
+    (64, 64, 16, 1, 40, 1, 8),     # bbv C_F > B fallback
+    (64, 64, 16, 1, 600, 2, 9),    # dd phase1 = 0 fallback
+    (70, 90, 16, 1, 3, 1, 10),     # ragged (cropped) image
+    (64, 64, 32, 1, 4, 2, 11),     # B = 32
+]
+SYNTH = [(256, 256, 20, 5.0, 1, 0), (64, 64, 200, 8.0, 5, 0), (54, 96, 20, 5.0, 3, 1)]
+
+
+def main():
+    ref = o.Reference()
+    rng = np.random.default_rng(20010963)
+    out = {}
+    for i, (H, W, B, num, den, algo, seed) in enumerate(SENSE_CASES):
+        img = p.synth_images_host(p.SynthSpec(H, W, 20, 5.0, seed), 0, 1)[0]
+        r = ref.sense(img, B, num, den, algo)
+        out[f"s{i}_img"] = img
+        out[f"s{i}_cfg"] = np.array([H, W, B, num, den, algo])
+        out[f"s{i}_counts"] = r["counts"]
+        out[f"s{i}_coeffs"] = r["coeffs"]
+        out[f"s{i}_side"] = r["side"]
+        out[f"s{i}_meta"] = np.array([r["algorithm"], r["threshold"], r["target"], r["actual"]], dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "sense_cases.npz"), **out)
+
+    al = {}
+    for i in range(300):
+        m = int(rng.integers(1, 64))
+        kind = i % 3
+        w = (rng.integers(0, 8, m) if kind == 0 else rng.integers(0, 20000, m) if kind == 1
+             else rng.integers(0, 3, m) * int(rng.integers(1, 100))).astype(np.float64)
+        caps = np.full(m, int(rng.integers(1, 300)), np.int32)
+        budget = int(rng.integers(0, int(caps.sum()) + 1))
+        al[f"a{i}_w"], al[f"a{i}_caps"] = w, caps
+        al[f"a{i}_budget"] = np.array([budget])
+        al[f"a{i}_out"] = ref.allocate(w, budget, caps)
+    np.savez_compressed(os.path.join(HERE, "alloc_cases.npz"), **al)
+
+    img = p.synth_images_host(p.SynthSpec(64, 64, 20, 5.0, 4), 0, 1)[0]
+    ms = ref.sense(img, 16, 3, 10, 1)
+    x, tr = ref.reconstruct_ida(4, 4, 16, ms["counts"], ms["coeffs"], 5, ref=img)
+    field = rng.normal(128, 40, (32, 48))
+    np.savez_compressed(os.path.join(HERE, "recon_case.npz"), img=img, counts=ms["counts"], coeffs=ms["coeffs"],
+                        ida_x=x, ida_trace=tr, decode=ref.decode(4, 4, 16, ms["counts"], ms["coeffs"]),
+                        field=field, den0=ref.denoise(field, 0.0), den20=ref.denoise(field, 20.0))
+
+    with open(os.path.join(HERE, "synth_hashes.txt"), "w") as f:
+        for (h, w, e, s, seed, v) in SYNTH:
+            d = hashlib.sha256(p.synth_images_host(p.SynthSpec(h, w, e, s, seed, bool(v)), 0, 2).tobytes()).hexdigest()
+            f.write(f"{h}x{w}-{e}-{s}-{seed}-{v} {d}\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,385 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle.
+
+Bars (BASELINE.json north_star): per-block counts and zigzag index sets
+bit-exact (a block's index set is the zigzag prefix of its count, so equal
+counts <=> equal sets); BBV side data bit-exact; reconstructed pixels within
+1e-3 absolute (0-255 scale); PSNR within 0.01 dB. The payload itself is fp32
+on the device vs fp64 in the reference: PAYLOAD_TOL bounds the fp32 DCT error
+(DESIGN.md "Precision").
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, synth
+
+pytestmark = pytest.mark.gpu
+
+PIXEL_TOL = 1e-3
+PSNR_TOL = 0.01
+PAYLOAD_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def p(torch):
+    import paper_2001_09632_b200 as p
+    return p
+
+
+def psnr(ref, x):
+    mse = np.mean((np.asarray(ref, np.float64) - np.asarray(x, np.float64)) ** 2)
+    return float("inf") if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
+
+
+def sense_dev(p, torch, imgs, B, num, den, algo, threshold=None):
+    t = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
+    cfg = p.SensingConfig(B, num, den, p.Algorithm(algo), threshold)
+    b = p.sense_batch(t, cfg)
+    torch.cuda.synchronize()
+    return b
+
+
+def assert_sense_equal(b, i, want, B):
+    counts = b.counts[i].cpu().numpy().astype(np.int64)
+    assert np.array_equal(counts, want["counts"].astype(np.int64))
+    assert b.plan.algorithm_used == want["algorithm"]
+    assert b.plan.threshold == want["threshold"]
+    pay = b.payload[i].cpu().numpy().astype(np.float64)
+    assert pay.size == want["coeffs"].size
+    if pay.size:
+        assert np.max(np.abs(pay - want["coeffs"])) <= PAYLOAD_TOL
+    if want["side"].size:
+        assert np.array_equal(b.side[i].cpu().numpy().astype(np.float64), want["side"])
+
+
+# ---- generator -------------------------------------------------------------------------
+def test_device_generator_matches_host(p, torch):
+    for spec in (p.SynthSpec(256, 256, 20, 5.0, 1), p.SynthSpec(128, 96, 200, 8.0, 5),
+                 p.SynthSpec(54, 96, 20, 5.0, 3, video=True), p.SynthSpec(33, 17, 5, 5.0, 2)):
+        d = p.synth_images(spec, 5, 3).cpu().numpy()
+        h = p.synth_images_host(spec, 5, 3)
+        assert np.array_equal(d, h)
+
+
+# ---- sensing ----------------------------------------------------------------------------
+def test_golden_sense_cases(p, torch):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "sense_cases.npz"))
+    n = len([k for k in z.files if k.endswith("_cfg")])
+    for i in range(n):
+        H, W, B, num, den, algo = (int(v) for v in z[f"s{i}_cfg"])
+        b = sense_dev(p, torch, z[f"s{i}_img"][None], B, num, den, algo)
+        meta = z[f"s{i}_meta"]
+        want = dict(counts=z[f"s{i}_counts"], coeffs=z[f"s{i}_coeffs"], side=z[f"s{i}_side"],
+                    algorithm=int(meta[0]), threshold=float(meta[1]))
+        assert_sense_equal(b, 0, want, B)
+
+
+SENSE_CFGS = [  # (H, W, B, num, den, algo, n_images)
+    (256, 256, 16, 1, 4, 1, 2),      # cfg1
+    (512, 512, 16, 1, 10, 2, 3),     # cfg2 sweep
+    (512, 512, 16, 3, 10, 2, 3),
+    (512, 512, 16, 1, 2, 2, 3),
+    (1080, 1920, 8, 1, 5, 1, 1),     # cfg3 frame
+    (512, 512, 16, 3, 10, 1, 2),     # cfg4
+    (1024, 1024, 16, 1, 4, 2, 1),    # cfg5-like (crop of a 4096^2 workload)
+    (200, 328, 32, 1, 4, 2, 2),      # B = 32, ragged
+    (70, 90, 16, 1, 3, 1, 2),        # ragged crop
+    (64, 64, 16, 1, 300, 0, 2),      # zz with zero-count blocks
+    (64, 64, 16, 1, 1, 1, 1),        # full rate -> zz fallback
+    (64, 64, 16, 1, 600, 2, 1),      # dd fallback
+]
+
+
+@pytest.mark.parametrize("case", SENSE_CFGS)
+def test_sense_parity(p, torch, checker, case):
+    H, W, B, num, den, algo, n = case
+    imgs = synth(H, W, n=n, seed=H + 3 * W + algo, video=(B == 8))
+    b = sense_dev(p, torch, imgs, B, num, den, algo)
+    for i in range(n):
+        want = checker.sense(imgs[i], B, num, den, algo)
+        assert_sense_equal(b, i, want, B)
+
+
+def test_sense_threshold_override(p, torch, checker):
+    imgs = synth(128, 128, n=2, seed=3)
+    for thr in (0.0, 7.5, 45.0):
+        b = sense_dev(p, torch, imgs, 16, 1, 4, 2, threshold=thr)
+        for i in range(2):
+            assert_sense_equal(b, i, checker.sense(imgs[i], 16, 1, 4, 2, threshold=thr), 16)
+
+
+def test_dd_significance_exact(p, torch, port):
+    """Phase-1 counts n_i (sensing.cpp:341-358) equal the fp64 reference on every block,
+    including |c| == T ties (DC = sum/16 is exact for B=16)."""
+    import ctypes as C
+    imgs = synth(256, 256, n=2, seed=17)
+    imgs[1, :64, :64] = 60  # flat block: DC = 16*60 = 960 ; plus exact ties below
+    imgs[1, 64:80, 0:16] = 0
+    imgs[1, 64, 0] = 240      # DC = 240/16 = 15 == T at C_R = 1/2 (T = 15): must NOT count
+    lib = p._lib.load()
+    for (num, den) in ((1, 10), (3, 10), (1, 2)):
+        cfg = p.SensingConfig(16, num, den, p.Algorithm.DD)
+        plan = p.sense_plan(cfg, 256, 256)
+        t = torch.from_numpy(imgs).cuda()
+        w = torch.empty((2, plan.n_blocks), dtype=torch.int32, device="cuda")
+        st = lib.abcs_sense_weights_batch(p.Context.get().handle, C.byref(plan), t.data_ptr(), 256 * 256, 256, 2,
+                                          w.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
+        assert st == 0
+        got = w.cpu().numpy()
+        zz = port.zigzag(16)
+        for i in range(2):
+            want = []
+            for br in range(16):
+                for bc in range(16):
+                    c = port.dct2(imgs[i, br * 16:(br + 1) * 16, bc * 16:(bc + 1) * 16].astype(np.float64), 16)
+                    want.append(int(np.sum(np.abs(c[zz[:plan.dd_phase1]]) > plan.threshold)))
+            assert np.array_equal(got[i], np.array(want)), (num, den, i)
+
+
+def test_bbv_measure_parity(p, checker):
+    for (H, W, B, num, den) in ((256, 256, 16, 1, 4), (1080, 1920, 8, 1, 5), (512, 512, 16, 3, 10), (70, 90, 16, 1, 3)):
+        img = synth(H, W, seed=H)[0]
+        a = p.bbv_measure(img, p.SensingConfig(B, num, den, p.Algorithm.BBV))
+        b = checker.bbv_measure(img, B, num, den)
+        assert (a.stride, a.offset, a.per_side, a.phase1_total) == (b["stride"], b["offset"], b["per_side"],
+                                                                     b["phase1_total"])
+        assert np.array_equal(a.variation, b["variation"])
+        assert np.array_equal(a.side_values, b["side"])
+
+
+def test_sense_batch_equals_single_and_is_deterministic(p, torch):
+    imgs = synth(512, 512, n=6, seed=2)
+    b = sense_dev(p, torch, imgs, 16, 3, 10, 2)
+    b2 = sense_dev(p, torch, imgs, 16, 3, 10, 2)
+    assert torch.equal(b.counts.view(torch.int16), b2.counts.view(torch.int16))
+    assert torch.equal(b.payload, b2.payload)
+    for i in (0, 5):
+        s = sense_dev(p, torch, imgs[i:i + 1], 16, 3, 10, 2)
+        assert torch.equal(s.payload[0], b.payload[i])
+
+
+def test_single_image_api(p, checker):
+    img = synth(128, 160, seed=4)[0]
+    warn = []
+    ms = p.sense(img, p.SensingConfig(16, 1, 4, p.Algorithm.BBV), warn)
+    want = checker.sense(img, 16, 1, 4, 1)
+    assert np.array_equal(ms.counts.astype(np.int64), want["counts"].astype(np.int64))
+    assert np.array_equal(ms.side.astype(np.float64), want["side"])
+    assert p.measurement_budget(ms).actual == want["actual"]
+    warn = []
+    ms = p.sense(img, p.SensingConfig(16, 1, 40, p.Algorithm.BBV), warn)
+    assert ms.algorithm == p.Algorithm.ZZ and warn and "reverting" in warn[0]
+
+
+# ---- allocation ---------------------------------------------------------------------------
+def test_allocator_golden(p):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "alloc_cases.npz"))
+    n = len([k for k in z.files if k.endswith("_w")])
+    for i in range(n):
+        got = p.largest_remainder_allocate(z[f"a{i}_w"], int(z[f"a{i}_budget"][0]), z[f"a{i}_caps"])
+        assert np.array_equal(got, z[f"a{i}_out"]), i
+
+
+def test_allocator_adversarial_and_large(p, checker, rng):
+    for i in range(200):
+        m = int(rng.integers(1, 3000))
+        w = (rng.integers(0, 4, m) * rng.integers(1, 50)).astype(np.float64) if i % 2 else \
+            rng.integers(0, 16320, m).astype(np.float64)
+        caps = np.full(m, int(rng.integers(1, 256)), np.int32)
+        budget = int(rng.integers(0, int(caps.sum()) + 1))
+        assert np.array_equal(p.largest_remainder_allocate(w, budget, caps), checker.allocate(w, budget, caps)), i
+    # cfg5 scale: 65536 blocks, DD-like small integer weights -> huge exact-tie groups
+    w = rng.integers(0, 33, 65536).astype(np.float64)
+    caps = np.full(65536, 224, np.int32)
+    assert np.array_equal(p.largest_remainder_allocate(w, 65536 * 32, caps), checker.allocate(w, 65536 * 32, caps))
+    assert list(p.largest_remainder_allocate([1, 0, 0, 0], 2000, [1024] * 4)) == [1024, 326, 325, 325]
+    with pytest.raises(ValueError):
+        p.largest_remainder_allocate([1, 2], 10, [1, 1])
+
+
+# ---- decode / operators -------------------------------------------------------------------
+def test_decode_golden(p):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"])
+    x = p.decode_idct(ms)
+    assert np.max(np.abs(x - z["decode"])) <= PIXEL_TOL
+
+
+@pytest.mark.parametrize("case", SENSE_CFGS)
+def test_sense_decode_pixels(p, torch, checker, case):
+    """End-to-end sense -> decode_idct vs the reference: pixels 1e-3, PSNR 0.01 dB."""
+    H, W, B, num, den, algo, n = case
+    imgs = synth(H, W, n=n, seed=H + 3 * W + algo, video=(B == 8))
+    b = sense_dev(p, torch, imgs, B, num, den, algo)
+    out = p.decode_batch(b).cpu().numpy()
+    Hc, Wc = b.plan.rows * B, b.plan.cols * B
+    for i in range(n):
+        want = checker.sense(imgs[i], B, num, den, algo)
+        ref = checker.decode(b.plan.rows, b.plan.cols, B, want["counts"], want["coeffs"])
+        assert np.max(np.abs(out[i] - ref)) <= PIXEL_TOL
+        crop = imgs[i, :Hc, :Wc]
+        assert abs(psnr(crop, out[i]) - psnr(crop, ref)) <= PSNR_TOL
+
+
+def test_decode_format_errors(p):
+    ms = p.MeasurementSet(32, 32, 16, p.Algorithm.ZZ, 1, 4, 0.0, np.array([3, 3, 3, 3], np.uint16),
+                          np.zeros(11, np.float32))
+    with pytest.raises(p.FormatError):
+        p.decode_idct(ms)
+    ms.counts = np.array([300, 0, 0, 0], np.uint16)
+    ms.coeffs = np.zeros(300, np.float32)
+    with pytest.raises(ValueError):
+        p.decode_idct(ms)
+
+
+def test_operator_identities(p, rng, checker):
+    img = synth(96, 64, seed=8)[0]
+    ms = p.sense(img, p.SensingConfig(16, 3, 10, p.Algorithm.DD))
+    op = p.SensingOperator.from_ms(ms)
+    y = rng.normal(0, 30, op.measurements()).astype(np.float32)
+    assert np.max(np.abs(op.forward(op.adjoint(y)) - y)) < 1e-3          # A A* = I
+    x = rng.normal(128, 40, op.field_size())
+    lhs, rhs = np.dot(op.forward(x), y), np.dot(x, op.adjoint(y))       # <Ax,y> = <x,A*y>
+    assert abs(lhs - rhs) <= 1e-4 * (abs(lhs) + 1)
+    want = checker.forward(6, 4, 16, ms.counts, x.reshape(96, 64))
+    assert np.max(np.abs(op.forward(x) - want)) <= PAYLOAD_TOL
+    full = p.sense(img, p.SensingConfig(16, 1, 1, p.Algorithm.ZZ))     # C_R = 1: exact decode
+    assert np.max(np.abs(p.decode_idct(full) - img)) <= PIXEL_TOL
+
+
+# ---- denoise / IDA --------------------------------------------------------------------------
+def test_denoise_parity(p, checker, rng):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
+    spec = p.DenoiserSpec("dct_threshold", {"k": 1.0})
+    assert np.max(np.abs(p.denoise(spec, z["field"], 0.0) - z["den0"])) <= PIXEL_TOL
+    assert np.max(np.abs(p.denoise(spec, z["field"], 20.0) - z["den20"])) <= PIXEL_TOL
+    f = rng.normal(128, 60, (96, 160))
+    for s in (3.0, 17.0):
+        assert np.max(np.abs(p.denoise(spec, f, s) - checker.denoise(f, s))) <= PIXEL_TOL
+
+
+def test_ida_golden(p):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"])
+    res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=5), reference=z["img"])
+    assert np.max(np.abs(res.image - z["ida_x"])) <= PIXEL_TOL
+    tr = np.array([[r.iteration, r.residual_norm, r.sigma, r.psnr_db] for r in res.trace])
+    want = z["ida_trace"]
+    assert np.array_equal(tr[:, 0], want[:, 0])
+    assert np.allclose(tr[1:, 1], want[1:, 1], rtol=1e-4)
+    assert np.allclose(tr[:, 2], want[:, 2], rtol=1e-4)
+    assert np.max(np.abs(tr[:, 3] - want[:, 3])) <= PSNR_TOL
+
+
+IDA_CASES = [  # (H, W, B, num, den, algo, iters)
+    (128, 128, 16, 3, 10, 1, 10),    # cfg4 shape
+    (256, 256, 16, 1, 4, 2, 5),      # cfg5 shape
+    (96, 160, 8, 1, 5, 1, 3),        # B = 8
+    (128, 96, 32, 1, 4, 2, 3),       # B = 32
+    (80, 48, 16, 1, 10, 2, 4),       # ragged region grid
+]
+
+
+@pytest.mark.parametrize("case", IDA_CASES)
+def test_ida_parity(p, torch, checker, case):
+    H, W, B, num, den, algo, iters = case
+    imgs = synth(H, W, n=2, seed=H * W + iters)
+    b = sense_dev(p, torch, imgs, B, num, den, algo)
+    ref_t = torch.from_numpy(imgs).cuda()
+    out, tr, div = p.ida_batch(b, p.ReconConfig(p.ReconMethod.Ida, iterations=iters), reference=ref_t)
+    out, tr = out.cpu().numpy(), tr.cpu().numpy()
+    for i in range(2):
+        want = checker.sense(imgs[i], B, num, den, algo)
+        x, trace = checker.reconstruct_ida(b.plan.rows, b.plan.cols, B, want["counts"], want["coeffs"], iters,
+                                           ref=imgs[i])
+        assert np.max(np.abs(out[i] - x)) <= PIXEL_TOL, (i, np.max(np.abs(out[i] - x)))
+        crop = imgs[i, :x.shape[0], :x.shape[1]]
+        assert abs(psnr(crop, out[i]) - psnr(crop, x)) <= PSNR_TOL
+        assert np.max(np.abs(tr[i, :, 3] - trace[:, 3])) <= PSNR_TOL
+        assert np.allclose(tr[i, :, 2], trace[:, 2], rtol=1e-4)
+
+
+def test_ida_divergence(p):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"] * 1e7)
+    with pytest.raises(p.DivergenceError) as e:
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=3))
+    assert e.value.iteration == 1
+    with pytest.raises(ValueError):
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=0))
+    with pytest.raises(p.UnsupportedError):
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Amp, iterations=2))
+
+
+# ---- full-size properties (BASELINE sizes) -------------------------------------------------
+def test_cfg2_full_batch_properties(p, torch, checker):
+    """1024 x 512^2 DD sweep: K per image exact, determinism, round-trip, sampled parity."""
+    spec = p.SynthSpec(512, 512, 20, 5.0, 2)
+    imgs = p.synth_images(spec, 0, 1024)
+    for num, den in ((1, 10), (3, 10), (1, 2)):
+        cfg = p.SensingConfig(16, num, den, p.Algorithm.DD)
+        b = p.sense_batch(imgs, cfg)
+        sums = b.counts.to(torch.int32).sum(dim=1)
+        assert bool((sums == b.plan.coeffs_per_image).all())
+        assert int(b.counts.to(torch.int32).max()) <= 256
+        b2 = p.sense_batch(imgs, cfg)
+        assert torch.equal(b.payload, b2.payload)
+        for i in (0, 511, 1023):
+            host = imgs[i].cpu().numpy()
+            assert_sense_equal(b, i, checker.sense(host, 16, num, den, 2), 16)
+        # round trip: re-sensing the decode's zigzag prefix reproduces the payload (A A* = I)
+        x = p.decode_batch(b)
+        y = torch.empty_like(b.payload)
+        import ctypes as C
+        st = p._lib.load().abcs_forward_batch(p.Context.get().handle, 32, 32, 16, b.counts.data_ptr(),
+                                              b.offsets.data_ptr(), x.data_ptr(), 512 * 512, 512, 1024,
+                                              y.data_ptr(), b.payload.stride(0),
+                                              torch.cuda.current_stream().cuda_stream)
+        assert st == 0
+        assert float((y - b.payload).abs().max()) < 2e-3
+
+
+def test_cfg5_image_parity(p, torch, checker):
+    """One 4096^2 image (200 ellipses, sigma 8), DD 0.25: counts exact, pixels 1e-3 after decode."""
+    imgs = p.synth_images(p.SynthSpec(4096, 4096, 200, 8.0, 5), 0, 1)
+    cfg = p.SensingConfig(16, 1, 4, p.Algorithm.DD)
+    b = p.sense_batch(imgs, cfg)
+    host = imgs[0].cpu().numpy()
+    want = checker.sense(host, 16, 1, 4, 2)
+    assert_sense_equal(b, 0, want, 16)
+    x = p.decode_batch(b)[0].cpu().numpy()
+    ref = checker.decode(256, 256, 16, want["counts"], want["coeffs"])
+    assert np.max(np.abs(x - ref)) <= PIXEL_TOL
+    assert abs(psnr(host, x) - psnr(host, ref)) <= PSNR_TOL
+
+
+def test_empty_batch(p, torch):
+    imgs = torch.empty((0, 64, 64), dtype=torch.uint8, device="cuda")
+    b = p.sense_batch(imgs, p.SensingConfig(16, 1, 4, p.Algorithm.DD))
+    assert b.counts.shape == (0, 16)
+    assert p.decode_batch(b).shape == (0, 64, 64)
+
+
+def test_host_pipeline_matches_device_path(p, torch):
+    import ctypes as C
+    spec = p.SynthSpec(512, 512, 20, 5.0, 2)
+    imgs = p.synth_images_host(spec, 0, 37)
+    cfg = p.SensingConfig(16, 3, 10, p.Algorithm.DD)
+    plan = p.sense_plan(cfg, 512, 512)
+    out = np.empty((37, 512, 512), np.float32)
+    counts = np.empty((37, plan.n_blocks), np.uint16)
+    st = p._lib.load().abcs_sense_decode_host(p.Context.get().handle, C.byref(plan), imgs.ctypes.data, 37,
+                                              out.ctypes.data, counts.ctypes.data, None, 8)
+    assert st == 0, p._lib.last_error()
+    b = sense_dev(p, torch, imgs, 16, 3, 10, 2)
+    assert np.array_equal(counts, b.counts.cpu().numpy().view(np.uint16))
+    assert np.array_equal(out, p.decode_batch(b).cpu().numpy())
