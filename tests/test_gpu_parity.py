@@ -40,6 +40,15 @@ def psnr(ref, x):
     return float("inf") if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
 
 
+def assert_psnr_close(a, b):
+    """PSNR within 0.01 dB. At C_R = 1 both decodes are lossless up to rounding (the
+    reference's ~1e-13 vs fp32's ~1e-6 residue puts both beyond 140 dB, where PSNR
+    differences carry no information); pixels are still held to 1e-3 there."""
+    if min(a, b) >= 120.0:
+        return
+    assert abs(a - b) <= PSNR_TOL, (a, b)
+
+
 def sense_dev(p, torch, imgs, B, num, den, algo, threshold=None):
     t = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
     cfg = p.SensingConfig(B, num, den, p.Algorithm(algo), threshold)
@@ -227,7 +236,7 @@ def test_sense_decode_pixels(p, torch, checker, case):
         ref = checker.decode(b.plan.rows, b.plan.cols, B, want["counts"], want["coeffs"])
         assert np.max(np.abs(out[i] - ref)) <= PIXEL_TOL
         crop = imgs[i, :Hc, :Wc]
-        assert abs(psnr(crop, out[i]) - psnr(crop, ref)) <= PSNR_TOL
+        assert_psnr_close(psnr(crop, out[i]), psnr(crop, ref))
 
 
 def test_decode_format_errors(p):
@@ -303,7 +312,7 @@ def test_ida_parity(p, torch, checker, case):
                                            ref=imgs[i])
         assert np.max(np.abs(out[i] - x)) <= PIXEL_TOL, (i, np.max(np.abs(out[i] - x)))
         crop = imgs[i, :x.shape[0], :x.shape[1]]
-        assert abs(psnr(crop, out[i]) - psnr(crop, x)) <= PSNR_TOL
+        assert_psnr_close(psnr(crop, out[i]), psnr(crop, x))
         assert np.max(np.abs(tr[i, :, 3] - trace[:, 3])) <= PSNR_TOL
         assert np.allclose(tr[i, :, 2], trace[:, 2], rtol=1e-4)
 
@@ -359,7 +368,7 @@ def test_cfg5_image_parity(p, torch, checker):
     x = p.decode_batch(b)[0].cpu().numpy()
     ref = checker.decode(256, 256, 16, want["counts"], want["coeffs"])
     assert np.max(np.abs(x - ref)) <= PIXEL_TOL
-    assert abs(psnr(host, x) - psnr(host, ref)) <= PSNR_TOL
+    assert_psnr_close(psnr(host, x), psnr(host, ref))
 
 
 def test_empty_batch(p, torch):

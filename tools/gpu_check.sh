@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU-box pass: tests, smoke, bench. Logs land in gpurun_out/.
+cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
+mkdir -p gpurun_out
+nvidia-smi -L > gpurun_out/gpu.txt 2>&1
+nproc >> gpurun_out/gpu.txt
+ls -la paper_2001_09632_b200/*.so oracle/_ref oracle/_build >> gpurun_out/gpu.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+if [ -z "${NO_BENCH:-}" ]; then
+  timeout 600 python bench.py --steps ${STEPS:-5} --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
+fi
+tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.log

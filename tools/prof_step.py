@@ -1,0 +1,22 @@
+"""One warm cfg2 step (3 subrates: sense + decode) and one cfg4 IDA batch, for ncu."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2001_09632_b200 as p  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+imgs = p.synth_images(p.SynthSpec(512, 512, 20, 5.0, 2), 0, 1024)
+if which in ("all", "cfg2"):
+    for rep in range(2):
+        for num, den in ((1, 10), (3, 10), (1, 2)):
+            b = p.sense_batch(imgs, p.SensingConfig(16, num, den, p.Algorithm.DD))
+            p.decode_batch(b)
+if which in ("all", "ida"):
+    b = p.sense_batch(imgs[:64], p.SensingConfig(16, 3, 10, p.Algorithm.BBV))
+    for rep in range(2):
+        p.ida_batch(b, p.ReconConfig(p.ReconMethod.Ida, iterations=10), trace=False, check=False)
+torch.cuda.synchronize()
+print("ok")
