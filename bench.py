@@ -210,25 +210,23 @@ def run_ours(args, world, rank, local):
     imgs = p.synth_images(spec, rank * n, n, device=local)  # disjoint global indices per rank
     cfgs = [p.SensingConfig(CFG2["B"], num, den, p.Algorithm.DD) for num, den in SUBRATES]
     plans = [p.sense_plan(c, CFG2["H"], CFG2["W"]) for c in cfgs]
-    batches = [p.sense_batch(imgs, c, pl) for c, pl in zip(cfgs, plans)]  # allocates outputs once
-    outs = [p.decode_batch(b) for b in batches]
+    # outputs allocated once: payload/counts/offsets per subrate + decoded images
+    fused = [p.sense_decode_batch(imgs, c, pl) for c, pl in zip(cfgs, plans)]
+    batches = [f[0] for f in fused]
+    outs = [f[1] for f in fused]
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(len(SUBRATES))]
-          for _ in range(args.steps)]
-    sense_ms = [0.0] * len(SUBRATES)
-    decode_ms = [0.0] * len(SUBRATES)
+    nsub = len(SUBRATES)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nsub + 1)] for _ in range(args.steps)]
 
     def step(evs):
+        # sense (DD phase 1 + allocation + zigzag gather) and decode_idct, fused over the payload
         for j, (c, pl, b) in enumerate(zip(cfgs, plans, batches)):
+            if evs and j == 0:
+                evs[0].record(stream)
+            p.sense_decode_batch(imgs, c, pl, out=b, image_out=outs[j])
             if evs:
-                evs[j][0].record(stream)
-            p.sense_batch(imgs, c, pl, out=b)
-            if evs:
-                evs[j][1].record(stream)
-            p.decode_batch(b, out=outs[j])
-            if evs:
-                evs[j][2].record(stream)
+                evs[j + 1].record(stream)
 
     for _ in range(args.warmup):
         step(None)
@@ -245,41 +243,51 @@ def run_ours(args, world, rank, local):
         step(ev[k])
     end.record(stream)
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        for j in range(len(SUBRATES)):
-            sense_ms[j] += ev[k][j][0].elapsed_time(ev[k][j][1])
-            decode_ms[j] += ev[k][j][1].elapsed_time(ev[k][j][2])
     launches = ctx.launches() - launches0
     clk = clocks.stop() if clocks else None
     barrier(world)
+    sub_ms = [sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps for j in range(nsub)]
     ms = start.elapsed_time(end)
     ms_max = max_over_ranks(ms, world, dev)
     ms_step = ms_max / args.steps
-    px_step = len(SUBRATES) * n * CFG2["H"] * CFG2["W"]
+    px_step = nsub * n * CFG2["H"] * CFG2["W"]
     value = world * px_step * args.steps / (ms_max / 1e3) / 1e6
 
-    # algorithmic bytes: sense = N + 4K + 2nB ; decode = 4K + 2nB + 4N  (per image)
+    # unfused split (sense_batch, then decode_batch from the payload) for the per-kernel roofline
+    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    sense_ms, decode_ms = [0.0] * nsub, [0.0] * nsub
+    reps = max(1, min(args.steps, 5))
+    for _ in range(reps):
+        for j, (c, pl, b) in enumerate(zip(cfgs, plans, batches)):
+            s_ev[0].record(stream)
+            p.sense_batch(imgs, c, pl, out=b)
+            s_ev[1].record(stream)
+            p.decode_batch(b, out=outs[j])
+            s_ev[2].record(stream)
+            torch.cuda.synchronize()
+            sense_ms[j] += s_ev[0].elapsed_time(s_ev[1]) / reps
+            decode_ms[j] += s_ev[1].elapsed_time(s_ev[2]) / reps
+
+    # algorithmic bytes, per image: sense = N + 4K + 2nB ; decode = 4K + 2nB + 4N
     N = CFG2["H"] * CFG2["W"]
     per_j = []
     for j, pl in enumerate(plans):
         K, nB = pl.coeffs_per_image, pl.n_blocks
         sense_b = n * (N + 4 * K + 2 * nB)
         dec_b = n * (4 * K + 2 * nB + 4 * N)
-        per_j.append(dict(subrate=f"{SUBRATES[j][0]}/{SUBRATES[j][1]}", K=K,
-                          sense_ms=sense_ms[j] / args.steps, decode_ms=decode_ms[j] / args.steps,
+        per_j.append(dict(subrate=f"{SUBRATES[j][0]}/{SUBRATES[j][1]}", K=K, fused_ms=round(sub_ms[j], 4),
+                          fused_frac=round((sense_b + dec_b) / (sub_ms[j] / 1e3) / 1e9 / hbm, 4),
+                          unfused_sense_ms=round(sense_ms[j], 4), unfused_decode_ms=round(decode_ms[j], 4),
                           sense_bytes=sense_b, decode_bytes=dec_b))
     dec_bytes = sum(x["decode_bytes"] for x in per_j)
-    dec_ms = sum(x["decode_ms"] for x in per_j)
     sen_bytes = sum(x["sense_bytes"] for x in per_j)
-    sen_ms = sum(x["sense_ms"] for x in per_j)
-    dominant = "decode_kernel" if dec_ms >= sen_ms else "sense (dd_weights+alloc+gather)"
+    dec_ms, sen_ms = sum(decode_ms), sum(sense_ms)
     if dec_ms >= sen_ms:
-        ach = dec_bytes / (dec_ms / 1e3) / 1e9
-        traffic_alg = dec_bytes / len(SUBRATES)
+        dominant, ach, traffic_alg = "decode16_kernel", dec_bytes / (dec_ms / 1e3) / 1e9, dec_bytes / nsub
     else:
-        ach = sen_bytes / (sen_ms / 1e3) / 1e9
-        traffic_alg = sen_bytes / len(SUBRATES)
-    pipe_ach = (dec_bytes + sen_bytes) / ((dec_ms + sen_ms) / 1e3) / 1e9
+        dominant, ach, traffic_alg = "sense (dd pass 1 + allocation + gather)", sen_bytes / (sen_ms / 1e3) / 1e9, \
+            sen_bytes / nsub
+    pipe_ach = (dec_bytes + sen_bytes) / (sum(sub_ms) / 1e3) / 1e9
 
     # e2e through the C ABI with host buffers (pinned), H2D + kernels + D2H in the timed region
     import ctypes as C
@@ -331,8 +339,8 @@ def run_ours(args, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": hbm,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / hbm, 4),
                          "algorithmic_bytes_per_launch": int(traffic_alg), "traffic": None},
-            "pipeline_roofline": {"achieved": round(pipe_ach, 1), "frac": round(pipe_ach / hbm, 4),
-                                  "phases": per_j},
+            "pipeline_roofline": {"what": "fused sense+decode step vs algorithmic bytes (SURVEY 8d)",
+                                  "achieved": round(pipe_ach, 1), "frac": round(pipe_ach / hbm, 4), "phases": per_j},
             "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
             "ida": ida,

@@ -151,6 +151,15 @@ int abcs_sense_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* 
                      int64_t image_stride, int32_t pitch, int32_t n_images, uint16_t* d_counts,
                      int32_t* d_offsets, float* d_payload, float* d_side, void* stream);
 
+/* abcs::sense followed by decode_idct of the result, fused: the decoded image
+ * is computed from the same fp32 payload values the call writes (identical
+ * to abcs_decode_batch on d_payload) without re-reading them from HBM.
+ * d_out: image i at d_out + i*out_stride, rows out_pitch floats apart. */
+int abcs_sense_decode_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_images,
+                            int64_t image_stride, int32_t pitch, int32_t n_images, uint16_t* d_counts,
+                            int32_t* d_offsets, float* d_payload, float* d_side, float* d_out,
+                            int64_t out_stride, int32_t out_pitch, void* stream);
+
 /* Phase-1 weights only (bbv_measure variation / DD significance counts n_i),
  * u32 per block — exposes the pre-measurement of sensing.cpp:266-294 / :341-358. */
 int abcs_sense_weights_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_images,

@@ -369,6 +369,36 @@ def sense_batch(images, cfg: SensingConfig, plan: Optional[SensePlanC] = None,
     return out
 
 
+def sense_decode_batch(images, cfg: SensingConfig, plan: Optional[SensePlanC] = None,
+                       out: Optional[MeasurementBatch] = None, image_out=None):
+    """sense then decode_idct on a (n, H, W) uint8 CUDA tensor in one fused pass over the
+    payload; returns (MeasurementBatch, (n, Hc, Wc) float32 decoded images)."""
+    torch = _torch()
+    if images.dtype != torch.uint8 or images.dim() != 3 or not images.is_cuda:
+        raise ValueError("images must be a (n, H, W) uint8 CUDA tensor")
+    n, H, W = images.shape
+    if plan is None:
+        plan = sense_plan(cfg, H, W)
+    dev = images.device
+    if out is None:
+        K, S, NB = plan.coeffs_per_image, plan.side_per_image, plan.n_blocks
+        out = MeasurementBatch(
+            plan=plan, cfg=cfg,
+            counts=torch.empty((n, NB), dtype=torch.uint16, device=dev),
+            offsets=torch.empty((n, NB), dtype=torch.int32, device=dev),
+            payload=torch.empty((n, max(K, 1)), dtype=torch.float32, device=dev)[:, :K],
+            side=torch.empty((n, S), dtype=torch.float32, device=dev) if S > 0 else None)
+    Hc, Wc = plan.rows * plan.block, plan.cols * plan.block
+    if image_out is None:
+        image_out = torch.empty((n, Hc, Wc), dtype=torch.float32, device=dev)
+    images = images.contiguous()
+    ctx = Context.get(dev.index)
+    _check(_lib.load().abcs_sense_decode_batch(
+        ctx.handle, C.byref(plan), images.data_ptr(), H * W, W, n, _ptr(out.counts), _ptr(out.offsets),
+        _ptr(out.payload), _ptr(out.side), image_out.data_ptr(), Hc * Wc, Wc, _stream_ptr(torch)))
+    return out, image_out
+
+
 def decode_batch(batch: MeasurementBatch, out=None):
     """decode_idct on every set of the batch -> (n, Hc, Wc) float32 CUDA tensor."""
     torch = _torch()

@@ -273,10 +273,331 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
   if (tid == 0 && status) status[v] = st;
 }
 
+// ---------------------------------------------------------------------------
+// Weight-class allocator (the production path for sense). Blocks with equal
+// weights get equal shares and equal fraction keys, so each round needs one
+// exact RN64 key per DISTINCT weight (DD: <= phase1 + 1 classes; BBV: the
+// distinct boundary variations) instead of one per block. Per round:
+// histogram of active weights -> compacted class table (count, whole, key) ->
+// MSB radix select of the leftover threshold over the classes weighted by
+// their counts -> exact ties resolved by block index (ordered CTA scan) ->
+// clamp. Results are identical to alloc_kernel / the reference.
+// 256 threads; each thread owns a contiguous range of blocks and of weight
+// values so every CTA-wide scan is a single BlockScan. Per-block state (weight,
+// allocation) lives in shared memory when it fits, else in global scratch.
+constexpr int kClassThreads = 256;
+
+template <typename T>
+struct Arr {
+  T* p;
+  __device__ __forceinline__ T& operator[](int i) const { return p[i]; }
+};
+
+size_t class_smem_bytes(int wmax, int n_blocks, bool arrays_in_smem) {
+  const size_t ncls = (size_t)std::min(n_blocks, wmax + 1);
+  size_t b = 4 * (size_t)(wmax + 1) + ncls * (8 + 4 + 4 + 1) + 64;
+  if (arrays_in_smem) b += (size_t)n_blocks * 4 + 16;
+  return b;
+}
+
+template <bool kSmemArrays>
+__global__ void __launch_bounds__(kClassThreads)
+alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64_t budget, int cap, int base,
+                   uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status,
+                   uint32_t* __restrict__ gscratch) {
+  using Reduce64 = cub::BlockReduce<unsigned long long, kClassThreads>;
+  using ScanI = cub::BlockScan<int, kClassThreads>;
+  __shared__ union {
+    typename Reduce64::TempStorage r;
+    typename ScanI::TempStorage s;
+  } tmp;
+  __shared__ unsigned int hist8[256];
+  __shared__ long long sh_ll[4];
+  __shared__ int sh_int[4];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const int ncls_cap = min(nb, wmax + 1);
+  unsigned char* p = dyn;
+  uint64_t* ckey = reinterpret_cast<uint64_t*>(p);
+  p += 8 * (size_t)ncls_cap;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+  p += 4 * (size_t)(wmax + 1);
+  uint32_t* ccnt = reinterpret_cast<uint32_t*>(p);
+  p += 4 * (size_t)ncls_cap;
+  uint32_t* cwhole = reinterpret_cast<uint32_t*>(p);
+  p += 4 * (size_t)ncls_cap;
+  uint8_t* cflag = p;
+  p += ncls_cap;
+  const int v = blockIdx.x, tid = threadIdx.x;
+  Arr<uint16_t> wv, av;  // weight and allocation per block
+  if constexpr (kSmemArrays) {
+    uint16_t* q = reinterpret_cast<uint16_t*>(dyn + ((p - dyn + 15) & ~15));
+    wv.p = q;
+    av.p = q + nb;
+  } else {
+    wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)v * 2 * nb;
+    av.p = wv.p + nb;
+  }
+  const uint32_t* w = weights + (int64_t)v * nb;
+  const int per_b = (nb + kClassThreads - 1) / kClassThreads;  // contiguous block range per thread
+  const int b0 = min(nb, tid * per_b), b1 = min(nb, b0 + per_b);
+  const int per_c = (wmax + 1 + kClassThreads - 1) / kClassThreads;
+  const int c0 = min(wmax + 1, tid * per_c), c1 = min(wmax + 1, c0 + per_c);
+  if (tid == 0) sh_int[3] = 0;
+  __syncthreads();
+  for (int i = b0; i < b1; ++i) {
+    const uint32_t wi = w[i];
+    if (wi > (uint32_t)wmax) sh_int[3] = 1;  // caller's weight bound violated
+    wv[i] = (uint16_t)min(wi, (uint32_t)wmax);
+    av[i] = 0;
+  }
+  if (budget < 0 || (unsigned long long)budget > (unsigned long long)cap * (unsigned long long)nb || cap < 0 ||
+      cap > 65535) {
+    if (tid == 0 && status) status[v] = ABCS_ERR_INVALID_ARGUMENT;
+    return;
+  }
+  __syncthreads();
+  long long remaining = budget;
+  int st = sh_int[3] ? ABCS_ERR_LOGIC : ABCS_OK;
+  int round = 0;
+  while (remaining > 0 && st == ABCS_OK) {
+    if (++round > nb + 1) {
+      st = ABCS_ERR_LOGIC;
+      break;
+    }
+    for (int c = c0; c < c1; ++c) hist[c] = 0;
+    __syncthreads();
+    unsigned long long tw = 0, na = 0;
+    for (int i = b0; i < b1; ++i) {
+      if ((int)av[i] < cap) {
+        atomicAdd(&hist[wv[i]], 1u);
+        tw += wv[i];
+        na += 1;
+      }
+    }
+    const unsigned long long T0 = Reduce64(tmp.r).Sum(tw);
+    __syncthreads();
+    const unsigned long long n_active = Reduce64(tmp.r).Sum(na);
+    if (tid == 0) {
+      sh_ll[0] = (long long)T0;
+      sh_ll[1] = (long long)n_active;
+    }
+    __syncthreads();
+    const bool uniform = sh_ll[0] == 0;
+    const uint64_t T = uniform ? (uint64_t)sh_ll[1] : (uint64_t)sh_ll[0];
+    const long long n_act = sh_ll[1];
+    // compact the nonempty classes (ordered by weight) and compute their shares
+    int mine = 0;
+    for (int c = c0; c < c1; ++c) mine += hist[c] ? 1 : 0;
+    int id, ncls;
+    ScanI(tmp.s).ExclusiveSum(mine, id, ncls);
+    unsigned long long handed = 0;
+    for (int c = c0; c < c1; ++c) {
+      const uint32_t h = hist[c];
+      if (!h) continue;
+      const int k = id++;
+      ccnt[k] = h;
+      const ak_u128 P = (ak_u128)(uint64_t)remaining * (uniform ? 1u : (uint32_t)c);
+      const ak_share sh = ak_compute(P, T);  // sensing.cpp:144-148
+      cwhole[k] = (uint32_t)sh.whole;
+      ckey[k] = sh.key;
+      cflag[k] = (uint8_t)sh.flag;
+      hist[c] = (uint32_t)k;
+      handed += (unsigned long long)h * sh.whole;
+    }
+    __syncthreads();
+    const unsigned long long hsum = Reduce64(tmp.r).Sum(handed);
+    if (tid == 0) sh_ll[2] = (long long)hsum;
+    __syncthreads();
+    const long long leftover = remaining - sh_ll[2];
+    // leftover units -> largest fractions, ties to the lower index (sensing.cpp:150-158)
+    const bool sel_all = leftover > 0 && leftover >= n_act;
+    const bool none = leftover <= 0;
+    unsigned long long prefix = 0;
+    int passes = 0, flag_sel = -1;
+    bool all_equal_taken = false;
+    long long need = leftover;
+    bool rank_mode = false;
+    uint64_t thr_key = 0;
+    int thr_flag = 0;
+    if (!sel_all && !none && ncls <= kClassThreads) {
+      // few classes: each class counts the blocks ranking strictly above it and tied with it
+      rank_mode = true;
+      if (tid < ncls) {
+        const uint64_t kk = ckey[tid];
+        const int fk = cflag[tid];
+        long long above = 0, eqc = 0;
+        for (int j = 0; j < ncls; ++j) {
+          const uint64_t kj = ckey[j];
+          const int fj = cflag[j];
+          if (kj > kk || (kj == kk && fj > fk)) above += ccnt[j];
+          else if (kj == kk && fj == fk) eqc += ccnt[j];
+        }
+        if (above < need && need <= above + eqc) {  // the tie group holding the threshold
+          sh_ll[3] = above;
+          sh_int[2] = (int)eqc;
+          sh_int[1] = fk;
+          sh_ll[2] = (long long)kk;
+        }
+      }
+      __syncthreads();
+      need -= sh_ll[3];
+      all_equal_taken = need == (long long)sh_int[2];
+      thr_key = (uint64_t)sh_ll[2];
+      thr_flag = sh_int[1];
+      __syncthreads();
+    } else if (!sel_all && !none) {
+      for (int pass = 0; pass < 9; ++pass) {
+        const int nbins = pass < 8 ? 256 : 2;
+        hist8[tid] = 0;
+        __syncthreads();
+        const int shift_hi = 64 - 8 * pass;
+        for (int k = tid; k < ncls; k += kClassThreads) {
+          const uint64_t kk = ckey[k];
+          const bool match = (pass == 0) ? true : (pass < 8 ? ((kk >> shift_hi) == prefix) : (kk == prefix));
+          if (!match) continue;
+          const unsigned d = pass < 8 ? (unsigned)((kk >> (56 - 8 * pass)) & 0xffu) : (unsigned)cflag[k];
+          atomicAdd(&hist8[d], ccnt[k]);
+        }
+        __syncthreads();
+        if (tid < 32) {
+          const int lane = tid;
+          const int per = (nbins + 31) / 32;
+          unsigned local = 0;
+          for (int q = 0; q < per; ++q) {
+            const int d = nbins - 1 - (lane * per + q);
+            if (d >= 0) local += hist8[d];
+          }
+          unsigned incl = local;
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const unsigned excl = incl - local;
+          const bool hit = ((long long)excl < need) && ((long long)incl >= need);
+          const unsigned ball = __ballot_sync(0xffffffffu, hit);
+          const int src = __ffs(ball) - 1;
+          if (lane == src) {
+            unsigned cum = excl;
+            for (int q = 0; q < per; ++q) {
+              const int d = nbins - 1 - (lane * per + q);
+              if (d < 0) break;
+              if ((long long)cum + hist8[d] >= need) {
+                sh_int[1] = d;
+                sh_int[2] = (int)hist8[d];
+                sh_ll[3] = (long long)cum;
+                break;
+              }
+              cum += hist8[d];
+            }
+          }
+        }
+        __syncthreads();
+        const int g = sh_int[1];
+        const int eq = sh_int[2];
+        need -= sh_ll[3];
+        if (pass < 8) prefix = (prefix << 8) | (unsigned long long)g;
+        else flag_sel = g;
+        passes = pass + 1;
+        __syncthreads();
+        if (eq == need) {
+          all_equal_taken = true;
+          break;
+        }
+      }
+    }
+    // classify: 1 = above the threshold, 2 = in the exact-tie group
+    auto cls_rel = [&](int k) -> int {
+      if (sel_all) return 1;
+      if (none) return 0;
+      const uint64_t kk = ckey[k];
+      if (rank_mode) {
+        if (kk != thr_key) return kk > thr_key ? 1 : 0;
+        return (int)cflag[k] > thr_flag ? 1 : ((int)cflag[k] == thr_flag ? 2 : 0);
+      }
+      if (passes <= 8) {
+        const int sh = 64 - 8 * passes;
+        const unsigned long long top = sh >= 64 ? 0ull : (kk >> sh);
+        return top > prefix ? 1 : (top == prefix ? 2 : 0);
+      }
+      if (kk != prefix) return kk > prefix ? 1 : 0;
+      return (int)cflag[k] > flag_sel ? 1 : ((int)cflag[k] == flag_sel ? 2 : 0);
+    };
+    int tie_base = 0;
+    if (!sel_all && !none && !all_equal_taken) {
+      int ties = 0;
+      for (int i = b0; i < b1; ++i)
+        if ((int)av[i] < cap && cls_rel((int)hist[wv[i]]) == 2) ++ties;
+      int tot;
+      ScanI(tmp.s).ExclusiveSum(ties, tie_base, tot);
+      __syncthreads();
+    }
+    unsigned long long taken_sum = 0, still = 0;
+    for (int i = b0; i < b1; ++i) {
+      if ((int)av[i] >= cap) continue;
+      const int k = (int)hist[wv[i]];
+      const int rel = cls_rel(k);
+      bool sel = rel == 1;
+      if (rel == 2) sel = all_equal_taken || (long long)(tie_base++) < need;
+      const long long give = (long long)cwhole[k] + (sel ? 1 : 0);
+      const long long room = (long long)cap - av[i];
+      const long long taken = give < room ? give : room;  // sensing.cpp:162-171
+      av[i] = (uint16_t)(av[i] + taken);
+      taken_sum += (unsigned long long)taken;
+      if ((int)av[i] < cap) still += 1;
+    }
+    const unsigned long long tk = Reduce64(tmp.r).Sum(taken_sum);
+    __syncthreads();
+    const unsigned long long st_open = Reduce64(tmp.r).Sum(still);
+    if (tid == 0) {
+      sh_ll[0] = (long long)tk;
+      sh_ll[1] = (long long)st_open;
+    }
+    __syncthreads();
+    remaining -= sh_ll[0];
+    if (remaining > 0 && sh_ll[1] == 0) st = ABCS_ERR_LOGIC;  // capacity exhausted
+    __syncthreads();
+  }
+  // counts = base + allocation, offsets = exclusive scan (contiguous ranges: one scan)
+  int mine = 0;
+  for (int i = b0; i < b1; ++i) mine += base + (int)av[i];
+  int ex, total;
+  ScanI(tmp.s).ExclusiveSum(mine, ex, total);
+  for (int i = b0; i < b1; ++i) {
+    const int c = base + (int)av[i];
+    counts[(int64_t)v * nb + i] = (uint16_t)c;
+    if (offsets) offsets[(int64_t)v * nb + i] = ex;
+    ex += c;
+  }
+  if (tid == 0 && status) status[v] = st;
+}
+
 int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
                     const int32_t* caps, int32_t cap, int32_t base, uint16_t* counts, int32_t* offsets,
-                    int32_t* status, void* scratch, cudaStream_t s) {
+                    int32_t* status, void* scratch, cudaStream_t s, int32_t wmax) {
   if (n_vectors == 0 || n_blocks == 0) return ABCS_OK;
+  if (!caps && wmax >= 0 && wmax < 65536 && cap <= 65535) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(alloc_class_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(alloc_class_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    uint32_t* gscr = reinterpret_cast<uint32_t*>(scratch);  // n_vectors * n_blocks * 2 u16
+    const size_t smem_in = class_smem_bytes(wmax, n_blocks, true);
+    const size_t smem_out = class_smem_bytes(wmax, n_blocks, false);
+    if (smem_in <= 56 * 1024) {  // keep >= 4 CTAs per SM
+      alloc_class_kernel<true><<<n_vectors, kClassThreads, smem_in, s>>>(weights, n_blocks, wmax, budget, cap, base,
+                                                                         counts, offsets, status, gscr);
+    } else if (smem_out <= 200 * 1024) {
+      alloc_class_kernel<false><<<n_vectors, kClassThreads, smem_out, s>>>(weights, n_blocks, wmax, budget, cap,
+                                                                           base, counts, offsets, status, gscr);
+    } else {
+      goto generic;
+    }
+    ctx->launches++;
+    return cuda_status(cudaGetLastError(), "allocate(class) launch");
+  }
+generic:
   AllocScratch scr;
   char* p = reinterpret_cast<char*>(scratch);
   const size_t n = (size_t)n_blocks * n_vectors;

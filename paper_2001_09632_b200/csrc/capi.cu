@@ -104,8 +104,11 @@ int abcs_sense_weights_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_
   if (!p || (!d_images && n > 0) || !d_weights || n < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
   Ctx* ctx = reinterpret_cast<Ctx*>(c);
   cudaSetDevice(ctx->device);
-  return launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, d_weights, d_side,
-                              reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  uint32_t* fix = static_cast<uint32_t*>(ctx_scratch(ctx, sense_fix_words((int64_t)n * p->n_blocks) * 4, s, &st));
+  if (st) return st;
+  return launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, d_weights, d_side, s, fix);
 }
 
 }  // extern "C"
@@ -117,7 +120,8 @@ static size_t sense_scratch_bytes(const abcs_sense_plan* p, int32_t n, bool have
   const size_t off_bytes = have_offsets ? 0 : align_up(nbt * 4, 256);
   const size_t w_bytes = align_up(nbt * 4, 256);
   const size_t a_bytes = align_up(allocate_scratch_bytes(p->n_blocks, n), 256);
-  return off_bytes + w_bytes + a_bytes;
+  const size_t f_bytes = align_up(sense_fix_words(nbt) * 4, 256);
+  return off_bytes + w_bytes + a_bytes + f_bytes;
 }
 
 static int sense_validate(const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride, int32_t pitch,
@@ -132,10 +136,12 @@ static int sense_validate(const abcs_sense_plan* p, const uint8_t* d_images, int
   return ABCS_OK;
 }
 
-// sense() on n images with caller-provided scratch (sense_scratch_bytes).
+// sense() on n images with caller-provided scratch (sense_scratch_bytes);
+// with d_out, also the decode of the result (fused into the payload pass when
+// the tensor-core path applies).
 static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride, int32_t pitch,
                       int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload, float* d_side, char* scr,
-                      cudaStream_t s) {
+                      cudaStream_t s, float* d_out = nullptr, int64_t out_stride = 0, int32_t out_pitch = 0) {
   if (n == 0) return ABCS_OK;
   const int64_t nbt = (int64_t)n * p->n_blocks;
   const size_t off_bytes = d_offsets ? 0 : align_up(nbt * 4, 256);
@@ -143,19 +149,30 @@ static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_image
   int32_t* offsets = d_offsets ? d_offsets : reinterpret_cast<int32_t*>(scr);
   uint32_t* weights = reinterpret_cast<uint32_t*>(scr + off_bytes);
   void* ascr = scr + off_bytes + w_bytes;
+  uint32_t* fix = reinterpret_cast<uint32_t*>(scr + off_bytes + w_bytes + align_up(allocate_scratch_bytes(p->n_blocks, n), 256));
   int st;
   if (p->algorithm_used == ABCS_ALGO_ZZ) {
     st = launch_zz_counts(ctx, *p, n, d_counts, offsets, s);
     if (st) return st;
   } else {
-    st = launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, weights, d_side, s);
+    st = launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, weights, d_side, s, fix);
     if (st) return st;
+    // largest possible phase-1 weight: DD counts <= phase1; BBV sums <= 4 * valid probes * 255
+    const int32_t wmax = p->algorithm_used == ABCS_ALGO_DD ? p->dd_phase1 : 4 * p->bbv_valid_probes * 255;
     st = launch_allocate(ctx, weights, p->n_blocks, n, p->alloc_budget, nullptr, p->cap, p->count_base, d_counts,
-                         offsets, nullptr, ascr, s);
+                         offsets, nullptr, ascr, s, wmax);
     if (st) return st;
   }
-  return launch_gather(ctx, p->rows, p->cols, p->block, d_images, nullptr, image_stride, pitch, n, d_counts, offsets,
-                       d_payload, p->coeffs_per_image, s);
+  if (d_out && p->block == 16 && mma16_supported(p->rows, p->cols, n) && out_pitch % 2 == 0 && out_stride % 2 == 0 &&
+      ((uintptr_t)d_out % 8) == 0) {
+    return launch_sense16(ctx, 3, p->rows, p->cols, n, d_images, image_stride, pitch, 0, 0.0, nullptr, d_counts,
+                          offsets, d_payload, p->coeffs_per_image, d_out, out_stride, out_pitch, s);
+  }
+  st = launch_gather(ctx, p->rows, p->cols, p->block, d_images, nullptr, image_stride, pitch, n, d_counts, offsets,
+                     d_payload, p->coeffs_per_image, s);
+  if (st || !d_out) return st;
+  return launch_decode(ctx, p->rows, p->cols, p->block, d_counts, offsets, d_payload, p->coeffs_per_image, n, d_out,
+                       out_stride, out_pitch, s);
 }
 
 }  // namespace abcs_b200
@@ -174,6 +191,24 @@ int abcs_sense_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_ima
   char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
   if (st) return st;
   return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s);
+}
+
+int abcs_sense_decode_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
+                            int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
+                            float* d_side, float* d_out, int64_t out_stride, int32_t out_pitch, void* stream) {
+  CHECK_CTX(c);
+  int st = sense_validate(p, d_images, image_stride, pitch, n, d_counts, d_payload, d_side);
+  if (st || n == 0) return st;
+  const int Wc = p->cols * p->block, Hc = p->rows * p->block;
+  if (!d_out || out_pitch < Wc || out_stride < (int64_t)out_pitch * (Hc - 1) + Wc)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch/stride smaller than the image");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
+  if (st) return st;
+  return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s, d_out,
+                    out_stride, out_pitch);
 }
 
 int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
@@ -387,10 +422,8 @@ int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t*
     cudaStream_t s = ctx->pipe[k];
     cudaError_t e = cudaMemcpyAsync(img, h_images + first * px_in, cnt * px_in, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) { st = cuda_status(e, "h2d"); break; }
-    st = sense_impl(ctx, p, img, px_in, p->width, cnt, counts, offsets, payload, side, scr, s);
-    if (st) break;
-    st = launch_decode(ctx, p->rows, p->cols, p->block, counts, offsets, payload, K, cnt, out, px_out,
-                       p->cols * p->block, s);
+    st = sense_impl(ctx, p, img, px_in, p->width, cnt, counts, offsets, payload, side, scr, s, out, px_out,
+                    p->cols * p->block);
     if (st) break;
     e = cudaMemcpyAsync(h_out + first * px_out, out, cnt * px_out * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && h_counts)

@@ -104,11 +104,30 @@ __device__ __forceinline__ void store_row_f32(float* __restrict__ dst, const flo
   }
 }
 
+// Exact unsigned division by a runtime-constant divisor for n, d < 2^31
+// (Granlund-Montgomery round-up multiplier): q = (umulhi(m, n) + n) >> l.
+struct FastDiv {
+  uint32_t d = 1, m = 0, l = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    l = 0;
+    while ((1ull << l) < div) ++l;
+    m = (uint32_t)((((1ull << 32) * ((1ull << l) - div)) / div) + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(m, n) + n) >> l);
+  }
+};
+
 // zigzag_order (zigzag.cpp:8-26) and the fp64 reference basis as device tables.
 template <int B> __device__ __forceinline__ const unsigned short* zigzag_dev();
 template <> __device__ __forceinline__ const unsigned short* zigzag_dev<8>() { return abcs_gen::kZigzagDev8; }
 template <> __device__ __forceinline__ const unsigned short* zigzag_dev<16>() { return abcs_gen::kZigzagDev16; }
 template <> __device__ __forceinline__ const unsigned short* zigzag_dev<32>() { return abcs_gen::kZigzagDev32; }
+template <int B> __device__ __forceinline__ const unsigned short* zigzag_rank_dev();
+template <> __device__ __forceinline__ const unsigned short* zigzag_rank_dev<8>() { return abcs_gen::kZigzagRankDev8; }
+template <> __device__ __forceinline__ const unsigned short* zigzag_rank_dev<16>() { return abcs_gen::kZigzagRankDev16; }
+template <> __device__ __forceinline__ const unsigned short* zigzag_rank_dev<32>() { return abcs_gen::kZigzagRankDev32; }
 template <int B> __device__ __forceinline__ const double* basis_dev();
 template <> __device__ __forceinline__ const double* basis_dev<8>() { return abcs_gen::kBasisDev8; }
 template <> __device__ __forceinline__ const double* basis_dev<16>() { return abcs_gen::kBasisDev16; }

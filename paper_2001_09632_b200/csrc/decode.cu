@@ -103,7 +103,10 @@ int launch_decode(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint16_
   const int64_t gpc = kDecodeThreads / B;
   const unsigned grid = (unsigned)((total + gpc - 1) / gpc);
   const bool al = ((uintptr_t)out % 16 == 0) && (out_stride % 4 == 0) && (out_pitch % 4 == 0);
-  if (B == 8)
+  if (B == 16 && out_pitch % 2 == 0 && out_stride % 2 == 0 && ((uintptr_t)out % 8) == 0 &&
+      mma16_supported(rows, cols, n)) {
+    return launch_decode16(ctx, rows, cols, n, counts, offsets, payload, payload_stride, out, out_stride, out_pitch, s);
+  } else if (B == 8)
     decode_kernel<8><<<grid, kDecodeThreads, 0, s>>>(rows, cols, n, counts, offsets, payload, payload_stride, out,
                                                      out_stride, out_pitch, al);
   else if (B == 16)

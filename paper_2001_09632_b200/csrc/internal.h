@@ -36,10 +36,13 @@ int cuda_status(cudaError_t e, const char* what);
 
 // Kernel launchers (return abcs_status).
 int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs, int64_t img_stride,
-                         int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s);
+                         int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s,
+                         uint32_t* fix_scratch = nullptr);
+// u32 words of fixup scratch launch_sense_weights needs (count + one entry per block)
+inline size_t sense_fix_words(int64_t n_blocks_total) { return (size_t)n_blocks_total + 4; }
 int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors,
                     int64_t budget, const int32_t* caps, int32_t cap, int32_t base, uint16_t* counts,
-                    int32_t* offsets, int32_t* status, void* scratch, cudaStream_t s);
+                    int32_t* offsets, int32_t* status, void* scratch, cudaStream_t s, int32_t wmax = -1);
 size_t allocate_scratch_bytes(int32_t n_blocks, int32_t n_vectors);
 int launch_zz_counts(Ctx* ctx, const abcs_sense_plan& p, int32_t n, uint16_t* counts, int32_t* offsets,
                      cudaStream_t s);
@@ -61,6 +64,15 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
                void* scratch, cudaStream_t s);
 size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
                          const abcs_ida_config& cfg);
+bool mma16_supported(int rows, int cols, int n);
+// mode 1: DD weights; 2: payload; 3: payload + fused decode
+int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
+                   int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
+                   float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
+                   cudaStream_t s, uint32_t* fix_scratch = nullptr);
+int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts, const int32_t* offsets,
+                    const float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
+                    cudaStream_t s);
 int launch_synth(Ctx* ctx, const abcs_synth_spec& spec, int64_t first, int32_t n, uint8_t* out,
                  int64_t stride, void* scratch, cudaStream_t s);
 

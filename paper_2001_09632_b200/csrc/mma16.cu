@@ -1,0 +1,462 @@
+// B = 16 hot path on tensor cores (mma.sync, fp16 hi/lo split; mma_dct.cuh).
+//
+//  * sense16_kernel<kWeights, kPayload, kDecode>: u8 image blocks ->
+//      kWeights: DD phase-1 significance counts n_i (sensing.cpp:341-358)
+//      kPayload: zigzag-prefix payload (gather_prefixes, sensing.cpp:192-227)
+//      kDecode:  decode_idct of that payload (recon.cpp:109-117), fused: the
+//                inverse transform consumes the same fp32 values that were
+//                written to the payload, so the pixels equal decode(payload)
+//                bit for bit without re-reading the payload from HBM.
+//  * decode16_kernel: decode_idct from a packed payload.
+//
+// A warp owns a pair of horizontally adjacent blocks per step (lane L loads row
+// L%16 of block L/16 with one 16-B load; the pair's rows share a 32-B sector),
+// stages them in shared memory and gathers its B-fragment bytes from there; the
+// next pair is prefetched into registers meanwhile. Coefficients travel through
+// a per-warp zigzag-ordered buffer: prefix writes to the payload are coalesced
+// and the inverse transform reads buf[rank] for rank < count (zeros above),
+// so no tile has to be cleared between blocks.
+#include "common.cuh"
+#include "internal.h"
+#include "mma_dct.cuh"
+
+namespace abcs_b200 {
+
+constexpr int kM16Threads = 256;
+constexpr int kM16Warps = kM16Threads / 32;
+
+struct Grid16 {
+  int rows, cols;
+  uint32_t nb;                // rows * cols
+  uint32_t pairs_per_row;     // ceil(cols / 2)
+  uint32_t units_per_img;     // rows * pairs_per_row
+  uint32_t total_units;
+  uint32_t runs_per_row;      // ceil(cols / 32): a run = up to 32 consecutive blocks of a block-row
+  uint32_t total_runs;
+  FastDiv div_units, div_pairs, div_nb, div_cols, div_runs_img, div_runs_row;
+};
+
+static Grid16 make_grid16(int rows, int cols, int n) {
+  Grid16 g;
+  g.rows = rows;
+  g.cols = cols;
+  g.nb = (uint32_t)rows * cols;
+  g.pairs_per_row = (uint32_t)(cols + 1) / 2;
+  g.units_per_img = (uint32_t)rows * g.pairs_per_row;
+  g.total_units = g.units_per_img * (uint32_t)n;
+  g.runs_per_row = (uint32_t)(cols + 31) / 32;
+  g.total_runs = g.runs_per_row * (uint32_t)rows * (uint32_t)n;
+  g.div_runs_img = FastDiv(g.runs_per_row * (uint32_t)rows);
+  g.div_runs_row = FastDiv(g.runs_per_row);
+  g.div_units = FastDiv(g.units_per_img);
+  g.div_pairs = FastDiv(g.pairs_per_row);
+  g.div_nb = FastDiv(g.nb);
+  g.div_cols = FastDiv((uint32_t)cols);
+  return g;
+}
+
+__device__ __forceinline__ void unit_pos(const Grid16& G, uint32_t u, uint32_t& img, int& br, int& bc0) {
+  img = G.div_units.div(u);
+  const uint32_t rem = u - img * G.units_per_img;
+  const uint32_t r = G.div_pairs.div(rem);
+  br = (int)r;
+  bc0 = 2 * (int)(rem - r * G.pairs_per_row);
+}
+
+__device__ __forceinline__ uint4 load_row16(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch,
+                                            const Grid16& G, uint32_t img, int br, int bc0, bool aligned) {
+  const int lane = threadIdx.x & 31, b = lane >> 4, r = lane & 15;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (bc0 + b < G.cols) {
+    const uint8_t* p = imgs + (int64_t)img * img_stride + (int64_t)(br * 16 + r) * pitch + (bc0 + b) * 16;
+    if (aligned) {
+      v = __ldg(reinterpret_cast<const uint4*>(p));
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = (uint32_t)p[4 * q] | ((uint32_t)p[4 * q + 1] << 8) | ((uint32_t)p[4 * q + 2] << 16) |
+               ((uint32_t)p[4 * q + 3] << 24);
+      v = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  return v;
+}
+
+// exact-fp16 B fragments of block b of the staged pair
+__device__ __forceinline__ void staged_bfrag(const uint8_t* st, int b, uint32_t (&bx)[2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const uint8_t* base = st + b * 256;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = 8 * j + g;
+    bx[j][0] = u8pair_to_h2(base[(2 * t) * 16 + c], base[(2 * t + 1) * 16 + c]);
+    bx[j][1] = u8pair_to_h2(base[(2 * t + 8) * 16 + c], base[(2 * t + 9) * 16 + c]);
+  }
+}
+
+// fp64 |c| for the DD guard band, reference operation order (dct.cpp:30-49)
+[[maybe_unused]] __device__ __forceinline__ double exact_coef16(const uint8_t* __restrict__ blk, int pitch, int flat) {
+  const double* C = basis_dev<16>();
+  const int u = flat >> 4, v = flat & 15;
+  double y = 0.0;
+  for (int c = 0; c < 16; ++c) {
+    double t = 0.0;
+    for (int r = 0; r < 16; ++r) t = __dadd_rn(t, __dmul_rn(C[u * 16 + r], (double)blk[(size_t)r * pitch + c]));
+    y = __dadd_rn(y, __dmul_rn(t, C[v * 16 + c]));
+  }
+  return y;
+}
+
+__device__ __forceinline__ void store_dfrag(float* __restrict__ blk_out, int pitch, const Acc16& X) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  float* p0 = blk_out + g * pitch + 2 * t;
+  float* p1 = p0 + 8 * pitch;
+  *reinterpret_cast<float2*>(p0) = make_float2(X.v[0][0], X.v[0][1]);
+  *reinterpret_cast<float2*>(p1) = make_float2(X.v[0][2], X.v[0][3]);
+  *reinterpret_cast<float2*>(p0 + 8) = make_float2(X.v[1][0], X.v[1][1]);
+  *reinterpret_cast<float2*>(p1 + 8) = make_float2(X.v[1][2], X.v[1][3]);
+}
+
+struct Sense16Args {
+  const uint8_t* imgs;
+  int64_t img_stride;
+  int pitch;
+  bool aligned;
+  // weights (DD phase 1)
+  int phase1;
+  double T;
+  float Tf, band;
+  uint32_t* weights;
+  uint32_t* fix_list;   // blocks needing the fp64 recount (capacity: all blocks)
+  uint32_t* fix_count;
+  // payload
+  const uint16_t* counts;
+  const int32_t* offsets;
+  float* payload;
+  int64_t payload_stride;
+  // decode
+  float* out;
+  int64_t out_stride;
+  int out_pitch;
+};
+
+__device__ __forceinline__ void run_pos(const Grid16& G, uint32_t r, uint32_t& img, int& br, int& bc_first,
+                                        int& nblk) {
+  img = G.div_runs_img.div(r);
+  const uint32_t rem = r - img * (G.runs_per_row * (uint32_t)G.rows);
+  const uint32_t row = G.div_runs_row.div(rem);
+  br = (int)row;
+  bc_first = 32 * (int)(rem - row * G.runs_per_row);
+  nblk = min(32, G.cols - bc_first);
+}
+
+template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false>
+__global__ void __launch_bounds__(kM16Threads, 3)
+sense16_kernel(Grid16 G, Sense16Args A) {
+  __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
+  __shared__ float s_buf[kM16Warps][2][256];
+  Frag16 f;
+  load_frag16(f);
+  uint32_t rank_d[8], rank_b[8];
+  unsigned in_p1 = 0;  // D slots inside the phase-1 zigzag prefix
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    rank_d[s] = zigzag_rank_dev<16>()[dslot_row(s) * 16 + dslot_col(s)];
+    rank_b[s] = zigzag_rank_dev<16>()[bslot_row(s) * 16 + bslot_col(s)];
+    if ((int)rank_d[s] < A.phase1) in_p1 |= 1u << s;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* st = s_stage[warp];
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < G.total_runs; r += nwarps) {
+    uint32_t img;
+    int br, bcf, nblk;
+    run_pos(G, r, img, br, bcf, nblk);
+    const uint32_t bidx_first = img * G.nb + (uint32_t)(br * G.cols + bcf);
+    // lane i <-> block bcf + i of the run: counts/offsets in one coalesced load each
+    int my_cnt = 0;
+    int32_t my_off = 0;
+    if constexpr (kPayload || kDecode) {
+      if (lane < nblk) {
+        my_cnt = A.counts[bidx_first + lane];
+        if constexpr (kPayload) my_off = A.offsets[bidx_first + lane];
+      }
+    }
+    uint4 nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bcf, A.aligned);
+    for (int p = 0; 2 * p < nblk; ++p) {
+      const int bc0 = bcf + 2 * p;
+      const bool two = 2 * p + 1 < nblk;
+      __syncwarp();
+      reinterpret_cast<uint4*>(st)[lane] = nxt;
+      __syncwarp();
+      if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
+      uint32_t bx[2][2][2];
+      staged_bfrag(st, 0, bx[0]);
+      staged_bfrag(st, 1, bx[1]);
+      Acc16 Y[2];
+      if constexpr (kLowCols) dct16_fwd_exact_x2_lo(f, bx, Y);
+      else dct16_fwd_exact_x2(f, bx, Y);
+      const uint32_t bidx0 = bidx_first + 2 * p;
+      if constexpr (kWeights) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !two) break;
+          int sig = 0;
+          bool near_any = false;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const float d = fabsf(Y[q].v[s >> 2][s & 3]) - A.Tf;
+            const bool in = (in_p1 >> s) & 1u;
+            const bool near = fabsf(d) < A.band;
+            sig += (in && !near && d > 0.f) ? 1 : 0;
+            near_any |= in && near;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+          const bool fix = __any_sync(0xffffffffu, near_any);
+          if (lane == 0) {
+            A.weights[bidx0 + q] = (uint32_t)sig;
+            // some |c| lies within the fp32 error band of T: dd_fixup16_kernel recounts this
+            // block in fp64 exactly as the reference does (sensing.cpp:354)
+            if (fix) A.fix_list[atomicAdd(A.fix_count, 1u)] = bidx0 + q;
+          }
+        }
+      }
+      if constexpr (kPayload || kDecode) {
+        int cnt[2];
+        cnt[0] = __shfl_sync(0xffffffffu, my_cnt, 2 * p);
+        cnt[1] = two ? __shfl_sync(0xffffffffu, my_cnt, (2 * p + 1) & 31) : 0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            if ((int)rank_d[s] < cnt[q]) s_buf[warp][q][rank_d[s]] = Y[q].v[s >> 2][s & 3];
+        __syncwarp();
+        if constexpr (kPayload) {
+          const int32_t o0 = __shfl_sync(0xffffffffu, my_off, 2 * p);
+          const int32_t o1 = __shfl_sync(0xffffffffu, my_off, (2 * p + 1) & 31);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            float* dst = A.payload + (int64_t)img * A.payload_stride + (q ? o1 : o0);
+            for (int k = lane; k < cnt[q]; k += 32) dst[k] = s_buf[warp][q][k];
+          }
+        }
+        if constexpr (kDecode) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (q == 1 && !two) break;
+            float yv[2][4];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              yv[s >> 2][s & 3] = (int)rank_b[s] < cnt[q] ? s_buf[warp][q][rank_b[s]] : 0.f;
+            const Acc16 X = dct16_inv_f32(f, yv);
+            store_dfrag(A.out + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
+                        A.out_pitch, X);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+constexpr float kMmaSafeMax = 8192.f;  // |coef| bound keeping the fp16 split in range
+
+// decode_idct from a packed payload. A warp walks a run of up to 32 consecutive
+// blocks of a block-row: counts/offsets arrive in one coalesced load (lane i <->
+// block i) and each block's prefix (8 values per lane at most) is prefetched
+// one block ahead while the current block is transformed.
+__global__ void __launch_bounds__(kM16Threads, 3)
+decode16_kernel(Grid16 G, uint32_t total_blocks, const uint16_t* __restrict__ counts,
+                const int32_t* __restrict__ offsets, const float* __restrict__ payload, int64_t payload_stride,
+                float* __restrict__ out, int64_t out_stride, int out_pitch) {
+  __shared__ float s_buf[kM16Warps][256];
+  Frag16 f;
+  load_frag16(f);
+  uint32_t rank_b[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) rank_b[s] = zigzag_rank_dev<16>()[bslot_row(s) * 16 + bslot_col(s)];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* zb = s_buf[warp];
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < G.total_runs; r += nwarps) {
+    uint32_t img;
+    int br, bcf, nblk;
+    run_pos(G, r, img, br, bcf, nblk);
+    const uint32_t bidx_first = img * G.nb + (uint32_t)(br * G.cols + bcf);
+    const int my_cnt = lane < nblk ? counts[bidx_first + lane] : 0;
+    const int32_t my_off = lane < nblk ? offsets[bidx_first + lane] : 0;
+    const float* base = payload + (int64_t)img * payload_stride;
+    float* obase = out + (int64_t)img * out_stride + (int64_t)(br * 16) * out_pitch;
+    int c0 = __shfl_sync(0xffffffffu, my_cnt, 0);
+    const float* s0 = base + __shfl_sync(0xffffffffu, my_off, 0);
+    float pv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pv[q] = lane + 32 * q < c0 ? __ldg(s0 + lane + 32 * q) : 0.f;
+    for (int i = 0; i < nblk; ++i) {
+      // prefetch block i+1
+      float pn[8];
+      const int c1 = __shfl_sync(0xffffffffu, my_cnt, (i + 1) & 31);
+      const float* s1 = base + __shfl_sync(0xffffffffu, my_off, (i + 1) & 31);
+      const bool more = i + 1 < nblk;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pn[q] = (more && lane + 32 * q < c1) ? __ldg(s1 + lane + 32 * q) : 0.f;
+      bool big = false;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (lane + 32 * q < c0) zb[lane + 32 * q] = pv[q];
+        big |= !(fabsf(pv[q]) <= kMmaSafeMax);
+      }
+      __syncwarp();
+      float yv[2][4];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) yv[s >> 2][s & 3] = (int)rank_b[s] < c0 ? zb[rank_b[s]] : 0.f;
+      __syncwarp();
+      float scale = 1.f;
+      if (__any_sync(0xffffffffu, big)) {
+        // rare: rescale by a power of two so the fp16 split stays in range (exact)
+        float mx = 0.f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) mx = fmaxf(mx, fabsf(yv[s >> 2][s & 3]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (isfinite(mx) && mx > kMmaSafeMax) {
+          int e;
+          frexpf(mx / kMmaSafeMax, &e);
+          scale = ldexpf(1.f, e);
+#pragma unroll
+          for (int s = 0; s < 8; ++s) yv[s >> 2][s & 3] = ldexpf(yv[s >> 2][s & 3], -e);
+        }
+      }
+      Acc16 X = dct16_inv_f32(f, yv);
+      if (scale != 1.f) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) X.v[j][k] *= scale;
+      }
+      store_dfrag(obase + (bcf + i) * 16, out_pitch, X);
+      c0 = c1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pv[q] = pn[q];
+    }
+  }
+}
+
+// DD phase-1 recount in fp64 for the (rare) blocks whose fp32/MMA coefficients
+// came within the error band of T: warp per listed block; tmp[u][c] for the
+// rows the prefix needs, then each prefix coefficient, all in the reference's
+// exact operation order (dct.cpp:30-49), |c| > T strict (sensing.cpp:354).
+__global__ void __launch_bounds__(256)
+dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch, Grid16 G, int phase1, double T,
+                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint32_t* __restrict__ weights) {
+  __shared__ double s_tmp[8][16 * 16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* C = basis_dev<16>();
+  const unsigned short* zz = zigzag_dev<16>();
+  int umax = 0;
+  for (int k = 0; k < phase1; ++k) umax = max(umax, (int)(zz[k] >> 4));
+  const uint32_t n = *count;
+  for (uint32_t e = blockIdx.x * 8 + warp; e < n; e += gridDim.x * 8) {
+    const uint32_t bidx = list[e];
+    const uint32_t img = G.div_nb.div(bidx);
+    const uint32_t bi = bidx - img * G.nb;
+    const uint32_t br = G.div_cols.div(bi), bc = bi - br * (uint32_t)G.cols;
+    const uint8_t* blk = imgs + (int64_t)img * img_stride + (int64_t)(br * 16) * pitch + bc * 16;
+    double* tmp = s_tmp[warp];
+    for (int i = lane; i < (umax + 1) * 16; i += 32) {
+      const int u = i >> 4, c = i & 15;
+      double t = 0.0;
+      for (int r = 0; r < 16; ++r) t = __dadd_rn(t, __dmul_rn(C[u * 16 + r], (double)blk[(size_t)r * pitch + c]));
+      tmp[u * 16 + c] = t;
+    }
+    __syncwarp();
+    int sig = 0;
+    for (int k = lane; k < phase1; k += 32) {
+      const int u = zz[k] >> 4, v = zz[k] & 15;
+      double y = 0.0;
+      for (int c = 0; c < 16; ++c) y = __dadd_rn(y, __dmul_rn(tmp[u * 16 + c], C[v * 16 + c]));
+      sig += fabs(y) > T ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+    if (lane == 0) weights[bidx] = (uint32_t)sig;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+static unsigned grid_for(Ctx* ctx, uint32_t warps_needed) {
+  const uint32_t ctas = (warps_needed + kM16Warps - 1) / kM16Warps;
+  const uint32_t cap = (uint32_t)ctx->sm_count * 6;
+  return ctas < cap ? (ctas ? ctas : 1) : cap;
+}
+
+bool mma16_supported(int rows, int cols, int n) {
+  const uint64_t blocks = (uint64_t)rows * cols * (uint64_t)n;
+  return blocks < (1ull << 31);
+}
+
+int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
+                   int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
+                   float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
+                   cudaStream_t s, uint32_t* fix_scratch) {
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_units == 0) return ABCS_OK;
+  Sense16Args A{};
+  A.imgs = imgs;
+  A.img_stride = img_stride;
+  A.pitch = pitch;
+  A.aligned = ((uintptr_t)imgs % 16 == 0) && (img_stride % 16 == 0) && (pitch % 16 == 0);
+  A.phase1 = phase1;
+  A.T = T;
+  A.Tf = (float)T;
+  A.band = (float)(2e-2 + fabs(T - (double)A.Tf));  // error bound of the fp32/MMA transform + rounding of T
+  A.weights = weights;
+  if (mode == 1) {
+    if (!fix_scratch) return set_error(ABCS_ERR_LOGIC, "sense16: missing fixup scratch");
+    A.fix_count = fix_scratch;
+    A.fix_list = fix_scratch + 1;
+    cudaError_t e = cudaMemsetAsync(A.fix_count, 0, 4, s);
+    if (e != cudaSuccess) return cuda_status(e, "fixup reset");
+  }
+  A.counts = counts;
+  A.offsets = offsets;
+  A.payload = payload;
+  A.payload_stride = payload_stride;
+  A.out = out;
+  A.out_stride = out_stride;
+  A.out_pitch = out_pitch;
+  const unsigned grid = grid_for(ctx, G.total_runs);
+  switch (mode) {
+    case 1:
+      if (phase1 <= 36)  // zigzag prefix of <= 36 entries lives in columns 0..7
+        sense16_kernel<true, false, false, true><<<grid, kM16Threads, 0, s>>>(G, A);
+      else
+        sense16_kernel<true, false, false><<<grid, kM16Threads, 0, s>>>(G, A);
+      ctx->launches++;
+      dd_fixup16_kernel<<<(unsigned)ctx->sm_count * 2, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1, T, A.fix_list,
+                                                                   A.fix_count, weights);
+      break;
+    case 2: sense16_kernel<false, true, false><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    case 3: sense16_kernel<false, true, true><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    default: return set_error(ABCS_ERR_LOGIC, "bad sense16 mode");
+  }
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "sense16 launch");
+}
+
+int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts, const int32_t* offsets,
+                    const float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
+                    cudaStream_t s) {
+  const Grid16 G = make_grid16(rows, cols, n);
+  const uint32_t total = G.nb * (uint32_t)n;
+  if (total == 0) return ABCS_OK;
+  decode16_kernel<<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, total, counts, offsets, payload,
+                                                                      payload_stride, out, out_stride, out_pitch);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "decode16 launch");
+}
+
+}  // namespace abcs_b200

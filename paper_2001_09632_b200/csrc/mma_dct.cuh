@@ -1,0 +1,216 @@
+// Tensor-core 16x16 block DCTs (warp per block) with an fp16 hi/lo split that
+// keeps fp32-level accuracy.
+//
+// Y = C X C^T (forward) and X = C^T Y C (inverse) are two 16x16x16 products
+// each. With mma.sync.m16n8k16 (fp16 in, fp32 accumulate) the accumulator of
+// stage 1 is, register for register, the A fragment of stage 2, so no
+// transpose or shared-memory round trip sits between the stages. fp32 operands
+// are split v = hi + lo (two fp16, 22 significant bits) and products are
+// accumulated as lo-terms first, then hi*hi; u8 pixels are exact in fp16 and
+// need no split. Accuracy ~1e-4 absolute on 8-bit blocks (DESIGN.md
+// "Precision"), the same order as the fp32 CUDA-core transform.
+//
+// Fragment layout (PTX ISA, m16n8k16, lane = 4g + t):
+//   A (16x16 row-major): a0={A[g][2t],A[g][2t+1]} a1={A[g+8][2t],..} a2={A[g][2t+8],..} a3={A[g+8][2t+8],..}
+//   B (16x8):            b0={B[2t][g],B[2t+1][g]} b1={B[2t+8][g],B[2t+9][g]}
+//   D (16x8 fp32):       d0=D[g][2t] d1=D[g][2t+1] d2=D[g+8][2t] d3=D[g+8][2t+1]
+// For a 16x16 operand split in two n-tiles j (columns 8j..8j+7).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace abcs_b200 {
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// {a, b} -> hi = fp16(a,b), lo = fp16(a - hi, b - hi)
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  hi = h2u(h);
+  lo = h2u(__floats2half2_rn(a - hf.x, b - hf.y));
+}
+
+// two u8 values (zero-extended) -> exact fp16 pair {lo, hi}
+__device__ __forceinline__ uint32_t u8pair_to_h2(uint32_t lo, uint32_t hi) {
+  const uint32_t v = __byte_perm(lo, hi, 0x5410) | 0x64006400u;  // 1024 + value
+  __half2 h = *reinterpret_cast<const __half2*>(&v);
+  h = __hsub2(h, __floats2half2_rn(1024.f, 1024.f));
+  return h2u(h);
+}
+
+// Per-lane fragments of the B=16 reference basis (dct.cpp:9-21), hi/lo split.
+//   c*: C as the A operand (forward stage 1) == C^T as the B operand (forward stage 2)
+//   t*: C^T as the A operand (inverse stage 1) == C as the B operand (inverse stage 2)
+struct Frag16 {
+  uint32_t ch[4], cl[4], th[4], tl[4];
+  // the same values regrouped as stage-2 B operands (adjacent registers per n-tile):
+  // cb*[j] = {c*[j], c*[j+2]} (C^T as B), tb*[j] = {t*[j], t*[j+2]} (C as B)
+  uint32_t cbh[2][2], cbl[2][2], tbh[2][2], tbl[2][2];
+};
+
+__device__ __forceinline__ void load_frag16(Frag16& f) {
+  const double* Cd = basis_dev<16>();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  auto C = [&](int r, int c) { return (float)Cd[r * 16 + c]; };
+  const int rows[4] = {g, g + 8, g, g + 8};
+  const int cols[4] = {2 * t, 2 * t, 2 * t + 8, 2 * t + 8};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    split2(C(rows[i], cols[i]), C(rows[i], cols[i] + 1), f.ch[i], f.cl[i]);       // C[r][c], C[r][c+1]
+    split2(C(cols[i], rows[i]), C(cols[i] + 1, rows[i]), f.th[i], f.tl[i]);       // C^T[r][c] = C[c][r]
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    f.cbh[j][0] = f.ch[j];
+    f.cbh[j][1] = f.ch[j + 2];
+    f.cbl[j][0] = f.cl[j];
+    f.cbl[j][1] = f.cl[j + 2];
+    f.tbh[j][0] = f.th[j];
+    f.tbh[j][1] = f.th[j + 2];
+    f.tbl[j][0] = f.tl[j];
+    f.tbl[j][1] = f.tl[j + 2];
+  }
+}
+
+// D fragments of a 16x16 result: v[j][0..3] for n-tile j.
+struct Acc16 {
+  float v[2][4];
+};
+
+// Stage-2 helper: A = S (from accumulator frags, split hi/lo), B = M given per n-tile
+// as adjacent register pairs bh[j], bl[j]. Returns S * M.
+__device__ __forceinline__ Acc16 stage2(const Acc16& S, const uint32_t (&bh)[2][2], const uint32_t (&bl)[2][2]) {
+  uint32_t ah[4], al[4];
+  split2(S.v[0][0], S.v[0][1], ah[0], al[0]);
+  split2(S.v[0][2], S.v[0][3], ah[1], al[1]);
+  split2(S.v[1][0], S.v[1][1], ah[2], al[2]);
+  split2(S.v[1][2], S.v[1][3], ah[3], al[3]);
+  Acc16 R;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    R.v[j][0] = R.v[j][1] = R.v[j][2] = R.v[j][3] = 0.f;
+    mma16816(R.v[j], al, bh[j][0], bh[j][1]);
+    mma16816(R.v[j], ah, bl[j][0], bl[j][1]);
+    mma16816(R.v[j], ah, bh[j][0], bh[j][1]);
+  }
+  return R;
+}
+
+// Forward DCT of an exact-fp16 block given as B fragments bx[j][0..1] (n-tile j):
+//   T = C X (stage 1), Y = T C^T (stage 2). Returns Y in D-fragment layout.
+__device__ __forceinline__ Acc16 dct16_fwd_exact(const Frag16& f, const uint32_t (&bx)[2][2]) {
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.cl, bx[j][0], bx[j][1]);
+    mma16816(T.v[j], f.ch, bx[j][0], bx[j][1]);
+  }
+  return stage2(T, f.cbh, f.cbl);
+}
+
+// Two exact-fp16 blocks at once (independent MMA chains interleave).
+__device__ __forceinline__ void dct16_fwd_exact_x2(const Frag16& f, const uint32_t (&bx)[2][2][2], Acc16 (&Y)[2]) {
+  Acc16 T[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) T[q].v[j][0] = T[q].v[j][1] = T[q].v[j][2] = T[q].v[j][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.cl, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.ch, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) Y[q] = stage2(T[q], f.cbh, f.cbl);
+}
+
+// Same, computing only output columns 0..7 (n-tile 0) of stage 2: enough when every
+// wanted coefficient has v <= 7 (DD phase 1 with a zigzag prefix of <= 36 entries).
+__device__ __forceinline__ void dct16_fwd_exact_x2_lo(const Frag16& f, const uint32_t (&bx)[2][2][2], Acc16 (&Y)[2]) {
+  Acc16 T[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) T[q].v[j][0] = T[q].v[j][1] = T[q].v[j][2] = T[q].v[j][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.cl, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.ch, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    uint32_t ah[4], al[4];
+    split2(T[q].v[0][0], T[q].v[0][1], ah[0], al[0]);
+    split2(T[q].v[0][2], T[q].v[0][3], ah[1], al[1]);
+    split2(T[q].v[1][0], T[q].v[1][1], ah[2], al[2]);
+    split2(T[q].v[1][2], T[q].v[1][3], ah[3], al[3]);
+    Y[q].v[0][0] = Y[q].v[0][1] = Y[q].v[0][2] = Y[q].v[0][3] = 0.f;
+    Y[q].v[1][0] = Y[q].v[1][1] = Y[q].v[1][2] = Y[q].v[1][3] = 0.f;
+    mma16816(Y[q].v[0], al, f.cbh[0][0], f.cbh[0][1]);
+    mma16816(Y[q].v[0], ah, f.cbl[0][0], f.cbl[0][1]);
+    mma16816(Y[q].v[0], ah, f.cbh[0][0], f.cbh[0][1]);
+  }
+}
+
+// Forward DCT of an fp32 block given as B-fragment values xv[j][0..3] =
+// {X[2t][8j+g], X[2t+1][8j+g], X[2t+8][8j+g], X[2t+9][8j+g]}.
+__device__ __forceinline__ Acc16 dct16_fwd_f32(const Frag16& f, const float (&xv)[2][4]) {
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    uint32_t h0, l0, h1, l1;
+    split2(xv[j][0], xv[j][1], h0, l0);
+    split2(xv[j][2], xv[j][3], h1, l1);
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.ch, l0, l1);
+    mma16816(T.v[j], f.cl, h0, h1);
+    mma16816(T.v[j], f.ch, h0, h1);
+  }
+  return stage2(T, f.cbh, f.cbl);
+}
+
+// Inverse DCT of an fp32 coefficient block given as B-fragment values yv[j][0..3]
+// (same positions as dct16_fwd_f32). Returns X in D-fragment layout.
+__device__ __forceinline__ Acc16 dct16_inv_f32(const Frag16& f, const float (&yv)[2][4]) {
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    uint32_t h0, l0, h1, l1;
+    split2(yv[j][0], yv[j][1], h0, l0);
+    split2(yv[j][2], yv[j][3], h1, l1);
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.th, l0, l1);
+    mma16816(T.v[j], f.tl, h0, h1);
+    mma16816(T.v[j], f.th, h0, h1);
+  }
+  return stage2(T, f.tbh, f.tbl);
+}
+
+// Positions of the D-fragment slots: slot s = 4j + i -> (row, col)
+__device__ __forceinline__ int dslot_row(int s) { return ((threadIdx.x & 31) >> 2) + ((s & 3) >= 2 ? 8 : 0); }
+__device__ __forceinline__ int dslot_col(int s) { return 8 * (s >> 2) + 2 * (threadIdx.x & 3) + (s & 1); }
+// Positions of the B-fragment value slots xv[j][i]: (row, col)
+__device__ __forceinline__ int bslot_row(int s) {
+  return 2 * (threadIdx.x & 3) + (s & 1) + ((s & 3) >= 2 ? 8 : 0);
+}
+__device__ __forceinline__ int bslot_col(int s) { return 8 * (s >> 2) + ((threadIdx.x & 31) >> 2); }
+
+}  // namespace abcs_b200

@@ -39,7 +39,7 @@ __device__ __forceinline__ void block_dct(const InT* __restrict__ row_src, bool 
 // (dct.cpp:30-49: tmp[u][c] accumulated over r ascending from 0.0, then
 // Y[u][v] accumulated over c ascending), no FMA contraction, reference basis.
 template <int B>
-__device__ __noinline__ double exact_coef(const uint8_t* __restrict__ blk, int pitch, int flat) {
+__device__ __forceinline__ double exact_coef(const uint8_t* __restrict__ blk, int pitch, int flat) {
   const double* C = basis_dev<B>();
   const int u = flat / B, v = flat % B;
   double y = 0.0;
@@ -189,7 +189,8 @@ static bool aligned_rows(const void* base, int64_t img_stride_bytes, int64_t pit
 }
 
 int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs, int64_t img_stride,
-                         int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s) {
+                         int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s,
+                         uint32_t* fix_scratch) {
   const int64_t total = (int64_t)n * p.n_blocks;
   if (total == 0) return ABCS_OK;
   if (p.algorithm_used == ABCS_ALGO_BBV) {
@@ -198,6 +199,10 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
     bbv_weights_kernel<<<(unsigned)grid, threads, 0, s>>>(imgs, img_stride, pitch, p.rows, p.cols, n, p.block,
                                                           (int)p.bbv_stride, p.bbv_offset, p.bbv_per_side,
                                                           p.bbv_valid_probes, weights, side, p.side_per_image);
+  } else if (p.algorithm_used == ABCS_ALGO_DD && p.block == 16 && mma16_supported(p.rows, p.cols, n) &&
+             fix_scratch) {
+    return launch_sense16(ctx, 1, p.rows, p.cols, n, imgs, img_stride, pitch, p.dd_phase1, p.threshold, weights,
+                          nullptr, nullptr, nullptr, 0, nullptr, 0, 0, s, fix_scratch);
   } else if (p.algorithm_used == ABCS_ALGO_DD) {
     const bool al = aligned_rows(imgs, img_stride, pitch, p.block);
     const int B = p.block;
@@ -239,7 +244,10 @@ int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint8_t
   if (total == 0) return ABCS_OK;
   const int64_t gpc = kGatherThreads / B;
   const unsigned grid = (unsigned)((total + gpc - 1) / gpc);
-  if (imgs) {
+  if (imgs && B == 16 && mma16_supported(rows, cols, n)) {
+    return launch_sense16(ctx, 2, rows, cols, n, imgs, img_stride, pitch, 0, 0.0, nullptr, counts, offsets, payload,
+                          payload_stride, nullptr, 0, 0, s);
+  } else if (imgs) {
     const bool al = aligned_rows(imgs, img_stride, pitch, B);
     if (B == 8)
       gather_kernel<8, uint8_t><<<grid, kGatherThreads, 0, s>>>(imgs, img_stride, pitch, rows, cols, n, al, counts,

@@ -239,6 +239,19 @@ def test_sense_decode_pixels(p, torch, checker, case):
         assert_psnr_close(psnr(crop, out[i]), psnr(crop, ref))
 
 
+@pytest.mark.parametrize("case", [c for c in SENSE_CFGS if c[2] in (8, 16, 32)][:9])
+def test_fused_sense_decode_equals_decode_of_payload(p, torch, case):
+    """abcs_sense_decode_batch: the decoded images equal decode_idct(payload) bit for bit."""
+    H, W, B, num, den, algo, n = case
+    imgs = torch.from_numpy(synth(H, W, n=n, seed=H + 3 * W + algo, video=(B == 8))).cuda()
+    cfg = p.SensingConfig(B, num, den, p.Algorithm(algo))
+    b, x = p.sense_decode_batch(imgs, cfg)
+    ref = p.sense_batch(imgs, cfg)
+    assert torch.equal(b.counts.view(torch.int16), ref.counts.view(torch.int16))
+    assert torch.equal(b.payload, ref.payload)
+    assert torch.equal(x, p.decode_batch(ref))
+
+
 def test_decode_format_errors(p):
     ms = p.MeasurementSet(32, 32, 16, p.Algorithm.ZZ, 1, 4, 0.0, np.array([3, 3, 3, 3], np.uint16),
                           np.zeros(11, np.float32))

@@ -14,6 +14,10 @@ if which in ("all", "cfg2"):
         for num, den in ((1, 10), (3, 10), (1, 2)):
             b = p.sense_batch(imgs, p.SensingConfig(16, num, den, p.Algorithm.DD))
             p.decode_batch(b)
+if which in ("all", "fused"):
+    for rep in range(2):
+        for num, den in ((1, 10), (3, 10), (1, 2)):
+            p.sense_decode_batch(imgs, p.SensingConfig(16, num, den, p.Algorithm.DD))
 if which in ("all", "ida"):
     b = p.sense_batch(imgs[:64], p.SensingConfig(16, 3, 10, p.Algorithm.BBV))
     for rep in range(2):
