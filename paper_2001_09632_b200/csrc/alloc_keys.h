@@ -46,6 +46,14 @@ typedef struct {
 
 // floor(R * 2^64 / T) and whether the division leaves a remainder; requires R < T.
 AK_HD uint64_t ak_frac64(uint64_t R, uint64_t T, int* sticky) {
+  if (T < (1ull << 32)) {  // two 32-bit digits with 64-bit divisions (R < T < 2^32)
+    const uint64_t n1 = R << 32;
+    const uint64_t q1 = n1 / T;
+    const uint64_t n2 = (n1 - q1 * T) << 32;
+    const uint64_t q2 = n2 / T;
+    *sticky = (n2 - q2 * T) != 0;
+    return (q1 << 32) | q2;
+  }
   const ak_u128 num = (ak_u128)R << 64;
   const ak_u128 q = num / T;
   const ak_u128 rem = num - q * T;
@@ -57,8 +65,17 @@ AK_HD uint64_t ak_frac64(uint64_t R, uint64_t T, int* sticky) {
 // fractional part. P = remaining * w (exact), T = total weight > 0.
 AK_HD ak_share ak_compute(ak_u128 P, uint64_t T) {
   ak_share s;
-  const ak_u128 I128 = P / T;
-  const uint64_t R = (uint64_t)(P - I128 * T);
+  ak_u128 I128;
+  uint64_t R;
+  if ((uint64_t)(P >> 64) == 0) {  // common case: 64-bit division
+    const uint64_t p = (uint64_t)P;
+    const uint64_t q = p / T;
+    I128 = q;
+    R = p - q * T;
+  } else {
+    I128 = P / T;
+    R = (uint64_t)(P - I128 * T);
+  }
   s.flag = 0;
   if (R == 0) {  // exact
     s.whole = (uint64_t)I128;

@@ -88,6 +88,9 @@ int abcs_ctx_destroy(abcs_ctx* c) {
   cudaDeviceSynchronize();
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (auto& e : ctx->ev_join)
+    if (e) cudaEventDestroy(e);
   for (auto& st : ctx->pipe)
     if (st) cudaStreamDestroy(st);
   delete ctx;
@@ -151,14 +154,29 @@ static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_image
   void* ascr = scr + off_bytes + w_bytes;
   uint32_t* fix = reinterpret_cast<uint32_t*>(scr + off_bytes + w_bytes + align_up(allocate_scratch_bytes(p->n_blocks, n), 256));
   int st;
+  // largest possible phase-1 weight: DD counts <= phase1; BBV sums <= 4 * valid probes * 255
+  const int32_t wmax = p->algorithm_used == ABCS_ALGO_DD ? p->dd_phase1 : 4 * p->bbv_valid_probes * 255;
   if (p->algorithm_used == ABCS_ALGO_ZZ) {
     st = launch_zz_counts(ctx, *p, n, d_counts, offsets, s);
+    if (st) return st;
+  } else if (p->algorithm_used == ABCS_ALGO_DD && p->block == 16 &&
+             fused_alloc_supported(ctx, p->rows, p->cols, n, wmax)) {
+    // DD phase 1 + allocation in one launch: the last warp to finish an image allocates it
+    FusedAlloc fa;
+    fa.runs_done = nullptr;
+    fa.status = nullptr;
+    fa.counts = d_counts;
+    fa.offsets = offsets;
+    fa.budget = p->alloc_budget;
+    fa.cap = p->cap;
+    fa.base = p->count_base;
+    fa.wmax = wmax;
+    st = launch_sense16(ctx, 1, p->rows, p->cols, n, d_images, image_stride, pitch, p->dd_phase1, p->threshold,
+                        weights, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, s, fix, &fa);
     if (st) return st;
   } else {
     st = launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, weights, d_side, s, fix);
     if (st) return st;
-    // largest possible phase-1 weight: DD counts <= phase1; BBV sums <= 4 * valid probes * 255
-    const int32_t wmax = p->algorithm_used == ABCS_ALGO_DD ? p->dd_phase1 : 4 * p->bbv_valid_probes * 255;
     st = launch_allocate(ctx, weights, p->n_blocks, n, p->alloc_budget, nullptr, p->cap, p->count_base, d_counts,
                          offsets, nullptr, ascr, s, wmax);
     if (st) return st;
@@ -175,6 +193,51 @@ static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_image
                        out_stride, out_pitch, s);
 }
 
+// Batch pipelining across the ctx's streams: the batch is cut into chunks that run
+// on the three pipe streams (each with its own scratch), so one chunk's
+// latency-bound steps (fp64 fixup, per-image allocation, kernel tails) overlap
+// the other chunks' transform kernels. Joined back to the caller's stream.
+static int sense_chunked(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
+                         int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
+                         float* d_side, cudaStream_t s, float* d_out, int64_t out_stride, int32_t out_pitch) {
+  constexpr int kStreams = 3;
+  const int min_chunk = 64;
+  int nchunks = std::min<int>(kStreams, n / min_chunk);
+  if (nchunks < 2) {
+    int st;
+    char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
+    if (st) return st;
+    return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s, d_out,
+                      out_stride, out_pitch);
+  }
+  const int chunk = (n + nchunks - 1) / nchunks;
+  const size_t per = align_up(sense_scratch_bytes(p, chunk, d_offsets != nullptr), 256);
+  int st;
+  char* scr = static_cast<char*>(ctx_scratch(ctx, per * nchunks, s, &st));
+  if (st) return st;
+  if (!ctx->ev_fork) {
+    cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    for (auto& e : ctx->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  cudaError_t e = cudaEventRecord(ctx->ev_fork, s);
+  if (e != cudaSuccess) return cuda_status(e, "fork");
+  const int64_t NB = p->n_blocks, K = p->coeffs_per_image, S = p->side_per_image;
+  for (int k = 0; k < nchunks; ++k) {
+    const int first = k * chunk, cnt = std::min(chunk, n - first);
+    cudaStream_t cs = ctx->pipe[k];
+    cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
+    st = sense_impl(ctx, p, d_images + first * image_stride, image_stride, pitch, cnt, d_counts + first * NB,
+                    d_offsets ? d_offsets + first * NB : nullptr, d_payload + first * K,
+                    d_side ? d_side + first * S : nullptr, scr + per * k, cs,
+                    d_out ? d_out + first * out_stride : nullptr, out_stride, out_pitch);
+    if (st) return st;
+    e = cudaEventRecord(ctx->ev_join[k], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_join[k], 0);
+    if (e != cudaSuccess) return cuda_status(e, "join");
+  }
+  return ABCS_OK;
+}
+
 }  // namespace abcs_b200
 
 extern "C" {
@@ -188,9 +251,8 @@ int abcs_sense_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_ima
   Ctx* ctx = reinterpret_cast<Ctx*>(c);
   cudaSetDevice(ctx->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
-  if (st) return st;
-  return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s);
+  return sense_chunked(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, s, nullptr,
+                       0, 0);
 }
 
 int abcs_sense_decode_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
@@ -205,10 +267,8 @@ int abcs_sense_decode_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t
   Ctx* ctx = reinterpret_cast<Ctx*>(c);
   cudaSetDevice(ctx->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
-  if (st) return st;
-  return sense_impl(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, scr, s, d_out,
-                    out_stride, out_pitch);
+  return sense_chunked(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, s, d_out,
+                       out_stride, out_pitch);
 }
 
 int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
@@ -397,11 +457,12 @@ int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t*
                b_scr = align_up(sense_scratch_bytes(p, chunk, true), 256);
   const size_t per_slot = b_img + b_cnt + b_off + b_pay + b_side + b_out + b_scr;
   if (per_slot * kSlots > ctx->pipe_bytes) {
-    cudaDeviceSynchronize();
-    if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && ctx->pipe_buf) e = cudaFree(ctx->pipe_buf);
+    if (e != cudaSuccess) return cuda_status(e, "pipeline realloc");
     ctx->pipe_buf = nullptr;
     ctx->pipe_bytes = 0;
-    cudaError_t e = cudaMalloc(&ctx->pipe_buf, per_slot * kSlots);
+    e = cudaMalloc(&ctx->pipe_buf, per_slot * kSlots);
     if (e != cudaSuccess) return cuda_status(e, "pipeline alloc");
     ctx->pipe_bytes = per_slot * kSlots;
   }

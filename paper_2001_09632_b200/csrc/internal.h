@@ -25,6 +25,7 @@ struct Ctx {
   size_t scratch_bytes = 0;
   int64_t launches = 0;
   void* pipe_buf = nullptr;  // abcs_sense_decode_host slot buffers
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   size_t pipe_bytes = 0;
   // pinned staging for abcs_sense_decode_host is caller-provided; nothing here
 };
@@ -39,7 +40,7 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
                          int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s,
                          uint32_t* fix_scratch = nullptr);
 // u32 words of fixup scratch launch_sense_weights needs (count + one entry per block)
-inline size_t sense_fix_words(int64_t n_blocks_total) { return (size_t)n_blocks_total + 4; }
+inline size_t sense_fix_words(int64_t n_blocks_total) { return (size_t)n_blocks_total * 5 + 8; }
 int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors,
                     int64_t budget, const int32_t* caps, int32_t cap, int32_t base, uint16_t* counts,
                     int32_t* offsets, int32_t* status, void* scratch, cudaStream_t s, int32_t wmax = -1);
@@ -65,11 +66,21 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
 size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
                          const abcs_ida_config& cfg);
 bool mma16_supported(int rows, int cols, int n);
+// allocation fused into the B=16 DD weights pass (small images: n_blocks <= 4096, phase1 <= 127)
+struct FusedAlloc {
+  uint32_t* runs_done;  // n u32 scratch
+  int32_t* status;      // n u32 scratch
+  uint16_t* counts;
+  int32_t* offsets;
+  long long budget;
+  int cap, base, wmax;
+};
+bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax);
 // mode 1: DD weights; 2: payload; 3: payload + fused decode
 int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
                    int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
                    float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
-                   cudaStream_t s, uint32_t* fix_scratch = nullptr);
+                   cudaStream_t s, uint32_t* fix_scratch = nullptr, const FusedAlloc* fa = nullptr);
 int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts, const int32_t* offsets,
                     const float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
                     cudaStream_t s);

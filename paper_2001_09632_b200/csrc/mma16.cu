@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "mma_dct.cuh"
+#include "warp_alloc.cuh"
 
 namespace abcs_b200 {
 
@@ -128,8 +129,10 @@ struct Sense16Args {
   double T;
   float Tf, band;
   uint32_t* weights;
-  uint32_t* fix_list;   // blocks needing the fp64 recount (capacity: all blocks)
+  uint32_t* fix_list;   // (block, coefficient) pairs for the fp64 decision
   uint32_t* fix_count;
+  uint32_t fix_cap;
+  uint8_t* fix_flag;    // per block: had a near-threshold coefficient (overflow fallback)
   // payload
   const uint16_t* counts;
   const int32_t* offsets;
@@ -155,19 +158,21 @@ template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false>
 __global__ void __launch_bounds__(kM16Threads, 3)
 sense16_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
-  __shared__ float s_buf[kM16Warps][2][256];
+  constexpr int kWbuf = 256;
+  __shared__ float s_buf[kM16Warps][2][kWbuf];
   Frag16 f;
   load_frag16(f);
-  uint32_t rank_d[8], rank_b[8];
+  // The forward runs transposed (Y^T = C X^T C^T): D slot s holds Y[dslot_col(s)][dslot_row(s)].
+  uint32_t rank_d[8];
   unsigned in_p1 = 0;  // D slots inside the phase-1 zigzag prefix
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    rank_d[s] = zigzag_rank_dev<16>()[dslot_row(s) * 16 + dslot_col(s)];
-    rank_b[s] = zigzag_rank_dev<16>()[bslot_row(s) * 16 + bslot_col(s)];
+    rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
     if ((int)rank_d[s] < A.phase1) in_p1 |= 1u << s;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* st = s_stage[warp];
+  float* zb0 = &s_buf[warp][0][0];
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < G.total_runs; r += nwarps) {
     uint32_t img;
@@ -192,70 +197,77 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       __syncwarp();
       if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
       uint32_t bx[2][2][2];
-      staged_bfrag(st, 0, bx[0]);
-      staged_bfrag(st, 1, bx[1]);
-      Acc16 Y[2];
+      u8_bfragT(st, bx[0]);
+      u8_bfragT(st + 256, bx[1]);
+      Acc16 Y[2];  // Y^T of each block
       if constexpr (kLowCols) dct16_fwd_exact_x2_lo(f, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
       if constexpr (kWeights) {
+        // phase-1 test on the zigzag-ordered prefix: Y -> smem at rank, lane k tests coefficient k
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           if (q == 1 && !two) break;
           int sig = 0;
-          bool near_any = false;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const float d = fabsf(Y[q].v[s >> 2][s & 3]) - A.Tf;
-            const bool in = (in_p1 >> s) & 1u;
-            const bool near = fabsf(d) < A.band;
-            sig += (in && !near && d > 0.f) ? 1 : 0;
-            near_any |= in && near;
+#pragma unroll 1
+          for (int k0 = 0; k0 < A.phase1; k0 += 32) {
+            const int k = k0 + lane;
+            const bool in = k < A.phase1;
+            const float a = in ? fabsf(zb0[kWbuf * q + k]) : 0.f;
+            const bool clear_hi = in && a >= A.Tf + A.band;
+            const bool near = in && !clear_hi && a > A.Tf - A.band;
+            sig += __popc(__ballot_sync(0xffffffffu, clear_hi));
+            if (near) {  // rare: within the MMA error band of T; dd_fixup16_kernel decides in fp64
+              A.fix_flag[bidx0 + q] = 1;
+              const uint32_t e = atomicAdd(A.fix_count, 1u);
+              if (e < A.fix_cap) {
+                A.fix_list[2 * e] = bidx0 + q;
+                A.fix_list[2 * e + 1] = (uint32_t)zigzag_dev<16>()[k];
+              }
+            }
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
-          const bool fix = __any_sync(0xffffffffu, near_any);
-          if (lane == 0) {
-            A.weights[bidx0 + q] = (uint32_t)sig;
-            // some |c| lies within the fp32 error band of T: dd_fixup16_kernel recounts this
-            // block in fp64 exactly as the reference does (sensing.cpp:354)
-            if (fix) A.fix_list[atomicAdd(A.fix_count, 1u)] = bidx0 + q;
-          }
+          if (lane == 0) A.weights[bidx0 + q] = (uint32_t)sig;
         }
+        __syncwarp();
       }
       if constexpr (kPayload || kDecode) {
         int cnt[2];
         cnt[0] = __shfl_sync(0xffffffffu, my_cnt, 2 * p);
         cnt[1] = two ? __shfl_sync(0xffffffffu, my_cnt, (2 * p + 1) & 31) : 0;
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            if ((int)rank_d[s] < cnt[q]) s_buf[warp][q][rank_d[s]] = Y[q].v[s >> 2][s & 3];
-        __syncwarp();
         if constexpr (kPayload) {
+          // zigzag-ordered copy in smem -> coalesced prefix writes
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int s = 0; s < 8; ++s) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+          __syncwarp();
           const int32_t o0 = __shfl_sync(0xffffffffu, my_off, 2 * p);
           const int32_t o1 = __shfl_sync(0xffffffffu, my_off, (2 * p + 1) & 31);
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             float* dst = A.payload + (int64_t)img * A.payload_stride + (q ? o1 : o0);
-            for (int k = lane; k < cnt[q]; k += 32) dst[k] = s_buf[warp][q][k];
+#pragma unroll 1
+            for (int k = lane; k < cnt[q]; k += 32) dst[k] = zb0[kWbuf * q + k];
           }
+          __syncwarp();
         }
         if constexpr (kDecode) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             if (q == 1 && !two) break;
-            float yv[2][4];
+            Acc16 Ym;  // zero the coefficients outside the block's zigzag prefix
 #pragma unroll
-            for (int s = 0; s < 8; ++s)
-              yv[s >> 2][s & 3] = (int)rank_b[s] < cnt[q] ? s_buf[warp][q][rank_b[s]] : 0.f;
-            const Acc16 X = dct16_inv_f32(f, yv);
+            for (int s = 0; s < 8; ++s) Ym.v[s >> 2][s & 3] = (int)rank_d[s] < cnt[q] ? Y[q].v[s >> 2][s & 3] : 0.f;
+            const Acc16 X = dct16_inv_from_yt(f, Ym);
             store_dfrag(A.out + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
                         A.out_pitch, X);
           }
         }
-        __syncwarp();
       }
     }
   }
@@ -344,46 +356,71 @@ decode16_kernel(Grid16 G, uint32_t total_blocks, const uint16_t* __restrict__ co
   }
 }
 
-// DD phase-1 recount in fp64 for the (rare) blocks whose fp32/MMA coefficients
-// came within the error band of T: warp per listed block; tmp[u][c] for the
-// rows the prefix needs, then each prefix coefficient, all in the reference's
-// exact operation order (dct.cpp:30-49), |c| > T strict (sensing.cpp:354).
+// fp64 decision for the (rare) phase-1 coefficients whose MMA value came within
+// the error band of T: one thread per listed (block, coefficient), computed in the
+// reference's exact operation order (dct.cpp:30-49) with no FMA contraction and
+// the reference basis, |c| > T strict (sensing.cpp:354). Should the list overflow
+// (only adversarial inputs: capacity is 2 entries per block), every flagged block
+// is recounted in full in fp64 instead.
 __global__ void __launch_bounds__(256)
 dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch, Grid16 G, int phase1, double T,
-                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint32_t* __restrict__ weights) {
-  __shared__ double s_tmp[8][16 * 16];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* C = basis_dev<16>();
-  const unsigned short* zz = zigzag_dev<16>();
-  int umax = 0;
-  for (int k = 0; k < phase1; ++k) umax = max(umax, (int)(zz[k] >> 4));
+                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint32_t cap,
+                  const uint8_t* __restrict__ flags, uint32_t total_blocks, uint32_t* __restrict__ weights) {
   const uint32_t n = *count;
-  for (uint32_t e = blockIdx.x * 8 + warp; e < n; e += gridDim.x * 8) {
-    const uint32_t bidx = list[e];
+  const double* C = basis_dev<16>();
+  const int lane = threadIdx.x & 31, c = lane & 15;
+  const unsigned half = 0xffffu << (lane & 16);
+  if (n <= cap) {
+    // 16 lanes per entry: lane c forms tmp[u][c] = sum_r C[u][r] x[r][c] (r ascending), then the
+    // group's first lane accumulates y = sum_c tmp[u][c] C[v][c] in c order -- the reference's order.
+    const uint32_t groups = (gridDim.x * blockDim.x) >> 4;
+    for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 4; e < ((n + 1) & ~1u); e += groups) {
+      const bool valid = e < n;
+      const uint32_t bidx = valid ? list[2 * e] : 0;
+      const int flat = valid ? (int)list[2 * e + 1] : 0;
+      const int u = flat >> 4, v = flat & 15;
+      const uint32_t img = G.div_nb.div(bidx);
+      const uint32_t bi = bidx - img * G.nb;
+      const uint32_t br = G.div_cols.div(bi), bc = bi - br * (uint32_t)G.cols;
+      const uint8_t* col = imgs + (int64_t)img * img_stride + (int64_t)(br * 16) * pitch + bc * 16 + c;
+      double x[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) x[r] = valid ? (double)col[(size_t)r * pitch] : 0.0;
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) t = __dadd_rn(t, __dmul_rn(C[u * 16 + r], x[r]));
+      double y = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) y = __dadd_rn(y, __dmul_rn(__shfl_sync(half, t, k, 16), C[v * 16 + k]));
+      if (valid && c == 0 && fabs(y) > T) atomicAdd(weights + bidx, 1u);
+    }
+    return;
+  }
+  const unsigned short* zz = zigzag_dev<16>();
+  for (uint32_t bidx = blockIdx.x * blockDim.x + threadIdx.x; bidx < total_blocks; bidx += gridDim.x * blockDim.x) {
+    if (!flags[bidx]) continue;
     const uint32_t img = G.div_nb.div(bidx);
     const uint32_t bi = bidx - img * G.nb;
     const uint32_t br = G.div_cols.div(bi), bc = bi - br * (uint32_t)G.cols;
     const uint8_t* blk = imgs + (int64_t)img * img_stride + (int64_t)(br * 16) * pitch + bc * 16;
-    double* tmp = s_tmp[warp];
-    for (int i = lane; i < (umax + 1) * 16; i += 32) {
-      const int u = i >> 4, c = i & 15;
-      double t = 0.0;
-      for (int r = 0; r < 16; ++r) t = __dadd_rn(t, __dmul_rn(C[u * 16 + r], (double)blk[(size_t)r * pitch + c]));
-      tmp[u * 16 + c] = t;
-    }
-    __syncwarp();
-    int sig = 0;
-    for (int k = lane; k < phase1; k += 32) {
-      const int u = zz[k] >> 4, v = zz[k] & 15;
-      double y = 0.0;
-      for (int c = 0; c < 16; ++c) y = __dadd_rn(y, __dmul_rn(tmp[u * 16 + c], C[v * 16 + c]));
-      sig += fabs(y) > T ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
-    if (lane == 0) weights[bidx] = (uint32_t)sig;
-    __syncwarp();
+    uint32_t sig = 0;
+    for (int k = 0; k < phase1; ++k) sig += fabs(exact_coef16(blk, pitch, zz[k])) > T ? 1u : 0u;
+    weights[bidx] = sig;
   }
+}
+
+// largest_remainder_allocate with one warp per image (no CTA barriers).
+__global__ void __launch_bounds__(128)
+alloc_warp_kernel(const uint32_t* __restrict__ weights, int nb, int n, int wmax, long long budget, int cap, int base,
+                  uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int warp = threadIdx.x >> 5;
+  const int img = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (img >= n) return;
+  WarpAllocSmem& S = reinterpret_cast<WarpAllocSmem*>(s_dyn)[warp];
+  const int st = warp_allocate(S, weights + (int64_t)img * nb, nb, wmax, budget, cap, base, counts + (int64_t)img * nb,
+                               offsets + (int64_t)img * nb);
+  if ((threadIdx.x & 31) == 0 && status) status[img] = st;
 }
 
 // ---------------------------------------------------------------------------
@@ -393,15 +430,25 @@ static unsigned grid_for(Ctx* ctx, uint32_t warps_needed) {
   return ctas < cap ? (ctas ? ctas : 1) : cap;
 }
 
+
 bool mma16_supported(int rows, int cols, int n) {
   const uint64_t blocks = (uint64_t)rows * cols * (uint64_t)n;
   return blocks < (1ull << 31);
 }
 
+bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(alloc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * sizeof(WarpAllocSmem));
+    attr = true;
+  }
+  return (int64_t)rows * cols <= kWarpAllocMaxBlocks && wmax <= kWarpAllocMaxW && mma16_supported(rows, cols, n);
+}
+
 int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
                    int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
                    float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
-                   cudaStream_t s, uint32_t* fix_scratch) {
+                   cudaStream_t s, uint32_t* fix_scratch, const FusedAlloc* fa) {
   const Grid16 G = make_grid16(rows, cols, n);
   if (G.total_units == 0) return ABCS_OK;
   Sense16Args A{};
@@ -412,13 +459,17 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
   A.phase1 = phase1;
   A.T = T;
   A.Tf = (float)T;
-  A.band = (float)(2e-2 + fabs(T - (double)A.Tf));  // error bound of the fp32/MMA transform + rounding of T
+  A.band = (float)(1e-2 + fabs(T - (double)A.Tf));  // >= worst-case MMA transform error + rounding of T
   A.weights = weights;
   if (mode == 1) {
     if (!fix_scratch) return set_error(ABCS_ERR_LOGIC, "sense16: missing fixup scratch");
+    const int64_t nbt = (int64_t)G.nb * n;
     A.fix_count = fix_scratch;
-    A.fix_list = fix_scratch + 1;
+    A.fix_list = fix_scratch + 4;
+    A.fix_cap = (uint32_t)(nbt * 2);
+    A.fix_flag = reinterpret_cast<uint8_t*>(fix_scratch + 4 + 2 * (int64_t)A.fix_cap);
     cudaError_t e = cudaMemsetAsync(A.fix_count, 0, 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(A.fix_flag, 0, (size_t)nbt, s);
     if (e != cudaSuccess) return cuda_status(e, "fixup reset");
   }
   A.counts = counts;
@@ -436,8 +487,17 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
       else
         sense16_kernel<true, false, false><<<grid, kM16Threads, 0, s>>>(G, A);
       ctx->launches++;
-      dd_fixup16_kernel<<<(unsigned)ctx->sm_count * 2, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1, T, A.fix_list,
-                                                                   A.fix_count, weights);
+      dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1, T, A.fix_list,
+                                                               A.fix_count, A.fix_cap, A.fix_flag, G.nb * (uint32_t)n,
+                                                               weights);
+      ctx->launches++;
+      if (fa) {  // allocation: one warp per image (warp_alloc.cuh)
+        const int warps_per_cta = 4;
+        alloc_warp_kernel<<<(n + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta,
+                            warps_per_cta * sizeof(WarpAllocSmem), s>>>(weights, (int)G.nb, n, fa->wmax, fa->budget,
+                                                                         fa->cap, fa->base, fa->counts, fa->offsets,
+                                                                         fa->status);
+      }
       break;
     case 2: sense16_kernel<false, true, false><<<grid, kM16Threads, 0, s>>>(G, A); break;
     case 3: sense16_kernel<false, true, true><<<grid, kM16Threads, 0, s>>>(G, A); break;

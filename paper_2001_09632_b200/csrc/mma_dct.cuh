@@ -204,6 +204,42 @@ __device__ __forceinline__ Acc16 dct16_inv_f32(const Frag16& f, const float (&yv
   return stage2(T, f.tbh, f.tbl);
 }
 
+// Inverse DCT X = C^T Y C where Y is given TRANSPOSED in D-fragment layout, i.e. the
+// output of a forward transform computed as Y^T = C X^T C^T: the accumulator pairs of
+// Y^T are exactly the stage-1 B fragments of Y (tile 0: {D0.d0,d1},{D1.d0,d1};
+// tile 1: {D0.d2,d3},{D1.d2,d3}), so the fused decode needs no shuffle or smem.
+__device__ __forceinline__ Acc16 dct16_inv_from_yt(const Frag16& f, const Acc16& Yt) {
+  uint32_t bh[2][2], bl[2][2];
+  split2(Yt.v[0][0], Yt.v[0][1], bh[0][0], bl[0][0]);
+  split2(Yt.v[1][0], Yt.v[1][1], bh[0][1], bl[0][1]);
+  split2(Yt.v[0][2], Yt.v[0][3], bh[1][0], bl[1][0]);
+  split2(Yt.v[1][2], Yt.v[1][3], bh[1][1], bl[1][1]);
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.th, bl[j][0], bl[j][1]);
+    mma16816(T.v[j], f.tl, bh[j][0], bh[j][1]);
+    mma16816(T.v[j], f.th, bh[j][0], bh[j][1]);
+  }
+  return stage2(T, f.tbh, f.tbl);
+}
+
+// B fragments of X^T (for the transposed forward) from a u8 block in smem with a
+// 16-byte row pitch: tile j: {X[8j+g][2t], X[8j+g][2t+1]}, {X[8j+g][2t+8], X[8j+g][2t+9]}
+// -- contiguous byte pairs, one 16-bit load each.
+__device__ __forceinline__ void u8_bfragT(const uint8_t* blk, uint32_t (&bx)[2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint8_t* row = blk + (8 * j + g) * 16 + 2 * t;
+    const uint32_t p0 = *reinterpret_cast<const uint16_t*>(row);
+    const uint32_t p1 = *reinterpret_cast<const uint16_t*>(row + 8);
+    bx[j][0] = u8pair_to_h2(p0 & 0xffu, p0 >> 8);
+    bx[j][1] = u8pair_to_h2(p1 & 0xffu, p1 >> 8);
+  }
+}
+
 // Positions of the D-fragment slots: slot s = 4j + i -> (row, col)
 __device__ __forceinline__ int dslot_row(int s) { return ((threadIdx.x & 31) >> 2) + ((s & 3) >= 2 ? 8 : 0); }
 __device__ __forceinline__ int dslot_col(int s) { return 8 * (s >> 2) + 2 * (threadIdx.x & 3) + (s & 1); }

@@ -199,8 +199,7 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
     bbv_weights_kernel<<<(unsigned)grid, threads, 0, s>>>(imgs, img_stride, pitch, p.rows, p.cols, n, p.block,
                                                           (int)p.bbv_stride, p.bbv_offset, p.bbv_per_side,
                                                           p.bbv_valid_probes, weights, side, p.side_per_image);
-  } else if (p.algorithm_used == ABCS_ALGO_DD && p.block == 16 && mma16_supported(p.rows, p.cols, n) &&
-             fix_scratch) {
+  } else if (p.algorithm_used == ABCS_ALGO_DD && p.block == 16 && mma16_supported(p.rows, p.cols, n)) {
     return launch_sense16(ctx, 1, p.rows, p.cols, n, imgs, img_stride, pitch, p.dd_phase1, p.threshold, weights,
                           nullptr, nullptr, nullptr, 0, nullptr, 0, 0, s, fix_scratch);
   } else if (p.algorithm_used == ABCS_ALGO_DD) {
