@@ -1,4 +1,5 @@
-// IDA refinement (reconstruct() with ReconMethod::Ida, recon.cpp:199-259) and
+// IDA refinement for B = 32 on CUDA cores (B = 8/16: ida_mma.cu) -- reconstruct() with
+// ReconMethod::Ida, recon.cpp:199-259 -- and
 // the dct_threshold denoiser (denoise.cpp:52-92).
 //
 // State carried between launches is pseudo_t = x_t + A* z_t (recon.cpp:75-79)
@@ -16,6 +17,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "ida_common.cuh"
 #include "internal.h"
 
 namespace abcs_b200 {
@@ -29,39 +31,7 @@ constexpr int kAccPitch = kRegion + 1;
 constexpr int kTileSlots = kIdaThreads / 8;  // 32 concurrent 8x8 tiles
 constexpr int kTileFloats = 8 * 9;
 
-struct IdaParams {
-  int rows, cols, n;
-  int Hc, Wc;
-  int regions_x, regions_y, regions_per_img;
-  const uint16_t* counts;
-  const int32_t* offsets;
-  const float* y;
-  int64_t y_stride;
-  float* z;                // in place
-  const float* pseudo_in;  // step: pseudo_t
-  float* pseudo_out;       // pseudo_{t+1} (nullptr on the last step)
-  float* x_out;            // clamped estimate on the last step
-  int64_t out_stride;
-  int out_pitch;
-  const uint8_t* ref;
-  int64_t ref_stride;
-  int ref_pitch;
-  float onsager;           // 1/D_F (0 for the warm start)
-  double k;                // threshold multiplier
-  const double* sigma_in;  // sigma_t per image (step); unused for init
-  double* sigma_out;       // sigma_{t+1} per image
-  double* msize;           // M per image (written by init, read by steps)
-  double* partials;        // [n][regions_per_img][4]
-  unsigned int* counters;  // [n]
-  double* trace;           // [n][iters+1][4] or nullptr
-  int trace_row;
-  int trace_rows;
-  int32_t* diverged;       // [n][2] or nullptr
-  unsigned long long* badx;  // [n] min (index*2 + kind) for x, ~0 = none
-  unsigned long long* badz;  // [n] min index for z
-  int iteration;           // iteration number after this launch (0 for init)
-  int is_init;
-};
+
 
 // ---------------------------------------------------------------------------
 // dct_soft_threshold over one 32x32 output region: s_in holds the field on
@@ -298,59 +268,6 @@ __device__ void block_phase(const IdaParams& P, int img, int R0, int C0, const f
   }
 }
 
-// Last CTA of an image folds the region partials (fixed order, so the result
-// is deterministic) into sigma, the trace row and the divergence record.
-__device__ void finish_image(const IdaParams& P, int img, int region, const double* mine) {
-  __shared__ bool s_last;
-  if (threadIdx.x == 0) {
-    double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
-    for (int q = 0; q < 4; ++q) part[q] = mine[q];
-    __threadfence();
-    const unsigned prev = atomicAdd(P.counters + img, 1u);
-    s_last = (prev == (unsigned)P.regions_per_img - 1);
-  }
-  __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
-  __threadfence();
-  double a[4] = {0.0, 0.0, 0.0, 0.0};
-  const volatile double* pp = P.partials + (int64_t)img * P.regions_per_img * 4;
-  for (int r = 0; r < P.regions_per_img; ++r)
-    for (int q = 0; q < 4; ++q) a[q] += pp[4 * r + q];
-  P.counters[img] = 0;  // ready for the next launch
-  double M;
-  if (P.is_init) {
-    M = a[3];
-    P.msize[img] = M;
-  } else {
-    M = P.msize[img];
-  }
-  const double znorm = sqrt(a[0]);
-  // init_state: sigma0 = ||y|| / sqrt(M) (recon.cpp:129); finish_step: ||z|| / sqrt(M) (:91)
-  const double sigma = (P.is_init ? sqrt(a[2]) : znorm) / sqrt(M);
-  P.sigma_out[img] = sigma;
-  if (P.trace) {
-    double* row = P.trace + ((int64_t)img * P.trace_rows + P.trace_row) * 4;
-    row[0] = (double)P.iteration;
-    row[1] = znorm;
-    row[2] = sigma;
-    double psnr = __longlong_as_double(0x7ff8000000000000ll);  // NaN without a reference
-    if (P.ref) {
-      const double mse = a[1] / ((double)P.Hc * (double)P.Wc);  // metrics.cpp:63-77
-      psnr = (mse == 0.0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(255.0 * 255.0 / mse);
-    }
-    row[3] = psnr;
-  }
-  if (!P.is_init) {
-    const unsigned long long bx = P.badx[img], bz = P.badz[img];
-    if ((bx != ~0ull || bz != ~0ull) && P.diverged && P.diverged[2 * img] == 0) {
-      P.diverged[2 * img] = P.iteration;
-      P.diverged[2 * img + 1] = (bx != ~0ull) ? ((bx & 1ull) ? 2 : 1) : 3;
-    }
-  }
-  P.badx[img] = ~0ull;
-  P.badz[img] = ~0ull;
-}
-
 // Warm start: x0 = A* y (decode into smem), then the block phase with onsager 0.
 template <int B>
 __global__ void __launch_bounds__(kIdaThreads) ida_init_kernel(IdaParams P) {
@@ -417,36 +334,6 @@ __global__ void __launch_bounds__(kIdaThreads) ida_step_kernel(IdaParams P) {
   finish_image(P, img, region, s_mine);
 }
 
-// Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109).
-__global__ void __launch_bounds__(kIdaThreads)
-denoise_kernel(const float* __restrict__ field, int H, int W, int64_t stride, const double* __restrict__ thr,
-               float* __restrict__ out, int regions_x) {
-  __shared__ float s_in[kIn * kInPitch];
-  __shared__ float s_x[kRegion * kAccPitch];
-  __shared__ float s_tile[kTileSlots * kTileFloats];
-  const int img = blockIdx.y, region = blockIdx.x;
-  const int R0 = (region / regions_x) * kRegion, C0 = (region % regions_x) * kRegion;
-  load_halo(field + (int64_t)img * stride, W, R0, C0, H, W, s_in);
-  denoise_region(s_in, s_x, s_tile, R0, C0, H, W, (float)thr[img]);
-  for (int i = threadIdx.x; i < kRegion * kRegion; i += kIdaThreads) {
-    const int r = i / kRegion, c = i % kRegion;
-    if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s_x[r * kAccPitch + c];
-  }
-}
-
-int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t stride, int32_t n,
-                   const double* thresholds_dev, float* out, cudaStream_t s) {
-  const int rx = (w + kRegion - 1) / kRegion, ry = (h + kRegion - 1) / kRegion;
-  for (int done = 0; done < n;) {
-    const int cnt = std::min(n - done, 65535);
-    denoise_kernel<<<dim3(rx * ry, cnt), kIdaThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
-                                                              thresholds_dev + done, out + (int64_t)done * stride, rx);
-    ctx->launches++;
-    done += cnt;
-  }
-  return cuda_status(cudaGetLastError(), "denoise launch");
-}
-
 static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
@@ -469,7 +356,9 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
                int64_t ref_stride, int32_t ref_pitch, float* out, int64_t out_stride, int32_t out_pitch,
                double* trace, int32_t* diverged, void* scratch, cudaStream_t s) {
   const int64_t Hc = (int64_t)rows * block, Wc = (int64_t)cols * block;
-  const int rx = (int)((Wc + kRegion - 1) / kRegion), ry = (int)((Hc + kRegion - 1) / kRegion);
+  const bool mma = (block == 8 || block == 16);  // tensor-core kernels (ida_mma.cu), 64x64 regions
+  const int region_side = mma ? ida_mma_region() : kRegion;
+  const int rx = (int)((Wc + region_side - 1) / region_side), ry = (int)((Hc + region_side - 1) / region_side);
   const int64_t regions = (int64_t)rx * ry;
   char* p = static_cast<char*>(scratch);
   float* pseudo[2];
@@ -526,6 +415,11 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
   P.badz = badz;
   const dim3 grid((unsigned)regions, (unsigned)n);
   if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "IDA batch limited to 65535 images per call");
+  auto launch = [&](auto kern) {
+    if (mma) launch_ida_mma_kernel(block, P, grid, s);
+    else kern<<<grid, kIdaThreads, 0, s>>>(P);
+    ctx->launches++;
+  };
   auto init = [&](auto kern) {
     P.is_init = 1;
     P.onsager = 0.f;
@@ -536,8 +430,7 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
     P.sigma_out = sigma;
     P.trace_row = 0;
     P.iteration = 0;
-    kern<<<grid, kIdaThreads, 0, s>>>(P);
-    ctx->launches++;
+    launch(kern);
   };
   auto step = [&](auto kern, int t) {
     P.is_init = 0;
@@ -550,17 +443,10 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
     P.sigma_out = sigma + (int64_t)(t + 1) * n;
     P.trace_row = t + 1;
     P.iteration = t + 1;
-    kern<<<grid, kIdaThreads, 0, s>>>(P);
-    ctx->launches++;
+    launch(kern);
   };
-  if (block == 8) {
-    init(ida_init_kernel<8>);
-    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<8>, t);
-  } else if (block == 16) {
-    init(ida_init_kernel<16>);
-    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<16>, t);
-  } else if (block == 32) {
-    init(ida_init_kernel<32>);
+  if (block == 8 || block == 16 || block == 32) {
+    init(ida_init_kernel<32>);  // the kernel argument is ignored on the tensor-core path
     for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<32>, t);
   } else {
     return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");

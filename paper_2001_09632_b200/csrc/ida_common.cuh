@@ -1,0 +1,99 @@
+// State shared by the IDA kernels (ida.cu: CUDA-core path for B = 32; ida_mma.cu:
+// tensor-core path for B = 8, 16): launch parameters and the per-image fold of the
+// region partials into sigma / trace / divergence (recon.cpp:81-93, 53-73).
+#pragma once
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace abcs_b200 {
+
+struct IdaParams {
+  int rows, cols, n;
+  int Hc, Wc;
+  int regions_x, regions_y, regions_per_img;
+  const uint16_t* counts;
+  const int32_t* offsets;
+  const float* y;
+  int64_t y_stride;
+  float* z;                // in place
+  const float* pseudo_in;  // step: pseudo_t
+  float* pseudo_out;       // pseudo_{t+1} (nullptr on the last step)
+  float* x_out;            // clamped estimate on the last step
+  int64_t out_stride;
+  int out_pitch;
+  const uint8_t* ref;
+  int64_t ref_stride;
+  int ref_pitch;
+  float onsager;           // 1/D_F (0 for the warm start)
+  double k;                // threshold multiplier
+  const double* sigma_in;  // sigma_t per image (step); unused for init
+  double* sigma_out;       // sigma_{t+1} per image
+  double* msize;           // M per image (written by init, read by steps)
+  double* partials;        // [n][regions_per_img][4]
+  unsigned int* counters;  // [n]
+  double* trace;           // [n][iters+1][4] or nullptr
+  int trace_row;
+  int trace_rows;
+  int32_t* diverged;       // [n][2] or nullptr
+  unsigned long long* badx;  // [n] min (index*2 + kind) for x, ~0 = none
+  unsigned long long* badz;  // [n] min index for z
+  int iteration;           // iteration number after this launch (0 for init)
+  int is_init;
+};
+
+// Last CTA of an image folds the region partials (fixed order, so the result
+// is deterministic) into sigma, the trace row and the divergence record.
+static __device__ void finish_image(const IdaParams& P, int img, int region, const double* mine) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
+    for (int q = 0; q < 4; ++q) part[q] = mine[q];
+    __threadfence();
+    const unsigned prev = atomicAdd(P.counters + img, 1u);
+    s_last = (prev == (unsigned)P.regions_per_img - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  const volatile double* pp = P.partials + (int64_t)img * P.regions_per_img * 4;
+  for (int r = 0; r < P.regions_per_img; ++r)
+    for (int q = 0; q < 4; ++q) a[q] += pp[4 * r + q];
+  P.counters[img] = 0;  // ready for the next launch
+  double M;
+  if (P.is_init) {
+    M = a[3];
+    P.msize[img] = M;
+  } else {
+    M = P.msize[img];
+  }
+  const double znorm = sqrt(a[0]);
+  // init_state: sigma0 = ||y|| / sqrt(M) (recon.cpp:129); finish_step: ||z|| / sqrt(M) (:91)
+  const double sigma = (P.is_init ? sqrt(a[2]) : znorm) / sqrt(M);
+  P.sigma_out[img] = sigma;
+  if (P.trace) {
+    double* row = P.trace + ((int64_t)img * P.trace_rows + P.trace_row) * 4;
+    row[0] = (double)P.iteration;
+    row[1] = znorm;
+    row[2] = sigma;
+    double psnr = __longlong_as_double(0x7ff8000000000000ll);  // NaN without a reference
+    if (P.ref) {
+      const double mse = a[1] / ((double)P.Hc * (double)P.Wc);  // metrics.cpp:63-77
+      psnr = (mse == 0.0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(255.0 * 255.0 / mse);
+    }
+    row[3] = psnr;
+  }
+  if (!P.is_init) {
+    const unsigned long long bx = P.badx[img], bz = P.badz[img];
+    if ((bx != ~0ull || bz != ~0ull) && P.diverged && P.diverged[2 * img] == 0) {
+      P.diverged[2 * img] = P.iteration;
+      P.diverged[2 * img + 1] = (bx != ~0ull) ? ((bx & 1ull) ? 2 : 1) : 3;
+    }
+  }
+  P.badx[img] = ~0ull;
+  P.badz[img] = ~0ull;
+}
+
+
+}  // namespace abcs_b200

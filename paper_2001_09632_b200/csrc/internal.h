@@ -63,6 +63,9 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
                const abcs_ida_config& cfg, const uint8_t* ref, int64_t ref_stride, int32_t ref_pitch,
                float* out, int64_t out_stride, int32_t out_pitch, double* trace, int32_t* diverged,
                void* scratch, cudaStream_t s);
+struct IdaParams;
+int ida_mma_region();
+void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s);
 size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
                          const abcs_ida_config& cfg);
 bool mma16_supported(int rows, int cols, int n);

@@ -240,6 +240,76 @@ __device__ __forceinline__ void u8_bfragT(const uint8_t* blk, uint32_t (&bx)[2][
   }
 }
 
+// ---------------------------------------------------------------------------
+// 8x8 transforms, two blocks per warp-MMA. Stage 1 uses m16n8k16 with the block-
+// diagonal A = diag(M, M) (so the two 8x8 operands stacked in B never mix), stage 2
+// uses m16n8k8 whose A fragment is the stage-1 accumulator. As for B = 16 the
+// forward runs transposed (Y^T = C8 P^T C8^T) so its accumulator pairs are the
+// inverse's stage-1 B fragments. Slot layout of the 16x8 results: rows g / g+8 =
+// row g of block 0 / block 1, columns 2t, 2t+1.
+__device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+
+struct Frag8 {
+  uint32_t ah[4], al[4];  // diag(C8, C8) as A: {p, 0, 0, p}, p = {C8[g][2t], C8[g][2t+1]}  (== C8^T as B)
+  uint32_t th[4], tl[4];  // diag(C8^T, C8^T) as A: p = {C8[2t][g], C8[2t+1][g]}            (== C8 as B)
+};
+
+__device__ __forceinline__ void load_frag8(Frag8& f) {
+  const double* C = basis_dev<8>();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint32_t h, l;
+  split2((float)C[g * 8 + 2 * t], (float)C[g * 8 + 2 * t + 1], h, l);
+  f.ah[0] = f.ah[3] = h;
+  f.al[0] = f.al[3] = l;
+  f.ah[1] = f.ah[2] = f.al[1] = f.al[2] = 0u;
+  split2((float)C[(2 * t) * 8 + g], (float)C[(2 * t + 1) * 8 + g], h, l);
+  f.th[0] = f.th[3] = h;
+  f.tl[0] = f.tl[3] = l;
+  f.th[1] = f.th[2] = f.tl[1] = f.tl[2] = 0u;
+}
+
+// Y^T of two 8x8 blocks from fp32 pixel pairs p0 = {P0[g][2t], P0[g][2t+1]},
+// p1 = {P1[g][2t], P1[g][2t+1]} (row-contiguous pairs).
+__device__ __forceinline__ void dct8x2_fwdT(const Frag8& f, float2 p0, float2 p1, float (&Y)[4]) {
+  uint32_t h0, l0, h1, l1;
+  split2(p0.x, p0.y, h0, l0);
+  split2(p1.x, p1.y, h1, l1);
+  float Q[4] = {0.f, 0.f, 0.f, 0.f};
+  mma16816(Q, f.ah, l0, l1);
+  mma16816(Q, f.al, h0, h1);
+  mma16816(Q, f.ah, h0, h1);
+  uint32_t qh0, ql0, qh1, ql1;
+  split2(Q[0], Q[1], qh0, ql0);
+  split2(Q[2], Q[3], qh1, ql1);
+  Y[0] = Y[1] = Y[2] = Y[3] = 0.f;
+  mma1688(Y, ql0, ql1, f.ah[0]);
+  mma1688(Y, qh0, qh1, f.al[0]);
+  mma1688(Y, qh0, qh1, f.ah[0]);
+}
+
+// X = C8^T Y C8 of two blocks given as Y^T in the slot layout (output of dct8x2_fwdT).
+__device__ __forceinline__ void dct8x2_inv_from_yt(const Frag8& f, const float (&Yt)[4], float (&X)[4]) {
+  uint32_t h0, l0, h1, l1;
+  split2(Yt[0], Yt[1], h0, l0);
+  split2(Yt[2], Yt[3], h1, l1);
+  float R[4] = {0.f, 0.f, 0.f, 0.f};
+  mma16816(R, f.th, l0, l1);
+  mma16816(R, f.tl, h0, h1);
+  mma16816(R, f.th, h0, h1);
+  uint32_t rh0, rl0, rh1, rl1;
+  split2(R[0], R[1], rh0, rl0);
+  split2(R[2], R[3], rh1, rl1);
+  X[0] = X[1] = X[2] = X[3] = 0.f;
+  mma1688(X, rl0, rl1, f.th[0]);
+  mma1688(X, rh0, rh1, f.tl[0]);
+  mma1688(X, rh0, rh1, f.th[0]);
+}
+
 // Positions of the D-fragment slots: slot s = 4j + i -> (row, col)
 __device__ __forceinline__ int dslot_row(int s) { return ((threadIdx.x & 31) >> 2) + ((s & 3) >= 2 ? 8 : 0); }
 __device__ __forceinline__ int dslot_col(int s) { return 8 * (s >> 2) + 2 * (threadIdx.x & 3) + (s & 1); }

@@ -22,5 +22,15 @@ if which in ("all", "ida"):
     b = p.sense_batch(imgs[:64], p.SensingConfig(16, 3, 10, p.Algorithm.BBV))
     for rep in range(2):
         p.ida_batch(b, p.ReconConfig(p.ReconMethod.Ida, iterations=10), trace=False, check=False)
+if which in ("all", "den"):
+    import ctypes as C
+    from paper_2001_09632_b200 import _lib
+    f = imgs[:64].float().contiguous()
+    out = torch.empty_like(f)
+    sig = (C.c_double * 64)(*([7.0] * 64))
+    for rep in range(3):
+        rc = _lib.load().abcs_denoise_dct_batch(p.Context.get().handle, f.data_ptr(), 512, 512, 512 * 512, 64, sig,
+                                                1.0, 8, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert rc == 0, rc
 torch.cuda.synchronize()
 print("ok")
