@@ -212,6 +212,32 @@ int abcs_ida_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
                    void* stream);
 int abcs_ida_check(const int32_t* h_diverged, int32_t n_images, int32_t* first_image);
 
+/* init_state (recon.cpp:119-131) on caller-owned device state, n images at once:
+ * warm != 0: x0 = A* y, z0 = y - A x0; warm == 0: x0 = 0, z0 = y. Either way
+ * sigma0 = ||y|| / sqrt(M) (M = sum of counts). d_x: n*(rows*B)*(cols*B) f32,
+ * d_z: n*y_stride f32, d_sigma: n f64. Replaces abcs::init_state (recon.hpp:61). */
+int abcs_ida_init_state(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                        const uint16_t* d_counts, const int32_t* d_offsets, const float* d_y,
+                        int64_t y_stride, int32_t n_images, int32_t warm, float* d_x, float* d_z,
+                        double* d_sigma, void* stream);
+
+/* damp_step with variant Ida (recon.cpp:170-197 + finish_step :81-93) on that state,
+ * in place: pseudo = A* z + x; x <- dct_threshold(pseudo, k*sigma); z <- (y - A x) + z/D_F;
+ * sigma <- ||z|| / sqrt(M). `iteration` is the state's iteration count after the step
+ * (recorded in d_diverged like abcs_ida_batch). Uses cfg->damping, cfg->k,
+ * cfg->denoiser_block. Replaces abcs::damp_step(.., ReconMethod::Ida, ..) (recon.hpp:67-69). */
+int abcs_ida_step_state(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                        const uint16_t* d_counts, const int32_t* d_offsets, const float* d_y,
+                        int64_t y_stride, int32_t n_images, const abcs_ida_config* cfg, float* d_x,
+                        float* d_z, double* d_sigma, int32_t iteration, int32_t* d_diverged,
+                        void* stream);
+
+/* psnr (metrics.cpp:63-77) of f32 images against u8 references, per image (f64,
+ * +inf when mse == 0): reconstruct()'s Idct trace row (recon.cpp:217-221). */
+int abcs_psnr_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch,
+                    const float* d_img, int64_t img_stride, int32_t img_pitch, int32_t height,
+                    int32_t width, int32_t n_images, double* d_psnr, void* stream);
+
 /* Synthetic inputs on the device (same bytes as abcs_synth_generate_host). */
 int abcs_synth_generate(abcs_ctx* ctx, const abcs_synth_spec* spec, int64_t first_index,
                         int32_t n_images, uint8_t* d_out, int64_t image_stride, void* stream);

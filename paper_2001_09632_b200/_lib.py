@@ -88,6 +88,10 @@ SIGNATURES = {
     "abcs_ida_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC),
                                  P, I64, I32, P, I64, I32, P, P, P]),
     "abcs_ida_check": (C.c_int, [P, I32, C.POINTER(I32)]),
+    "abcs_psnr_batch": (C.c_int, [P, P, I64, I32, P, I64, I32, I32, I32, I32, P, P]),
+    "abcs_ida_init_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, I32, P, P, P, P]),
+    "abcs_ida_step_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC), P, P, P, I32,
+                                      P, P]),
     "abcs_synth_generate": (C.c_int, [P, C.POINTER(SynthSpecC), I64, I32, P, I64, P]),
     "abcs_sense_decode_host": (C.c_int, [P, C.POINTER(SensePlanC), P, I32, P, P, P, I32]),
 }

@@ -756,10 +756,14 @@ def reconstruct(ms: MeasurementSet, cfg: ReconConfig, reference=None) -> ReconRe
     if cfg.method == ReconMethod.Idct:
         img = decode_idct(ms)
         trace = []
-        if ref_t is not None:
-            refc = ref_t[0, :g.cropped_height(), :g.cropped_width()].double()
-            mse = float(((refc - torch.from_numpy(img).cuda().double()) ** 2).mean())
-            trace.append(TraceRow(0, 0.0, 0.0, float("inf") if mse == 0 else 10 * np.log10(255 * 255 / mse)))
+        if ref_t is not None:  # psnr vs the cropped reference (recon.cpp:217-221, metrics.cpp:63-77)
+            xt = torch.from_numpy(np.ascontiguousarray(img)).to(ref_t.device)
+            out = torch.empty(1, dtype=torch.float64, device=ref_t.device)
+            _check(_lib.load().abcs_psnr_batch(Context.get(ref_t.device.index).handle, ref_t.data_ptr(),
+                                               ref_t[0].numel(), ref_t.shape[2], xt.data_ptr(), xt.numel(),
+                                               g.cropped_width(), g.cropped_height(), g.cropped_width(), 1,
+                                               out.data_ptr(), _stream_ptr(torch)))
+            trace.append(TraceRow(0, 0.0, 0.0, float(out.item())))
         return ReconResult(img, trace)
     if cfg.method != ReconMethod.Ida:
         raise UnsupportedError(f"method {recon_method_name(cfg.method)} is not on the device path (IDA and IDCT are)")
@@ -769,6 +773,70 @@ def reconstruct(ms: MeasurementSet, cfg: ReconConfig, reference=None) -> ReconRe
     out, tr, _ = ida_batch(b, cfg, reference=ref_t, trace=True, check=True)
     rows = [TraceRow(int(r[0]), float(r[1]), float(r[2]), float(r[3])) for r in tr[0].cpu().numpy()]
     return ReconResult(out[0].cpu().numpy(), rows)
+
+
+@dataclass
+class ReconState:
+    """recon.hpp:46-51 — x (pixel field, flat f32), z (residual), sigma, iteration."""
+    x: np.ndarray
+    z: np.ndarray
+    sigma: float = 0.0
+    iteration: int = 0
+
+
+def init_state(op: "SensingOperator", y, warm: bool) -> ReconState:
+    """recon.cpp:119-131 via abcs_ida_init_state (x0 = A* y or 0, z0 = y - A x0, sigma0 = ||y||/sqrt(M))."""
+    torch = _torch()
+    yy = np.ascontiguousarray(np.asarray(y, dtype=np.float32).reshape(-1))
+    if yy.size != op.measurements():
+        raise ValueError("init_state: measurement vector length mismatch")
+    b = _batch_from_host(op._ms(yy))
+    g = op.grid()
+    dev = b.counts.device
+    x = torch.empty(op.field_size(), dtype=torch.float32, device=dev)
+    z = torch.empty(max(yy.size, 1), dtype=torch.float32, device=dev)
+    sig = torch.zeros(1, dtype=torch.float64, device=dev)
+    _check(_lib.load().abcs_ida_init_state(Context.get(dev.index).handle, g.rows, g.cols, g.block, _ptr(b.counts),
+                                           _ptr(b.offsets), _ptr(b.payload), yy.size, 1, 1 if warm else 0,
+                                           x.data_ptr(), z.data_ptr(), sig.data_ptr(), _stream_ptr(torch)))
+    return ReconState(x.cpu().numpy(), z[:yy.size].cpu().numpy(), float(sig.item()), 0)
+
+
+def damp_step(state: ReconState, op: "SensingOperator", y, denoiser: DenoiserSpec, variant: ReconMethod,
+              damping: float, seed: int = 42) -> None:
+    """recon.cpp:170-197 (variant Ida) via abcs_ida_step_state; updates `state` in place and raises
+    DivergenceError like finish_step/check_finite (recon.cpp:81-93, 53-73)."""
+    torch = _torch()
+    if variant not in (ReconMethod.Damp, ReconMethod.DampD, ReconMethod.Ida):
+        raise ValueError("damp_step: variant must be damp, dampd or ida")
+    if variant != ReconMethod.Ida:
+        raise UnsupportedError("damp_step: only the Ida variant is on the device path")
+    cfg = ReconConfig(ReconMethod.Ida, 1, damping, denoiser)
+    if damping < 1.0:
+        raise ValueError("damping factor D_F must be >= 1")
+    yy = np.ascontiguousarray(np.asarray(y, dtype=np.float32).reshape(-1))
+    if yy.size != op.measurements() or np.size(state.z) != yy.size or np.size(state.x) != op.field_size():
+        raise ValueError("damp_step: state / measurement size mismatch")
+    b = _batch_from_host(op._ms(yy))
+    g = op.grid()
+    dev = b.counts.device
+    x = torch.from_numpy(np.ascontiguousarray(np.asarray(state.x, dtype=np.float32).reshape(-1))).to(dev)
+    z = torch.from_numpy(np.ascontiguousarray(np.asarray(state.z, dtype=np.float32).reshape(-1))).to(dev)
+    sig = torch.tensor([float(state.sigma)], dtype=torch.float64, device=dev)
+    div = torch.zeros(2, dtype=torch.int32, device=dev)
+    c = cfg._ida_c()
+    _check(_lib.load().abcs_ida_step_state(Context.get(dev.index).handle, g.rows, g.cols, g.block, _ptr(b.counts),
+                                           _ptr(b.offsets), _ptr(b.payload), yy.size, 1, C.byref(c), x.data_ptr(),
+                                           z.data_ptr(), sig.data_ptr(), state.iteration + 1, div.data_ptr(),
+                                           _stream_ptr(torch)))
+    state.x = x.cpu().numpy()
+    state.z = z.cpu().numpy()
+    state.sigma = float(sig.item())
+    state.iteration += 1
+    d = div.cpu().numpy()
+    if d[0] > 0:
+        what = {1: "non-finite estimate", 2: "|x| > 1e6"}.get(int(d[1]), "non-finite residual")
+        raise DivergenceError(f"solver diverged ({what}) at iteration {int(d[0])}", int(d[0]))
 
 
 def denoise(spec: DenoiserSpec, field_values, sigma: float) -> np.ndarray:

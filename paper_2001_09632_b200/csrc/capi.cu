@@ -402,6 +402,84 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
                     d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, s);
 }
 
+// Shared argument checks and offsets for the explicit-state entry points.
+static int ida_state_common(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                            const int32_t* d_offsets, const float* d_y, int32_t n, const float* d_x, const float* d_z,
+                            const double* d_sigma, int64_t y_stride, void* stream, char** scr_out,
+                            const int32_t** offsets_out) {
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_x || !d_z || !d_sigma)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st;
+  const size_t off_bytes = d_offsets ? 0 : align_up((size_t)n * rows * cols * 4, 256);
+  const size_t need = off_bytes + ida_state_scratch_bytes(rows, cols, block, y_stride, n);
+  char* scr = static_cast<char*>(ctx_scratch(ctx, need, s, &st));
+  if (st) return st;
+  const int32_t* offsets = d_offsets;
+  if (!offsets) {
+    st = launch_offsets(ctx, rows * cols, n, block, d_counts, reinterpret_cast<int32_t*>(scr), nullptr, nullptr, s);
+    if (st) return st;
+    offsets = reinterpret_cast<int32_t*>(scr);
+  }
+  *scr_out = scr + off_bytes;
+  *offsets_out = offsets;
+  return ABCS_OK;
+}
+
+int abcs_ida_init_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                        const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n, int32_t warm,
+                        float* d_x, float* d_z, double* d_sigma, void* stream) {
+  CHECK_CTX(c);
+  if (n == 0) return ABCS_OK;
+  char* scr;
+  const int32_t* offsets;
+  int st = ida_state_common(c, rows, cols, block, d_counts, d_offsets, d_y, n, d_x, d_z, d_sigma, y_stride, stream,
+                            &scr, &offsets);
+  if (st) return st;
+  return launch_ida_state(reinterpret_cast<Ctx*>(c), true, rows, cols, block, d_counts, offsets, d_y, y_stride, n,
+                          warm ? 1 : 0, 1.0, 0.0, d_x, d_z, d_sigma, 0, nullptr, scr,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_ida_step_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                        const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n,
+                        const abcs_ida_config* cfg, float* d_x, float* d_z, double* d_sigma, int32_t iteration,
+                        int32_t* d_diverged, void* stream) {
+  CHECK_CTX(c);
+  if (!cfg) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null config");
+  if (cfg->damping < 1.0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "damping factor D_F must be >= 1");
+  const int Hc = rows * block, Wc = cols * block;
+  const int b = std::max(1, std::min(cfg->denoiser_block, std::min(Hc, Wc)));
+  if (b != 8) return set_error(ABCS_ERR_UNSUPPORTED, "device IDA supports the 8x8 dct_threshold denoiser");
+  if (iteration < 1) return set_error(ABCS_ERR_INVALID_ARGUMENT, "iteration numbers start at 1");
+  if (n == 0) return ABCS_OK;
+  char* scr;
+  const int32_t* offsets;
+  int st = ida_state_common(c, rows, cols, block, d_counts, d_offsets, d_y, n, d_x, d_z, d_sigma, y_stride, stream,
+                            &scr, &offsets);
+  if (st) return st;
+  return launch_ida_state(reinterpret_cast<Ctx*>(c), false, rows, cols, block, d_counts, offsets, d_y, y_stride, n, 1,
+                          cfg->damping, cfg->k, d_x, d_z, d_sigma, iteration, d_diverged, scr,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_psnr_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, const float* d_img,
+                    int64_t img_stride, int32_t img_pitch, int32_t height, int32_t width, int32_t n, double* d_psnr,
+                    void* stream) {
+  CHECK_CTX(c);
+  if (height < 1 || width < 1 || n < 0 || ref_pitch < width || img_pitch < width ||
+      (n > 0 && (!d_ref || !d_img || !d_psnr)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_psnr(ctx, d_ref, ref_stride, ref_pitch, d_img, img_stride, img_pitch, height, width, n, d_psnr,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
 int abcs_ida_check(const int32_t* h_diverged, int32_t n, int32_t* first_image) {
   if (first_image) *first_image = -1;
   if (!h_diverged) return ABCS_OK;

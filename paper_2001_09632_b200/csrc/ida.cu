@@ -235,7 +235,7 @@ __device__ void block_phase(const IdaParams& P, int img, int R0, int C0, const f
       } else {
         dst = P.x_out + (int64_t)img * P.out_stride + (int64_t)gr * P.out_pitch + gc0;
 #pragma unroll
-        for (int c = 0; c < B; ++c) o[c] = fminf(fmaxf(xr[c], 0.f), 255.f);  // recon.cpp:255-257
+        for (int c = 0; c < B; ++c) o[c] = P.clamp_out ? fminf(fmaxf(xr[c], 0.f), 255.f) : xr[c];  // recon.cpp:255-257
         store_row_f32<B>(dst, o, (P.out_pitch % 4 == 0) && (P.out_stride % 4 == 0));
       }
     }
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kIdaThreads) ida_init_kernel(IdaParams P) {
       Dct<B>::inv(col, cx);
       const int lr = (g / BPR) * B + lane, lc0 = (g % BPR) * B;
 #pragma unroll
-      for (int c = 0; c < B; ++c) s_x[lr * kAccPitch + lc0 + c] = cnt ? cx[c] : 0.f;
+      for (int c = 0; c < B; ++c) s_x[lr * kAccPitch + lc0 + c] = (cnt && P.warm) ? cx[c] : 0.f;
     }
   }
   __syncthreads();
@@ -339,7 +339,7 @@ static size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n,
                          const abcs_ida_config& cfg) {
   const int64_t Hc = (int64_t)rows * block, Wc = (int64_t)cols * block;
-  const int64_t regions = ((Hc + kRegion - 1) / kRegion) * ((Wc + kRegion - 1) / kRegion);
+  const int64_t regions = ((Hc + kRegion - 1) / kRegion) * ((Wc + kRegion - 1) / kRegion);  // >= the 64x64 grid
   size_t b = 0;
   b += 2 * align256((size_t)n * Hc * Wc * 4);               // pseudo ping-pong
   b += align256((size_t)n * y_stride * 4);                  // z
@@ -351,107 +351,201 @@ size_t ida_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_st
   return b;
 }
 
-int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts, const int32_t* offsets,
-               const float* y, int64_t y_stride, int32_t n, const abcs_ida_config& cfg, const uint8_t* ref,
-               int64_t ref_stride, int32_t ref_pitch, float* out, int64_t out_stride, int32_t out_pitch,
-               double* trace, int32_t* diverged, void* scratch, cudaStream_t s) {
-  const int64_t Hc = (int64_t)rows * block, Wc = (int64_t)cols * block;
-  const bool mma = (block == 8 || block == 16);  // tensor-core kernels (ida_mma.cu), 64x64 regions
-  const int region_side = mma ? ida_mma_region() : kRegion;
-  const int rx = (int)((Wc + region_side - 1) / region_side), ry = (int)((Hc + region_side - 1) / region_side);
-  const int64_t regions = (int64_t)rx * ry;
-  char* p = static_cast<char*>(scratch);
-  float* pseudo[2];
-  pseudo[0] = reinterpret_cast<float*>(p);
-  p += align256((size_t)n * Hc * Wc * 4);
-  pseudo[1] = reinterpret_cast<float*>(p);
-  p += align256((size_t)n * Hc * Wc * 4);
-  float* z = reinterpret_cast<float*>(p);
-  p += align256((size_t)n * y_stride * 4);
-  double* sigma = reinterpret_cast<double*>(p);
-  p += align256((size_t)n * (cfg.iterations + 1) * 8);
-  double* msize = reinterpret_cast<double*>(p);
-  p += align256((size_t)n * 8);
-  double* partials = reinterpret_cast<double*>(p);
-  p += align256((size_t)n * regions * 4 * 8);
-  unsigned int* counters = reinterpret_cast<unsigned int*>(p);
-  p += align256((size_t)n * 4);
-  unsigned long long* badx = reinterpret_cast<unsigned long long*>(p);
-  p += align256((size_t)n * 8);
-  unsigned long long* badz = reinterpret_cast<unsigned long long*>(p);
-  cudaError_t e = cudaMemsetAsync(counters, 0, (size_t)n * 4, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(badx, 0xff, (size_t)n * 8, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(badz, 0xff, (size_t)n * 8, s);
-  if (e == cudaSuccess && diverged) e = cudaMemsetAsync(diverged, 0, (size_t)n * 2 * 4, s);
-  if (e != cudaSuccess) return cuda_status(e, "ida scratch init");
+namespace {
 
+struct IdaLayout {
+  float* pseudo[2];
+  float* z;
+  double* sigma;
+  double* msize;
+  double* partials;
+  unsigned int* counters;
+  unsigned long long* badx;
+  unsigned long long* badz;
+};
+
+IdaLayout carve(void* scratch, int64_t Hc, int64_t Wc, int64_t y_stride, int n, int iterations, int64_t regions) {
+  IdaLayout L;
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += align256(bytes);
+    return r;
+  };
+  L.pseudo[0] = reinterpret_cast<float*>(take((size_t)n * Hc * Wc * 4));
+  L.pseudo[1] = reinterpret_cast<float*>(take((size_t)n * Hc * Wc * 4));
+  L.z = reinterpret_cast<float*>(take((size_t)n * y_stride * 4));
+  L.sigma = reinterpret_cast<double*>(take((size_t)n * (iterations + 1) * 8));
+  L.msize = reinterpret_cast<double*>(take((size_t)n * 8));
+  L.partials = reinterpret_cast<double*>(take((size_t)n * regions * 4 * 8));
+  L.counters = reinterpret_cast<unsigned int*>(take((size_t)n * 4));
+  L.badx = reinterpret_cast<unsigned long long*>(take((size_t)n * 8));
+  L.badz = reinterpret_cast<unsigned long long*>(take((size_t)n * 8));
+  return L;
+}
+
+struct IdaGeometry {
+  bool mma;
+  int rx, ry;
+  int64_t Hc, Wc, regions;
+};
+
+IdaGeometry geometry(int rows, int cols, int block) {
+  IdaGeometry G;
+  G.Hc = (int64_t)rows * block;
+  G.Wc = (int64_t)cols * block;
+  G.mma = (block == 8 || block == 16);  // tensor-core kernels (ida_mma.cu), 64x64 regions
+  const int side = G.mma ? ida_mma_region() : kRegion;
+  G.rx = (int)((G.Wc + side - 1) / side);
+  G.ry = (int)((G.Hc + side - 1) / side);
+  G.regions = (int64_t)G.rx * G.ry;
+  return G;
+}
+
+cudaError_t reset_reductions(const IdaLayout& L, int n, int32_t* diverged, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(L.counters, 0, (size_t)n * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L.badx, 0xff, (size_t)n * 8, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L.badz, 0xff, (size_t)n * 8, s);
+  if (e == cudaSuccess && diverged) e = cudaMemsetAsync(diverged, 0, (size_t)n * 2 * 4, s);
+  return e;
+}
+
+IdaParams base_params(const IdaGeometry& G, const IdaLayout& L, int rows, int cols, int n, const uint16_t* counts,
+                      const int32_t* offsets, const float* y, int64_t y_stride, double k) {
   IdaParams P{};
   P.rows = rows;
   P.cols = cols;
   P.n = n;
-  P.Hc = (int)Hc;
-  P.Wc = (int)Wc;
-  P.regions_x = rx;
-  P.regions_y = ry;
-  P.regions_per_img = (int)regions;
+  P.Hc = (int)G.Hc;
+  P.Wc = (int)G.Wc;
+  P.regions_x = G.rx;
+  P.regions_y = G.ry;
+  P.regions_per_img = (int)G.regions;
   P.counts = counts;
   P.offsets = offsets;
   P.y = y;
   P.y_stride = y_stride;
-  P.z = z;
+  P.z = L.z;
+  P.k = k;
+  P.msize = L.msize;
+  P.partials = L.partials;
+  P.counters = L.counters;
+  P.badx = L.badx;
+  P.badz = L.badz;
+  P.warm = 1;
+  P.clamp_out = 1;
+  return P;
+}
+
+void launch_one(Ctx* ctx, int block, const IdaGeometry& G, const IdaParams& P, cudaStream_t s) {
+  const dim3 grid((unsigned)G.regions, (unsigned)P.n);
+  if (G.mma) launch_ida_mma_kernel(block, P, grid, s);
+  else if (P.is_init) ida_init_kernel<32><<<grid, kIdaThreads, 0, s>>>(P);
+  else ida_step_kernel<32><<<grid, kIdaThreads, 0, s>>>(P);
+  ctx->launches++;
+}
+
+}  // namespace
+
+int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts, const int32_t* offsets,
+               const float* y, int64_t y_stride, int32_t n, const abcs_ida_config& cfg, const uint8_t* ref,
+               int64_t ref_stride, int32_t ref_pitch, float* out, int64_t out_stride, int32_t out_pitch,
+               double* trace, int32_t* diverged, void* scratch, cudaStream_t s) {
+  if (block != 8 && block != 16 && block != 32)
+    return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "IDA batch limited to 65535 images per call");
+  const IdaGeometry G = geometry(rows, cols, block);
+  const IdaLayout L = carve(scratch, G.Hc, G.Wc, y_stride, n, cfg.iterations, G.regions);
+  cudaError_t e = reset_reductions(L, n, diverged, s);
+  if (e != cudaSuccess) return cuda_status(e, "ida scratch init");
+  IdaParams P = base_params(G, L, rows, cols, n, counts, offsets, y, y_stride, cfg.k);
   P.out_stride = out_stride;
   P.out_pitch = out_pitch;
   P.ref = ref;
   P.ref_stride = ref_stride;
   P.ref_pitch = ref_pitch;
-  P.k = cfg.k;
-  P.msize = msize;
-  P.partials = partials;
-  P.counters = counters;
   P.trace = trace;
   P.trace_rows = cfg.iterations + 1;
   P.diverged = diverged;
-  P.badx = badx;
-  P.badz = badz;
-  const dim3 grid((unsigned)regions, (unsigned)n);
-  if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "IDA batch limited to 65535 images per call");
-  auto launch = [&](auto kern) {
-    if (mma) launch_ida_mma_kernel(block, P, grid, s);
-    else kern<<<grid, kIdaThreads, 0, s>>>(P);
-    ctx->launches++;
-  };
-  auto init = [&](auto kern) {
-    P.is_init = 1;
-    P.onsager = 0.f;
-    P.pseudo_in = nullptr;
-    P.pseudo_out = pseudo[0];
-    P.x_out = nullptr;
-    P.sigma_in = nullptr;
-    P.sigma_out = sigma;
-    P.trace_row = 0;
-    P.iteration = 0;
-    launch(kern);
-  };
-  auto step = [&](auto kern, int t) {
+  // warm start (init_state, recon.cpp:119-131) -> pseudo_0
+  P.is_init = 1;
+  P.onsager = 0.f;
+  P.pseudo_out = L.pseudo[0];
+  P.sigma_out = L.sigma;
+  P.trace_row = 0;
+  P.iteration = 0;
+  launch_one(ctx, block, G, P, s);
+  for (int t = 0; t < cfg.iterations; ++t) {  // damp_step(Ida) x iterations (recon.cpp:236-253)
     P.is_init = 0;
     P.onsager = (float)(1.0 / cfg.damping);  // IDA: onsager = 1/D_F (recon.cpp:183-184)
-    P.pseudo_in = pseudo[t & 1];
+    P.pseudo_in = L.pseudo[t & 1];
     const bool last = (t + 1 == cfg.iterations);
-    P.pseudo_out = last ? nullptr : pseudo[(t + 1) & 1];
+    P.pseudo_out = last ? nullptr : L.pseudo[(t + 1) & 1];
     P.x_out = last ? out : nullptr;
-    P.sigma_in = sigma + (int64_t)t * n;
-    P.sigma_out = sigma + (int64_t)(t + 1) * n;
+    P.sigma_in = L.sigma + (int64_t)t * n;
+    P.sigma_out = L.sigma + (int64_t)(t + 1) * n;
     P.trace_row = t + 1;
     P.iteration = t + 1;
-    launch(kern);
-  };
-  if (block == 8 || block == 16 || block == 32) {
-    init(ida_init_kernel<32>);  // the kernel argument is ignored on the tensor-core path
-    for (int t = 0; t < cfg.iterations; ++t) step(ida_step_kernel<32>, t);
-  } else {
-    return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+    launch_one(ctx, block, G, P, s);
   }
   return cuda_status(cudaGetLastError(), "ida launch");
+}
+
+// ---- explicit solver state (init_state / damp_step with variant Ida) -----------------------
+__global__ void add_field_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+size_t ida_state_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n) {
+  abcs_ida_config one{};
+  one.iterations = 1;
+  return ida_scratch_bytes(rows, cols, block, y_stride, n, one);
+}
+
+int launch_ida_state(Ctx* ctx, bool init, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
+                     const int32_t* offsets, const float* y, int64_t y_stride, int32_t n, int warm, double damping,
+                     double k, float* x, float* z, double* sigma, int32_t iteration, int32_t* diverged, void* scratch,
+                     cudaStream_t s) {
+  if (block != 8 && block != 16 && block != 32)
+    return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "IDA batch limited to 65535 images per call");
+  const IdaGeometry G = geometry(rows, cols, block);
+  const IdaLayout L = carve(scratch, G.Hc, G.Wc, y_stride, n, 1, G.regions);
+  cudaError_t e = reset_reductions(L, n, diverged, s);
+  if (e != cudaSuccess) return cuda_status(e, "ida scratch init");
+  IdaParams P = base_params(G, L, rows, cols, n, counts, offsets, y, y_stride, k);
+  P.z = z;  // the caller's residual, updated in place
+  P.x_out = x;
+  P.out_stride = G.Hc * G.Wc;
+  P.out_pitch = (int)G.Wc;
+  P.clamp_out = 0;
+  P.diverged = diverged;
+  P.pseudo_out = nullptr;  // write x, not pseudo
+  P.sigma_out = L.sigma + n;
+  P.iteration = iteration;
+  if (init) {
+    P.is_init = 1;
+    P.warm = warm;
+    P.onsager = 0.f;
+  } else {
+    // pseudo = A* z + x (pseudo_data, recon.cpp:75-79) into the scratch field
+    int st = launch_decode(ctx, rows, cols, block, counts, offsets, z, y_stride, n, L.pseudo[0], G.Hc * G.Wc,
+                           (int)G.Wc, s);
+    if (st) return st;
+    const int64_t cnt = (int64_t)n * G.Hc * G.Wc;
+    add_field_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, (int64_t)ctx->sm_count * 8), 256, 0, s>>>(
+        L.pseudo[0], x, cnt);
+    ctx->launches++;
+    P.is_init = 0;
+    P.onsager = (float)(1.0 / damping);
+    P.pseudo_in = L.pseudo[0];
+    P.sigma_in = sigma;
+  }
+  launch_one(ctx, block, G, P, s);
+  e = cudaMemcpyAsync(sigma, L.sigma + n, (size_t)n * 8, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "ida sigma copy");
+  return cuda_status(cudaGetLastError(), "ida state launch");
 }
 
 }  // namespace abcs_b200

@@ -19,7 +19,7 @@ struct IdaParams {
   float* z;                // in place
   const float* pseudo_in;  // step: pseudo_t
   float* pseudo_out;       // pseudo_{t+1} (nullptr on the last step)
-  float* x_out;            // clamped estimate on the last step
+  float* x_out;            // estimate x on the last step (clamped when clamp_out)
   int64_t out_stride;
   int out_pitch;
   const uint8_t* ref;
@@ -40,6 +40,8 @@ struct IdaParams {
   unsigned long long* badz;  // [n] min index for z
   int iteration;           // iteration number after this launch (0 for init)
   int is_init;
+  int warm;                // init: x0 = A* y (1) or x0 = 0 (0) (init_state, recon.cpp:119-131)
+  int clamp_out;           // x_out gets clamp(x, 0, 255) (reconstruct's final estimate) or raw x (damp_step state)
 };
 
 // Last CTA of an image folds the region partials (fixed order, so the result
@@ -61,13 +63,8 @@ static __device__ void finish_image(const IdaParams& P, int img, int region, con
   for (int r = 0; r < P.regions_per_img; ++r)
     for (int q = 0; q < 4; ++q) a[q] += pp[4 * r + q];
   P.counters[img] = 0;  // ready for the next launch
-  double M;
-  if (P.is_init) {
-    M = a[3];
-    P.msize[img] = M;
-  } else {
-    M = P.msize[img];
-  }
+  const double M = a[3];  // op.measurements() = sum of counts, re-summed every launch (exact in fp64)
+  if (P.is_init && P.msize) P.msize[img] = M;
   const double znorm = sqrt(a[0]);
   // init_state: sigma0 = ||y|| / sqrt(M) (recon.cpp:129); finish_step: ||z|| / sqrt(M) (:91)
   const double sigma = (P.is_init ? sqrt(a[2]) : znorm) / sqrt(M);

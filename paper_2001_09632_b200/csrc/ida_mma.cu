@@ -204,9 +204,10 @@ __device__ __forceinline__ void store_out(const IdaParams& P, int img, int gr, i
   if (P.pseudo_out) {
     float2 o = make_float2(x.x + az.x, x.y + az.y);
     *reinterpret_cast<float2*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc + (int64_t)gr * P.Wc + gc) = o;
-  } else {  // last iteration: clamp (recon.cpp:255-257)
+  } else {  // last iteration: clamp (recon.cpp:255-257), or the raw state x for damp_step
     float* d = P.x_out + (int64_t)img * P.out_stride + (int64_t)gr * P.out_pitch + gc;
-    const float o0 = fminf(fmaxf(x.x, 0.f), 255.f), o1 = fminf(fmaxf(x.y, 0.f), 255.f);
+    const float o0 = P.clamp_out ? fminf(fmaxf(x.x, 0.f), 255.f) : x.x;
+    const float o1 = P.clamp_out ? fminf(fmaxf(x.y, 0.f), 255.f) : x.y;
     if (((P.out_pitch | P.out_stride) & 1) == 0) {
       *reinterpret_cast<float2*>(d) = make_float2(o0, o1);
     } else {
@@ -475,8 +476,14 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
   if (P.is_init) {
-    if (B == 16) init_x16(P, img, R0, C0, s);
-    else init_x8(P, img, R0, C0, s);
+    if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
+      for (int i = threadIdx.x; i < kMIn * kMP / 4; i += kMThreads)
+        reinterpret_cast<float4*>(s.acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (B == 16) {
+      init_x16(P, img, R0, C0, s);
+    } else {
+      init_x8(P, img, R0, C0, s);
+    }
     __syncthreads();
   } else {
     const float thr = (float)(P.k * P.sigma_in[img]);

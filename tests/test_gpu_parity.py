@@ -330,6 +330,63 @@ def test_ida_parity(p, torch, checker, case):
         assert np.allclose(tr[i, :, 2], trace[:, 2], rtol=1e-4)
 
 
+@pytest.mark.parametrize("B", [16, 8, 32])
+def test_ida_state_api_matches_reconstruct(p, checker, B):
+    """init_state(warm) + damp_step(Ida) x T on explicit state == reconstruct(method=Ida) of the reference."""
+    H, W, iters = (96, 128, 4)
+    img = synth(H, W, n=1, seed=77 + B)[0]
+    ms = p.sense(img, p.SensingConfig(B, 1, 4, p.Algorithm.BBV if B != 32 else p.Algorithm.DD))
+    want = checker.sense(img, B, 1, 4, 1 if B != 32 else 2)
+    x_ref, trace = checker.reconstruct_ida(ms.grid().rows, ms.grid().cols, B, want["counts"], want["coeffs"], iters,
+                                           ref=img)
+    op = p.SensingOperator.from_ms(ms)
+    st = p.init_state(op, ms.coeffs, True)
+    assert st.iteration == 0
+    assert st.sigma == pytest.approx(trace[0, 2], rel=1e-5)
+    spec = p.DenoiserSpec("dct_threshold", {"k": 2.7})
+    for t in range(iters):
+        p.damp_step(st, op, ms.coeffs, spec, p.ReconMethod.Ida, 2.0)
+        assert st.iteration == t + 1
+        assert st.sigma == pytest.approx(trace[t + 1, 2], rel=1e-4)
+    x = np.clip(st.x.reshape(x_ref.shape), 0, 255)
+    assert np.max(np.abs(x - x_ref)) <= PIXEL_TOL
+    assert np.linalg.norm(st.z) == pytest.approx(trace[iters, 1], rel=1e-4)
+
+
+def test_ida_state_cold_start_and_divergence(p):
+    z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"])
+    op = p.SensingOperator.from_ms(ms)
+    st = p.init_state(op, ms.coeffs, False)                 # x0 = 0, z0 = y (recon.cpp:124-128)
+    assert not np.any(st.x)
+    assert np.array_equal(st.z, ms.coeffs.astype(np.float32))
+    y = ms.coeffs.astype(np.float64)
+    assert st.sigma == pytest.approx(np.linalg.norm(y) / np.sqrt(y.size), rel=1e-6)
+    with pytest.raises(ValueError):
+        p.init_state(op, ms.coeffs[:-1], True)
+    with pytest.raises(ValueError):
+        p.damp_step(st, op, ms.coeffs, p.DenoiserSpec(), p.ReconMethod.Ista, 2.0)
+    with pytest.raises(p.UnsupportedError):
+        p.damp_step(st, op, ms.coeffs, p.DenoiserSpec(), p.ReconMethod.Damp, 2.0)
+    big = ms.coeffs * 1e7
+    sb = p.init_state(op, big, True)
+    with pytest.raises(p.DivergenceError) as e:
+        p.damp_step(sb, op, big, p.DenoiserSpec(), p.ReconMethod.Ida, 2.0)
+    assert e.value.iteration == 1 and sb.iteration == 1
+
+
+def test_reconstruct_idct_trace_psnr(p, checker):
+    img = synth(100, 90, n=1, seed=5)[0]                     # ragged crop: 96 x 80
+    ms = p.sense(img, p.SensingConfig(16, 1, 4, p.Algorithm.DD))
+    res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Idct), reference=img)
+    assert len(res.trace) == 1 and res.trace[0].iteration == 0
+    want = checker.decode(ms.grid().rows, ms.grid().cols, 16, ms.counts, ms.coeffs.astype(np.float64))
+    assert np.max(np.abs(res.image - want)) <= PIXEL_TOL
+    assert abs(res.trace[0].psnr_db - psnr(img[:96, :80], want)) <= PSNR_TOL
+    full = p.sense(img, p.SensingConfig(16, 1, 1, p.Algorithm.ZZ))
+    assert p.reconstruct(full, p.ReconConfig(p.ReconMethod.Idct), reference=img).trace[0].psnr_db > 100
+
+
 def test_ida_divergence(p):
     z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
     ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"] * 1e7)
