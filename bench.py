@@ -115,6 +115,17 @@ def dist_setup(args):
     return world, rank, local
 
 
+def shard(rank, per_rank):
+    """Global image indices [first, first + per_rank) of this rank: each rank senses its own
+    images of one global seeded dataset; no data moves between ranks."""
+    return rank * per_rank, per_rank
+
+
+def aggregate_rate(units_per_rank, world, seconds_max):
+    """Whole-job throughput: the units all ranks processed / the slowest rank's time."""
+    return world * units_per_rank / seconds_max
+
+
 def max_over_ranks(v, world, device=None):
     if world == 1:
         return v
@@ -152,6 +163,19 @@ def cpu_sample(checker, imgs, threads):
     return time.perf_counter() - t0, px
 
 
+CPU_TARGET_CORE_S = 20.0  # bounded CPU sample: ~10-30 s of CPU work (core-seconds)
+
+
+def calibrated_count(checker, imgs, threads, cap):
+    """Images per CPU sample so one sample is ~CPU_TARGET_CORE_S core-seconds (a multiple of threads)."""
+    n0 = min(len(imgs), threads)
+    sec, _ = cpu_sample(checker, imgs[:n0], threads)  # also the warm-up
+    per_img = sec * min(threads, n0) / n0  # core-seconds per image (all subrates)
+    n = int(CPU_TARGET_CORE_S / max(per_img, 1e-6))
+    n = max(threads, (n // threads) * threads)
+    return min(n, cap)
+
+
 def sample_images(n):
     import paper_2001_09632_b200 as p
     return p.synth_images_host(p.SynthSpec(CFG2["H"], CFG2["W"], CFG2["ellipses"], CFG2["sigma"], CFG2["seed"]), 0, n)
@@ -170,9 +194,9 @@ def run_reference(args, world, rank):
         return 0
     checker, kind = get_checker()
     threads = host_cores()
-    n = max(2 * threads, 8)
+    n = calibrated_count(checker, sample_images(threads), threads, cap=1024)
     imgs = sample_images(n)
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup - 1, 0)):
         cpu_sample(checker, imgs[: min(n, threads)], threads)
     times, px = [], 0
     for _ in range(args.steps):
@@ -207,7 +231,8 @@ def run_ours(args, world, rank, local):
     hbm, peak_src = peaks()
     n = CFG2["n"]
     spec = p.SynthSpec(CFG2["H"], CFG2["W"], CFG2["ellipses"], CFG2["sigma"], CFG2["seed"])
-    imgs = p.synth_images(spec, rank * n, n, device=local)  # disjoint global indices per rank
+    first, n = shard(rank, n)
+    imgs = p.synth_images(spec, first, n, device=local)  # disjoint global indices per rank
     cfgs = [p.SensingConfig(CFG2["B"], num, den, p.Algorithm.DD) for num, den in SUBRATES]
     plans = [p.sense_plan(c, CFG2["H"], CFG2["W"]) for c in cfgs]
     # outputs allocated once: payload/counts/offsets per subrate + decoded images
@@ -251,7 +276,7 @@ def run_ours(args, world, rank, local):
     ms_max = max_over_ranks(ms, world, dev)
     ms_step = ms_max / args.steps
     px_step = nsub * n * CFG2["H"] * CFG2["W"]
-    value = world * px_step * args.steps / (ms_max / 1e3) / 1e6
+    value = aggregate_rate(px_step * args.steps, world, ms_max / 1e3) / 1e6
 
     # unfused split (sense_batch, then decode_batch from the payload) for the per-kernel roofline
     s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -308,7 +333,7 @@ def run_ours(args, world, rank, local):
         if it > 0:
             e2e_times.append(dt)
     e2e_s = max_over_ranks(float(np.mean(e2e_times)), world, dev)
-    e2e_value = world * px_step / e2e_s / 1e6
+    e2e_value = aggregate_rate(px_step, world, e2e_s) / 1e6
     h2d = len(SUBRATES) * n * N
     d2h = len(SUBRATES) * n * N * 4
 
@@ -319,12 +344,12 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         checker, kind = get_checker()
         threads = host_cores()
-        ns = max(threads, 8)
+        ns = calibrated_count(checker, imgs[:threads].cpu().numpy(), threads, cap=imgs.shape[0])
         himgs = imgs[:ns].cpu().numpy()
-        cpu_sample(checker, himgs[: min(ns, threads)], threads)  # warm
         sec, pxs = cpu_sample(checker, himgs, threads)
         cpu = {"value": round(pxs / sec / 1e6, 3), "unit": "MP/s", "cores": threads, "kind": kind,
-               "sample": f"{ns} of this rank's cfg2 images x subrates {{0.1,0.3,0.5}} ({sec:.2f} s wall)"}
+               "sample": f"{ns} of this rank's cfg2 images x subrates {{0.1,0.3,0.5}} "
+                         f"({sec:.2f} s wall, ~{sec * threads:.0f} core-s)"}
 
     if rank == 0:
         line = {
@@ -354,7 +379,8 @@ def run_ours(args, world, rank, local):
 def run_ida(p, torch, local, rank, hbm, world, dev):
     c = CFG4
     spec = p.SynthSpec(c["H"], c["W"], c["ellipses"], c["sigma"], c["seed"])
-    imgs = p.synth_images(spec, rank * c["n"], c["n"], device=local)
+    first, cnt = shard(rank, c["n"])
+    imgs = p.synth_images(spec, first, cnt, device=local)
     cfg = p.SensingConfig(c["B"], c["num"], c["den"], p.Algorithm.BBV)
     b = p.sense_batch(imgs, cfg)
     rc = p.ReconConfig(p.ReconMethod.Ida, iterations=c["iters"])
