@@ -36,6 +36,15 @@ CFG2 = dict(H=512, W=512, B=16, n=1024, ellipses=20, sigma=5.0, seed=2)
 CFG4 = dict(H=512, W=512, B=16, n=64, ellipses=20, sigma=5.0, seed=4, num=3, den=10, iters=10)
 
 
+def load_traffic():
+    """DRAM bytes per image of the hot kernels from the committed ncu --set full capture summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -262,6 +271,7 @@ def run_ours(args, world, rank, local):
         clocks.start()
     launches0 = ctx.launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.kernel_timing(True)  # per-kernel CUDA events on the launching streams (read after the region)
     torch.cuda.synchronize()
     start.record(stream)
     for k in range(args.steps):
@@ -269,6 +279,23 @@ def run_ours(args, world, rank, local):
     end.record(stream)
     torch.cuda.synchronize()
     launches = ctx.launches() - launches0
+    ktimes_conc = ctx.kernel_times()
+    ctx.kernel_timing(False)
+    # The timed region pipelines each batch over 3 streams, so concurrent kernels stretch each
+    # other's event times. The per-kernel roofline therefore comes from a serialised pass of the
+    # same steps (1 stream) right after it; kernel shares of that pass are the ncu-comparable ones.
+    ctx.set_pipeline_streams(1)
+    ctx.kernel_timing(True)
+    ser0, ser1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ser0.record(stream)
+    for k in range(args.steps):
+        step(None)
+    ser1.record(stream)
+    torch.cuda.synchronize()
+    ktimes = ctx.kernel_times()
+    ctx.kernel_timing(False)
+    ctx.set_pipeline_streams(3)
+    ser_step_ms = ser0.elapsed_time(ser1) / args.steps
     clk = clocks.stop() if clocks else None
     barrier(world)
     sub_ms = [sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps for j in range(nsub)]
@@ -278,41 +305,46 @@ def run_ours(args, world, rank, local):
     px_step = nsub * n * CFG2["H"] * CFG2["W"]
     value = aggregate_rate(px_step * args.steps, world, ms_max / 1e3) / 1e6
 
-    # unfused split (sense_batch, then decode_batch from the payload) for the per-kernel roofline
-    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    sense_ms, decode_ms = [0.0] * nsub, [0.0] * nsub
-    reps = max(1, min(args.steps, 5))
-    for _ in range(reps):
-        for j, (c, pl, b) in enumerate(zip(cfgs, plans, batches)):
-            s_ev[0].record(stream)
-            p.sense_batch(imgs, c, pl, out=b)
-            s_ev[1].record(stream)
-            p.decode_batch(b, out=outs[j])
-            s_ev[2].record(stream)
-            torch.cuda.synchronize()
-            sense_ms[j] += s_ev[0].elapsed_time(s_ev[1]) / reps
-            decode_ms[j] += s_ev[1].elapsed_time(s_ev[2]) / reps
-
-    # algorithmic bytes, per image: sense = N + 4K + 2nB ; decode = 4K + 2nB + 4N
+    # per-kernel roofline from the library's CUDA events (launching streams) over the timed region:
+    # algorithmic bytes per image of each kernel of the fused DD step
     N = CFG2["H"] * CFG2["W"]
+    Ks = [pl.coeffs_per_image for pl in plans]
+    nB = plans[0].n_blocks
+    alg_bytes = {  # per step (all subrates)
+        "sense16_gather_decode": sum(n * (N + 4 * K + 6 * nB + 4 * N) for K in Ks),  # u8 in, payload+counts/offsets, f32 out
+        "sense16_weights": nsub * n * (N + 4 * nB),                                    # u8 in, n_i out
+        "alloc_warp": nsub * n * (4 * nB + 6 * nB),                                    # n_i in, counts+offsets out
+    }
+    kt = {k: v for k, v in ktimes.items()}
+    dom = max(kt, key=lambda k: kt[k][1]) if kt else None
+    roof = None
+    if dom is not None:
+        launches_k, total_ms, _ = kt[dom]
+        per_step_ms = total_ms / args.steps
+        lps = launches_k / args.steps
+        bytes_step = alg_bytes.get(dom)
+        ach = bytes_step / (per_step_ms / 1e3) / 1e9 if bytes_step else None
+        traffic = None
+        tr = load_traffic().get(dom)
+        if tr and bytes_step:
+            traffic = round(tr["dram_bytes_per_image"] * (nsub * n / lps))
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1) if ach else None, "peak": hbm,
+                "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / hbm, 4) if ach else None,
+                "traffic": traffic, "algorithmic_bytes_per_launch": round(bytes_step / lps) if bytes_step else None,
+                "avg_launch_ms": round(total_ms / launches_k, 4), "launches_per_step": lps,
+                "share_of_step": round(per_step_ms / ser_step_ms, 4), "measured_on": "serialised pass (1 stream)",
+                "traffic_source": tr.get("source") if tr else None}
+    kernels = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 4),
+                   "share_of_step": round(v[1] / args.steps / ser_step_ms, 4),
+                   "concurrent_ms_per_step": round(ktimes_conc.get(k, (0, 0.0, 0))[1] / args.steps, 4),
+                   "achieved_gbs": (round(alg_bytes[k] / (v[1] / args.steps / 1e3) / 1e9, 1) if k in alg_bytes
+                                    else None)} for k, v in kt.items()}
     per_j = []
-    for j, pl in enumerate(plans):
-        K, nB = pl.coeffs_per_image, pl.n_blocks
-        sense_b = n * (N + 4 * K + 2 * nB)
-        dec_b = n * (4 * K + 2 * nB + 4 * N)
-        per_j.append(dict(subrate=f"{SUBRATES[j][0]}/{SUBRATES[j][1]}", K=K, fused_ms=round(sub_ms[j], 4),
-                          fused_frac=round((sense_b + dec_b) / (sub_ms[j] / 1e3) / 1e9 / hbm, 4),
-                          unfused_sense_ms=round(sense_ms[j], 4), unfused_decode_ms=round(decode_ms[j], 4),
-                          sense_bytes=sense_b, decode_bytes=dec_b))
-    dec_bytes = sum(x["decode_bytes"] for x in per_j)
-    sen_bytes = sum(x["sense_bytes"] for x in per_j)
-    dec_ms, sen_ms = sum(decode_ms), sum(sense_ms)
-    if dec_ms >= sen_ms:
-        dominant, ach, traffic_alg = "decode16_kernel", dec_bytes / (dec_ms / 1e3) / 1e9, dec_bytes / nsub
-    else:
-        dominant, ach, traffic_alg = "sense (dd pass 1 + allocation + gather)", sen_bytes / (sen_ms / 1e3) / 1e9, \
-            sen_bytes / nsub
-    pipe_ach = (dec_bytes + sen_bytes) / (sum(sub_ms) / 1e3) / 1e9
+    for j, K in enumerate(Ks):
+        b_j = n * (N + 4 * K + 2 * nB) + n * (4 * K + 2 * nB + 4 * N)
+        per_j.append(dict(subrate=f"{SUBRATES[j][0]}/{SUBRATES[j][1]}", K=K, ms=round(sub_ms[j], 4),
+                          algorithmic_bytes=b_j, frac=round(b_j / (sub_ms[j] / 1e3) / 1e9 / hbm, 4)))
+    pipe_ach = sum(x["algorithmic_bytes"] for x in per_j) / (sum(sub_ms) / 1e3) / 1e9
 
     # e2e through the C ABI with host buffers (pinned), H2D + kernels + D2H in the timed region
     import ctypes as C
@@ -361,10 +393,10 @@ def run_ours(args, world, rank, local):
                        "global_batch": world * n, "l2": "inputs+outputs >> L2 (no flush needed)",
                        "parallelism": f"dp{world} (independent images, no collective)"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": hbm,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                         "algorithmic_bytes_per_launch": int(traffic_alg), "traffic": None},
-            "pipeline_roofline": {"what": "fused sense+decode step vs algorithmic bytes (SURVEY 8d)",
+            "roofline": roof,
+            "kernels": kernels,
+            "serialised_ms_per_step": round(ser_step_ms, 3),
+            "pipeline_roofline": {"what": "whole fused step vs its algorithmic bytes (SURVEY 8d)",
                                   "achieved": round(pipe_ach, 1), "frac": round(pipe_ach / hbm, 4), "phases": per_j},
             "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
@@ -390,23 +422,39 @@ def run_ida(p, torch, local, rank, hbm, world, dev):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 5
+    ctx = p.Context.get(local)
+    ctx.kernel_timing(True)
     s.record()
     for _ in range(reps):
         p.ida_batch(b, rc, out=out, trace=False, check=False)
     e.record()
     torch.cuda.synchronize()
+    kt = ctx.kernel_times()
+    ctx.kernel_timing(False)
     ms = max_over_ranks(s.elapsed_time(e) / reps, world, dev)
     N, K = c["H"] * c["W"], b.plan.coeffs_per_image
     per_iter = c["n"] * (8 * N + 12 * K)
     init = c["n"] * (8 * K + 4 * N)
     alg = per_iter * c["iters"] + init
     ach = alg / (ms / 1e3) / 1e9
+    step_roof = None
+    if "ida_step" in kt:  # the dominant kernel: one launch per iteration
+        launches_k, total_ms, _ = kt["ida_step"]
+        avg = total_ms / launches_k
+        a_k = per_iter / (avg / 1e3) / 1e9
+        tr = load_traffic().get("ida_step")
+        step_roof = {"kernel": "ida_step (ida_mma_kernel<16>)", "bound": "hbm", "achieved": round(a_k, 1),
+                     "peak": hbm, "unit": "GB/s", "frac": round(a_k / hbm, 4), "avg_launch_ms": round(avg, 4),
+                     "algorithmic_bytes_per_launch": int(per_iter),
+                     "traffic": round(tr["dram_bytes_per_image"] * c["n"]) if tr else None,
+                     "share_of_batch": round(total_ms / reps / ms, 4)}
     return {"metric": "IDA image-iterations/s (cfg4: 64 x 512^2, BBV 0.3, 10 it, dct_threshold)",
             "value": round(world * c["n"] * c["iters"] / (ms / 1e3), 1), "unit": "it/s",
             "mp_it_per_s": round(world * c["n"] * c["iters"] * N / (ms / 1e3) / 1e6, 1),
             "ms_per_batch": round(ms, 3),
             "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(ach / hbm, 4), "algorithmic_bytes": int(alg)}}
+                         "frac": round(ach / hbm, 4), "algorithmic_bytes": int(alg)},
+            "kernel_roofline": step_roof}
 
 
 def main():

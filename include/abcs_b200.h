@@ -125,6 +125,23 @@ int abcs_ctx_destroy(abcs_ctx* ctx);
 /* number of kernels this ctx has launched (for bench's gpu_launches claim) */
 int64_t abcs_ctx_launch_count(const abcs_ctx* ctx);
 
+/* Opt-in per-kernel timing: with timing enabled the ctx records a CUDA event pair on
+ * the launching stream around each hot kernel; abcs_ctx_kernel_times synchronizes the
+ * device and returns per-kernel-name launch counts and summed/max durations (first-seen
+ * order, at most `capacity` entries; *count = number of names). Enabling clears. */
+typedef struct {
+  char name[48];
+  int64_t launches;
+  double total_ms;
+  double max_ms;
+} abcs_kernel_time;
+int abcs_ctx_kernel_timing(abcs_ctx* ctx, int32_t enable);
+/* Batch calls split into up to `streams` chunks run on the ctx's pipeline streams so the
+ * latency-bound phases of one chunk overlap the bandwidth-bound phases of another
+ * (default 3; 1 = one stream, kernels serialised). */
+int abcs_ctx_set_pipeline_streams(abcs_ctx* ctx, int32_t streams);
+int abcs_ctx_kernel_times(abcs_ctx* ctx, abcs_kernel_time* out, int32_t capacity, int32_t* count);
+
 /* ---- host-side logic (no GPU needed) -------------------------------------- */
 /* SensingConfig::parse_ratio (sensing.cpp:46-80) */
 int abcs_parse_ratio(const char* text, uint32_t* num, uint32_t* den);

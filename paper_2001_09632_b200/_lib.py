@@ -63,6 +63,10 @@ class SynthSpecC(C.Structure):
     ]
 
 
+class KernelTimeC(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("total_ms", C.c_double), ("max_ms", C.c_double)]
+
+
 P = C.c_void_p
 I32, I64, U32, U64, D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 
@@ -73,6 +77,9 @@ SIGNATURES = {
     "abcs_ctx_create": (C.c_int, [C.c_int, C.POINTER(P)]),
     "abcs_ctx_destroy": (C.c_int, [P]),
     "abcs_ctx_launch_count": (I64, [P]),
+    "abcs_ctx_kernel_timing": (C.c_int, [P, I32]),
+    "abcs_ctx_set_pipeline_streams": (C.c_int, [P, I32]),
+    "abcs_ctx_kernel_times": (C.c_int, [P, C.POINTER(KernelTimeC), I32, C.POINTER(I32)]),
     "abcs_parse_ratio": (C.c_int, [C.c_char_p, C.POINTER(U32), C.POINTER(U32)]),
     "abcs_dd_threshold": (D, [I32, U32, U32]),
     "abcs_zigzag_order": (C.c_int, [I32, P]),

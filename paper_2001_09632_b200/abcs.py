@@ -287,6 +287,23 @@ class Context:
     def launches(self) -> int:
         return int(_lib.load().abcs_ctx_launch_count(self.handle))
 
+    def set_pipeline_streams(self, streams: int) -> None:
+        """Chunked batch pipelining width (1..3; 1 serialises the kernels of a batch call)."""
+        _check(_lib.load().abcs_ctx_set_pipeline_streams(self.handle, int(streams)))
+
+    def kernel_timing(self, enable: bool) -> None:
+        """Start (clearing) or stop per-kernel CUDA-event timing on this context."""
+        _check(_lib.load().abcs_ctx_kernel_timing(self.handle, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        """{kernel name: (launches, total_ms, max_ms)} recorded since kernel_timing(True); synchronizes."""
+        cap = 64
+        buf = (_lib.KernelTimeC * cap)()
+        cnt = C.c_int32()
+        _check(_lib.load().abcs_ctx_kernel_times(self.handle, buf, cap, C.byref(cnt)))
+        return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms), float(buf[i].max_ms))
+                for i in range(min(cnt.value, cap))}
+
 
 def _torch():
     import torch

@@ -585,6 +585,7 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
     uint32_t* gscr = reinterpret_cast<uint32_t*>(scratch);  // n_vectors * n_blocks * 2 u16
     const size_t smem_in = class_smem_bytes(wmax, n_blocks, true);
     const size_t smem_out = class_smem_bytes(wmax, n_blocks, false);
+    const int kt = ktimer_begin(ctx, s, "alloc_class");
     if (smem_in <= 56 * 1024) {  // keep >= 4 CTAs per SM
       alloc_class_kernel<true><<<n_vectors, kClassThreads, smem_in, s>>>(weights, n_blocks, wmax, budget, cap, base,
                                                                          counts, offsets, status, gscr);
@@ -592,8 +593,10 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
       alloc_class_kernel<false><<<n_vectors, kClassThreads, smem_out, s>>>(weights, n_blocks, wmax, budget, cap,
                                                                            base, counts, offsets, status, gscr);
     } else {
+      ktimer_end(ctx, s, -1);
       goto generic;
     }
+    ktimer_end(ctx, s, kt);
     ctx->launches++;
     return cuda_status(cudaGetLastError(), "allocate(class) launch");
   }
@@ -608,8 +611,10 @@ generic:
   scr.alloc = reinterpret_cast<uint32_t*>(p);
   p += n * 4;
   scr.flag = reinterpret_cast<uint8_t*>(p);
+  const int kt = ktimer_begin(ctx, s, "alloc_radix");
   alloc_kernel<<<n_vectors, kAllocThreads, 0, s>>>(weights, n_blocks, budget, caps, cap, base, counts, offsets,
                                                    status, scr);
+  ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "allocate launch");
 }

@@ -93,12 +93,59 @@ int abcs_ctx_destroy(abcs_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& st : ctx->pipe)
     if (st) cudaStreamDestroy(st);
+  for (auto& e : ctx->kpool) cudaEventDestroy(e);
   delete ctx;
   return ABCS_OK;
 }
 
 int64_t abcs_ctx_launch_count(const abcs_ctx* c) {
   return c ? reinterpret_cast<const Ctx*>(c)->launches : 0;
+}
+
+int abcs_ctx_set_pipeline_streams(abcs_ctx* c, int32_t streams) {
+  CHECK_CTX(c);
+  if (streams < 1 || streams > 3) return set_error(ABCS_ERR_INVALID_ARGUMENT, "pipeline streams must be in [1, 3]");
+  reinterpret_cast<Ctx*>(c)->pipe_streams = streams;
+  return ABCS_OK;
+}
+
+int abcs_ctx_kernel_timing(abcs_ctx* c, int32_t enable) {
+  CHECK_CTX(c);
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  ctx->krecs.clear();
+  ctx->kpool_used = 0;
+  ctx->timing = enable != 0;
+  return cuda_status(e, "kernel timing");
+}
+
+int abcs_ctx_kernel_times(abcs_ctx* c, abcs_kernel_time* out, int32_t capacity, int32_t* count) {
+  CHECK_CTX(c);
+  if (!count || capacity < 0 || (capacity > 0 && !out)) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_status(e, "kernel times");
+  std::vector<abcs_kernel_time> agg;
+  for (const auto& r : ctx->krecs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.start, r.stop) != cudaSuccess) continue;
+    abcs_kernel_time* k = nullptr;
+    for (auto& a : agg)
+      if (std::strncmp(a.name, r.name, sizeof(a.name)) == 0) k = &a;
+    if (!k) {
+      agg.push_back(abcs_kernel_time{});
+      k = &agg.back();
+      std::strncpy(k->name, r.name, sizeof(k->name) - 1);
+    }
+    k->launches += 1;
+    k->total_ms += ms;
+    k->max_ms = std::max(k->max_ms, (double)ms);
+  }
+  *count = (int32_t)agg.size();
+  for (int i = 0; i < (int)agg.size() && i < capacity; ++i) out[i] = agg[i];
+  return ABCS_OK;
 }
 
 int abcs_sense_weights_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
@@ -200,9 +247,8 @@ static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_image
 static int sense_chunked(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
                          int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
                          float* d_side, cudaStream_t s, float* d_out, int64_t out_stride, int32_t out_pitch) {
-  constexpr int kStreams = 3;
   const int min_chunk = 64;
-  int nchunks = std::min<int>(kStreams, n / min_chunk);
+  int nchunks = std::min<int>(ctx->pipe_streams, n / min_chunk);
   if (nchunks < 2) {
     int st;
     char* scr = static_cast<char*>(ctx_scratch(ctx, sense_scratch_bytes(p, n, d_offsets != nullptr), s, &st));
@@ -236,6 +282,29 @@ static int sense_chunked(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_im
     if (e != cudaSuccess) return cuda_status(e, "join");
   }
   return ABCS_OK;
+}
+
+// ---- per-kernel timing -----------------------------------------------------------------
+static cudaEvent_t take_event(Ctx* ctx) {
+  if (ctx->kpool_used == ctx->kpool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    ctx->kpool.push_back(e);
+  }
+  return ctx->kpool[ctx->kpool_used++];
+}
+
+int ktimer_begin(Ctx* ctx, cudaStream_t s, const char* name) {
+  if (!ctx->timing) return -1;
+  cudaEvent_t a = take_event(ctx), b = take_event(ctx);
+  if (!a || !b) return -1;
+  cudaEventRecord(a, s);
+  ctx->krecs.push_back({name, a, b});
+  return (int)ctx->krecs.size() - 1;
+}
+
+void ktimer_end(Ctx* ctx, cudaStream_t s, int slot) {
+  if (slot >= 0) cudaEventRecord(ctx->krecs[slot].stop, s);
 }
 
 }  // namespace abcs_b200

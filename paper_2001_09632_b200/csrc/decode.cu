@@ -106,7 +106,9 @@ int launch_decode(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint16_
   if (B == 16 && out_pitch % 2 == 0 && out_stride % 2 == 0 && ((uintptr_t)out % 8) == 0 &&
       mma16_supported(rows, cols, n)) {
     return launch_decode16(ctx, rows, cols, n, counts, offsets, payload, payload_stride, out, out_stride, out_pitch, s);
-  } else if (B == 8)
+  }
+  const int kt = ktimer_begin(ctx, s, "decode");
+  if (B == 8)
     decode_kernel<8><<<grid, kDecodeThreads, 0, s>>>(rows, cols, n, counts, offsets, payload, payload_stride, out,
                                                      out_stride, out_pitch, al);
   else if (B == 16)
@@ -117,6 +119,7 @@ int launch_decode(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint16_
                                                       out_stride, out_pitch, al);
   else
     return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "decode launch");
 }

@@ -439,9 +439,11 @@ IdaParams base_params(const IdaGeometry& G, const IdaLayout& L, int rows, int co
 
 void launch_one(Ctx* ctx, int block, const IdaGeometry& G, const IdaParams& P, cudaStream_t s) {
   const dim3 grid((unsigned)G.regions, (unsigned)P.n);
+  const int kt = ktimer_begin(ctx, s, P.is_init ? "ida_init" : "ida_step");
   if (G.mma) launch_ida_mma_kernel(block, P, grid, s);
   else if (P.is_init) ida_init_kernel<32><<<grid, kIdaThreads, 0, s>>>(P);
   else ida_step_kernel<32><<<grid, kIdaThreads, 0, s>>>(P);
+  ktimer_end(ctx, s, kt);
   ctx->launches++;
 }
 

@@ -519,12 +519,14 @@ int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t s
   for (int done = 0; done < n;) {
     const int cnt = std::min(n - done, 65535);
     const dim3 grid(rx * ry, cnt);
+    const int kt = ktimer_begin(ctx, s, "denoise");
     if (vec)
       denoise_mma_kernel<true><<<grid, kMThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
                                                            thresholds_dev + done, out + (int64_t)done * stride, rx);
     else
       denoise_mma_kernel<false><<<grid, kMThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
                                                             thresholds_dev + done, out + (int64_t)done * stride, rx);
+    ktimer_end(ctx, s, kt);
     ctx->launches++;
     done += cnt;
   }

@@ -1,6 +1,7 @@
 // Internal declarations shared by the host entry points (capi.cu, plan.cpp)
 // and the kernel translation units.
 #pragma once
+#include <vector>
 #include <cstdint>
 #include <string>
 
@@ -27,8 +28,22 @@ struct Ctx {
   void* pipe_buf = nullptr;  // abcs_sense_decode_host slot buffers
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   size_t pipe_bytes = 0;
-  // pinned staging for abcs_sense_decode_host is caller-provided; nothing here
+  // opt-in per-kernel CUDA-event timing (abcs_ctx_kernel_timing): events recorded on the
+  // launching stream around each hot kernel, drained by abcs_ctx_kernel_times
+  struct KRec {
+    const char* name;
+    cudaEvent_t start, stop;
+  };
+  int pipe_streams = 3;  // abcs_ctx_set_pipeline_streams: chunked batch pipelining width (1 = serial)
+  bool timing = false;
+  std::vector<KRec> krecs;
+  std::vector<cudaEvent_t> kpool;
+  size_t kpool_used = 0;
 };
+
+// Kernel timing brackets (no-ops unless timing is enabled on the ctx).
+int ktimer_begin(Ctx* ctx, cudaStream_t s, const char* name);
+void ktimer_end(Ctx* ctx, cudaStream_t s, int slot);
 
 // Stream-ordered scratch owned by the ctx (grows; never shrinks).
 void* ctx_scratch(Ctx* ctx, size_t bytes, cudaStream_t stream, int* status);

@@ -480,27 +480,42 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
   A.out_stride = out_stride;
   A.out_pitch = out_pitch;
   const unsigned grid = grid_for(ctx, G.total_runs);
+  int kt;
   switch (mode) {
     case 1:
+      kt = ktimer_begin(ctx, s, "sense16_weights");
       if (phase1 <= 36)  // zigzag prefix of <= 36 entries lives in columns 0..7
         sense16_kernel<true, false, false, true><<<grid, kM16Threads, 0, s>>>(G, A);
       else
         sense16_kernel<true, false, false><<<grid, kM16Threads, 0, s>>>(G, A);
+      ktimer_end(ctx, s, kt);
       ctx->launches++;
+      kt = ktimer_begin(ctx, s, "dd_fixup16");
       dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1, T, A.fix_list,
                                                                A.fix_count, A.fix_cap, A.fix_flag, G.nb * (uint32_t)n,
                                                                weights);
-      ctx->launches++;
+      ktimer_end(ctx, s, kt);
       if (fa) {  // allocation: one warp per image (warp_alloc.cuh)
+        ctx->launches++;
         const int warps_per_cta = 4;
+        kt = ktimer_begin(ctx, s, "alloc_warp");
         alloc_warp_kernel<<<(n + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta,
                             warps_per_cta * sizeof(WarpAllocSmem), s>>>(weights, (int)G.nb, n, fa->wmax, fa->budget,
                                                                          fa->cap, fa->base, fa->counts, fa->offsets,
                                                                          fa->status);
+        ktimer_end(ctx, s, kt);
       }
       break;
-    case 2: sense16_kernel<false, true, false><<<grid, kM16Threads, 0, s>>>(G, A); break;
-    case 3: sense16_kernel<false, true, true><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    case 2:
+      kt = ktimer_begin(ctx, s, "sense16_gather");
+      sense16_kernel<false, true, false><<<grid, kM16Threads, 0, s>>>(G, A);
+      ktimer_end(ctx, s, kt);
+      break;
+    case 3:
+      kt = ktimer_begin(ctx, s, "sense16_gather_decode");
+      sense16_kernel<false, true, true><<<grid, kM16Threads, 0, s>>>(G, A);
+      ktimer_end(ctx, s, kt);
+      break;
     default: return set_error(ABCS_ERR_LOGIC, "bad sense16 mode");
   }
   ctx->launches++;
@@ -513,8 +528,10 @@ int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts,
   const Grid16 G = make_grid16(rows, cols, n);
   const uint32_t total = G.nb * (uint32_t)n;
   if (total == 0) return ABCS_OK;
+  const int kt = ktimer_begin(ctx, s, "decode16");
   decode16_kernel<<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, total, counts, offsets, payload,
                                                                       payload_stride, out, out_stride, out_pitch);
+  ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "decode16 launch");
 }

@@ -196,9 +196,11 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
   if (p.algorithm_used == ABCS_ALGO_BBV) {
     const int threads = 256;
     const int64_t grid = (total + threads - 1) / threads;
+    const int kt = ktimer_begin(ctx, s, "bbv_weights");
     bbv_weights_kernel<<<(unsigned)grid, threads, 0, s>>>(imgs, img_stride, pitch, p.rows, p.cols, n, p.block,
                                                           (int)p.bbv_stride, p.bbv_offset, p.bbv_per_side,
                                                           p.bbv_valid_probes, weights, side, p.side_per_image);
+    ktimer_end(ctx, s, kt);
   } else if (p.algorithm_used == ABCS_ALGO_DD && p.block == 16 && mma16_supported(p.rows, p.cols, n)) {
     return launch_sense16(ctx, 1, p.rows, p.cols, n, imgs, img_stride, pitch, p.dd_phase1, p.threshold, weights,
                           nullptr, nullptr, nullptr, 0, nullptr, 0, 0, s, fix_scratch);
@@ -207,6 +209,7 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
     const int B = p.block;
     const int64_t groups_per_cta = kGatherThreads / B;
     const int64_t grid = (total + groups_per_cta - 1) / groups_per_cta;
+    const int kt = ktimer_begin(ctx, s, "dd_weights");
     if (B == 8)
       dd_weights_kernel<8><<<(unsigned)grid, kGatherThreads, 0, s>>>(imgs, img_stride, pitch, p.rows, p.cols, n, al,
                                                                      p.dd_phase1, p.threshold, weights);
@@ -218,6 +221,7 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
                                                                        p.dd_phase1, p.threshold, weights);
     else
       return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+    ktimer_end(ctx, s, kt);
   } else {
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "zz sensing has no phase-1 weights");
   }
@@ -246,7 +250,9 @@ int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint8_t
   if (imgs && B == 16 && mma16_supported(rows, cols, n)) {
     return launch_sense16(ctx, 2, rows, cols, n, imgs, img_stride, pitch, 0, 0.0, nullptr, counts, offsets, payload,
                           payload_stride, nullptr, 0, 0, s);
-  } else if (imgs) {
+  }
+  const int kt = ktimer_begin(ctx, s, "gather");
+  if (imgs) {
     const bool al = aligned_rows(imgs, img_stride, pitch, B);
     if (B == 8)
       gather_kernel<8, uint8_t><<<grid, kGatherThreads, 0, s>>>(imgs, img_stride, pitch, rows, cols, n, al, counts,
@@ -273,6 +279,7 @@ int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint8_t
     else
       return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
   }
+  ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "gather launch");
 }

@@ -9,6 +9,7 @@ import paper_2001_09632_b200 as p  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 imgs = p.synth_images(p.SynthSpec(512, 512, 20, 5.0, 2), 0, 1024)
+p.Context.get().set_pipeline_streams(int(os.environ.get("PROF_STREAMS", "1")))  # 1: one launch = 1024 images
 if which in ("all", "cfg2"):
     for rep in range(2):
         for num, den in ((1, 10), (3, 10), (1, 2)):
