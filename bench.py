@@ -313,7 +313,7 @@ def run_ours(args, world, rank, local):
     alg_bytes = {  # per step (all subrates)
         "sense16_gather_decode": sum(n * (N + 4 * K + 6 * nB + 4 * N) for K in Ks),  # u8 in, payload+counts/offsets, f32 out
         "sense16_weights": nsub * n * (N + 4 * nB),                                    # u8 in, n_i out
-        "alloc_warp": nsub * n * (4 * nB + 6 * nB),                                    # n_i in, counts+offsets out
+        "alloc_cta": nsub * n * (4 * nB + 6 * nB),                                     # n_i in, counts+offsets out
     }
     kt = {k: v for k, v in ktimes.items()}
     dom = max(kt, key=lambda k: kt[k][1]) if kt else None

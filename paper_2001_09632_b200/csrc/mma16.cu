@@ -19,7 +19,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "mma_dct.cuh"
-#include "warp_alloc.cuh"
+#include "cta_alloc.cuh"
 
 namespace abcs_b200 {
 
@@ -410,17 +410,15 @@ dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitc
 }
 
 // largest_remainder_allocate with one warp per image (no CTA barriers).
-__global__ void __launch_bounds__(128)
-alloc_warp_kernel(const uint32_t* __restrict__ weights, int nb, int n, int wmax, long long budget, int cap, int base,
-                  uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status) {
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  const int warp = threadIdx.x >> 5;
-  const int img = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (img >= n) return;
-  WarpAllocSmem& S = reinterpret_cast<WarpAllocSmem*>(s_dyn)[warp];
-  const int st = warp_allocate(S, weights + (int64_t)img * nb, nb, wmax, budget, cap, base, counts + (int64_t)img * nb,
-                               offsets + (int64_t)img * nb);
-  if ((threadIdx.x & 31) == 0 && status) status[img] = st;
+// Allocation for the fused DD path: one CTA per image (cta_alloc.cuh).
+__global__ void __launch_bounds__(kCtaAllocThreads)
+alloc_cta_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, long long budget, int cap, int base,
+                 uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status) {
+  __shared__ CtaAllocSmem S;
+  const int img = blockIdx.x;
+  const int st = cta_allocate(S, weights + (int64_t)img * nb, nb, wmax, budget, cap, base, counts + (int64_t)img * nb,
+                              offsets + (int64_t)img * nb);
+  if (threadIdx.x == 0 && status) status[img] = st;
 }
 
 // ---------------------------------------------------------------------------
@@ -437,12 +435,9 @@ bool mma16_supported(int rows, int cols, int n) {
 }
 
 bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(alloc_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * sizeof(WarpAllocSmem));
-    attr = true;
-  }
-  return (int64_t)rows * cols <= kWarpAllocMaxBlocks && wmax <= kWarpAllocMaxW && mma16_supported(rows, cols, n);
+  (void)ctx;
+  return (int64_t)rows * cols <= kCtaAllocMaxBlocks && wmax <= kCtaAllocMaxW &&
+         mma16_supported(rows, cols, n);
 }
 
 int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
@@ -495,14 +490,11 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
                                                                A.fix_count, A.fix_cap, A.fix_flag, G.nb * (uint32_t)n,
                                                                weights);
       ktimer_end(ctx, s, kt);
-      if (fa) {  // allocation: one warp per image (warp_alloc.cuh)
+      if (fa) {  // allocation: one CTA per image (cta_alloc.cuh)
         ctx->launches++;
-        const int warps_per_cta = 4;
-        kt = ktimer_begin(ctx, s, "alloc_warp");
-        alloc_warp_kernel<<<(n + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta,
-                            warps_per_cta * sizeof(WarpAllocSmem), s>>>(weights, (int)G.nb, n, fa->wmax, fa->budget,
-                                                                         fa->cap, fa->base, fa->counts, fa->offsets,
-                                                                         fa->status);
+        kt = ktimer_begin(ctx, s, "alloc_cta");
+        alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa->wmax, fa->budget, fa->cap,
+                                                                   fa->base, fa->counts, fa->offsets, fa->status);
         ktimer_end(ctx, s, kt);
       }
       break;
