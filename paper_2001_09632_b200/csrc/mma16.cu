@@ -164,11 +164,15 @@ sense16_kernel(Grid16 G, Sense16Args A) {
   load_frag16(f);
   // The forward runs transposed (Y^T = C X^T C^T): D slot s holds Y[dslot_col(s)][dslot_row(s)].
   uint32_t rank_d[8];
-  unsigned in_p1 = 0;  // D slots inside the phase-1 zigzag prefix
+  float thr_hi[kWeights ? 8 : 1], thr_lo[kWeights ? 8 : 1];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
-    if ((int)rank_d[s] < A.phase1) in_p1 |= 1u << s;
+    if constexpr (kWeights) {
+      const bool in = (int)rank_d[s] < A.phase1;
+      thr_hi[s] = in ? A.Tf + A.band : INFINITY;
+      thr_lo[s] = in ? A.Tf - A.band : INFINITY;
+    }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* st = s_stage[warp];
@@ -193,47 +197,51 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       const int bc0 = bcf + 2 * p;
       const bool two = 2 * p + 1 < nblk;
       __syncwarp();
-      reinterpret_cast<uint4*>(st)[lane] = nxt;
+      reinterpret_cast<uint4*>(st)[lane] = interleave_row16(nxt);
       __syncwarp();
       if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
       uint32_t bx[2][2][2];
-      u8_bfragT(st, bx[0]);
-      u8_bfragT(st + 256, bx[1]);
+      u8_bfragT_il(st, bx[0]);
+      u8_bfragT_il(st + 256, bx[1]);
       Acc16 Y[2];  // Y^T of each block
       if constexpr (kLowCols) dct16_fwd_exact_x2_lo(f, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
       if constexpr (kWeights) {
-        // phase-1 test on the zigzag-ordered prefix: Y -> smem at rank, lane k tests coefficient k
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-          for (int s = 0; s < 8; ++s) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
-        __syncwarp();
+        // phase-1 test in registers: slot s is in the prefix iff rank_d[s] < phase1 (thresholds
+        // pre-masked to +inf outside it); counts reduce across the warp. A coefficient within the
+        // MMA error band of T is neither counted nor dropped: dd_fixup16_kernel decides it in fp64.
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           if (q == 1 && !two) break;
-          int sig = 0;
-#pragma unroll 1
-          for (int k0 = 0; k0 < A.phase1; k0 += 32) {
-            const int k = k0 + lane;
-            const bool in = k < A.phase1;
-            const float a = in ? fabsf(zb0[kWbuf * q + k]) : 0.f;
-            const bool clear_hi = in && a >= A.Tf + A.band;
-            const bool near = in && !clear_hi && a > A.Tf - A.band;
-            sig += __popc(__ballot_sync(0xffffffffu, clear_hi));
-            if (near) {  // rare: within the MMA error band of T; dd_fixup16_kernel decides in fp64
+          int cnt = 0;
+          bool nr = false;
+#pragma unroll
+          for (int s = 0; s < (kLowCols ? 2 : 8); ++s) {
+            const float a = fabsf(Y[q].v[s >> 2][s & 3]);
+            const bool hi = a >= thr_hi[s];
+            cnt += hi ? 1 : 0;
+            nr |= !hi && a > thr_lo[s];
+          }
+          const int sig = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+          if (__any_sync(0xffffffffu, nr)) {  // rare: record the near-threshold coefficients
+            if (nr) {
               A.fix_flag[bidx0 + q] = 1;
-              const uint32_t e = atomicAdd(A.fix_count, 1u);
-              if (e < A.fix_cap) {
-                A.fix_list[2 * e] = bidx0 + q;
-                A.fix_list[2 * e + 1] = (uint32_t)zigzag_dev<16>()[k];
+#pragma unroll
+              for (int s = 0; s < (kLowCols ? 2 : 8); ++s) {
+                const float a = fabsf(Y[q].v[s >> 2][s & 3]);
+                if (!(a >= thr_hi[s]) && a > thr_lo[s]) {
+                  const uint32_t e = atomicAdd(A.fix_count, 1u);
+                  if (e < A.fix_cap) {
+                    A.fix_list[2 * e] = bidx0 + q;
+                    A.fix_list[2 * e + 1] = (uint32_t)(dslot_col(s) * 16 + dslot_row(s));  // flat u*16+v
+                  }
+                }
               }
             }
           }
           if (lane == 0) A.weights[bidx0 + q] = (uint32_t)sig;
         }
-        __syncwarp();
       }
       if constexpr (kPayload || kDecode) {
         int cnt[2];

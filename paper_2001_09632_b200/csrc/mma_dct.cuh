@@ -139,8 +139,8 @@ __device__ __forceinline__ void dct16_fwd_exact_x2(const Frag16& f, const uint32
   for (int q = 0; q < 2; ++q) Y[q] = stage2(T[q], f.cbh, f.cbl);
 }
 
-// Same, computing only output columns 0..7 (n-tile 0) of stage 2: enough when every
-// wanted coefficient has v <= 7 (DD phase 1 with a zigzag prefix of <= 36 entries).
+// Same, computing only rows 0..7 and columns 0..7 of Y^T (n-tile 0, A rows g): enough when
+// every wanted coefficient has u, v <= 7 (DD phase 1 with a zigzag prefix of <= 36 entries).
 __device__ __forceinline__ void dct16_fwd_exact_x2_lo(const Frag16& f, const uint32_t (&bx)[2][2][2], Acc16 (&Y)[2]) {
   Acc16 T[2];
 #pragma unroll
@@ -157,11 +157,11 @@ __device__ __forceinline__ void dct16_fwd_exact_x2_lo(const Frag16& f, const uin
     for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.ch, bx[q][j][0], bx[q][j][1]);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
+    // output rows 8..15 (v >= 8) are not wanted: their A rows (a1, a3) stay zero
     uint32_t ah[4], al[4];
     split2(T[q].v[0][0], T[q].v[0][1], ah[0], al[0]);
-    split2(T[q].v[0][2], T[q].v[0][3], ah[1], al[1]);
     split2(T[q].v[1][0], T[q].v[1][1], ah[2], al[2]);
-    split2(T[q].v[1][2], T[q].v[1][3], ah[3], al[3]);
+    ah[1] = al[1] = ah[3] = al[3] = 0u;
     Y[q].v[0][0] = Y[q].v[0][1] = Y[q].v[0][2] = Y[q].v[0][3] = 0.f;
     Y[q].v[1][0] = Y[q].v[1][1] = Y[q].v[1][2] = Y[q].v[1][3] = 0.f;
     mma16816(Y[q].v[0], al, f.cbh[0][0], f.cbh[0][1]);
@@ -223,6 +223,33 @@ __device__ __forceinline__ Acc16 dct16_inv_from_yt(const Frag16& f, const Acc16&
     mma16816(T.v[j], f.th, bh[j][0], bh[j][1]);
   }
   return stage2(T, f.tbh, f.tbl);
+}
+
+// A 16-byte block row with its bytes reordered to [0,1,8,9 | 2,3,10,11 | 4,5,12,13 | 6,7,14,15]:
+// word t then holds exactly the two byte pairs lane (g, t) needs (see u8_bfragT_il).
+__device__ __forceinline__ uint4 interleave_row16(uint4 v) {
+  return make_uint4(__byte_perm(v.x, v.z, 0x5410), __byte_perm(v.x, v.z, 0x7632), __byte_perm(v.y, v.w, 0x5410),
+                    __byte_perm(v.y, v.w, 0x7632));
+}
+
+// bytes 0,1 (sel 0x4140) or 2,3 (sel 0x4342) of w -> exact fp16 pair: 0x64 high bytes make 1024 + v
+__device__ __forceinline__ uint32_t u8sel_to_h2(uint32_t w, uint32_t sel) {
+  const uint32_t v = __byte_perm(w, 0x64646464u, sel);
+  __half2 h = *reinterpret_cast<const __half2*>(&v);
+  h = __hadd2(h, __floats2half2_rn(-1024.f, -1024.f));
+  return h2u(h);
+}
+
+// B fragments of X^T from a block staged with interleave_row16 rows (16-byte pitch): one
+// 32-bit load per n-tile gives {X[8j+g][2t], X[8j+g][2t+1]} and {X[8j+g][2t+8], X[8j+g][2t+9]}.
+__device__ __forceinline__ void u8_bfragT_il(const uint8_t* blk, uint32_t (&bx)[2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(blk + (8 * j + g) * 16 + 4 * t);
+    bx[j][0] = u8sel_to_h2(w, 0x4140);
+    bx[j][1] = u8sel_to_h2(w, 0x4342);
+  }
 }
 
 // B fragments of X^T (for the transposed forward) from a u8 block in smem with a
