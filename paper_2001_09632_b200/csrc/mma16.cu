@@ -254,13 +254,19 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll
             for (int s = 0; s < 8; ++s) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
           __syncwarp();
+          // the pair's prefixes are adjacent in the payload (offset1 = offset0 + cnt0): one
+          // coalesced copy of cnt0 + cnt1 values, two loads in flight per iteration
           const int32_t o0 = __shfl_sync(0xffffffffu, my_off, 2 * p);
-          const int32_t o1 = __shfl_sync(0xffffffffu, my_off, (2 * p + 1) & 31);
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            float* dst = A.payload + (int64_t)img * A.payload_stride + (q ? o1 : o0);
+          float* dst = A.payload + (int64_t)img * A.payload_stride + o0;
+          const int total = cnt[0] + cnt[1], skip = kWbuf - cnt[0];
 #pragma unroll 1
-            for (int k = lane; k < cnt[q]; k += 32) dst[k] = zb0[kWbuf * q + k];
+          for (int k = lane; k < total; k += 64) {
+            const int k2 = k + 32;
+            const float v0 = zb0[k < cnt[0] ? k : k + skip];
+            float v1 = 0.f;
+            if (k2 < total) v1 = zb0[k2 < cnt[0] ? k2 : k2 + skip];
+            dst[k] = v0;
+            if (k2 < total) dst[k2] = v1;
           }
           __syncwarp();
         }
