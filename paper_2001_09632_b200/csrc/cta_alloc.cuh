@@ -5,7 +5,7 @@
 // index order is (thread, position) order and the reference's "ties -> lower index"
 // rule becomes a CTA exclusive scan. Bit-exact via alloc_keys.h: blocks with equal
 // weights share one exact RN64 share/fraction key, so each round computes <= wmax+1
-// keys (one thread per class), ranks the classes (two threads per class), and hands
+// keys (one thread per class), ranks the classes (2-4 threads per class), and hands
 // the leftover units to the classes above the threshold key plus the first `need`
 // tied blocks in index order. Cap rounds repeat while capped blocks release budget.
 #pragma once
@@ -25,18 +25,13 @@ struct CtaAllocSmem {
   uint64_t key[kCtaAllocMaxW + 1];
   uint32_t whole[kCtaAllocMaxW + 1];
   uint8_t flag[kCtaAllocMaxW + 1];
-  long long red[kCtaAllocWarps][2];
+  int red[kCtaAllocWarps][2];
   int scan[kCtaAllocWarps];
   long long thr_above, thr_eq;
   uint64_t thr_key;
   int thr_flag;
 };
 
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
   const int lane = threadIdx.x & 31;
@@ -51,9 +46,13 @@ __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
 }
 
 // CTA-wide sums of (x, y), returned to every thread. Starts and ends with a barrier.
-__device__ __forceinline__ void cta_sum2(long long& x, long long& y, CtaAllocSmem& S) {
-  x = warp_sum_ll(x);
-  y = warp_sum_ll(y);
+// (Every per-image total here is < 2^31: <= 4096 blocks x 256 coefficients.)
+__device__ __forceinline__ void cta_sum2(int& x, int& y, CtaAllocSmem& S) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+    y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
   const int w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) {
@@ -110,7 +109,7 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
     for (int c = tid; c <= wmax; c += kCtaAllocThreads) S.hist[c] = 0;
     __syncthreads();
     // active blocks: warp-aggregated class histogram (DD weights cluster on few values)
-    long long tw = 0, na = 0;
+    int tw = 0, na = 0;
     for (int k = 0; k < per; ++k) {
       const int i = b0 + k;
       const bool act = i < b1 && (int)S.a[i] < cap;
@@ -126,7 +125,7 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
     // total <= 0 -> uniform weights over the active blocks (sensing.cpp:137-141)
     const bool uniform = tw == 0;
     const uint64_t T = uniform ? (uint64_t)na : (uint64_t)tw;
-    long long handed = 0, unused = 0;
+    int handed = 0, unused = 0;
     for (int c = tid; c <= wmax; c += kCtaAllocThreads) {
       const uint32_t h = S.hist[c];
       if (!h) continue;
@@ -134,10 +133,10 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
       S.whole[c] = (uint32_t)sh.whole;
       S.key[c] = sh.key;
       S.flag[c] = (uint8_t)sh.flag;
-      handed += (long long)h * (long long)sh.whole;
+      handed += (int)h * (int)sh.whole;
     }
     cta_sum2(handed, unused, S);
-    const long long leftover = remaining - handed;
+    const long long leftover = remaining - (long long)handed;
     const bool sel_all = leftover > 0 && leftover >= na;
     const bool none = leftover <= 0;
     long long need = leftover;
@@ -145,29 +144,33 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
     int thr_flag = 0;
     bool all_taken = false;
     if (!sel_all && !none) {
-      // threshold class: blocks strictly above it < need <= above + tied; two threads per class
-      const int half = tid & 1;
-      for (int c0 = 0; c0 <= wmax; c0 += kCtaAllocThreads / 2) {
-        const int c = c0 + (tid >> 1);
+      // threshold class: blocks strictly above it < need <= above + tied. `tpc` threads per class
+      // walk the class table branch-free (classes with hist 0 contribute 0 whatever their stale key).
+      const int tpc = wmax < 64 ? 4 : 2;
+      const int sub = tid & (tpc - 1);
+      for (int c0 = 0; c0 <= wmax; c0 += kCtaAllocThreads / tpc) {
+        const int c = c0 + tid / tpc;
         const uint32_t h = c <= wmax ? S.hist[c] : 0u;
-        long long above = 0, eqc = 0;
+        int above = 0, eqc = 0;
         uint64_t kk = 0;
         int fk = 0;
         if (h) {
           kk = S.key[c];
           fk = S.flag[c];
-          for (int d = half; d <= wmax; d += 2) {
-            const uint32_t hd = S.hist[d];
-            if (!hd) continue;
+#pragma unroll 4
+          for (int d = sub; d <= wmax; d += tpc) {
+            const int hd = (int)S.hist[d];
             const uint64_t kd = S.key[d];
             const int fd = S.flag[d];
-            if (kd > kk || (kd == kk && fd > fk)) above += hd;
-            else if (kd == kk && fd == fk) eqc += hd;
+            above += (kd > kk || (kd == kk && fd > fk)) ? hd : 0;
+            eqc += (kd == kk && fd == fk) ? hd : 0;
           }
         }
-        above += __shfl_xor_sync(0xffffffffu, above, 1);
-        eqc += __shfl_xor_sync(0xffffffffu, eqc, 1);
-        if (h && half == 0 && above < need && need <= above + eqc) {  // every tied class writes the same values
+        for (int o = 1; o < tpc; o <<= 1) {
+          above += __shfl_xor_sync(0xffffffffu, above, o);
+          eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
+        }
+        if (h && sub == 0 && above < need && need <= (long long)above + eqc) {  // tied classes write the same
           S.thr_above = above;
           S.thr_eq = eqc;
           S.thr_key = kk;
@@ -196,7 +199,7 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
       int tot;
       tie_base = cta_excl_scan(ties, tot, S);
     }
-    long long taken_sum = 0, still = 0;
+    int taken_sum = 0, still = 0;
     for (int i = b0; i < b1; ++i) {
       if ((int)S.a[i] >= cap) continue;
       const int c = S.w[i];
@@ -207,7 +210,7 @@ __device__ int cta_allocate(CtaAllocSmem& S, const uint32_t* __restrict__ weight
       const long long room = (long long)cap - S.a[i];
       const long long taken = give < room ? give : room;  // sensing.cpp:162-171
       S.a[i] = (uint16_t)(S.a[i] + taken);
-      taken_sum += taken;
+      taken_sum += (int)taken;
       if ((int)S.a[i] < cap) ++still;
     }
     cta_sum2(taken_sum, still, S);
