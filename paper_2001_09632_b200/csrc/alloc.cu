@@ -28,7 +28,8 @@ struct AllocScratch {
 };
 
 size_t allocate_scratch_bytes(int32_t n_blocks, int32_t n_vectors) {
-  const size_t per = (size_t)n_blocks * (8 + 4 + 4 + 1);
+  // radix kernel: 17 B per block; class kernel: 2 u16 per block, padded to 1024-thread spans
+  const size_t per = std::max((size_t)n_blocks * (8 + 4 + 4 + 1), ((size_t)n_blocks + 1024) * 4);
   return per * (size_t)n_vectors + 256;
 }
 
@@ -285,7 +286,8 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
 // 256 threads; each thread owns a contiguous range of blocks and of weight
 // values so every CTA-wide scan is a single BlockScan. Per-block state (weight,
 // allocation) lives in shared memory when it fits, else in global scratch.
-constexpr int kClassThreads = 256;
+constexpr int kClassThreads = 1024;  // one CTA per weight vector: small batches need wide CTAs
+static_assert(kClassThreads <= 1024, "allocate_scratch_bytes pads spans by 1024");
 
 template <typename T>
 struct Arr {
@@ -293,10 +295,15 @@ struct Arr {
   __device__ __forceinline__ T& operator[](int i) const { return p[i]; }
 };
 
+// entries per per-block array: ceil(nb / threads) * threads (thread-strided layout)
+__host__ __device__ __forceinline__ int class_span(int nb) {
+  return (nb + kClassThreads - 1) / kClassThreads * kClassThreads;
+}
+
 size_t class_smem_bytes(int wmax, int n_blocks, bool arrays_in_smem) {
   const size_t ncls = (size_t)std::min(n_blocks, wmax + 1);
   size_t b = 4 * (size_t)(wmax + 1) + ncls * (8 + 4 + 4 + 1) + 64;
-  if (arrays_in_smem) b += (size_t)n_blocks * 4 + 16;
+  if (arrays_in_smem) b += (size_t)class_span(n_blocks) * 4 + 16;
   return b;
 }
 
@@ -329,13 +336,16 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   p += ncls_cap;
   const int v = blockIdx.x, tid = threadIdx.x;
   Arr<uint16_t> wv, av;  // weight and allocation per block
+  // per-block state laid out thread-strided (thread t's k-th block at k * kClassThreads + t) so
+  // the warps' loads coalesce while each thread still walks its blocks in index order
+  const int span = class_span(nb);
   if constexpr (kSmemArrays) {
     uint16_t* q = reinterpret_cast<uint16_t*>(dyn + ((p - dyn + 15) & ~15));
     wv.p = q;
-    av.p = q + nb;
+    av.p = q + span;
   } else {
-    wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)v * 2 * nb;
-    av.p = wv.p + nb;
+    wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)v * 2 * span;
+    av.p = wv.p + span;
   }
   const uint32_t* w = weights + (int64_t)v * nb;
   const int per_b = (nb + kClassThreads - 1) / kClassThreads;  // contiguous block range per thread
@@ -344,11 +354,11 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   const int c0 = min(wmax + 1, tid * per_c), c1 = min(wmax + 1, c0 + per_c);
   if (tid == 0) sh_int[3] = 0;
   __syncthreads();
-  for (int i = b0; i < b1; ++i) {
+  for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
     const uint32_t wi = w[i];
     if (wi > (uint32_t)wmax) sh_int[3] = 1;  // caller's weight bound violated
-    wv[i] = (uint16_t)min(wi, (uint32_t)wmax);
-    av[i] = 0;
+    wv[ph] = (uint16_t)min(wi, (uint32_t)wmax);
+    av[ph] = 0;
   }
   if (budget < 0 || (unsigned long long)budget > (unsigned long long)cap * (unsigned long long)nb || cap < 0 ||
       cap > 65535) {
@@ -367,10 +377,14 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     for (int c = c0; c < c1; ++c) hist[c] = 0;
     __syncthreads();
     unsigned long long tw = 0, na = 0;
-    for (int i = b0; i < b1; ++i) {
-      if ((int)av[i] < cap) {
-        atomicAdd(&hist[wv[i]], 1u);
-        tw += wv[i];
+    for (int k = 0; k < per_b; ++k) {  // warp-aggregated histogram (uniform trip count for match_any)
+      const int i = b0 + k, ph = k * kClassThreads + tid;
+      const bool act = i < b1 && (int)av[ph] < cap;
+      const int wi = act ? (int)wv[ph] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, wi);
+      if (act && (__ffs(peers) - 1) == (tid & 31)) atomicAdd(&hist[wi], (unsigned)__popc(peers));
+      if (act) {
+        tw += (unsigned)wi;
         na += 1;
       }
     }
@@ -419,7 +433,7 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     bool rank_mode = false;
     uint64_t thr_key = 0;
     int thr_flag = 0;
-    if (!sel_all && !none && ncls <= kClassThreads) {
+    if (!sel_all && !none && ncls <= 512) {
       // few classes: each class counts the blocks ranking strictly above it and tied with it
       rank_mode = true;
       if (tid < ncls) {
@@ -448,7 +462,7 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     } else if (!sel_all && !none) {
       for (int pass = 0; pass < 9; ++pass) {
         const int nbins = pass < 8 ? 256 : 2;
-        hist8[tid] = 0;
+        if (tid < 256) hist8[tid] = 0;
         __syncthreads();
         const int shift_hi = 64 - 8 * pass;
         for (int k = tid; k < ncls; k += kClassThreads) {
@@ -525,25 +539,25 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     int tie_base = 0;
     if (!sel_all && !none && !all_equal_taken) {
       int ties = 0;
-      for (int i = b0; i < b1; ++i)
-        if ((int)av[i] < cap && cls_rel((int)hist[wv[i]]) == 2) ++ties;
+      for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads)
+        if ((int)av[ph] < cap && cls_rel((int)hist[wv[ph]]) == 2) ++ties;
       int tot;
       ScanI(tmp.s).ExclusiveSum(ties, tie_base, tot);
       __syncthreads();
     }
     unsigned long long taken_sum = 0, still = 0;
-    for (int i = b0; i < b1; ++i) {
-      if ((int)av[i] >= cap) continue;
-      const int k = (int)hist[wv[i]];
+    for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
+      if ((int)av[ph] >= cap) continue;
+      const int k = (int)hist[wv[ph]];
       const int rel = cls_rel(k);
       bool sel = rel == 1;
       if (rel == 2) sel = all_equal_taken || (long long)(tie_base++) < need;
       const long long give = (long long)cwhole[k] + (sel ? 1 : 0);
-      const long long room = (long long)cap - av[i];
+      const long long room = (long long)cap - av[ph];
       const long long taken = give < room ? give : room;  // sensing.cpp:162-171
-      av[i] = (uint16_t)(av[i] + taken);
+      av[ph] = (uint16_t)(av[ph] + taken);
       taken_sum += (unsigned long long)taken;
-      if ((int)av[i] < cap) still += 1;
+      if ((int)av[ph] < cap) still += 1;
     }
     const unsigned long long tk = Reduce64(tmp.r).Sum(taken_sum);
     __syncthreads();
@@ -559,11 +573,11 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   }
   // counts = base + allocation, offsets = exclusive scan (contiguous ranges: one scan)
   int mine = 0;
-  for (int i = b0; i < b1; ++i) mine += base + (int)av[i];
+  for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) mine += base + (int)av[ph];
   int ex, total;
   ScanI(tmp.s).ExclusiveSum(mine, ex, total);
-  for (int i = b0; i < b1; ++i) {
-    const int c = base + (int)av[i];
+  for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
+    const int c = base + (int)av[ph];
     counts[(int64_t)v * nb + i] = (uint16_t)c;
     if (offsets) offsets[(int64_t)v * nb + i] = ex;
     ex += c;
@@ -586,7 +600,7 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
     const size_t smem_in = class_smem_bytes(wmax, n_blocks, true);
     const size_t smem_out = class_smem_bytes(wmax, n_blocks, false);
     const int kt = ktimer_begin(ctx, s, "alloc_class");
-    if (smem_in <= 56 * 1024) {  // keep >= 4 CTAs per SM
+    if (smem_in <= 100 * 1024) {  // keep 2 CTAs (2048 threads) per SM
       alloc_class_kernel<true><<<n_vectors, kClassThreads, smem_in, s>>>(weights, n_blocks, wmax, budget, cap, base,
                                                                          counts, offsets, status, gscr);
     } else if (smem_out <= 200 * 1024) {
