@@ -435,23 +435,35 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     int thr_flag = 0;
     if (!sel_all && !none && ncls <= 512) {
       // few classes: each class counts the blocks ranking strictly above it and tied with it
+      // (a power-of-two group of tpc threads per class splits the scan; shuffle-reduced)
       rank_mode = true;
-      if (tid < ncls) {
-        const uint64_t kk = ckey[tid];
-        const int fk = cflag[tid];
-        long long above = 0, eqc = 0;
-        for (int j = 0; j < ncls; ++j) {
+      int tpc = 1;
+      while (tpc < 32 && 2 * tpc * ncls <= kClassThreads) tpc *= 2;
+      const int cls = tid / tpc, sub = tid & (tpc - 1);
+      int above = 0, eqc = 0;
+      uint64_t kk = 0;
+      int fk = 0;
+      if (cls < ncls) {
+        kk = ckey[cls];
+        fk = cflag[cls];
+#pragma unroll 4
+        for (int j = sub; j < ncls; j += tpc) {
           const uint64_t kj = ckey[j];
           const int fj = cflag[j];
-          if (kj > kk || (kj == kk && fj > fk)) above += ccnt[j];
-          else if (kj == kk && fj == fk) eqc += ccnt[j];
+          const int cj = (int)ccnt[j];
+          above += (kj > kk || (kj == kk && fj > fk)) ? cj : 0;
+          eqc += (kj == kk && fj == fk) ? cj : 0;
         }
-        if (above < need && need <= above + eqc) {  // the tie group holding the threshold
-          sh_ll[3] = above;
-          sh_int[2] = (int)eqc;
-          sh_int[1] = fk;
-          sh_ll[2] = (long long)kk;
-        }
+      }
+      for (int o = 1; o < tpc; o <<= 1) {
+        above += __shfl_xor_sync(0xffffffffu, above, o);
+        eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
+      }
+      if (cls < ncls && sub == 0 && above < need && need <= (long long)above + eqc) {  // the threshold tie group
+        sh_ll[3] = above;
+        sh_int[2] = eqc;
+        sh_int[1] = fk;
+        sh_ll[2] = (long long)kk;
       }
       __syncthreads();
       need -= sh_ll[3];
