@@ -233,6 +233,11 @@ static int sense_impl(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_image
     return launch_sense16(ctx, 3, p->rows, p->cols, n, d_images, image_stride, pitch, 0, 0.0, nullptr, d_counts,
                           offsets, d_payload, p->coeffs_per_image, d_out, out_stride, out_pitch, s);
   }
+  if (d_out && p->block == 8 && mma16_supported(p->rows, p->cols, n) && out_pitch % 2 == 0 && out_stride % 2 == 0 &&
+      ((uintptr_t)d_out % 8) == 0) {
+    return launch_sense8(ctx, true, true, p->rows, p->cols, n, d_images, image_stride, pitch, d_counts, offsets,
+                         d_payload, p->coeffs_per_image, d_out, out_stride, out_pitch, s);
+  }
   st = launch_gather(ctx, p->rows, p->cols, p->block, d_images, nullptr, image_stride, pitch, n, d_counts, offsets,
                      d_payload, p->coeffs_per_image, s);
   if (st || !d_out) return st;

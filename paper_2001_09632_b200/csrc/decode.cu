@@ -107,6 +107,11 @@ int launch_decode(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint16_
       mma16_supported(rows, cols, n)) {
     return launch_decode16(ctx, rows, cols, n, counts, offsets, payload, payload_stride, out, out_stride, out_pitch, s);
   }
+  if (B == 8 && out_pitch % 2 == 0 && out_stride % 2 == 0 && ((uintptr_t)out % 8) == 0 &&
+      mma16_supported(rows, cols, n)) {
+    return launch_sense8(ctx, false, true, rows, cols, n, nullptr, 0, 0, counts, offsets, const_cast<float*>(payload),
+                         payload_stride, out, out_stride, out_pitch, s);
+  }
   const int kt = ktimer_begin(ctx, s, "decode");
   if (B == 8)
     decode_kernel<8><<<grid, kDecodeThreads, 0, s>>>(rows, cols, n, counts, offsets, payload, payload_stride, out,

@@ -106,6 +106,9 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
                    int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
                    float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
                    cudaStream_t s, uint32_t* fix_scratch = nullptr, const FusedAlloc* fa = nullptr);
+int launch_sense8(Ctx* ctx, bool from_image, bool decode, int rows, int cols, int n, const uint8_t* imgs,
+                  int64_t img_stride, int pitch, const uint16_t* counts, const int32_t* offsets, float* payload,
+                  int64_t payload_stride, float* out, int64_t out_stride, int out_pitch, cudaStream_t s);
 int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts, const int32_t* offsets,
                     const float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,
                     cudaStream_t s);

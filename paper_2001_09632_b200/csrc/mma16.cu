@@ -443,6 +443,152 @@ static unsigned grid_for(Ctx* ctx, uint32_t warps_needed) {
 }
 
 
+// ---------------------------------------------------------------------------
+// B = 8 on the tensor cores (mma_dct.cuh Frag8: two 8x8 blocks per warp-MMA).
+//  * kFromImage: u8 blocks -> Y (forward, exact u8 operands) -> zigzag prefix payload
+//    (gather_prefixes, sensing.cpp:192-227); kDecode additionally inverts the masked Y
+//    straight from the accumulators (decode_idct, recon.cpp:109-117).
+//  * !kFromImage: decode_idct from a packed payload.
+// A warp walks a run of <= 32 consecutive blocks of a block-row in quads of 8 blocks: lane
+// L stages row L%8 of the block pair L/8 (16 bytes, rows interleaved so each lane's
+// fragment bytes are one 32-bit word); the quad's 8 prefixes are contiguous in the payload
+// and go through a per-warp smem buffer for one coalesced copy.
+constexpr int kQuadFloats = 8 * 64;
+
+template <bool kFromImage, bool kDecode>
+__global__ void __launch_bounds__(kM16Threads, 3)
+sense8_kernel(Grid16 G, Sense16Args A) {
+  __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
+  __shared__ float s_buf[kM16Warps][kQuadFloats];
+  Frag8 f;
+  load_frag8(f);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  uint32_t rank[2];  // Y^T slot e of a block: row g, col 2t+e -> Y[2t+e][g]
+#pragma unroll
+  for (int e = 0; e < 2; ++e) rank[e] = zigzag_rank_dev<8>()[(2 * t + e) * 8 + g];
+  uint8_t* st = s_stage[warp];
+  float* zb = s_buf[warp];
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < G.total_runs; r += nwarps) {
+    uint32_t img;
+    int br, bcf, nblk;
+    run_pos(G, r, img, br, bcf, nblk);
+    const uint32_t bidx_first = img * G.nb + (uint32_t)(br * G.cols + bcf);
+    const int my_cnt = lane < nblk ? A.counts[bidx_first + lane] : 0;
+    const int32_t my_off = lane < nblk ? A.offsets[bidx_first + lane] : 0;
+    int tot;
+    const int my_pre = warp_excl_scan(my_cnt, tot);  // prefix of the run's counts (lane = block)
+    for (int qb = 0; qb < nblk; qb += 8) {
+      const int pre0 = __shfl_sync(0xffffffffu, my_pre, qb);
+      const int32_t off0 = __shfl_sync(0xffffffffu, my_off, qb);
+      const int qend = min(qb + 8, nblk);
+      const int qtot = (qend < 32 ? __shfl_sync(0xffffffffu, my_pre, qend & 31) : tot) - pre0;
+      if constexpr (kFromImage) {
+        // stage the quad: lane -> pair L/8, row L%8 (16 bytes = blocks 2p, 2p+1 of the quad)
+        const int pp = lane >> 3, row = lane & 7;
+        const int b = qb + 2 * pp;  // run-relative block
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (b < nblk) {
+          const uint8_t* src = A.imgs + (int64_t)img * A.img_stride + (int64_t)(br * 8 + row) * A.pitch + (bcf + b) * 8;
+          const bool both = b + 1 < nblk;
+          if (A.aligned && both) {
+            v = __ldg(reinterpret_cast<const uint4*>(src));
+          } else {
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (q < 8 || both) w[q >> 2] |= (uint32_t)src[q] << (8 * (q & 3));
+            v = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        __syncwarp();
+        reinterpret_cast<uint4*>(st)[lane] = interleave_row16(v);
+        __syncwarp();
+      } else {
+        // the quad's prefixes (contiguous in the payload) -> smem, coalesced
+        const float* src = A.payload + (int64_t)img * A.payload_stride + off0;
+        __syncwarp();
+        for (int k = lane; k < qtot; k += 32) zb[k] = __ldg(src + k);
+        __syncwarp();
+      }
+#pragma unroll 1
+      for (int pp = 0; pp < 4; ++pp) {
+        const int b = qb + 2 * pp;
+        if (b >= nblk) break;
+        const bool two = b + 1 < nblk;
+        const int c0 = __shfl_sync(0xffffffffu, my_cnt, b & 31);
+        const int c1 = two ? __shfl_sync(0xffffffffu, my_cnt, (b + 1) & 31) : 0;
+        const int p0 = __shfl_sync(0xffffffffu, my_pre, b & 31) - pre0;
+        const int p1 = p0 + c0;
+        float Y[4];
+        if constexpr (kFromImage) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(st + pp * 128 + g * 16 + 4 * t);
+          dct8x2_fwdT_exact(f, u8sel_to_h2(w, 0x4140), u8sel_to_h2(w, 0x4342), Y);
+          // zigzag-ordered prefix of each block -> the quad buffer
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if ((int)rank[e] < c0) zb[p0 + rank[e]] = Y[e];
+            if ((int)rank[e] < c1) zb[p1 + rank[e]] = Y[2 + e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            Y[e] = (int)rank[e] < c0 ? zb[p0 + rank[e]] : 0.f;
+            Y[2 + e] = (int)rank[e] < c1 ? zb[p1 + rank[e]] : 0.f;
+          }
+        }
+        if constexpr (kDecode) {
+          float Ym[4];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            Ym[e] = (int)rank[e] < c0 ? Y[e] : 0.f;
+            Ym[2 + e] = (int)rank[e] < c1 ? Y[2 + e] : 0.f;
+          }
+          float X[4];
+          dct8x2_inv_from_yt(f, Ym, X);
+          float* o = A.out + (int64_t)img * A.out_stride + (int64_t)(br * 8 + g) * A.out_pitch + (bcf + b) * 8 + 2 * t;
+          *reinterpret_cast<float2*>(o) = make_float2(X[0], X[1]);
+          if (two) *reinterpret_cast<float2*>(o + 8) = make_float2(X[2], X[3]);
+        }
+      }
+      if constexpr (kFromImage) {
+        __syncwarp();
+        float* dst = A.payload + (int64_t)img * A.payload_stride + off0;
+        for (int k = lane; k < qtot; k += 32) dst[k] = zb[k];
+      }
+      __syncwarp();
+    }
+  }
+}
+
+int launch_sense8(Ctx* ctx, bool from_image, bool decode, int rows, int cols, int n, const uint8_t* imgs,
+                  int64_t img_stride, int pitch, const uint16_t* counts, const int32_t* offsets, float* payload,
+                  int64_t payload_stride, float* out, int64_t out_stride, int out_pitch, cudaStream_t s) {
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_runs == 0) return ABCS_OK;
+  Sense16Args A{};
+  A.imgs = imgs;
+  A.img_stride = img_stride;
+  A.pitch = pitch;
+  A.aligned = imgs && ((uintptr_t)imgs % 16 == 0) && (img_stride % 16 == 0) && (pitch % 16 == 0);
+  A.counts = counts;
+  A.offsets = offsets;
+  A.payload = payload;
+  A.payload_stride = payload_stride;
+  A.out = out;
+  A.out_stride = out_stride;
+  A.out_pitch = out_pitch;
+  const unsigned grid = grid_for(ctx, G.total_runs);
+  const char* name = from_image ? (decode ? "sense8_gather_decode" : "sense8_gather") : "decode8";
+  const int kt = ktimer_begin(ctx, s, name);
+  if (from_image && decode) sense8_kernel<true, true><<<grid, kM16Threads, 0, s>>>(G, A);
+  else if (from_image) sense8_kernel<true, false><<<grid, kM16Threads, 0, s>>>(G, A);
+  else sense8_kernel<false, true><<<grid, kM16Threads, 0, s>>>(G, A);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "sense8 launch");
+}
+
 bool mma16_supported(int rows, int cols, int n) {
   const uint64_t blocks = (uint64_t)rows * cols * (uint64_t)n;
   return blocks < (1ull << 31);

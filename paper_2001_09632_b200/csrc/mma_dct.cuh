@@ -319,6 +319,21 @@ __device__ __forceinline__ void dct8x2_fwdT(const Frag8& f, float2 p0, float2 p1
   mma1688(Y, qh0, qh1, f.ah[0]);
 }
 
+// Same from exact-fp16 (u8) B fragments b0 = {P0[g][2t..2t+1]}, b1 = {P1[g][2t..2t+1]}: the
+// data needs no split, so stage 1 is hi/lo of the basis only.
+__device__ __forceinline__ void dct8x2_fwdT_exact(const Frag8& f, uint32_t b0, uint32_t b1, float (&Y)[4]) {
+  float Q[4] = {0.f, 0.f, 0.f, 0.f};
+  mma16816(Q, f.al, b0, b1);
+  mma16816(Q, f.ah, b0, b1);
+  uint32_t qh0, ql0, qh1, ql1;
+  split2(Q[0], Q[1], qh0, ql0);
+  split2(Q[2], Q[3], qh1, ql1);
+  Y[0] = Y[1] = Y[2] = Y[3] = 0.f;
+  mma1688(Y, ql0, ql1, f.ah[0]);
+  mma1688(Y, qh0, qh1, f.al[0]);
+  mma1688(Y, qh0, qh1, f.ah[0]);
+}
+
 // X = C8^T Y C8 of two blocks given as Y^T in the slot layout (output of dct8x2_fwdT).
 __device__ __forceinline__ void dct8x2_inv_from_yt(const Frag8& f, const float (&Yt)[4], float (&X)[4]) {
   uint32_t h0, l0, h1, l1;

@@ -247,7 +247,10 @@ int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t B, const uint8_t
   if (total == 0) return ABCS_OK;
   const int64_t gpc = kGatherThreads / B;
   const unsigned grid = (unsigned)((total + gpc - 1) / gpc);
-  if (imgs && B == 16 && mma16_supported(rows, cols, n)) {
+  if (imgs && B == 8 && mma16_supported(rows, cols, n)) {
+    return launch_sense8(ctx, true, false, rows, cols, n, imgs, img_stride, pitch, counts, offsets, payload,
+                         payload_stride, nullptr, 0, 0, s);
+  } else if (imgs && B == 16 && mma16_supported(rows, cols, n)) {
     return launch_sense16(ctx, 2, rows, cols, n, imgs, img_stride, pitch, 0, 0.0, nullptr, counts, offsets, payload,
                           payload_stride, nullptr, 0, 0, s);
   }
