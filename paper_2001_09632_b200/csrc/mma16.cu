@@ -436,9 +436,10 @@ alloc_cta_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, long lo
 }
 
 // ---------------------------------------------------------------------------
-static unsigned grid_for(Ctx* ctx, uint32_t warps_needed) {
+// Grid-stride CTAs: two full waves of `per_sm` resident CTAs per SM (equal work per CTA).
+static unsigned grid_for(Ctx* ctx, uint32_t warps_needed, uint32_t per_sm = 3) {
   const uint32_t ctas = (warps_needed + kM16Warps - 1) / kM16Warps;
-  const uint32_t cap = (uint32_t)ctx->sm_count * 6;
+  const uint32_t cap = (uint32_t)ctx->sm_count * per_sm * 2;
   return ctas < cap ? (ctas ? ctas : 1) : cap;
 }
 
@@ -456,7 +457,7 @@ static unsigned grid_for(Ctx* ctx, uint32_t warps_needed) {
 constexpr int kQuadFloats = 8 * 64;
 
 template <bool kFromImage, bool kDecode>
-__global__ void __launch_bounds__(kM16Threads, 3)
+__global__ void __launch_bounds__(kM16Threads, 4)
 sense8_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
   __shared__ float s_buf[kM16Warps][kQuadFloats];
@@ -578,7 +579,7 @@ int launch_sense8(Ctx* ctx, bool from_image, bool decode, int rows, int cols, in
   A.out = out;
   A.out_stride = out_stride;
   A.out_pitch = out_pitch;
-  const unsigned grid = grid_for(ctx, G.total_runs);
+  const unsigned grid = grid_for(ctx, G.total_runs, 4);
   const char* name = from_image ? (decode ? "sense8_gather_decode" : "sense8_gather") : "decode8";
   const int kt = ktimer_begin(ctx, s, name);
   if (from_image && decode) sense8_kernel<true, true><<<grid, kM16Threads, 0, s>>>(G, A);
