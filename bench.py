@@ -372,6 +372,15 @@ def run_ours(args, world, rank, local):
     # secondary: cfg4 IDA (64 x 512^2, BBV 0.3, 10 iterations)
     ida = run_ida(p, torch, local, rank, hbm, world, dev)
 
+    # the other BASELINE configs (parity-test workloads, not bench lines): device throughput and
+    # algorithmic-bytes roofline fraction of sense+decode (and IDA) on this rank's GPU
+    configs = None
+    if rank == 0 and not args.no_config_sweep:
+        try:
+            configs = config_sweep(p, torch, hbm)
+        except Exception as e:  # informative only; never fail the headline line
+            configs = {"error": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         checker, kind = get_checker()
@@ -401,11 +410,57 @@ def run_ours(args, world, rank, local):
             "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
             "ida": ida,
+            "configs": configs,
             "clocks": clk,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+SWEEP = [  # (name, H, W, n, B, num, den, algorithm, ellipses, sigma, seed, video, ida_iterations)
+    ("cfg1 1x256^2 B16 BBV0.25", 256, 256, 1, 16, 1, 4, "BBV", 20, 5.0, 1, False, 0),
+    ("cfg3 256x1920x1080 B8 BBV0.2", 1080, 1920, 256, 8, 1, 5, "BBV", 20, 5.0, 3, True, 0),
+    ("cfg4 64x512^2 B16 BBV0.3 + IDA10", 512, 512, 64, 16, 3, 10, "BBV", 20, 5.0, 4, False, 10),
+    ("cfg5 16x4096^2 B16 DD0.25 + IDA5 (one GPU's shard of 128)", 4096, 4096, 16, 16, 1, 4, "DD", 200, 8.0, 5,
+     False, 5),
+]
+
+
+def config_sweep(p, torch, hbm):
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    out = {}
+    for name, H, W, n, B, num, den, algo, ell, sig, seed, video, iters in SWEEP:
+        imgs = p.synth_images(p.SynthSpec(H, W, ell, sig, seed, video=video), 0, n)
+        cfg = p.SensingConfig(B, num, den, getattr(p.Algorithm, algo))
+        plan = p.sense_plan(cfg, H, W)
+        b, dec = p.sense_decode_batch(imgs, cfg, plan)
+        ms = timed(lambda: p.sense_decode_batch(imgs, cfg, plan, out=b, image_out=dec))
+        N, K, S, nB = H * W, plan.coeffs_per_image, plan.side_per_image, plan.n_blocks
+        Nc = plan.rows * B * plan.cols * B
+        alg = n * (N + 8 * K + 4 * nB + 4 * S + 4 * Nc)
+        row = {"sense_decode_ms": round(ms, 4), "MP_s": round(n * N / ms / 1e3, 1),
+               "hbm_frac": round(alg / (ms / 1e3) / 1e9 / hbm, 4)}
+        if iters:
+            rc = p.ReconConfig(p.ReconMethod.Ida, iterations=iters)
+            ms_i = timed(lambda: p.ida_batch(b, rc, out=dec, trace=False, check=False), reps=3)
+            alg_i = n * ((8 * Nc + 12 * K) * iters + 8 * K + 4 * Nc)
+            row.update({"ida_ms": round(ms_i, 3), "ida_it_s": round(n * iters / ms_i * 1e3, 1),
+                        "ida_hbm_frac": round(alg_i / (ms_i / 1e3) / 1e9 / hbm, 4)})
+        out[name] = row
+        del imgs, b, dec
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_ida(p, torch, local, rank, hbm, world, dev):
@@ -464,6 +519,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config-sweep", action="store_true", help="skip the cfg1/3/4/5 device sweep")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:
