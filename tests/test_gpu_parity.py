@@ -400,6 +400,40 @@ def test_ida_divergence(p):
 
 
 # ---- full-size properties (BASELINE sizes) -------------------------------------------------
+def test_spec_known_answers_on_device(p, torch):
+    """SPEC.md worked examples through the product path."""
+    assert list(p.largest_remainder_allocate([10, 20, 30, 40], 900, [1024] * 4)) == [90, 180, 270, 360]
+    assert list(p.largest_remainder_allocate([1, 0, 0, 0], 2000, [1024] * 4)) == [1024, 326, 325, 325]
+    assert list(p.largest_remainder_allocate([5, 3, 2, 0], 40, [246] * 4)) == [20, 12, 8, 0]
+    assert p.dd_threshold(256, 1, 5) == 60.0 and p.dd_threshold(512, 1, 4) == 30.0
+    assert p.sense_plan(p.SensingConfig(32, 1, 4, p.Algorithm.BBV), 256, 256).bbv_phase1_total == 1152
+    flat = np.full((8, 8), 128, np.uint8)                       # 8x8 constant 128 -> DC = 1024
+    ms = p.sense(flat, p.SensingConfig(8, 1, 1, p.Algorithm.ZZ))
+    assert abs(float(ms.coeffs[0]) - 1024.0) <= 1e-3 and np.max(np.abs(ms.coeffs[1:])) <= 1e-3
+    f = synth(64, 96, n=1, seed=8)[0].astype(np.float64)        # dct_threshold at sigma 0 is the identity
+    assert np.max(np.abs(p.denoise(p.DenoiserSpec("dct_threshold", {"k": 2.7}), f, 0.0) - f)) <= 1e-3
+
+
+def test_spec_properties_on_device(p, torch):
+    imgs = synth(128, 96, n=2, seed=13)
+    for algo in (p.Algorithm.ZZ, p.Algorithm.BBV, p.Algorithm.DD):
+        for B in (8, 16):
+            b = sense_dev(p, torch, imgs, B, 3, 10, int(algo))
+            assert int(b.counts.to(torch.int32).max()) <= B * B                    # cap <= B^2 (SPEC:233)
+            b2 = sense_dev(p, torch, imgs, B, 3, 10, int(algo))
+            assert torch.equal(b.counts, b2.counts) and torch.equal(b.payload, b2.payload)  # determinism
+    zz = p.sense(imgs[0], p.SensingConfig(16, 1, 1, p.Algorithm.ZZ))              # BBV at C_R = 1 == zz (SPEC:235)
+    warn = []
+    bbv = p.sense(imgs[0], p.SensingConfig(16, 1, 1, p.Algorithm.BBV), warn)
+    assert warn and bbv.algorithm == p.Algorithm.ZZ
+    assert np.array_equal(bbv.counts, zz.counts) and np.array_equal(bbv.coeffs, zz.coeffs)
+    ms = p.sense(imgs[0], p.SensingConfig(16, 1, 4, p.Algorithm.BBV))           # sigma^2 = ||z||^2 / M (SPEC:379)
+    res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=3))
+    M = float(ms.total_coeffs())
+    for r in res.trace[1:]:
+        assert r.sigma ** 2 == pytest.approx(r.residual_norm ** 2 / M, rel=1e-9)
+
+
 def test_cfg2_full_batch_properties(p, torch, checker):
     """1024 x 512^2 DD sweep: K per image exact, determinism, round-trip, sampled parity."""
     spec = p.SynthSpec(512, 512, 20, 5.0, 2)
