@@ -255,6 +255,36 @@ int abcs_psnr_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, int
                     const float* d_img, int64_t img_stride, int32_t img_pitch, int32_t height,
                     int32_t width, int32_t n_images, double* d_psnr, void* stream);
 
+/* ---- .abcs v1 measurement container (container.cpp:58-149) ------------------
+ * Layout (little-endian, packed): "ABCS" | version u16 = 1 | H u32 | W u32 | B u16 |
+ * algorithm u8 | C_R num u32 | C_R den u32 | threshold f64 | n_B u32 | counts u16[n_B] |
+ * coeffs f32[K] | side count u32 | side f32[S]. A batch of containers shares one plan. */
+typedef struct {
+  int32_t algorithm;  /* header algorithm id */
+  uint32_t cr_num, cr_den;
+  int32_t status;     /* ABCS_OK or ABCS_ERR_FORMAT (the reference reader's checks) */
+  double threshold;
+} abcs_container_info;
+
+/* bytes of one container of this plan: 41 + 2 n_B + 4 K + 4 S */
+int64_t abcs_container_size(const abcs_sense_plan* plan);
+/* write_measurement_set's byte image for n sensed images, straight from the device
+ * buffers of abcs_sense_batch (header from the plan; container i at d_out + i*out_stride,
+ * out_stride % 4 == 0). Byte-identical to the reference writer on the same set. */
+int abcs_container_pack_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint16_t* d_counts,
+                              const float* d_payload, const float* d_side, int32_t n_images,
+                              uint8_t* d_out, int64_t out_stride, void* stream);
+/* read_measurement_set on the device for n containers of the plan's layout: counts,
+ * payload and side into the batched buffers, plus per-container header fields and a
+ * status (ABCS_ERR_FORMAT where the reference reader would throw FormatError). */
+int abcs_container_unpack_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_in,
+                                int64_t in_stride, int32_t n_images, uint16_t* d_counts,
+                                float* d_payload, float* d_side, abcs_container_info* d_info,
+                                void* stream);
+/* Host: the layout of one container (header checks, counts summed for K, side count,
+ * exact size) as a plan for abcs_container_unpack_batch. */
+int abcs_container_parse(const uint8_t* h_bytes, int64_t size, abcs_sense_plan* plan);
+
 /* Synthetic inputs on the device (same bytes as abcs_synth_generate_host). */
 int abcs_synth_generate(abcs_ctx* ctx, const abcs_synth_spec* spec, int64_t first_index,
                         int32_t n_images, uint8_t* d_out, int64_t image_stride, void* stream);

@@ -165,6 +165,17 @@ class CPort:
         return out, trace
 
 
+def container_bytes(height, width, block, algorithm, cr_num, cr_den, threshold, counts, coeffs, side) -> bytes:
+    """write_measurement_set's byte image (container.cpp:58-93): little-endian, packed;
+    coefficients and side data narrowed to f32 (container.cpp:83,85)."""
+    import struct
+    c = np.asarray(counts, dtype="<u2")
+    out = [b"ABCS", struct.pack("<HIIHBIIdI", 1, height, width, block, algorithm, cr_num, cr_den, threshold, c.size),
+           c.tobytes(), np.asarray(coeffs, dtype="<f4").tobytes(), struct.pack("<I", np.size(side)),
+           np.asarray(side, dtype="<f4").tobytes()]
+    return b"".join(out)
+
+
 class Reference:
     """oracle/_ref/libabcs_ref.so — the reference library itself (ref_capi.cpp shims)."""
 
@@ -275,6 +286,45 @@ class Reference:
         y = np.ascontiguousarray(coeffs, dtype=np.float64)
         return self.lib.ref_ms_make(rows * B, cols * B, B, 0, C.c_uint32(1), C.c_uint32(1), C.c_double(0.0),
                                     c.ctypes.data_as(P), c.size, y.ctypes.data_as(P), C.c_longlong(y.size))
+
+    def write_container(self, ms, path):
+        """abcs::write_measurement_set on a MeasurementSet given as a dict (sense()'s layout)."""
+        c = np.ascontiguousarray(ms["counts"], dtype=np.uint16)
+        y = np.ascontiguousarray(ms["coeffs"], dtype=np.float64)
+        sd = np.ascontiguousarray(ms.get("side", np.zeros(0)), dtype=np.float64)
+        h = self.lib.ref_ms_make(ms["height"], ms["width"], ms["block"], int(ms["algorithm"]),
+                                 C.c_uint32(ms["cr_num"]), C.c_uint32(ms["cr_den"]), C.c_double(ms["threshold"]),
+                                 c.ctypes.data_as(P), c.size, y.ctypes.data_as(P), C.c_longlong(y.size))
+        try:
+            self.lib.ref_ms_set_side.argtypes = [P, P, C.c_longlong]
+            self.lib.ref_ms_set_side(h, sd.ctypes.data_as(P), sd.size)
+            self.lib.ref_container_write.argtypes = [P, C.c_char_p]
+            self._err(self.lib.ref_container_write(h, str(path).encode()))
+        finally:
+            self.lib.ref_ms_free(h)
+
+    def read_container(self, path):
+        """abcs::read_measurement_set -> dict (counts, coeffs, side, header fields)."""
+        h = P()
+        self.lib.ref_container_read.argtypes = [C.c_char_p, C.POINTER(P)]
+        self._err(self.lib.ref_container_read(str(path).encode(), C.byref(h)))
+        try:
+            return self._ms_dict(h)
+        finally:
+            self.lib.ref_ms_free(h)
+
+    def _ms_dict(self, h):
+        info = (C.c_longlong * 11)()
+        thr = C.c_double()
+        self.lib.ref_ms_info(h, info, C.byref(thr))
+        counts = np.zeros(info[6], np.uint16)
+        coeffs = np.zeros(info[7])
+        side = np.zeros(info[8])
+        self.lib.ref_ms_counts(h, counts.ctypes.data_as(P))
+        self.lib.ref_ms_coeffs(h, coeffs.ctypes.data_as(P))
+        self.lib.ref_ms_side(h, side.ctypes.data_as(P))
+        return {"height": info[0], "width": info[1], "block": info[2], "algorithm": info[3], "cr_num": info[4],
+                "cr_den": info[5], "threshold": thr.value, "counts": counts, "coeffs": coeffs, "side": side}
 
     def decode(self, rows, cols, B, counts, coeffs):
         h = self._make(rows, cols, B, counts, coeffs)

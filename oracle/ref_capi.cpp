@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "abcs/container.hpp"
 #include "abcs/dct.hpp"
 #include "abcs/denoise.hpp"
 #include "abcs/image.hpp"
@@ -119,6 +120,28 @@ void* ref_ms_make(int h, int w, int block, int algo, uint32_t num, uint32_t den,
 }
 
 void ref_ms_free(void* p) { delete static_cast<Handle*>(p); }
+
+void ref_ms_set_side(void* p, const double* side, long long n) {
+  static_cast<Handle*>(p)->ms.side.assign(side, side + n);
+}
+
+// abcs::write_measurement_set / read_measurement_set (container.cpp:58-149)
+int ref_container_write(void* p, const char* path) {
+  return guarded([&] { abcs::write_measurement_set(static_cast<Handle*>(p)->ms, path); });
+}
+
+int ref_container_read(const char* path, void** out) {
+  return guarded([&] {
+    auto* hd = new Handle;
+    try {
+      hd->ms = abcs::read_measurement_set(path);
+    } catch (...) {
+      delete hd;
+      throw;
+    }
+    *out = hd;
+  });
+}
 
 // info: [height, width, block, algorithm, cr_num, cr_den, n_blocks, n_coeffs, n_side,
 //        budget.target, budget.actual]; threshold separately.

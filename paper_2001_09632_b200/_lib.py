@@ -63,6 +63,11 @@ class SynthSpecC(C.Structure):
     ]
 
 
+class ContainerInfoC(C.Structure):
+    _fields_ = [("algorithm", C.c_int32), ("cr_num", C.c_uint32), ("cr_den", C.c_uint32), ("status", C.c_int32),
+                ("threshold", C.c_double)]
+
+
 class KernelTimeC(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("launches", C.c_int64), ("total_ms", C.c_double), ("max_ms", C.c_double)]
 
@@ -95,6 +100,10 @@ SIGNATURES = {
     "abcs_ida_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC),
                                  P, I64, I32, P, I64, I32, P, P, P]),
     "abcs_ida_check": (C.c_int, [P, I32, C.POINTER(I32)]),
+    "abcs_container_size": (I64, [C.POINTER(SensePlanC)]),
+    "abcs_container_pack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, P, P, I32, P, I64, P]),
+    "abcs_container_unpack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, P, P, P, P, P]),
+    "abcs_container_parse": (C.c_int, [P, I64, C.POINTER(SensePlanC)]),
     "abcs_psnr_batch": (C.c_int, [P, P, I64, I32, P, I64, I32, I32, I32, I32, P, P]),
     "abcs_ida_init_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, I32, P, P, P, P]),
     "abcs_ida_step_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC), P, P, P, I32,

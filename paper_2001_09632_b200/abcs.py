@@ -878,6 +878,97 @@ def denoise(spec: DenoiserSpec, field_values, sigma: float) -> np.ndarray:
     return out.cpu().numpy()
 
 
+# ---- .abcs v1 container (container.hpp:8-14, container.cpp:58-149) --------------------
+def container_size(plan: SensePlanC) -> int:
+    return int(_lib.load().abcs_container_size(C.byref(plan)))
+
+
+def pack_containers(batch: MeasurementBatch, out=None):
+    """write_measurement_set's bytes for every set of the batch: (n, stride) uint8 CUDA tensor
+    (stride = size rounded up to 4; row i[:container_size(plan)] is container i)."""
+    torch = _torch()
+    plan = batch.plan
+    size = container_size(plan)
+    stride = (size + 3) // 4 * 4
+    dev = batch.counts.device
+    if out is None:
+        out = torch.empty((batch.n, stride), dtype=torch.uint8, device=dev)
+    _check(_lib.load().abcs_container_pack_batch(Context.get(dev.index).handle, C.byref(plan), _ptr(batch.counts),
+                                                 _ptr(batch.payload), _ptr(batch.side), batch.n, out.data_ptr(),
+                                                 out.stride(0), _stream_ptr(torch)))
+    return out
+
+
+def unpack_containers(data, plan: SensePlanC):
+    """read_measurement_set on the device for n containers of one layout: (MeasurementBatch,
+    [per-container (algorithm, cr_num, cr_den, threshold)]). Raises FormatError naming the
+    first invalid container."""
+    torch = _torch()
+    n = data.shape[0]
+    dev = data.device
+    K, S, nB = plan.coeffs_per_image, plan.side_per_image, plan.n_blocks
+    counts = torch.empty((n, nB), dtype=torch.int16, device=dev).view(torch.uint16)
+    payload = torch.empty((n, max(K, 1)), dtype=torch.float32, device=dev)
+    side = torch.empty((n, max(S, 1)), dtype=torch.float32, device=dev) if S else None
+    info = torch.empty((n, C.sizeof(_lib.ContainerInfoC)), dtype=torch.uint8, device=dev)
+    _check(_lib.load().abcs_container_unpack_batch(Context.get(dev.index).handle, C.byref(plan), data.data_ptr(),
+                                                   data.stride(0), n, counts.data_ptr(), payload.data_ptr(),
+                                                   _ptr(side), info.data_ptr(), _stream_ptr(torch)))
+    raw = info.cpu().numpy()
+    infos = [_lib.ContainerInfoC.from_buffer_copy(raw[i].tobytes()) for i in range(n)]
+    for i, inf in enumerate(infos):
+        if inf.status != _lib.OK:
+            raise FormatError(f"container {i}: invalid (header does not match the batch layout, "
+                              f"count > B^2, payload or side length mismatch)")
+    batch = MeasurementBatch(plan=plan, cfg=SensingConfig(plan.block, plan.cr_num, plan.cr_den,
+                                                          Algorithm(plan.algorithm_used)),
+                             counts=counts, offsets=None, payload=payload[:, :K], side=side)
+    return batch, [(Algorithm(i.algorithm), i.cr_num, i.cr_den, i.threshold) for i in infos]
+
+
+def write_measurement_set(ms: MeasurementSet, path) -> None:
+    """abcs::write_measurement_set (container.cpp:58-93): packed on the device."""
+    torch = _torch()
+    if ms.block < 2 or ms.block * ms.block > 65535:
+        raise ValueError("container: block size must fit u16 counts")
+    g = ms.grid()
+    if np.size(ms.counts) != g.count():
+        raise ValueError("container: count table does not match grid")
+    if ms.total_coeffs() != np.size(ms.coeffs):
+        raise ValueError("container: payload length does not match counts")
+    b = _batch_from_host(ms)
+    side = np.ascontiguousarray(np.asarray(ms.side, dtype=np.float32).reshape(-1))
+    b.plan.side_per_image = side.size
+    b.side = torch.from_numpy(side).to(b.counts.device).reshape(1, -1) if side.size else None
+    size = container_size(b.plan)
+    data = pack_containers(b)[0, :size].cpu().numpy()
+    with open(path, "wb") as f:
+        f.write(data.tobytes())
+
+
+def read_measurement_set(path) -> MeasurementSet:
+    """abcs::read_measurement_set (container.cpp:95-149): parsed and unpacked on the device."""
+    torch = _torch()
+    try:
+        with open(path, "rb") as f:
+            raw = f.read()
+    except OSError:
+        raise FormatError(f"cannot open container: {path}")
+    plan = SensePlanC()
+    buf = np.frombuffer(raw, dtype=np.uint8)
+    _check(_lib.load().abcs_container_parse(buf.ctypes.data if buf.size else None, buf.size, C.byref(plan)))
+    stride = (buf.size + 3) // 4 * 4
+    padded = np.zeros((1, stride), np.uint8)
+    padded[0, :buf.size] = buf
+    dev = torch.device("cuda", torch.cuda.current_device())
+    batch, infos = unpack_containers(torch.from_numpy(padded).to(dev), plan)
+    algo, num, den, thr = infos[0]
+    return MeasurementSet(height=plan.height, width=plan.width, block=plan.block, algorithm=algo, cr_num=num,
+                          cr_den=den, threshold=thr, counts=batch.counts[0].cpu().numpy().astype(np.uint16),
+                          coeffs=batch.payload[0].cpu().numpy(),
+                          side=(batch.side[0].cpu().numpy() if batch.side is not None else np.zeros(0, np.float32)))
+
+
 # ---- synthetic inputs (DESIGN.md "Inputs") ---------------------------------------------
 @dataclass
 class SynthSpec:

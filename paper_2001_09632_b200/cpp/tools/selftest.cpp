@@ -5,6 +5,7 @@
 #include <abcs_b200.h>
 
 #include <abcs/b200.hpp>
+#include <abcs/container.hpp>
 #include <abcs/recon.hpp>
 #include <algorithm>
 #include <cmath>
@@ -80,6 +81,22 @@ int main() {
     for (double& v : clamped) v = std::clamp(v, 0.0, 255.0);
     expect(max_abs_diff(clamped, r.image.data) <= 1e-3, "stepwise state == reconstruct");
     expect(std::fabs(st.sigma - r.trace.back().sigma) <= 1e-4 * r.trace.back().sigma, "sigma matches trace");
+  }
+
+  // .abcs container round trip (container.cpp:58-149)
+  {
+    SensingConfig cfg;
+    cfg.block = 16;
+    cfg.algorithm = Algorithm::BBV;
+    cfg.set_cr("1/4");
+    const MeasurementSet ms = sense(img, cfg);
+    const std::filesystem::path path = std::filesystem::temp_directory_path() / "abcs_selftest.abcs";
+    write_measurement_set(ms, path);
+    const MeasurementSet back = read_measurement_set(path);
+    expect(back.counts == ms.counts && back.coeffs == ms.coeffs && back.side == ms.side &&
+               back.threshold == ms.threshold && back.algorithm == ms.algorithm,
+           "container round trip");
+    std::filesystem::remove(path);
   }
 
   // reference error behaviour

@@ -79,5 +79,36 @@ def main():
             f.write(f"{h}x{w}-{e}-{s}-{seed}-{v} {d}\n")
 
 
+CONTAINER_CASES = [  # (H, W, B, num, den, algo, seed): zz, bbv (with side data), dd, ragged, B = 8
+    (64, 64, 16, 1, 4, 0, 21), (64, 64, 16, 1, 4, 1, 22), (64, 64, 16, 3, 10, 2, 23), (70, 90, 16, 1, 3, 1, 24),
+    (48, 40, 8, 1, 5, 1, 25)]
+
+
+def main_containers():
+    """tests/golden/container_cases.npz: write_measurement_set bytes of reference sense() results."""
+    import tempfile
+    ref = o.Reference()
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for i, (H, W, B, num, den, algo, seed) in enumerate(CONTAINER_CASES):
+            img = p.synth_images_host(p.SynthSpec(H, W, 20, 5.0, seed), 0, 1)[0]
+            r = ref.sense(img, B, num, den, algo)
+            ms = dict(height=H, width=W, block=B, algorithm=r["algorithm"], cr_num=num, cr_den=den,
+                      threshold=r["threshold"], counts=r["counts"], coeffs=r["coeffs"], side=r["side"])
+            path = os.path.join(d, f"c{i}.abcs")
+            ref.write_container(ms, path)
+            with open(path, "rb") as f:
+                out[f"c{i}_bytes"] = np.frombuffer(f.read(), np.uint8)
+            out[f"c{i}_hdr"] = np.array([H, W, B, r["algorithm"], num, den, r["threshold"]], dtype=np.float64)
+            out[f"c{i}_counts"] = r["counts"]
+            out[f"c{i}_coeffs"] = r["coeffs"]
+            out[f"c{i}_side"] = r["side"]
+    np.savez_compressed(os.path.join(HERE, "container_cases.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if "--containers" in sys.argv:
+        main_containers()
+    else:
+        main()
+        main_containers()

@@ -33,6 +33,8 @@ SIGNATURES = [
     "abcs::SensingConfig::validate() const",
     "abcs::make_grid(int, int, int)",
     "abcs::zigzag_order(int)",
+    "abcs::write_measurement_set(abcs::MeasurementSet const&, std::filesystem::__cxx11::path const&)",
+    "abcs::read_measurement_set(std::filesystem::__cxx11::path const&)",
 ]
 
 
