@@ -372,6 +372,14 @@ def run_ours(args, world, rank, local):
     # secondary: cfg4 IDA (64 x 512^2, BBV 0.3, 10 iterations)
     ida = run_ida(p, torch, local, rank, hbm, world, dev)
 
+    # the .abcs container of the subrate-0.3 batch, packed and unpacked on the device
+    container = None
+    if rank == 0:
+        try:
+            container = container_bench(p, torch, batches[1], hbm)
+        except Exception as e:
+            container = {"error": repr(e)[:200]}
+
     # the other BASELINE configs (parity-test workloads, not bench lines): device throughput and
     # algorithmic-bytes roofline fraction of sense+decode (and IDA) on this rank's GPU
     configs = None
@@ -410,12 +418,50 @@ def run_ours(args, world, rank, local):
             "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
             "ida": ida,
+            "container": container,
             "configs": configs,
             "clocks": clk,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+def container_bench(p, torch, b, hbm):
+    """write/read_measurement_set bytes for a 1024-image batch: pack (counts+payload -> containers) and
+    unpack (+ validation); algorithmic bytes = bytes read + bytes written."""
+    data = p.pack_containers(b)
+    p.unpack_containers(data, b.plan)
+    torch.cuda.synchronize()
+    size = p.container_size(b.plan)
+    nB, K = b.plan.n_blocks, b.plan.coeffs_per_image
+    src = b.n * (2 * nB + 4 * K)
+    dst = b.n * size
+
+    def t(fn, reps=10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    ms_pack = t(lambda: p.pack_containers(b, out=data))
+    # unpack: device time of its kernels (validate + unpack) from the ctx's CUDA events; the
+    # Python wrapper's per-container status readback is host work outside the device path
+    ctx = p.Context.get()
+    ctx.kernel_timing(True)
+    for _ in range(10):
+        p.unpack_containers(data, b.plan)
+    kt = ctx.kernel_times()
+    ctx.kernel_timing(False)
+    ms_unpack = sum(v[1] for k, v in kt.items() if k in ("container_validate", "container_unpack")) / 10
+    return {"workload": f"{b.n} containers of cfg2 DD 3/10 ({size} B each)",
+            "pack_ms": round(ms_pack, 4), "pack_gbs": round((src + dst) / ms_pack / 1e6, 1),
+            "pack_frac": round((src + dst) / ms_pack / 1e6 / hbm, 4),
+            "unpack_ms": round(ms_unpack, 4), "unpack_gbs": round((src + dst) / ms_unpack / 1e6, 1),
+            "unpack_frac": round((src + dst) / ms_unpack / 1e6 / hbm, 4)}
 
 
 SWEEP = [  # (name, H, W, n, B, num, den, algorithm, ellipses, sigma, seed, video, ida_iterations)

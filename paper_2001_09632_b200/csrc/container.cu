@@ -101,16 +101,15 @@ __device__ __forceinline__ uint32_t f32_bytes(const float* row, int64_t o) {
   return __funnelshift_r(lo, __float_as_uint(__ldg(row + (o >> 2) + 1)), sh);
 }
 
-__global__ void container_pack_kernel(ContainerArgs a, int64_t words_per) {
-  const int64_t total_words = words_per * a.n;
+// grid: x strides over the words of one container, y = container (image) index
+__global__ void container_pack_kernel(ContainerArgs a, int64_t words_per, int img0) {
   const ContainerLayout& L = a.L;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total_words;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t img = t / words_per, w = t - img * words_per;
+  const int64_t img = img0 + blockIdx.y;
+  uint8_t* base = a.out + img * a.stride;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words_per; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pos = 4 * w;
-    uint8_t* dst = a.out + img * a.stride + pos;
     if (pos + 4 > L.total) {  // trailing partial word
-      for (int64_t q = pos; q < L.total; ++q) dst[q - pos] = (uint8_t)pack_byte(a, img, q);
+      for (int64_t q = pos; q < L.total; ++q) base[q] = (uint8_t)pack_byte(a, img, q);
       continue;
     }
     uint32_t v;
@@ -122,7 +121,7 @@ __global__ void container_pack_kernel(ContainerArgs a, int64_t words_per) {
       v = pack_byte(a, img, pos) | (pack_byte(a, img, pos + 1) << 8) | (pack_byte(a, img, pos + 2) << 16) |
           (pack_byte(a, img, pos + 3) << 24);
     }
-    *reinterpret_cast<uint32_t*>(dst) = v;
+    *reinterpret_cast<uint32_t*>(base + pos) = v;
   }
 }
 
@@ -141,13 +140,12 @@ __device__ __forceinline__ uint32_t in_u32(const uint8_t* base, int64_t pos, int
   return sh ? __funnelshift_r(lo, word(w + 1), sh) : lo;
 }
 
-__global__ void container_unpack_kernel(ContainerArgs a) {
+__global__ void container_unpack_kernel(ContainerArgs a, int img0) {
   const ContainerLayout& L = a.L;
   const int64_t per = L.nB + L.K + L.S;
-  const int64_t total = per * a.n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t img = t / per, j = t - img * per;
-    const uint8_t* base = a.in + img * a.stride;
+  const int64_t img = img0 + blockIdx.y;
+  const uint8_t* base = a.in + img * a.stride;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < per; j += (int64_t)gridDim.x * blockDim.x) {
     if (j < L.nB) {
       a.counts_out[img * L.nB + j] = (uint16_t)(in_u32(base, kHdr + 2 * j, L.total) & 0xffffu);
     } else if (j < L.nB + L.K) {
@@ -242,12 +240,14 @@ int abcs_container_pack_batch(abcs_ctx* c, const abcs_sense_plan* plan, const ui
   a.stride = out_stride;
   a.n = n;
   const int64_t words = (L.total + 3) / 4;
-  const int64_t tot = words * n;
-  const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)ctx->sm_count * 16);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256,
+                                                                         ((int64_t)ctx->sm_count * 16 + n - 1) / n));
   const int kt = ktimer_begin(ctx, s, "container_pack");
-  container_pack_kernel<<<grid, 256, 0, s>>>(a, words);
+  for (int done = 0; done < n; done += 65535) {
+    container_pack_kernel<<<dim3(gx, (unsigned)std::min(n - done, 65535)), 256, 0, s>>>(a, words, done);
+    ctx->launches++;
+  }
   ktimer_end(ctx, s, kt);
-  ctx->launches++;
   return cuda_status(cudaGetLastError(), "container pack launch");
 }
 
@@ -279,12 +279,15 @@ int abcs_container_unpack_batch(abcs_ctx* c, const abcs_sense_plan* plan, const 
   container_validate_kernel<<<(unsigned)n, 256, 0, s>>>(a);
   ktimer_end(ctx, s, kt);
   ctx->launches++;
-  const int64_t tot = (L.nB + L.K + L.S) * n;
-  const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)ctx->sm_count * 16);
+  const int64_t per = L.nB + L.K + L.S;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256,
+                                                                         ((int64_t)ctx->sm_count * 16 + n - 1) / n));
   kt = ktimer_begin(ctx, s, "container_unpack");
-  container_unpack_kernel<<<grid, 256, 0, s>>>(a);
+  for (int done = 0; done < n; done += 65535) {
+    container_unpack_kernel<<<dim3(gx, (unsigned)std::min(n - done, 65535)), 256, 0, s>>>(a, done);
+    ctx->launches++;
+  }
   ktimer_end(ctx, s, kt);
-  ctx->launches++;
   return cuda_status(cudaGetLastError(), "container unpack launch");
 }
 
