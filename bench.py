@@ -380,6 +380,14 @@ def run_ours(args, world, rank, local):
         except Exception as e:
             container = {"error": repr(e)[:200]}
 
+    # batched quality metrics of the subrate-0.3 decode against its sources
+    metrics = None
+    if rank == 0:
+        try:
+            metrics = metrics_bench(p, torch, imgs, outs[1], hbm)
+        except Exception as e:
+            metrics = {"error": repr(e)[:200]}
+
     # the other BASELINE configs (parity-test workloads, not bench lines): device throughput and
     # algorithmic-bytes roofline fraction of sense+decode (and IDA) on this rank's GPU
     configs = None
@@ -419,6 +427,7 @@ def run_ours(args, world, rank, local):
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
             "ida": ida,
             "container": container,
+            "metrics": metrics,
             "configs": configs,
             "clocks": clk,
             "cpu_baseline": cpu,
@@ -462,6 +471,30 @@ def container_bench(p, torch, b, hbm):
             "pack_frac": round((src + dst) / ms_pack / 1e6 / hbm, 4),
             "unpack_ms": round(ms_unpack, 4), "unpack_gbs": round((src + dst) / ms_unpack / 1e6, 1),
             "unpack_frac": round((src + dst) / ms_unpack / 1e6 / hbm, 4)}
+
+
+def metrics_bench(p, torch, refs, dec, hbm):
+    """mse+psnr and ssim (metrics.cpp:63-125) of 1024 decoded 512^2 images: algorithmic bytes
+    = u8 reference + f32 image per pixel."""
+    n = refs.shape[0]
+    px = n * refs.shape[1] * refs.shape[2]
+
+    def t(want, reps=3):
+        p.quality_batch(refs, dec, want)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            p.quality_batch(refs, dec, want)
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    ms_p, ms_s = t(("mse", "psnr")), t(("ssim",))
+    return {"workload": f"{n} x 512^2 decoded (DD 3/10) vs sources",
+            "mse_psnr_ms": round(ms_p, 4), "mse_psnr_frac": round(5 * px / ms_p / 1e6 / hbm, 4),
+            "ssim_ms": round(ms_s, 4), "ssim_mp_s": round(px / ms_s / 1e3, 1),
+            "ssim_note": "fp64 11x11 Gaussian statistics in the reference's operation order (FP64-pipe bound)"}
 
 
 SWEEP = [  # (name, H, W, n, B, num, den, algorithm, ellipses, sigma, seed, video, ida_iterations)

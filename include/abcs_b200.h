@@ -255,6 +255,19 @@ int abcs_psnr_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, int
                     const float* d_img, int64_t img_stride, int32_t img_pitch, int32_t height,
                     int32_t width, int32_t n_images, double* d_psnr, void* stream);
 
+/* ssim (metrics.cpp:79-116) of f32 images against u8 references, per image (f64): 11x11
+ * Gaussian window (sigma 1.5), valid window positions only, fp64 statistics in the
+ * reference's operation order. Images must be at least 11x11. */
+int abcs_ssim_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch,
+                    const float* d_img, int64_t img_stride, int32_t img_pitch, int32_t height,
+                    int32_t width, int32_t n_images, double* d_ssim, void* stream);
+
+/* quality (metrics.cpp:63-130): mse, psnr and ssim per image (each output nullable; f64). */
+int abcs_quality_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch,
+                       const float* d_img, int64_t img_stride, int32_t img_pitch, int32_t height,
+                       int32_t width, int32_t n_images, double* d_mse, double* d_psnr, double* d_ssim,
+                       void* stream);
+
 /* ---- .abcs v1 measurement container (container.cpp:58-149) ------------------
  * Layout (little-endian, packed): "ABCS" | version u16 = 1 | H u32 | W u32 | B u16 |
  * algorithm u8 | C_R num u32 | C_R den u32 | threshold f64 | n_B u32 | counts u16[n_B] |

@@ -565,6 +565,59 @@ double o_psnr(const double* ref, const double* test, long long n) {
   return 10.0 * log10(255.0 * 255.0 / err);
 }
 
+/* metrics.cpp:27-48 (windowed_mean: horizontal then vertical Gaussian pass over the
+ * valid window positions) and metrics.cpp:79-116 (ssim). Returns NAN below 11x11. */
+static void o_windowed_mean(const double* img, int H, int W, const double* k, double* out) {
+  const int Hv = H - 10, Wv = W - 10;
+  double* horiz = (double*)malloc(sizeof(double) * (size_t)H * Wv);
+  for (int r = 0; r < H; ++r)
+    for (int c = 0; c < Wv; ++c) {
+      double acc = 0.0;
+      for (int i = 0; i < 11; ++i) acc += k[i] * img[(size_t)r * W + c + i];
+      horiz[(size_t)r * Wv + c] = acc;
+    }
+  for (int r = 0; r < Hv; ++r)
+    for (int c = 0; c < Wv; ++c) {
+      double acc = 0.0;
+      for (int j = 0; j < 11; ++j) acc += k[j] * horiz[(size_t)(r + j) * Wv + c];
+      out[(size_t)r * Wv + c] = acc;
+    }
+  free(horiz);
+}
+
+double o_ssim(const double* ref, const double* test, int H, int W) {
+  if (H < 11 || W < 11) return NAN;
+  double k[11], sum = 0.0;
+  for (int i = 0; i < 11; ++i) {
+    const double d = i - 5.0;
+    k[i] = exp(-0.5 * d * d / (1.5 * 1.5));
+    sum += k[i];
+  }
+  for (int i = 0; i < 11; ++i) k[i] /= sum;
+  const size_t n = (size_t)H * W, nv = (size_t)(H - 10) * (W - 10);
+  double* buf = (double*)malloc(sizeof(double) * (3 * n + 5 * nv));
+  double *xx = buf, *yy = buf + n, *xy = buf + 2 * n, *m = buf + 3 * n;
+  for (size_t i = 0; i < n; ++i) {
+    xx[i] = ref[i] * ref[i];
+    yy[i] = test[i] * test[i];
+    xy[i] = ref[i] * test[i];
+  }
+  o_windowed_mean(ref, H, W, k, m);
+  o_windowed_mean(test, H, W, k, m + nv);
+  o_windowed_mean(xx, H, W, k, m + 2 * nv);
+  o_windowed_mean(yy, H, W, k, m + 3 * nv);
+  o_windowed_mean(xy, H, W, k, m + 4 * nv);
+  const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+  double acc = 0.0;
+  for (size_t i = 0; i < nv; ++i) {
+    const double mx = m[i], my = m[nv + i];
+    const double vx = m[2 * nv + i] - mx * mx, vy = m[3 * nv + i] - my * my, cov = m[4 * nv + i] - mx * my;
+    acc += ((2.0 * mx * my + C1) * (2.0 * cov + C2)) / ((mx * mx + my * my + C1) * (vx + vy + C2));
+  }
+  free(buf);
+  return acc / (double)nv;
+}
+
 /* recon.cpp:53-73 */
 static int check_finite(const double* x, long long nx, const double* z, long long nz, int it) {
   char msg[128];

@@ -63,6 +63,7 @@ int o_reconstruct_ida(int rows, int cols, int B, const uint16_t* counts, const d
                       int* div_iter);
 
 double o_psnr(const double* ref, const double* test, long long n);
+double o_ssim(const double* ref, const double* test, int H, int W);
 
 #ifdef __cplusplus
 }

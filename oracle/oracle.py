@@ -149,6 +149,17 @@ class CPort:
                                          out.ctypes.data_as(P)))
         return out
 
+    def quality(self, ref, test):
+        """(mse, psnr, ssim) -- metrics.cpp:63-125 restated (o_psnr, o_ssim)."""
+        a = np.ascontiguousarray(ref, dtype=np.float64)
+        b = np.ascontiguousarray(test, dtype=np.float64)
+        self.lib.o_psnr.restype = C.c_double
+        self.lib.o_ssim.restype = C.c_double
+        mse = float(np.mean((a - b) ** 2))
+        ps = self.lib.o_psnr(a.ctypes.data_as(P), b.ctypes.data_as(P), C.c_longlong(a.size))
+        ss = self.lib.o_ssim(a.ctypes.data_as(P), b.ctypes.data_as(P), a.shape[0], a.shape[1])
+        return mse, ps, ss
+
     def reconstruct_ida(self, rows, cols, B, counts, coeffs, iters, damping=2.0, k=2.7, dblock=8, ref=None):
         c = np.ascontiguousarray(counts, dtype=np.uint16)
         y = np.ascontiguousarray(coeffs, dtype=np.float64)
@@ -286,6 +297,16 @@ class Reference:
         y = np.ascontiguousarray(coeffs, dtype=np.float64)
         return self.lib.ref_ms_make(rows * B, cols * B, B, 0, C.c_uint32(1), C.c_uint32(1), C.c_double(0.0),
                                     c.ctypes.data_as(P), c.size, y.ctypes.data_as(P), C.c_longlong(y.size))
+
+    def quality(self, ref, test):
+        """abcs::quality -> (mse, psnr, ssim)."""
+        a = np.ascontiguousarray(ref, dtype=np.float64)
+        b = np.ascontiguousarray(test, dtype=np.float64)
+        m, p_, s_ = C.c_double(), C.c_double(), C.c_double()
+        self.lib.ref_quality.argtypes = [P, P, C.c_int, C.c_int, P, P, P]
+        self._err(self.lib.ref_quality(a.ctypes.data_as(P), b.ctypes.data_as(P), a.shape[0], a.shape[1],
+                                       C.byref(m), C.byref(p_), C.byref(s_)))
+        return m.value, p_.value, s_.value
 
     def write_container(self, ms, path):
         """abcs::write_measurement_set on a MeasurementSet given as a dict (sense()'s layout)."""

@@ -125,6 +125,19 @@ void ref_ms_set_side(void* p, const double* side, long long n) {
   static_cast<Handle*>(p)->ms.side.assign(side, side + n);
 }
 
+// abcs::quality (metrics.cpp:118-125) of two images given as doubles.
+int ref_quality(const double* a, const double* b, int h, int w, double* mse, double* psnr, double* ssim) {
+  return guarded([&] {
+    abcs::PixelImage x(h, w), y(h, w);
+    x.data.assign(a, a + (size_t)h * w);
+    y.data.assign(b, b + (size_t)h * w);
+    const abcs::QualityReport q = abcs::quality(x, y);
+    *mse = q.mse;
+    *psnr = q.psnr_db;
+    *ssim = q.ssim;
+  });
+}
+
 // abcs::write_measurement_set / read_measurement_set (container.cpp:58-149)
 int ref_container_write(void* p, const char* path) {
   return guarded([&] { abcs::write_measurement_set(static_cast<Handle*>(p)->ms, path); });

@@ -104,6 +104,8 @@ SIGNATURES = {
     "abcs_container_pack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, P, P, I32, P, I64, P]),
     "abcs_container_unpack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, P, P, P, P, P]),
     "abcs_container_parse": (C.c_int, [P, I64, C.POINTER(SensePlanC)]),
+    "abcs_quality_batch": (C.c_int, [P, P, I64, I32, P, I64, I32, I32, I32, I32, P, P, P, P]),
+    "abcs_ssim_batch": (C.c_int, [P, P, I64, I32, P, I64, I32, I32, I32, I32, P, P]),
     "abcs_psnr_batch": (C.c_int, [P, P, I64, I32, P, I64, I32, I32, I32, I32, P, P]),
     "abcs_ida_init_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, I32, P, P, P, P]),
     "abcs_ida_step_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC), P, P, P, I32,

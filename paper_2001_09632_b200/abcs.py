@@ -878,6 +878,63 @@ def denoise(spec: DenoiserSpec, field_values, sigma: float) -> np.ndarray:
     return out.cpu().numpy()
 
 
+# ---- quality metrics (metrics.hpp; metrics.cpp:63-130) ---------------------------------
+@dataclass
+class QualityReport:
+    psnr_db: float = 0.0
+    ssim: float = 0.0
+    mse: float = 0.0
+
+
+def quality_batch(refs, images, want=("mse", "psnr", "ssim")):
+    """Per-image (mse, psnr, ssim) of f32 images (n,H,W) against u8 references (n,H',W') >= (H,W)
+    (references are cropped to the images), on the device. Returns a dict of float64 tensors."""
+    torch = _torch()
+    n, H, W = images.shape
+    dev = images.device
+    out = {k: torch.empty(n, dtype=torch.float64, device=dev) for k in want}
+    im = images.contiguous()
+    _check(_lib.load().abcs_quality_batch(Context.get(dev.index).handle, refs.data_ptr(), refs.stride(0),
+                                          refs.stride(1), im.data_ptr(), im.stride(0), im.stride(1), H, W, n,
+                                          _ptr(out.get("mse")), _ptr(out.get("psnr")), _ptr(out.get("ssim")),
+                                          _stream_ptr(torch)))
+    return out
+
+
+def _pair(ref, test):
+    torch = _torch()
+    r = _as_u8_image(ref)
+    t = np.ascontiguousarray(np.asarray(test, dtype=np.float32))
+    if r.shape != t.shape:
+        raise ValueError("metric: image dimensions differ")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return torch.from_numpy(np.ascontiguousarray(r)).to(dev)[None], torch.from_numpy(t).to(dev)[None]
+
+
+def quality(ref, test) -> QualityReport:
+    """abcs::quality (metrics.cpp:118-125); `ref` must hold 8-bit integer values (the device path)."""
+    r, t = _pair(ref, test)
+    q = quality_batch(r, t)
+    return QualityReport(float(q["psnr"][0]), float(q["ssim"][0]), float(q["mse"][0]))
+
+
+def mse(ref, test) -> float:
+    r, t = _pair(ref, test)
+    return float(quality_batch(r, t, ("mse",))["mse"][0])
+
+
+def psnr(ref, test) -> float:
+    r, t = _pair(ref, test)
+    return float(quality_batch(r, t, ("psnr",))["psnr"][0])
+
+
+def ssim(ref, test) -> float:
+    r, t = _pair(ref, test)
+    if r.shape[1] < 11 or r.shape[2] < 11:
+        raise ValueError("ssim: images smaller than the 11x11 window")
+    return float(quality_batch(r, t, ("ssim",))["ssim"][0])
+
+
 # ---- .abcs v1 container (container.hpp:8-14, container.cpp:58-149) --------------------
 def container_size(plan: SensePlanC) -> int:
     return int(_lib.load().abcs_container_size(C.byref(plan)))

@@ -554,6 +554,45 @@ int abcs_psnr_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
+int abcs_ssim_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, const float* d_img,
+                    int64_t img_stride, int32_t img_pitch, int32_t height, int32_t width, int32_t n, double* d_ssim,
+                    void* stream) {
+  CHECK_CTX(c);
+  if (height < 1 || width < 1 || n < 0 || ref_pitch < width || img_pitch < width ||
+      (n > 0 && (!d_ref || !d_img || !d_ssim)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (height < 11 || width < 11)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_ssim(ctx, d_ref, ref_stride, ref_pitch, d_img, img_stride, img_pitch, height, width, n, d_ssim,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_quality_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, const float* d_img,
+                       int64_t img_stride, int32_t img_pitch, int32_t height, int32_t width, int32_t n,
+                       double* d_mse, double* d_psnr, double* d_ssim, void* stream) {
+  CHECK_CTX(c);
+  if (height < 1 || width < 1 || n < 0 || ref_pitch < width || img_pitch < width ||
+      (n > 0 && (!d_ref || !d_img || (!d_mse && !d_psnr && !d_ssim))))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (d_ssim && (height < 11 || width < 11))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_mse || d_psnr) {
+    const int st = launch_psnr(ctx, d_ref, ref_stride, ref_pitch, d_img, img_stride, img_pitch, height, width, n,
+                               d_psnr, s, d_mse);
+    if (st) return st;
+  }
+  if (d_ssim) return launch_ssim(ctx, d_ref, ref_stride, ref_pitch, d_img, img_stride, img_pitch, height, width, n,
+                                 d_ssim, s);
+  return ABCS_OK;
+}
+
 int abcs_ida_check(const int32_t* h_diverged, int32_t n, int32_t* first_image) {
   if (first_image) *first_image = -1;
   if (!h_diverged) return ABCS_OK;

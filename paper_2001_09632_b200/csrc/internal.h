@@ -82,7 +82,9 @@ struct IdaParams;
 int ida_mma_region();
 void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s);
 int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s);
+                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr);
+int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
+                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s);
 size_t ida_state_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n);
 int launch_ida_state(Ctx* ctx, bool init, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
                      const int32_t* offsets, const float* y, int64_t y_stride, int32_t n, int warm, double damping,

@@ -2,6 +2,7 @@
 // mse accumulated in fp64 over the h x w pixels, psnr = 10 log10(255^2 / mse), +inf
 // when mse == 0. Row slabs -> per-CTA fp64 partials -> fixed-order fold per image
 // (deterministic). Used for the Idct branch of reconstruct()'s trace (recon.cpp:217-221).
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -37,17 +38,146 @@ sse_partials_kernel(const uint8_t* __restrict__ ref, int64_t ref_stride, int ref
 }
 
 __global__ void psnr_fold_kernel(const double* __restrict__ partials, int parts, int n, double pixels,
-                                 double* __restrict__ psnr) {
+                                 double* __restrict__ psnr, double* __restrict__ mse_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double sse = 0.0;
   for (int p = 0; p < parts; ++p) sse += partials[(int64_t)i * parts + p];
   const double mse = sse / pixels;
-  psnr[i] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(255.0 * 255.0 / mse);
+  if (mse_out) mse_out[i] = mse;
+  if (psnr) psnr[i] = mse == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(255.0 * 255.0 / mse);
+}
+
+// ---------------------------------------------------------------------------
+// ssim (metrics.cpp:79-116): 11x11 Gaussian window (sigma 1.5, normalised), means over
+// every fully interior window position, fp64 statistics. The separable passes run in
+// the reference's order (horizontal then vertical, taps ascending, multiply then add --
+// no fused multiply-add), so each window mean equals the reference's; the map average
+// is folded per image from per-tile fp64 partials in a fixed order.
+constexpr int kSsimWin = 11;
+constexpr int kSsimTR = 16, kSsimTC = 32;        // output (window) positions per tile: rows x cols
+constexpr int kSsimInR = kSsimTR + kSsimWin - 1, kSsimInC = kSsimTC + kSsimWin - 1;  // 26 x 42
+constexpr int kSsimThreads = 256;
+
+struct SsimKernel {
+  double k[kSsimWin];
+};
+
+static SsimKernel ssim_kernel_weights() {
+  SsimKernel w;
+  double sum = 0.0;
+  for (int i = 0; i < kSsimWin; ++i) {
+    const double d = i - (kSsimWin - 1) / 2.0;
+    w.k[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+    sum += w.k[i];
+  }
+  for (double& v : w.k) v /= sum;
+  return w;
+}
+
+__global__ void __launch_bounds__(kSsimThreads)
+ssim_tiles_kernel(const uint8_t* __restrict__ ref, int64_t ref_stride, int ref_pitch, const float* __restrict__ img,
+                  int64_t img_stride, int img_pitch, int H, int W, int tiles_x, SsimKernel kw,
+                  double* __restrict__ partials) {
+  __shared__ float s_x[kSsimInR][kSsimInC + 1], s_y[kSsimInR][kSsimInC + 1];
+  __shared__ double s_h[5][kSsimInR][kSsimTC];  // horizontal pass: x, y, xx, yy, xy
+  __shared__ double s_red[kSsimThreads / 32];
+  const int image = blockIdx.y, tile = blockIdx.x;
+  const int r0 = (tile / tiles_x) * kSsimTR, c0 = (tile % tiles_x) * kSsimTC;
+  const int Hv = H - kSsimWin + 1, Wv = W - kSsimWin + 1;
+  const uint8_t* R = ref + image * ref_stride;
+  const float* X = img + image * img_stride;
+  for (int i = threadIdx.x; i < kSsimInR * kSsimInC; i += kSsimThreads) {
+    const int r = i / kSsimInC, c = i % kSsimInC;
+    const int gr = r0 + r, gc = c0 + c;
+    const bool in = gr < H && gc < W;
+    s_x[r][c] = in ? (float)R[(int64_t)gr * ref_pitch + gc] : 0.f;
+    s_y[r][c] = in ? X[(int64_t)gr * img_pitch + gc] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSsimInR * kSsimTC; i += kSsimThreads) {
+    const int r = i / kSsimTC, c = i % kSsimTC;
+    double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < kSsimWin; ++t) {
+      const double x = s_x[r][c + t], y = s_y[r][c + t];
+      const double kt = kw.k[t];
+      a[0] = __dadd_rn(a[0], __dmul_rn(kt, x));
+      a[1] = __dadd_rn(a[1], __dmul_rn(kt, y));
+      a[2] = __dadd_rn(a[2], __dmul_rn(kt, __dmul_rn(x, x)));
+      a[3] = __dadd_rn(a[3], __dmul_rn(kt, __dmul_rn(y, y)));
+      a[4] = __dadd_rn(a[4], __dmul_rn(kt, __dmul_rn(x, y)));
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) s_h[q][r][c] = a[q];
+  }
+  __syncthreads();
+  const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kSsimTR * kSsimTC; i += kSsimThreads) {
+    const int r = i / kSsimTC, c = i % kSsimTC;
+    if (r0 + r >= Hv || c0 + c >= Wv) continue;
+    double m[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < kSsimWin; ++t) {
+      const double kt = kw.k[t];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) m[q] = __dadd_rn(m[q], __dmul_rn(kt, s_h[q][r + t][c]));
+    }
+    const double mx = m[0], my = m[1];
+    const double var_x = __dadd_rn(m[2], -__dmul_rn(mx, mx));
+    const double var_y = __dadd_rn(m[3], -__dmul_rn(my, my));
+    const double cov = __dadd_rn(m[4], -__dmul_rn(mx, my));
+    const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, mx), my), C1), __dadd_rn(__dmul_rn(2.0, cov), C2));
+    const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my)), C1),
+                                 __dadd_rn(__dadd_rn(var_x, var_y), C2));
+    acc += __ddiv_rn(num, den);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kSsimThreads / 32; ++w) t += s_red[w];
+    partials[(int64_t)image * gridDim.x + tile] = t;
+  }
+}
+
+__global__ void ssim_fold_kernel(const double* __restrict__ partials, int tiles, int n, double windows,
+                                 double* __restrict__ ssim) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int t = 0; t < tiles; ++t) s += partials[(int64_t)i * tiles + t];
+  ssim[i] = s / windows;
+}
+
+int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
+                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s) {
+  const int Hv = h - kSsimWin + 1, Wv = w - kSsimWin + 1;
+  const int tx = (Wv + kSsimTC - 1) / kSsimTC, ty = (Hv + kSsimTR - 1) / kSsimTR;
+  int st;
+  double* partials = static_cast<double*>(ctx_scratch(ctx, (size_t)n * tx * ty * 8, s, &st));
+  if (st) return st;
+  const SsimKernel kw = ssim_kernel_weights();
+  const int kt = ktimer_begin(ctx, s, "ssim");
+  for (int done = 0; done < n;) {
+    const int cnt = std::min(n - done, 65535);
+    ssim_tiles_kernel<<<dim3(tx * ty, cnt), kSsimThreads, 0, s>>>(ref + done * ref_stride, ref_stride, ref_pitch,
+                                                                  img + done * img_stride, img_stride, img_pitch, h,
+                                                                  w, tx, kw, partials + (int64_t)done * tx * ty);
+    ctx->launches++;
+    done += cnt;
+  }
+  ssim_fold_kernel<<<(n + 127) / 128, 128, 0, s>>>(partials, tx * ty, n, (double)Hv * (double)Wv, ssim);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "ssim launch");
 }
 
 int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s) {
+                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse) {
   const int parts = (h + kMetricRowsPerCta - 1) / kMetricRowsPerCta;
   int st;
   double* partials = static_cast<double*>(ctx_scratch(ctx, (size_t)n * parts * 8, s, &st));
@@ -60,7 +190,7 @@ int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch,
     ctx->launches++;
     done += cnt;
   }
-  psnr_fold_kernel<<<(n + 127) / 128, 128, 0, s>>>(partials, parts, n, (double)h * (double)w, psnr);
+  psnr_fold_kernel<<<(n + 127) / 128, 128, 0, s>>>(partials, parts, n, (double)h * (double)w, psnr, mse);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "psnr launch");
 }

@@ -400,6 +400,25 @@ def test_ida_divergence(p):
 
 
 # ---- full-size properties (BASELINE sizes) -------------------------------------------------
+def test_quality_metrics_on_device(p, torch, checker):
+    """mse / psnr / ssim (metrics.cpp:63-125) of decoded images against their sources."""
+    imgs = synth(100, 90, n=3, seed=17)
+    t = torch.from_numpy(imgs).cuda()
+    cfg = p.SensingConfig(16, 1, 4, p.Algorithm.DD)
+    b, dec = p.sense_decode_batch(t, cfg)
+    q = p.quality_batch(t, dec)
+    dec_h = dec.cpu().numpy()
+    for i in range(3):
+        m, ps, ss = checker.quality(imgs[i, :96, :80], dec_h[i])
+        assert float(q["mse"][i]) == pytest.approx(m, rel=1e-12)
+        assert abs(float(q["psnr"][i]) - ps) <= 1e-9
+        assert abs(float(q["ssim"][i]) - ss) <= 1e-12
+    rep = p.quality(imgs[0, :96, :80], dec_h[0])
+    assert rep.ssim == pytest.approx(float(q["ssim"][0]), abs=1e-15) and p.psnr(imgs[0], imgs[0]) == float("inf")
+    with pytest.raises(ValueError):
+        p.ssim(np.zeros((10, 30), np.uint8), np.zeros((10, 30), np.float32))
+
+
 def test_spec_known_answers_on_device(p, torch):
     """SPEC.md worked examples through the product path."""
     assert list(p.largest_remainder_allocate([10, 20, 30, 40], 900, [1024] * 4)) == [90, 180, 270, 360]

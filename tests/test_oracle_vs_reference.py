@@ -163,3 +163,14 @@ def test_ida_divergence_and_validation(port, ref):
     with pytest.raises(o.OracleError) as eb:
         port.reconstruct_ida(2, 2, 16, ms["counts"], huge, 3)
     assert ea.value.code == eb.value.code == 3 and ea.value.iteration == eb.value.iteration
+
+
+def test_quality_metrics(port, ref, rng):
+    """metrics.cpp:63-125: mse / psnr / ssim restated in the C port."""
+    for H, W in ((11, 11), (40, 53), (96, 64)):
+        a = rng.integers(0, 256, (H, W)).astype(np.float64)
+        b = np.clip(a + rng.normal(0, 7, a.shape), -20, 280)
+        m0, p0, s0 = ref.quality(a, b)
+        m1, p1, s1 = port.quality(a, b)
+        assert m1 == pytest.approx(m0, rel=1e-12) and p1 == p0 and s1 == s0
+    assert ref.quality(a, a)[1] == float("inf") and port.quality(a, a)[1] == float("inf")
