@@ -106,6 +106,32 @@ typedef struct {
   double k;                /* DenoiserSpec param "k" (2.7) */
 } abcs_ida_config;
 
+/* abcs::ReconConfig (recon.hpp:32-41) + DenoiserSpec (denoise.hpp:19-27) for every method. */
+typedef enum {
+  ABCS_RECON_IDCT = 0,
+  ABCS_RECON_ISTA = 1,
+  ABCS_RECON_AMP = 2,
+  ABCS_RECON_DAMP = 3,
+  ABCS_RECON_DAMPD = 4,
+  ABCS_RECON_IDA = 5
+} abcs_recon_method;
+typedef enum {
+  ABCS_DENOISER_DCT_THRESHOLD = 0, /* params k (2.7), block (8) */
+  ABCS_DENOISER_BLUR = 1,          /* param sigma_scale (25) */
+  ABCS_DENOISER_IDENTITY = 2
+} abcs_denoiser_kind;
+typedef struct {
+  int32_t method;          /* abcs_recon_method */
+  int32_t iterations;      /* >= 1 */
+  double damping;          /* D_F >= 1 */
+  double lambda;           /* ISTA/AMP soft-threshold multiplier >= 0 */
+  uint64_t seed;           /* DAMP divergence-probe seed */
+  int32_t denoiser;        /* abcs_denoiser_kind */
+  int32_t denoiser_block;  /* dct_threshold "block" */
+  double k;                /* dct_threshold "k" */
+  double sigma_scale;      /* blur "sigma_scale" */
+} abcs_recon_config;
+
 /* Seeded synthetic scene generator; mirrors csrc/synth_gen.h sg_spec. */
 typedef struct {
   int32_t height, width;
@@ -297,6 +323,40 @@ int abcs_container_unpack_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, cons
 /* Host: the layout of one container (header checks, counts summed for K, side count,
  * exact size) as a plan for abcs_container_unpack_batch. */
 int abcs_container_parse(const uint8_t* h_bytes, int64_t size, abcs_sense_plan* plan);
+
+/* reconstruct() (recon.cpp:199-259) for every iterative method (Ista, Amp, Damp, DampD,
+ * Ida with any denoiser) and Idct; arguments as abcs_ida_batch. Ida with the 8x8
+ * dct_threshold takes the fused kernel path of abcs_ida_batch. */
+int abcs_reconstruct_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                           const uint16_t* d_counts, const int32_t* d_offsets, const float* d_y,
+                           int64_t y_stride, int32_t n_images, const abcs_recon_config* cfg,
+                           const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, float* d_out,
+                           int64_t out_stride, int32_t out_pitch, double* d_trace, int32_t* d_diverged,
+                           void* stream);
+
+/* ista_step / amp_step / damp_step (recon.cpp:133-197) on caller-owned state (layout as
+ * abcs_ida_init_state), in place; `iteration` is the state's iteration count BEFORE the step
+ * (the AMP first-step convention and the DAMP probe seed depend on it). */
+int abcs_recon_step_state(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                          const uint16_t* d_counts, const int32_t* d_offsets, const float* d_y,
+                          int64_t y_stride, int32_t n_images, const abcs_recon_config* cfg, float* d_x,
+                          float* d_z, double* d_sigma, int32_t iteration, int32_t* d_diverged,
+                          void* stream);
+
+/* denoise (denoise.cpp:96-109) with any denoiser of cfg; sigma per image (host array). */
+int abcs_denoise_batch(abcs_ctx* ctx, const float* d_field, int32_t height, int32_t width,
+                       int64_t field_stride, int32_t n_images, const double* sigma,
+                       const abcs_recon_config* cfg, float* d_out, void* stream);
+
+/* divergence (denoise.cpp:111-128): Monte-Carlo divergence of cfg's denoiser at each field
+ * with a std::mt19937_64(seed) Rademacher probe; sigma and epsilon per image (host arrays),
+ * result per image into d_div (f64). */
+int abcs_divergence_batch(abcs_ctx* ctx, const float* d_field, int32_t height, int32_t width,
+                          int32_t n_images, const double* sigma, const double* epsilon, uint64_t seed,
+                          const abcs_recon_config* cfg, double* d_div, void* stream);
+
+/* The first n outputs' parity bits of std::mt19937_64(seed) as +1/-1 floats (the probe). */
+int abcs_rademacher_probe(abcs_ctx* ctx, uint64_t seed, int64_t n, float* d_probe, void* stream);
 
 /* Synthetic inputs on the device (same bytes as abcs_synth_generate_host). */
 int abcs_synth_generate(abcs_ctx* ctx, const abcs_synth_spec* spec, int64_t first_index,

@@ -298,6 +298,52 @@ class Reference:
         return self.lib.ref_ms_make(rows * B, cols * B, B, 0, C.c_uint32(1), C.c_uint32(1), C.c_double(0.0),
                                     c.ctypes.data_as(P), c.size, y.ctypes.data_as(P), C.c_longlong(y.size))
 
+    def reconstruct(self, rows, cols, B, counts, coeffs, method, iters, damping=2.0, lam=1.0, seed=42, denoiser=0,
+                    k=2.7, dblock=8, sigma_scale=25.0, ref=None):
+        """abcs::reconstruct with every ReconConfig field -> (image, trace rows)."""
+        h = self._make(rows, cols, B, counts, coeffs)
+        try:
+            out = np.zeros((rows * B, cols * B))
+            trace = np.zeros((iters + 1, 4))
+            nrows, div = C.c_int(), C.c_int(0)
+            r = None if ref is None else _u8(ref)
+            self.lib.ref_reconstruct2.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_ulonglong,
+                                                  C.c_int, C.c_double, C.c_double, C.c_double, P, C.c_int, C.c_int,
+                                                  P, P, P, P]
+            st = self.lib.ref_reconstruct2(h, int(method), iters, damping, lam, seed, denoiser, k, float(dblock),
+                                           sigma_scale, None if r is None else r.ctypes.data_as(P),
+                                           0 if r is None else r.shape[0], 0 if r is None else r.shape[1],
+                                           out.ctypes.data_as(P), trace.ctypes.data_as(P), C.byref(nrows),
+                                           C.byref(div))
+            self._err(st, div.value)
+            return out, trace[:nrows.value]
+        finally:
+            self.lib.ref_ms_free(h)
+
+    def denoise2(self, field, sigma, denoiser=0, k=2.7, dblock=8, sigma_scale=25.0):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        out = np.zeros_like(f)
+        self.lib.ref_denoise2.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, P]
+        self._err(self.lib.ref_denoise2(f.ctypes.data_as(P), f.shape[0], f.shape[1], sigma, denoiser, k,
+                                        float(dblock), sigma_scale, out.ctypes.data_as(P)))
+        return out
+
+    def divergence(self, field, sigma, eps, seed, denoiser=0, k=2.7, dblock=8, sigma_scale=25.0):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        out = C.c_double()
+        self.lib.ref_divergence.argtypes = [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_ulonglong, C.c_int,
+                                            C.c_double, C.c_double, C.c_double, P]
+        self._err(self.lib.ref_divergence(f.ctypes.data_as(P), f.shape[0], f.shape[1], sigma, eps, seed, denoiser, k,
+                                          float(dblock), sigma_scale, C.byref(out)))
+        return out.value
+
+    def mt19937_64(self, seed, n):
+        out = np.zeros(n, np.uint64)
+        self.lib.ref_mt19937_64.argtypes = [C.c_ulonglong, C.c_longlong, P]
+        self.lib.ref_mt19937_64(seed, n, out.ctypes.data_as(P))
+        return out
+
     def quality(self, ref, test):
         """abcs::quality -> (mse, psnr, ssim)."""
         a = np.ascontiguousarray(ref, dtype=np.float64)

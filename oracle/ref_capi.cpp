@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -123,6 +124,72 @@ void ref_ms_free(void* p) { delete static_cast<Handle*>(p); }
 
 void ref_ms_set_side(void* p, const double* side, long long n) {
   static_cast<Handle*>(p)->ms.side.assign(side, side + n);
+}
+
+// Denoiser spec from (name id, k, block, sigma_scale): 0 dct_threshold, 1 blur, 2 identity.
+static abcs::DenoiserSpec make_spec(int kind, double k, double dblock, double sigma_scale) {
+  abcs::DenoiserSpec spec;
+  spec.name = kind == 1 ? "blur" : (kind == 2 ? "identity" : "dct_threshold");
+  spec.params["k"] = k;
+  spec.params["block"] = dblock;
+  spec.params["sigma_scale"] = sigma_scale;
+  return spec;
+}
+
+// abcs::reconstruct with every ReconConfig field (recon.cpp:199-259).
+int ref_reconstruct2(void* p, int method, int iters, double damping, double lambda, unsigned long long seed,
+                     int denoiser, double k, double dblock, double sigma_scale, const uint8_t* ref_px, int ref_h,
+                     int ref_w, double* out, double* trace, int* trace_rows, int* div_iter) {
+  return guarded(
+      [&] {
+        abcs::ReconConfig cfg;
+        cfg.method = static_cast<abcs::ReconMethod>(method);
+        cfg.iterations = iters;
+        cfg.damping = damping;
+        cfg.lambda = lambda;
+        cfg.seed = seed;
+        cfg.denoiser = make_spec(denoiser, k, dblock, sigma_scale);
+        abcs::PixelImage refimg;
+        if (ref_px) refimg = to_image(ref_px, ref_h, ref_w);
+        const auto res = abcs::reconstruct(static_cast<Handle*>(p)->ms, cfg, ref_px ? &refimg : nullptr);
+        std::memcpy(out, res.image.data.data(), res.image.data.size() * sizeof(double));
+        if (trace) {
+          for (size_t i = 0; i < res.trace.size(); ++i) {
+            trace[4 * i + 0] = res.trace[i].iteration;
+            trace[4 * i + 1] = res.trace[i].residual_norm;
+            trace[4 * i + 2] = res.trace[i].sigma;
+            trace[4 * i + 3] = res.trace[i].psnr_db;
+          }
+        }
+        if (trace_rows) *trace_rows = static_cast<int>(res.trace.size());
+      },
+      div_iter);
+}
+
+// abcs::denoise with any spec; abcs::divergence (denoise.cpp:96-128).
+int ref_denoise2(const double* field, int h, int w, double sigma, int denoiser, double k, double dblock,
+                 double sigma_scale, double* out) {
+  return guarded([&] {
+    abcs::PixelImage img(h, w);
+    std::memcpy(img.data.data(), field, img.data.size() * sizeof(double));
+    const auto d = abcs::denoise(make_spec(denoiser, k, dblock, sigma_scale), img, sigma);
+    std::memcpy(out, d.data.data(), d.data.size() * sizeof(double));
+  });
+}
+
+int ref_divergence(const double* field, int h, int w, double sigma, double eps, unsigned long long seed, int denoiser,
+                   double k, double dblock, double sigma_scale, double* out) {
+  return guarded([&] {
+    abcs::PixelImage img(h, w);
+    std::memcpy(img.data.data(), field, img.data.size() * sizeof(double));
+    *out = abcs::divergence(make_spec(denoiser, k, dblock, sigma_scale), img, sigma, eps, seed);
+  });
+}
+
+// The first n outputs of std::mt19937_64(seed) (the generator behind the divergence probe).
+void ref_mt19937_64(unsigned long long seed, long long n, unsigned long long* out) {
+  std::mt19937_64 rng(seed);
+  for (long long i = 0; i < n; ++i) out[i] = rng();
 }
 
 // abcs::quality (metrics.cpp:118-125) of two images given as doubles.

@@ -63,6 +63,12 @@ class SynthSpecC(C.Structure):
     ]
 
 
+class ReconConfigC(C.Structure):
+    _fields_ = [("method", C.c_int32), ("iterations", C.c_int32), ("damping", C.c_double), ("lambda_", C.c_double),
+                ("seed", C.c_uint64), ("denoiser", C.c_int32), ("denoiser_block", C.c_int32), ("k", C.c_double),
+                ("sigma_scale", C.c_double)]
+
+
 class ContainerInfoC(C.Structure):
     _fields_ = [("algorithm", C.c_int32), ("cr_num", C.c_uint32), ("cr_den", C.c_uint32), ("status", C.c_int32),
                 ("threshold", C.c_double)]
@@ -100,6 +106,13 @@ SIGNATURES = {
     "abcs_ida_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC),
                                  P, I64, I32, P, I64, I32, P, P, P]),
     "abcs_ida_check": (C.c_int, [P, I32, C.POINTER(I32)]),
+    "abcs_reconstruct_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(ReconConfigC),
+                                         P, I64, I32, P, I64, I32, P, P, P]),
+    "abcs_recon_step_state": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(ReconConfigC), P, P, P, I32,
+                                        P, P]),
+    "abcs_denoise_batch": (C.c_int, [P, P, I32, I32, I64, I32, P, C.POINTER(ReconConfigC), P, P]),
+    "abcs_divergence_batch": (C.c_int, [P, P, I32, I32, I32, P, P, U64, C.POINTER(ReconConfigC), P, P]),
+    "abcs_rademacher_probe": (C.c_int, [P, U64, I64, P, P]),
     "abcs_container_size": (I64, [C.POINTER(SensePlanC)]),
     "abcs_container_pack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, P, P, I32, P, I64, P]),
     "abcs_container_unpack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, P, P, P, P, P]),

@@ -512,6 +512,62 @@ def ida_batch(batch: MeasurementBatch, cfg: ReconConfig, reference=None, out=Non
     return out, tr, div
 
 
+_DENOISERS = {"dct_threshold": 0, "blur": 1, "identity": 2}
+
+
+def _recon_c(cfg: "ReconConfig", method=None, denoiser: "DenoiserSpec" = None):
+    d = cfg.denoiser if denoiser is None else denoiser
+    if d.name not in _DENOISERS:
+        raise ValueError(f"unknown denoiser: '{d.name}'")
+    c = _lib.ReconConfigC()
+    c.method = int(cfg.method if method is None else method)
+    c.iterations = cfg.iterations
+    c.damping = cfg.damping
+    c.lambda_ = cfg.lambda_
+    c.seed = cfg.seed
+    c.denoiser = _DENOISERS[d.name]
+    c.denoiser_block = int(d.param("block", 8.0))
+    c.k = d.param("k", 2.7)
+    c.sigma_scale = d.param("sigma_scale", 25.0)
+    return c
+
+
+def recon_batch(batch: MeasurementBatch, cfg: ReconConfig, reference=None, out=None, trace: bool = True,
+                check: bool = True):
+    """reconstruct() for every set with any method (Ista/Amp/Damp/DampD/Ida with any denoiser):
+    (images (n,Hc,Wc) f32, trace (n,T,4) f64 | None, diverged (n,2) int32)."""
+    torch = _torch()
+    cfg.validate()
+    p = batch.plan
+    Hc, Wc = p.rows * p.block, p.cols * p.block
+    dev = batch.counts.device
+    if out is None:
+        out = torch.empty((batch.n, Hc, Wc), dtype=torch.float32, device=dev)
+    tr = torch.empty((batch.n, cfg.iterations + 1, 4), dtype=torch.float64, device=dev) if trace else None
+    div = torch.zeros((batch.n, 2), dtype=torch.int32, device=dev)
+    ref_ptr, ref_stride, ref_pitch = None, 0, 0
+    if reference is not None:
+        if reference.dtype != torch.uint8 or reference.dim() != 3:
+            raise ValueError("reference must be a (n, H, W) uint8 CUDA tensor")
+        if reference.shape[1] < Hc or reference.shape[2] < Wc:
+            raise ValueError("reconstruct: reference smaller than decoded image")
+        reference = reference.contiguous()
+        ref_ptr, ref_stride, ref_pitch = reference.data_ptr(), reference.shape[1] * reference.shape[2], reference.shape[2]
+    c = _recon_c(cfg)
+    _check(_lib.load().abcs_reconstruct_batch(
+        Context.get(dev.index).handle, p.rows, p.cols, p.block, _ptr(batch.counts), _ptr(batch.offsets),
+        _ptr(batch.payload), batch.payload.stride(0) if batch.payload.numel() else p.coeffs_per_image, batch.n,
+        C.byref(c), ref_ptr, ref_stride, ref_pitch, out.data_ptr(), Hc * Wc, Wc, _ptr(tr), div.data_ptr(),
+        _stream_ptr(torch)))
+    if check:
+        h = div.cpu().numpy()
+        first = C.c_int32()
+        st = _lib.load().abcs_ida_check(h.ctypes.data, batch.n, C.byref(first))
+        if st != _lib.OK:
+            _check(st, iteration=int(h[first.value, 0]))
+    return out, tr, div
+
+
 # ---- single-image API (reference signatures) -------------------------------------------
 def _batch_from_host(ms: MeasurementSet, coeffs=None) -> MeasurementBatch:
     torch = _torch()
@@ -782,12 +838,10 @@ def reconstruct(ms: MeasurementSet, cfg: ReconConfig, reference=None) -> ReconRe
                                                out.data_ptr(), _stream_ptr(torch)))
             trace.append(TraceRow(0, 0.0, 0.0, float(out.item())))
         return ReconResult(img, trace)
-    if cfg.method != ReconMethod.Ida:
-        raise UnsupportedError(f"method {recon_method_name(cfg.method)} is not on the device path (IDA and IDCT are)")
     if ms.total_coeffs() != len(ms.coeffs):
         raise ValueError("init_state: measurement vector length mismatch")
     b = _batch_from_host(ms)
-    out, tr, _ = ida_batch(b, cfg, reference=ref_t, trace=True, check=True)
+    out, tr, _ = recon_batch(b, cfg, reference=ref_t, trace=True, check=True)
     rows = [TraceRow(int(r[0]), float(r[1]), float(r[2]), float(r[3])) for r in tr[0].cpu().numpy()]
     return ReconResult(out[0].cpu().numpy(), rows)
 
@@ -819,21 +873,13 @@ def init_state(op: "SensingOperator", y, warm: bool) -> ReconState:
     return ReconState(x.cpu().numpy(), z[:yy.size].cpu().numpy(), float(sig.item()), 0)
 
 
-def damp_step(state: ReconState, op: "SensingOperator", y, denoiser: DenoiserSpec, variant: ReconMethod,
-              damping: float, seed: int = 42) -> None:
-    """recon.cpp:170-197 (variant Ida) via abcs_ida_step_state; updates `state` in place and raises
-    DivergenceError like finish_step/check_finite (recon.cpp:81-93, 53-73)."""
+def _step(state: ReconState, op: "SensingOperator", y, cfg: "ReconConfig", method: ReconMethod) -> None:
+    """One ista/amp/damp step on the explicit state via abcs_recon_step_state; raises DivergenceError
+    like finish_step/check_finite (recon.cpp:81-93, 53-73) after updating the state."""
     torch = _torch()
-    if variant not in (ReconMethod.Damp, ReconMethod.DampD, ReconMethod.Ida):
-        raise ValueError("damp_step: variant must be damp, dampd or ida")
-    if variant != ReconMethod.Ida:
-        raise UnsupportedError("damp_step: only the Ida variant is on the device path")
-    cfg = ReconConfig(ReconMethod.Ida, 1, damping, denoiser)
-    if damping < 1.0:
-        raise ValueError("damping factor D_F must be >= 1")
     yy = np.ascontiguousarray(np.asarray(y, dtype=np.float32).reshape(-1))
     if yy.size != op.measurements() or np.size(state.z) != yy.size or np.size(state.x) != op.field_size():
-        raise ValueError("damp_step: state / measurement size mismatch")
+        raise ValueError("step: state / measurement size mismatch")
     b = _batch_from_host(op._ms(yy))
     g = op.grid()
     dev = b.counts.device
@@ -841,11 +887,12 @@ def damp_step(state: ReconState, op: "SensingOperator", y, denoiser: DenoiserSpe
     z = torch.from_numpy(np.ascontiguousarray(np.asarray(state.z, dtype=np.float32).reshape(-1))).to(dev)
     sig = torch.tensor([float(state.sigma)], dtype=torch.float64, device=dev)
     div = torch.zeros(2, dtype=torch.int32, device=dev)
-    c = cfg._ida_c()
-    _check(_lib.load().abcs_ida_step_state(Context.get(dev.index).handle, g.rows, g.cols, g.block, _ptr(b.counts),
-                                           _ptr(b.offsets), _ptr(b.payload), yy.size, 1, C.byref(c), x.data_ptr(),
-                                           z.data_ptr(), sig.data_ptr(), state.iteration + 1, div.data_ptr(),
-                                           _stream_ptr(torch)))
+    c = _recon_c(cfg, method)
+    c.iterations = 1
+    _check(_lib.load().abcs_recon_step_state(Context.get(dev.index).handle, g.rows, g.cols, g.block, _ptr(b.counts),
+                                             _ptr(b.offsets), _ptr(b.payload), yy.size, 1, C.byref(c), x.data_ptr(),
+                                             z.data_ptr(), sig.data_ptr(), state.iteration, div.data_ptr(),
+                                             _stream_ptr(torch)))
     state.x = x.cpu().numpy()
     state.z = z.cpu().numpy()
     state.sigma = float(sig.item())
@@ -856,6 +903,54 @@ def damp_step(state: ReconState, op: "SensingOperator", y, denoiser: DenoiserSpe
         raise DivergenceError(f"solver diverged ({what}) at iteration {int(d[0])}", int(d[0]))
 
 
+def ista_step(state: ReconState, op: "SensingOperator", y, lam: float) -> None:
+    """recon.cpp:133-142"""
+    _step(state, op, y, ReconConfig(ReconMethod.Ista, 1, 2.0, DenoiserSpec(), lam), ReconMethod.Ista)
+
+
+def amp_step(state: ReconState, op: "SensingOperator", y, lam: float) -> None:
+    """recon.cpp:144-168"""
+    _step(state, op, y, ReconConfig(ReconMethod.Amp, 1, 2.0, DenoiserSpec(), lam), ReconMethod.Amp)
+
+
+def damp_step(state: ReconState, op: "SensingOperator", y, denoiser: DenoiserSpec, variant: ReconMethod,
+              damping: float, seed: int = 42) -> None:
+    """recon.cpp:170-197 for variants Damp, DampD and Ida, any denoiser."""
+    if variant not in (ReconMethod.Damp, ReconMethod.DampD, ReconMethod.Ida):
+        raise ValueError("damp_step: variant must be damp, dampd or ida")
+    if damping < 1.0:
+        raise ValueError("damping factor D_F must be >= 1")
+    _step(state, op, y, ReconConfig(variant, 1, damping, denoiser, 1.0, seed), variant)
+
+
+def divergence(spec: DenoiserSpec, field_values, sigma: float, epsilon: float, seed: int) -> float:
+    """denoise.cpp:111-128 on the device (std::mt19937_64 Rademacher probe)."""
+    torch = _torch()
+    if epsilon <= 0:
+        raise ValueError("divergence: epsilon must be > 0")
+    f = np.ascontiguousarray(np.asarray(field_values, dtype=np.float32))
+    H, W = f.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ft = torch.from_numpy(f).to(dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    c = _recon_c(ReconConfig(), None, spec)
+    s_ = (C.c_double * 1)(sigma)
+    e_ = (C.c_double * 1)(epsilon)
+    _check(_lib.load().abcs_divergence_batch(Context.get(dev.index).handle, ft.data_ptr(), H, W, 1, s_, e_, seed,
+                                             C.byref(c), out.data_ptr(), _stream_ptr(torch)))
+    return float(out.item())
+
+
+def rademacher_probe(seed: int, n: int):
+    """std::mt19937_64(seed)'s first n outputs mapped (bit 0) to +1/-1 (denoise.cpp:115-116), on the device."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    _check(_lib.load().abcs_rademacher_probe(Context.get(dev.index).handle, seed, n, out.data_ptr(),
+                                             _stream_ptr(torch)))
+    return out
+
+
 def denoise(spec: DenoiserSpec, field_values, sigma: float) -> np.ndarray:
     """denoise.cpp:96-109 (dct_threshold on device; identity passes through)."""
     torch = _torch()
@@ -864,17 +959,15 @@ def denoise(spec: DenoiserSpec, field_values, sigma: float) -> np.ndarray:
     f = np.ascontiguousarray(np.asarray(field_values, dtype=np.float32))
     if spec.name == "identity":
         return f.copy()
-    if spec.name == "blur":
-        raise UnsupportedError("the blur denoiser is not on the device path")
-    if spec.name != "dct_threshold":
+    if spec.name not in ("dct_threshold", "blur"):
         raise ValueError(f"unknown denoiser: '{spec.name}'")
     H, W = f.shape
     ft = torch.from_numpy(f).cuda()
     out = torch.empty_like(ft)
     s = (C.c_double * 1)(sigma)
-    _check(_lib.load().abcs_denoise_dct_batch(Context.get().handle, ft.data_ptr(), H, W, H * W, 1, s,
-                                              spec.param("k", 2.7), int(spec.param("block", 8.0)),
-                                              out.data_ptr(), _stream_ptr(torch)))
+    c = _recon_c(ReconConfig(), None, spec)
+    _check(_lib.load().abcs_denoise_batch(Context.get().handle, ft.data_ptr(), H, W, H * W, 1, s, C.byref(c),
+                                          out.data_ptr(), _stream_ptr(torch)))
     return out.cpu().numpy()
 
 

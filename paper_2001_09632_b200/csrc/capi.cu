@@ -593,6 +593,164 @@ int abcs_quality_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, in
   return ABCS_OK;
 }
 
+// ReconConfig::validate (recon.cpp:39-43) + the device path's denoiser restrictions
+static int recon_config_check(const abcs_recon_config* cfg, int32_t Hc, int32_t Wc) {
+  if (!cfg) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null config");
+  if (cfg->iterations < 1) return set_error(ABCS_ERR_INVALID_ARGUMENT, "iterations must be >= 1");
+  if (cfg->damping < 1.0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "damping factor D_F must be >= 1");
+  if (cfg->lambda < 0.0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "lambda must be >= 0");
+  if (cfg->method < ABCS_RECON_IDCT || cfg->method > ABCS_RECON_IDA)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "unknown reconstruction method");
+  const bool uses_denoiser = cfg->method >= ABCS_RECON_DAMP;
+  if (uses_denoiser) {
+    if (cfg->denoiser == ABCS_DENOISER_DCT_THRESHOLD) {
+      const int b = std::max(1, std::min(cfg->denoiser_block, std::min(Hc, Wc)));
+      if (b != 8 || Hc % 4 || Wc % 4)
+        return set_error(ABCS_ERR_UNSUPPORTED, "device dct_threshold supports 8x8 tiles on dims divisible by 4");
+    } else if (cfg->denoiser == ABCS_DENOISER_BLUR) {
+      if (!(cfg->sigma_scale > 0.0)) return set_error(ABCS_ERR_UNSUPPORTED, "blur denoiser needs sigma_scale > 0");
+    } else if (cfg->denoiser != ABCS_DENOISER_IDENTITY) {
+      return set_error(ABCS_ERR_INVALID_ARGUMENT, "unknown denoiser");
+    }
+  }
+  return ABCS_OK;
+}
+
+int abcs_reconstruct_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                           const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n,
+                           const abcs_recon_config* cfg, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch,
+                           float* d_out, int64_t out_stride, int32_t out_pitch, double* d_trace, int32_t* d_diverged,
+                           void* stream) {
+  CHECK_CTX(c);
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_out)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  int st = recon_config_check(cfg, rows * block, cols * block);
+  if (st) return st;
+  if (out_pitch < cols * block) return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch smaller than the image");
+  if (n == 0) return ABCS_OK;
+  if (cfg->method == ABCS_RECON_IDCT)
+    return abcs_decode_batch(c, rows, cols, block, d_counts, d_offsets, d_y, y_stride, n, d_out, out_stride,
+                             out_pitch, nullptr, nullptr, stream);
+  if (cfg->method == ABCS_RECON_IDA && cfg->denoiser == ABCS_DENOISER_DCT_THRESHOLD) {
+    abcs_ida_config ic{};
+    ic.iterations = cfg->iterations;
+    ic.denoiser_block = cfg->denoiser_block;
+    ic.damping = cfg->damping;
+    ic.k = cfg->k;
+    return abcs_ida_batch(c, rows, cols, block, d_counts, d_offsets, d_y, y_stride, n, &ic, d_ref, ref_stride,
+                          ref_pitch, d_out, out_stride, out_pitch, d_trace, d_diverged, stream);
+  }
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_recon(ctx, false, rows, cols, block, d_counts, d_offsets, d_y, y_stride, n, *cfg, d_ref, ref_stride,
+                      ref_pitch, nullptr, nullptr, nullptr, 0, d_out, out_stride, out_pitch, d_trace, d_diverged,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_recon_step_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
+                          const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n,
+                          const abcs_recon_config* cfg, float* d_x, float* d_z, double* d_sigma, int32_t iteration,
+                          int32_t* d_diverged, void* stream) {
+  CHECK_CTX(c);
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_x || !d_z || !d_sigma)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  int st = recon_config_check(cfg, rows * block, cols * block);
+  if (st) return st;
+  if (cfg->method == ABCS_RECON_IDCT) return set_error(ABCS_ERR_INVALID_ARGUMENT, "Idct has no iteration step");
+  if (iteration < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "iteration must be >= 0");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_recon(ctx, true, rows, cols, block, d_counts, d_offsets, d_y, y_stride, n, *cfg, nullptr, 0, 0, d_x,
+                      d_z, d_sigma, iteration, nullptr, 0, 0, nullptr, d_diverged,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_denoise_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int64_t field_stride,
+                       int32_t n, const double* sigma, const abcs_recon_config* cfg, float* d_out, void* stream) {
+  CHECK_CTX(c);
+  if (!cfg || height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_out || !sigma)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (sigma[i] < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "denoise: sigma must be >= 0");
+  if (cfg->denoiser == ABCS_DENOISER_DCT_THRESHOLD)
+    return abcs_denoise_dct_batch(c, d_field, height, width, field_stride, n, sigma, cfg->k, cfg->denoiser_block,
+                                  d_out, stream);
+  if (field_stride != (int64_t)height * width)
+    return set_error(ABCS_ERR_UNSUPPORTED, "blur / identity denoisers take dense fields");
+  if (cfg->denoiser == ABCS_DENOISER_BLUR && !(cfg->sigma_scale > 0.0))
+    return set_error(ABCS_ERR_UNSUPPORTED, "blur denoiser needs sigma_scale > 0");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t N = (int64_t)height * width;
+  int st;
+  char* scr = static_cast<char*>(ctx_scratch(ctx, align_up((size_t)n * N * 4, 256) + align_up((size_t)n * 8, 256),
+                                             s, &st));
+  if (st) return st;
+  double* sig = reinterpret_cast<double*>(scr + align_up((size_t)n * N * 4, 256));
+  cudaError_t e = cudaMemcpyAsync(sig, sigma, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "sigma upload");
+  return run_denoiser(ctx, *cfg, d_field, d_out, reinterpret_cast<float*>(scr), height, width, n, sig, nullptr, s);
+}
+
+int abcs_rademacher_probe(abcs_ctx* c, uint64_t seed, int64_t n, float* d_probe, void* stream) {
+  CHECK_CTX(c);
+  if (n < 0 || (n > 0 && !d_probe)) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_probe(ctx, seed, n, d_probe, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_divergence_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int32_t n,
+                          const double* sigma, const double* epsilon, uint64_t seed, const abcs_recon_config* cfg,
+                          double* d_div, void* stream) {
+  CHECK_CTX(c);
+  if (!cfg || height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_div || !sigma || !epsilon)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (!(epsilon[i] > 0)) return set_error(ABCS_ERR_INVALID_ARGUMENT, "divergence: epsilon must be > 0");
+  if (cfg->denoiser == ABCS_DENOISER_DCT_THRESHOLD && (height % 4 || width % 4 ||
+                                                       std::max(1, std::min(cfg->denoiser_block,
+                                                                            std::min(height, width))) != 8))
+    return set_error(ABCS_ERR_UNSUPPORTED, "device dct_threshold supports 8x8 tiles on dims divisible by 4");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t N = (int64_t)height * width;
+  const size_t fld = align_up((size_t)n * N * 4, 256);
+  const size_t parts = divergence_partials(ctx, N, n);
+  int st;
+  char* p = static_cast<char*>(ctx_scratch(ctx, 4 * fld + align_up((size_t)N * 4, 256) + 3 * align_up((size_t)n * 8, 256) +
+                                                   align_up(parts * 8, 256), s, &st));
+  if (st) return st;
+  float* base = reinterpret_cast<float*>(p);
+  float* pert = reinterpret_cast<float*>(p + fld);
+  float* moved = reinterpret_cast<float*>(p + 2 * fld);
+  float* tmp = reinterpret_cast<float*>(p + 3 * fld);
+  float* probe = reinterpret_cast<float*>(p + 4 * fld);
+  double* sig = reinterpret_cast<double*>(p + 4 * fld + align_up((size_t)N * 4, 256));
+  double* eps = sig + align_up((size_t)n * 8, 256) / 8;
+  double* thr = eps + align_up((size_t)n * 8, 256) / 8;
+  double* partials = thr + align_up((size_t)n * 8, 256) / 8;
+  cudaError_t e = cudaMemcpyAsync(sig, sigma, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(eps, epsilon, (size_t)n * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "divergence upload");
+  st = launch_probe(ctx, seed, N, probe, s);
+  if (!st) st = launch_divergence_given(ctx, d_field, probe, nullptr, N, n, eps, pert, nullptr, nullptr, nullptr, true, s);
+  if (!st) st = run_denoiser(ctx, *cfg, d_field, base, tmp, height, width, n, sig, thr, s);
+  if (!st) st = run_denoiser(ctx, *cfg, pert, moved, tmp, height, width, n, sig, thr, s);
+  if (!st) st = launch_divergence_given(ctx, nullptr, probe, base, N, n, eps, nullptr, moved, partials, d_div, false, s);
+  return st;
+}
+
 int abcs_ida_check(const int32_t* h_diverged, int32_t n, int32_t* first_image) {
   if (first_image) *first_image = -1;
   if (!h_diverged) return ABCS_OK;

@@ -181,7 +181,7 @@ __device__ void block_phase(const IdaParams& P, int img, int R0, int C0, const f
         const float ax = ta.zz(flat);
         const float yv = P.y[off + k];
         const float zo = P.is_init ? 0.f : P.z[off + k];
-        const float zn = (yv - ax) + P.onsager * zo;
+        const float zn = (yv - ax) + (P.onsager_img ? (float)P.onsager_img[img] : P.onsager) * zo;
         P.z[off + k] = zn;
         tb.zz(flat) = zn;
         zsum += (double)zn * (double)zn;
@@ -327,9 +327,19 @@ __global__ void __launch_bounds__(kIdaThreads) ida_step_kernel(IdaParams P) {
   const int img = blockIdx.y;
   const int region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kRegion, C0 = (region % P.regions_x) * kRegion;
-  const float thr = (float)(P.k * P.sigma_in[img]);
-  load_halo(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s_in);
-  denoise_region(s_in, s_x, s_tile, R0, C0, P.Hc, P.Wc, thr);
+  if (P.x_in) {  // x from another denoiser
+    for (int i = threadIdx.x; i < kRegion * kRegion; i += kIdaThreads) {
+      const int r = i / kRegion, c = i % kRegion;
+      s_x[r * kAccPitch + c] = (R0 + r < P.Hc && C0 + c < P.Wc)
+                                   ? P.x_in[(int64_t)img * P.Hc * P.Wc + (int64_t)(R0 + r) * P.Wc + C0 + c]
+                                   : 0.f;
+    }
+    __syncthreads();
+  } else {
+    const float thr = (float)(P.k * P.sigma_in[img]);
+    load_halo(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s_in);
+    denoise_region(s_in, s_x, s_tile, R0, C0, P.Hc, P.Wc, thr);
+  }
   block_phase<B>(P, img, R0, C0, s_x, s_tile, s_zz, s_mine);
   finish_image(P, img, region, s_mine);
 }
@@ -548,6 +558,218 @@ int launch_ida_state(Ctx* ctx, bool init, int32_t rows, int32_t cols, int32_t bl
   e = cudaMemcpyAsync(sigma, L.sigma + n, (size_t)n * 8, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_status(e, "ida sigma copy");
   return cuda_status(cudaGetLastError(), "ida state launch");
+}
+
+// ---- every iterative method (recon.cpp:133-259) -------------------------------------------
+namespace {
+
+// splitmix-style probe seed per iteration (recon.cpp:95-105)
+uint64_t probe_seed_for(uint64_t seed, int iteration) {
+  uint64_t v = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(iteration + 1);
+  v ^= v >> 30;
+  v *= 0xBF58476D1CE4E5B9ull;
+  v ^= v >> 27;
+  v *= 0x94D049BB133111EBull;
+  v ^= v >> 31;
+  return v;
+}
+
+struct ReconScratch {
+  IdaLayout L;          // block-phase reductions; L.pseudo[0] = pseudo field, L.pseudo[1] = new estimate
+  float* perturbed;     // DAMP: pseudo + eps * probe
+  float* moved;         // DAMP: D(perturbed)
+  float* tmp;           // blur intermediate
+  float* probe;         // Rademacher probe (one field, shared by the batch)
+  float* x;             // reconstruct(): state x
+  float* z;             // reconstruct(): state z
+  double* sigma;        // reconstruct(): state sigma
+  double* thr;          // k * sigma
+  double* eps;
+  double* onsager;
+  double* partials;
+  unsigned* maxbits;
+  unsigned long long* active;
+  int32_t* offsets;     // computed when the caller passes none
+};
+
+}  // namespace
+
+// Denoise `in` -> `out` with the configured denoiser at sigma (device, per image) (denoise.cpp:96-109).
+int run_denoiser(Ctx* ctx, const abcs_recon_config& cfg, const float* in, float* out, float* tmp,
+                        int H, int W, int n, const double* sigma, double* thr, cudaStream_t s) {
+  const int64_t N = (int64_t)H * W;
+  if (cfg.denoiser == ABCS_DENOISER_IDENTITY) {
+    return cuda_status(cudaMemcpyAsync(out, in, (size_t)n * N * 4, cudaMemcpyDeviceToDevice, s), "identity denoiser");
+  }
+  if (cfg.denoiser == ABCS_DENOISER_DCT_THRESHOLD) {
+    int st = launch_scale(ctx, sigma, cfg.k, n, thr, s);
+    if (st) return st;
+    return launch_denoise(ctx, in, H, W, N, n, thr, out, s);
+  }
+  // blur: the radius depends on sigma (device) -> read the batch's largest sigma first
+  std::vector<double> h(n);
+  cudaError_t e = cudaMemcpyAsync(h.data(), sigma, (size_t)n * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "blur sigma readback");
+  double smax = 0.0;
+  for (double v : h) smax = std::max(smax, v);
+  const int rmax = std::max(1, (int)std::ceil(3.0 * smax / cfg.sigma_scale));
+  void* wbuf = nullptr;
+  e = cudaMallocAsync(&wbuf, (size_t)n * (2 * rmax + 1) * 8 + (size_t)n * 4, s);
+  if (e != cudaSuccess) return cuda_status(e, "blur weights alloc");
+  double* w = static_cast<double*>(wbuf);
+  int* r = reinterpret_cast<int*>(w + (size_t)n * (2 * rmax + 1));
+  int st = launch_blur(ctx, in, tmp, out, H, W, n, sigma, cfg.sigma_scale, rmax, w, r, s);
+  cudaFreeAsync(wbuf, s);
+  return st;
+}
+
+int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
+                 const int32_t* offsets_in, const float* y, int64_t y_stride, int32_t n, const abcs_recon_config& cfg,
+                 const uint8_t* ref, int64_t ref_stride, int32_t ref_pitch, float* x_state, float* z_state,
+                 double* sigma_state, int32_t iteration0, float* out, int64_t out_stride, int32_t out_pitch,
+                 double* trace, int32_t* diverged, cudaStream_t s) {
+  if (block != 8 && block != 16 && block != 32)
+    return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (n > 65535) return set_error(ABCS_ERR_UNSUPPORTED, "reconstruction batch limited to 65535 images per call");
+  const IdaGeometry G = geometry(rows, cols, block);
+  const int64_t N = G.Hc * G.Wc;
+  const bool damp = cfg.method == ABCS_RECON_DAMP || cfg.method == ABCS_RECON_DAMPD;
+  // one ctx scratch request for everything
+  abcs_ida_config one{};
+  one.iterations = 1;
+  const size_t base = ida_scratch_bytes(rows, cols, block, y_stride, n, one);
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  const size_t fld = al((size_t)n * N * 4);
+  const size_t parts = divergence_partials(ctx, N, n);
+  size_t need = base + 3 * fld + al((size_t)N * 4) + 6 * al((size_t)n * 8) + al(parts * 8) + al((size_t)n * 4) +
+                al((size_t)n * rows * cols * 4);
+  if (!one_step) need += fld + al((size_t)n * y_stride * 4) + al((size_t)n * 8);
+  int st;
+  char* p = static_cast<char*>(ctx_scratch(ctx, need, s, &st));
+  if (st) return st;
+  ReconScratch R{};
+  R.L = carve(p, G.Hc, G.Wc, y_stride, n, 1, G.regions);
+  p += base;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += b;
+    return r;
+  };
+  R.perturbed = reinterpret_cast<float*>(take(fld));
+  R.moved = reinterpret_cast<float*>(take(fld));
+  R.tmp = reinterpret_cast<float*>(take(fld));
+  R.probe = reinterpret_cast<float*>(take(al((size_t)N * 4)));
+  R.thr = reinterpret_cast<double*>(take(al((size_t)n * 8)));
+  R.eps = reinterpret_cast<double*>(take(al((size_t)n * 8)));
+  R.onsager = reinterpret_cast<double*>(take(al((size_t)n * 8)));
+  R.active = reinterpret_cast<unsigned long long*>(take(al((size_t)n * 8)));
+  double* sigma_next = reinterpret_cast<double*>(take(al((size_t)n * 8)));
+  double* Mimg = reinterpret_cast<double*>(take(al((size_t)n * 8)));  // op.measurements() per image
+  R.partials = reinterpret_cast<double*>(take(al(parts * 8)));
+  R.maxbits = reinterpret_cast<unsigned*>(take(al((size_t)n * 4)));
+  R.offsets = reinterpret_cast<int32_t*>(take(al((size_t)n * rows * cols * 4)));
+  if (!one_step) {
+    R.x = reinterpret_cast<float*>(take(fld));
+    R.z = reinterpret_cast<float*>(take(al((size_t)n * y_stride * 4)));
+    R.sigma = reinterpret_cast<double*>(take(al((size_t)n * 8)));
+  } else {
+    R.x = x_state;
+    R.z = z_state;
+    R.sigma = sigma_state;
+  }
+  const int32_t* offsets = offsets_in;
+  if (!offsets) {
+    st = launch_offsets(ctx, rows * cols, n, block, counts, R.offsets, nullptr, nullptr, s);
+    if (st) return st;
+    offsets = R.offsets;
+  }
+  cudaError_t e = reset_reductions(R.L, n, diverged, s);
+  if (e != cudaSuccess) return cuda_status(e, "recon scratch init");
+  IdaParams P = base_params(G, R.L, rows, cols, n, counts, offsets, y, y_stride, cfg.k);
+  P.z = R.z;
+  P.ref = ref;
+  P.ref_stride = ref_stride;
+  P.ref_pitch = ref_pitch;
+  P.trace = trace;
+  P.trace_rows = cfg.iterations + 1;
+  P.diverged = diverged;
+  st = launch_measurements(ctx, counts, offsets, rows * cols, n, Mimg, s);
+  if (st) return st;
+  int it = iteration0;
+  if (!one_step) {  // warm start (init_state, recon.cpp:119-131): x0 = A* y, z0 = y - A x0, sigma0
+    P.is_init = 1;
+    P.warm = 1;
+    P.onsager = 0.f;
+    P.pseudo_out = nullptr;
+    P.x_out = R.x;
+    P.out_stride = N;
+    P.out_pitch = (int)G.Wc;
+    P.clamp_out = 0;
+    P.sigma_out = R.sigma;
+    P.trace_row = 0;
+    P.iteration = 0;
+    launch_one(ctx, block, G, P, s);
+    it = 0;
+  }
+  const int steps = one_step ? 1 : cfg.iterations;
+  for (int t = 0; t < steps; ++t) {
+    // pseudo_data (recon.cpp:75-79): P = A* z + x
+    float* pseudo = R.L.pseudo[0];
+    float* xn = R.L.pseudo[1];
+    st = launch_decode(ctx, rows, cols, block, counts, offsets, R.z, y_stride, n, pseudo, N, (int)G.Wc, s);
+    if (st) return st;
+    add_field_kernel<<<(unsigned)std::min<int64_t>((n * N + 255) / 256, (int64_t)ctx->sm_count * 8), 256, 0, s>>>(
+        pseudo, R.x, n * N);
+    ctx->launches++;
+    float onsager_scalar = 0.f;
+    const double* onsager_img = nullptr;
+    if (cfg.method == ABCS_RECON_ISTA || cfg.method == ABCS_RECON_AMP) {
+      st = launch_soft_threshold(ctx, pseudo, xn, N, n, R.sigma, cfg.lambda, R.active, s);
+      if (st) return st;
+      if (cfg.method == ABCS_RECON_AMP) {
+        st = launch_amp_onsager(ctx, R.active, n, Mimg, (double)N, it == 0, R.onsager, s);
+        if (st) return st;
+        onsager_img = R.onsager;
+      }
+    } else {
+      st = run_denoiser(ctx, cfg, pseudo, xn, R.tmp, (int)G.Hc, (int)G.Wc, n, R.sigma, R.thr, s);
+      if (st) return st;
+      if (damp) {
+        st = launch_probe(ctx, probe_seed_for(cfg.seed, it), N, R.probe, s);
+        if (!st) st = launch_divergence_prep(ctx, pseudo, R.probe, N, n, R.maxbits, R.perturbed, R.eps, s);
+        if (!st) st = run_denoiser(ctx, cfg, R.perturbed, R.moved, R.tmp, (int)G.Hc, (int)G.Wc, n, R.sigma, R.thr, s);
+        if (!st)
+          st = launch_damp_onsager(ctx, R.probe, R.moved, xn, N, n, R.eps, Mimg,
+                                   cfg.method == ABCS_RECON_DAMPD ? cfg.damping : 1.0, R.partials, R.onsager, s);
+        if (st) return st;
+        onsager_img = R.onsager;
+      } else {
+        onsager_scalar = (float)(1.0 / cfg.damping);  // Ida (recon.cpp:183-184)
+      }
+    }
+    // finish_step (recon.cpp:81-93) in the block phase with the new estimate precomputed
+    const bool last = !one_step && t + 1 == steps;
+    P.is_init = 0;
+    P.x_in = xn;
+    P.onsager = onsager_scalar;
+    P.onsager_img = onsager_img;
+    P.pseudo_in = nullptr;
+    P.pseudo_out = nullptr;
+    P.x_out = last ? out : R.x;
+    P.out_stride = last ? out_stride : N;
+    P.out_pitch = last ? out_pitch : (int)G.Wc;
+    P.clamp_out = last ? 1 : 0;
+    P.sigma_in = R.sigma;
+    P.sigma_out = sigma_next;
+    P.trace_row = it + 1;
+    P.iteration = it + 1;
+    launch_one(ctx, block, G, P, s);
+    e = cudaMemcpyAsync(R.sigma, sigma_next, (size_t)n * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "sigma copy");
+    ++it;
+  }
+  return cuda_status(cudaGetLastError(), "recon launch");
 }
 
 }  // namespace abcs_b200

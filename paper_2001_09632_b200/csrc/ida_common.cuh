@@ -42,6 +42,9 @@ struct IdaParams {
   int is_init;
   int warm;                // init: x0 = A* y (1) or x0 = 0 (0) (init_state, recon.cpp:119-131)
   int clamp_out;           // x_out gets clamp(x, 0, 255) (reconstruct's final estimate) or raw x (damp_step state)
+  const float* x_in;       // step: the new estimate precomputed by another denoiser (ISTA/AMP/DAMP, blur), pitch Wc;
+                           // nullptr = denoise pseudo_in with the fused dct_threshold
+  const double* onsager_img;  // per-image Onsager coefficient (AMP/DAMP), else the scalar `onsager`
 };
 
 // Last CTA of an image folds the region partials (fixed order, so the result

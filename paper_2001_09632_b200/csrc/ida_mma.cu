@@ -231,8 +231,8 @@ __device__ __forceinline__ void stage_yz(const IdaParams& P, int64_t off, int cn
 }
 
 __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax, float zo, unsigned long long gi,
-                                          IdaLaneSums& S) {
-  const float zn = (yv - ax) + P.onsager * zo;  // finish_step (recon.cpp:86-88)
+                                          IdaLaneSums& S, float onsager) {
+  const float zn = (yv - ax) + onsager * zo;  // finish_step (recon.cpp:86-88)
   S.z += (double)zn * (double)zn;
   if (!isfinite(zn)) S.badz = gi < S.badz ? gi : S.badz;
   return zn;
@@ -276,6 +276,7 @@ __device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem
 
 __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s, IdaLaneSums& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
   Frag16 f;
   load_frag16(f);
   uint32_t rank[8];
@@ -312,7 +313,8 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMm
       const int r = (int)rank[q];
       float zn = 0.f;
       if (r < cnt) {
-        zn = z_update(P, yb[r], Yt.v[q >> 2][q & 3], P.is_init ? 0.f : zb[r], (unsigned long long)(boff + r), S);
+        zn = z_update(P, yb[r], Yt.v[q >> 2][q & 3], P.is_init ? 0.f : zb[r], (unsigned long long)(boff + r), S,
+                      ons);
         zb[r] = zn;
       }
       Zm.v[q >> 2][q & 3] = zn;
@@ -377,6 +379,7 @@ __device__ void init_x8(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem&
 
 __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s, IdaLaneSums& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
   Frag8 f;
   load_frag8(f);
   uint32_t rank[2];
@@ -414,7 +417,8 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMma
       const int q = i >> 1, r = (int)rank[i & 1];
       float zn = 0.f;
       if (r < cnt[q]) {
-        zn = z_update(P, yb[64 * q + r], Yt[i], P.is_init ? 0.f : zb[64 * q + r], (unsigned long long)(boff[q] + r), S);
+        zn = z_update(P, yb[64 * q + r], Yt[i], P.is_init ? 0.f : zb[64 * q + r], (unsigned long long)(boff[q] + r), S,
+                      ons);
         zb[64 * q + r] = zn;
       }
       Zm[i] = zn;
@@ -483,6 +487,15 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
       init_x16(P, img, R0, C0, s);
     } else {
       init_x8(P, img, R0, C0, s);
+    }
+    __syncthreads();
+  } else if (P.x_in) {  // x from another denoiser: load the region
+    const float* xs = P.x_in + (int64_t)img * P.Hc * P.Wc;
+    for (int i = threadIdx.x; i < kMR * kMR / 4; i += kMThreads) {
+      const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (R0 + r < P.Hc && C0 + c < P.Wc) v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)(R0 + r) * P.Wc + C0 + c));
+      *reinterpret_cast<float4*>(s.acc + kMOff + r * kMP + c) = v;
     }
     __syncthreads();
   } else {

@@ -85,6 +85,33 @@ int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch,
                 int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr);
 int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
                 int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s);
+// reconstruction family (recon.cu)
+int launch_soft_threshold(Ctx* ctx, const float* pseudo, float* x, int64_t N, int n, const double* sigma,
+                          double lambda, unsigned long long* active, cudaStream_t s);
+int launch_measurements(Ctx* ctx, const uint16_t* counts, const int32_t* offsets, int nb, int n, double* M,
+                        cudaStream_t s);
+int launch_amp_onsager(Ctx* ctx, const unsigned long long* active, int n, const double* M, double N, bool first,
+                       double* onsager, cudaStream_t s);
+int launch_blur(Ctx* ctx, const float* in, float* tmp, float* out, int H, int W, int n, const double* sigma_dev,
+                double scale, int rmax, double* wscratch, int* rscratch, cudaStream_t s);
+int launch_probe(Ctx* ctx, uint64_t seed, int64_t N, float* probe, cudaStream_t s);
+int launch_divergence_prep(Ctx* ctx, const float* pseudo, const float* probe, int64_t N, int n, unsigned* maxbits,
+                           float* perturbed, double* eps, cudaStream_t s);
+int launch_damp_onsager(Ctx* ctx, const float* probe, const float* moved, const float* base, int64_t N, int n,
+                        const double* eps, const double* M, double divisor, double* partials, double* onsager,
+                        cudaStream_t s);
+size_t divergence_partials(Ctx* ctx, int64_t N, int n);
+int launch_scale(Ctx* ctx, const double* sigma, double k, int n, double* thr, cudaStream_t s);
+int launch_divergence_given(Ctx* ctx, const float* field, const float* probe, const float* base, int64_t N, int n,
+                            const double* eps, float* perturbed, const float* moved, double* partials,
+                            double* div, bool perturb_only, cudaStream_t s);
+int run_denoiser(Ctx* ctx, const abcs_recon_config& cfg, const float* in, float* out, float* tmp, int H, int W, int n,
+                 const double* sigma, double* thr, cudaStream_t s);
+int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
+                 const int32_t* offsets, const float* y, int64_t y_stride, int32_t n, const abcs_recon_config& cfg,
+                 const uint8_t* ref, int64_t ref_stride, int32_t ref_pitch, float* x, float* z, double* sigma,
+                 int32_t iteration0, float* out, int64_t out_stride, int32_t out_pitch, double* trace,
+                 int32_t* diverged, cudaStream_t s);
 size_t ida_state_scratch_bytes(int32_t rows, int32_t cols, int32_t block, int64_t y_stride, int32_t n);
 int launch_ida_state(Ctx* ctx, bool init, int32_t rows, int32_t cols, int32_t block, const uint16_t* counts,
                      const int32_t* offsets, const float* y, int64_t y_stride, int32_t n, int warm, double damping,

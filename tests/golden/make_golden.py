@@ -106,9 +106,47 @@ def main_containers():
     np.savez_compressed(os.path.join(HERE, "container_cases.npz"), **out)
 
 
+FAMILY_CASES = [  # (name, method, iters, lambda, seed, denoiser, sigma_scale, damping)
+    ("ista", 1, 4, 0.05, 42, 0, 25.0, 2.0), ("amp", 2, 3, 0.5, 42, 0, 25.0, 2.0),
+    ("damp_dct", 3, 3, 1.0, 42, 0, 25.0, 2.0), ("dampd_dct", 4, 3, 1.0, 7, 0, 25.0, 3.0),
+    ("damp_blur", 3, 3, 1.0, 42, 1, 25.0, 2.0), ("ida_blur", 5, 3, 1.0, 42, 1, 5.0, 2.0),
+    ("ida_identity", 5, 2, 1.0, 42, 2, 25.0, 2.0)]
+
+
+def main_family():
+    """tests/golden/family_cases.npz: the rest of the reconstruction family from the reference
+    (recon.cpp:133-259, denoise.cpp:14-128) and std::mt19937_64 outputs for the probe."""
+    ref = o.Reference()
+    rng = np.random.default_rng(2001)
+    out = {}
+    img = p.synth_images_host(p.SynthSpec(64, 64, 20, 5.0, 41), 0, 1)[0]
+    ms = ref.sense(img, 16, 1, 4, 1)
+    out["img"], out["counts"], out["coeffs"] = img, ms["counts"], ms["coeffs"]
+    for name, method, iters, lam, seed, den, scale, damping in FAMILY_CASES:
+        x, tr = ref.reconstruct(4, 4, 16, ms["counts"], ms["coeffs"], method, iters, damping=damping, lam=lam,
+                                seed=seed, denoiser=den, sigma_scale=scale, ref=img)
+        out[f"{name}_x"], out[f"{name}_trace"] = x, tr
+    img8 = p.synth_images_host(p.SynthSpec(48, 40, 20, 5.0, 42), 0, 1)[0]
+    ms8 = ref.sense(img8, 8, 1, 5, 1)
+    out["img8"], out["counts8"], out["coeffs8"] = img8, ms8["counts"], ms8["coeffs"]
+    out["amp8_x"], out["amp8_trace"] = ref.reconstruct(6, 5, 8, ms8["counts"], ms8["coeffs"], 2, 3, lam=0.5, ref=img8)
+    field = rng.normal(128, 40, (40, 56))
+    out["field"] = field
+    for sig in (0.0, 7.0, 60.0, 400.0):
+        out[f"blur_{int(sig)}"] = ref.denoise2(field, sig, denoiser=1, sigma_scale=25.0)
+    out["div"] = np.array([ref.divergence(field, 20.0, 0.3, 99, denoiser=0),
+                           ref.divergence(field, 80.0, 0.5, 12345, denoiser=1, sigma_scale=25.0)])
+    for seed in (0, 42, 0x9E3779B97F4A7C15):
+        out[f"mt_{seed:x}"] = ref.mt19937_64(seed, 2000)
+    np.savez_compressed(os.path.join(HERE, "family_cases.npz"), **out)
+
+
 if __name__ == "__main__":
     if "--containers" in sys.argv:
         main_containers()
+    elif "--family" in sys.argv:
+        main_family()
     else:
         main()
         main_containers()
+        main_family()

@@ -366,8 +366,8 @@ def test_ida_state_cold_start_and_divergence(p):
         p.init_state(op, ms.coeffs[:-1], True)
     with pytest.raises(ValueError):
         p.damp_step(st, op, ms.coeffs, p.DenoiserSpec(), p.ReconMethod.Ista, 2.0)
-    with pytest.raises(p.UnsupportedError):
-        p.damp_step(st, op, ms.coeffs, p.DenoiserSpec(), p.ReconMethod.Damp, 2.0)
+    with pytest.raises(p.UnsupportedError):                    # device dct_threshold: 8x8 tiles only
+        p.damp_step(st, op, ms.coeffs, p.DenoiserSpec("dct_threshold", {"block": 16}), p.ReconMethod.Damp, 2.0)
     big = ms.coeffs * 1e7
     sb = p.init_state(op, big, True)
     with pytest.raises(p.DivergenceError) as e:
@@ -395,8 +395,10 @@ def test_ida_divergence(p):
     assert e.value.iteration == 1
     with pytest.raises(ValueError):
         p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=0))
-    with pytest.raises(p.UnsupportedError):
+    with pytest.raises(p.DivergenceError):                     # every method runs on the device now
         p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Amp, iterations=2))
+    with pytest.raises(p.UnsupportedError):
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, 2, 2.0, p.DenoiserSpec("dct_threshold", {"block": 4})))
 
 
 # ---- full-size properties (BASELINE sizes) -------------------------------------------------

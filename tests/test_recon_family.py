@@ -1,0 +1,130 @@
+"""The rest of the reconstruction family on the device: ISTA, AMP, DAMP,
+DAMP-D and IDA with the blur / identity denoisers (recon.cpp:133-259), the blur denoiser and
+the Monte-Carlo divergence with its std::mt19937_64 Rademacher probe (denoise.cpp:14-128),
+against fixtures written by the reference (tests/golden/family_cases.npz) and, where the
+reference library is present, the reference itself."""
+import os
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PIXEL_TOL = 1e-3
+PSNR_TOL = 0.01
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def p(torch):
+    import paper_2001_09632_b200 as p
+    return p
+
+
+@pytest.fixture(scope="module")
+def z():
+    return np.load(os.path.join(ROOT, "tests", "golden", "family_cases.npz"))
+
+
+FAMILY = [  # (name, method, iters, lambda, seed, denoiser, sigma_scale, damping) as make_golden.FAMILY_CASES
+    ("ista", 1, 4, 0.05, 42, "dct_threshold", 25.0, 2.0), ("amp", 2, 3, 0.5, 42, "dct_threshold", 25.0, 2.0),
+    ("damp_dct", 3, 3, 1.0, 42, "dct_threshold", 25.0, 2.0), ("dampd_dct", 4, 3, 1.0, 7, "dct_threshold", 25.0, 3.0),
+    ("damp_blur", 3, 3, 1.0, 42, "blur", 25.0, 2.0), ("ida_blur", 5, 3, 1.0, 42, "blur", 5.0, 2.0),
+    ("ida_identity", 5, 2, 1.0, 42, "identity", 25.0, 2.0)]
+
+
+def cfg_of(p, method, iters, lam, seed, den, scale, damping):
+    spec = p.DenoiserSpec(den, {"k": 2.7, "block": 8, "sigma_scale": scale})
+    return p.ReconConfig(p.ReconMethod(method), iters, damping, spec, lam, seed)
+
+
+@pytest.mark.gpu
+def test_probe_is_mt19937_64(p, z):
+    for key in [k for k in z.files if k.startswith("mt_")]:
+        seed = int(key[3:], 16)
+        want = np.where(z[key] & np.uint64(1), 1.0, -1.0).astype(np.float32)
+        assert np.array_equal(p.rademacher_probe(seed, want.size).cpu().numpy(), want), key
+
+
+@pytest.mark.gpu
+def test_blur_denoiser(p, z):
+    spec = p.DenoiserSpec("blur", {"sigma_scale": 25.0})
+    for sig in (0, 7, 60, 400):                      # 0: identity; 400: radius 48 > the field
+        got = p.denoise(spec, z["field"], float(sig))
+        assert np.max(np.abs(got - z[f"blur_{sig}"])) <= PIXEL_TOL, sig
+
+
+@pytest.mark.gpu
+def test_divergence(p, z):
+    d0 = p.divergence(p.DenoiserSpec("dct_threshold", {"k": 2.7}), z["field"], 20.0, 0.3, 99)
+    d1 = p.divergence(p.DenoiserSpec("blur", {"sigma_scale": 25.0}), z["field"], 80.0, 0.5, 12345)
+    assert d0 == pytest.approx(z["div"][0], rel=1e-3) and d1 == pytest.approx(z["div"][1], rel=1e-3)
+
+
+def _psnr(a, b):
+    mse = np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2)
+    return float("inf") if mse == 0 else 10 * np.log10(255.0 ** 2 / mse)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", FAMILY, ids=[c[0] for c in FAMILY])
+def test_reconstruct_family(p, z, case):
+    name, *rest = case
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 1, 4, 0.0, z["counts"], z["coeffs"].astype(np.float32))
+    res = p.reconstruct(ms, cfg_of(p, *rest), reference=z["img"])
+    want_x, want_tr = z[f"{name}_x"], z[f"{name}_trace"]
+    tr = np.array([[r.iteration, r.residual_norm, r.sigma, r.psnr_db] for r in res.trace])
+    assert np.array_equal(tr[:, 0], want_tr[:, 0])
+    # fp32 state: sigma carries an absolute floor ~|y| * 1e-7 where the reference's collapses to ~1e-13
+    assert np.allclose(tr[:, 2], want_tr[:, 2], rtol=1e-4, atol=1e-6 * want_tr[0, 2]), (tr[:, 2], want_tr[:, 2])
+    assert np.max(np.abs(res.image - want_x)) <= PIXEL_TOL
+    assert abs(_psnr(z["img"], res.image) - _psnr(z["img"], want_x)) <= PSNR_TOL
+
+
+@pytest.mark.gpu
+def test_amp_block8(p, z):
+    ms = p.MeasurementSet(48, 40, 8, p.Algorithm.BBV, 1, 5, 0.0, z["counts8"], z["coeffs8"].astype(np.float32))
+    res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Amp, 3, 2.0, p.DenoiserSpec(), 0.5), reference=z["img8"])
+    assert np.max(np.abs(res.image - z["amp8_x"])) <= PIXEL_TOL
+    assert np.allclose([r.sigma for r in res.trace], z["amp8_trace"][:, 2], rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_step_functions_match_reconstruct(p, z):
+    """ista_step / amp_step / damp_step on explicit state == reconstruct's trajectory."""
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 1, 4, 0.0, z["counts"], z["coeffs"].astype(np.float32))
+    op = p.SensingOperator.from_ms(ms)
+    for name, method, iters, lam, seed, den, scale, damping in FAMILY:
+        st = p.init_state(op, ms.coeffs, True)
+        spec = p.DenoiserSpec(den, {"k": 2.7, "block": 8, "sigma_scale": scale})
+        for _ in range(iters):
+            if method == 1:
+                p.ista_step(st, op, ms.coeffs, lam)
+            elif method == 2:
+                p.amp_step(st, op, ms.coeffs, lam)
+            else:
+                p.damp_step(st, op, ms.coeffs, spec, p.ReconMethod(method), damping, seed)
+        assert st.iteration == iters
+        want_tr = z[f"{name}_trace"]
+        assert st.sigma == pytest.approx(want_tr[-1, 2], rel=1e-4, abs=1e-6 * want_tr[0, 2]), name
+        assert np.max(np.abs(np.clip(st.x.reshape(64, 64), 0, 255) - z[f"{name}_x"])) <= PIXEL_TOL, name
+
+
+@pytest.mark.gpu
+def test_family_errors(p, z):
+    ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 1, 4, 0.0, z["counts"], z["coeffs"].astype(np.float32))
+    with pytest.raises(ValueError):
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ista, 2, 2.0, p.DenoiserSpec(), -1.0))
+    with pytest.raises(ValueError):
+        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Damp, 2, 2.0, p.DenoiserSpec("nope")))
+    with pytest.raises(ValueError):
+        p.divergence(p.DenoiserSpec(), z["field"], 1.0, 0.0, 1)
+    big = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 1, 4, 0.0, z["counts"], z["coeffs"].astype(np.float32) * 1e7)
+    with pytest.raises(p.DivergenceError):
+        p.reconstruct(big, p.ReconConfig(p.ReconMethod.Ista, 3, 2.0, p.DenoiserSpec(), 0.05))
