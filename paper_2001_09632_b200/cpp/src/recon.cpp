@@ -88,14 +88,21 @@ PixelImage decode_idct(const MeasurementSet& ms) {  // recon.cpp:109-117
 
 namespace {
 
-abcs_ida_config ida_config(const DenoiserSpec& d, int iterations, double damping) {
-  if (d.name != "dct_threshold")
-    throw UnsupportedError("device IDA implements the dct_threshold denoiser, not '" + d.name + "'");
-  abcs_ida_config c{};
+abcs_recon_config recon_config(ReconMethod method, int iterations, double damping, double lambda, uint64_t seed,
+                                const DenoiserSpec& d) {
+  abcs_recon_config c{};
+  c.method = static_cast<int32_t>(method);
   c.iterations = iterations;
-  c.denoiser_block = static_cast<int32_t>(d.param("block", 8.0));
   c.damping = damping;
+  c.lambda = lambda;
+  c.seed = seed;
+  if (d.name == "dct_threshold") c.denoiser = ABCS_DENOISER_DCT_THRESHOLD;
+  else if (d.name == "blur") c.denoiser = ABCS_DENOISER_BLUR;
+  else if (d.name == "identity") c.denoiser = ABCS_DENOISER_IDENTITY;
+  else throw std::invalid_argument("unknown denoiser: '" + d.name + "'");
+  c.denoiser_block = static_cast<int32_t>(d.param("block", 8.0));
   c.k = d.param("k", 2.7);
+  c.sigma_scale = d.param("sigma_scale", 25.0);
   return c;
 }
 
@@ -137,24 +144,14 @@ ReconState init_state(const SensingOperator& op, std::span<const double> y, bool
   return st;
 }
 
-void ista_step(ReconState&, const SensingOperator&, std::span<const double>, double) {
-  throw UnsupportedError("ista_step is not on the device path (IDCT and IDA are)");
-}
+namespace {
 
-void amp_step(ReconState&, const SensingOperator&, std::span<const double>, double) {
-  throw UnsupportedError("amp_step is not on the device path (IDCT and IDA are)");
-}
-
-void damp_step(ReconState& state, const SensingOperator& op, std::span<const double> y, const DenoiserSpec& denoiser,
-               ReconMethod variant, double damping, uint64_t /*seed: only the DAMP divergence probe uses it*/) {
-  // recon.cpp:170-197 with variant Ida: pseudo = A* z + x; x <- D(pseudo, sigma); finish_step (:81-93)
-  if (variant != ReconMethod::Damp && variant != ReconMethod::DampD && variant != ReconMethod::Ida)
-    throw std::invalid_argument("damp_step: variant must be damp, dampd or ida");
-  if (variant != ReconMethod::Ida) throw UnsupportedError("damp_step: only the Ida variant is on the device path");
+// One step of any method on the explicit state via abcs_recon_step_state (recon.cpp:133-197).
+void device_step(ReconState& state, const SensingOperator& op, std::span<const double> y,
+                 const abcs_recon_config& cfg) {
   if (static_cast<long long>(y.size()) != op.measurements() || state.z.size() != y.size() ||
       static_cast<long long>(state.x.size()) != op.field_size())
-    throw std::invalid_argument("damp_step: state / measurement size mismatch");
-  const abcs_ida_config cfg = ida_config(denoiser, 1, damping);
+    throw std::invalid_argument("step: state / measurement size mismatch");
   const BlockGrid& g = op.grid();
   DeviceSet set(op, y);
   const std::vector<float> xf = detail::to_f32(state.x), zf = detail::to_f32(state.z);
@@ -162,15 +159,35 @@ void damp_step(ReconState& state, const SensingOperator& op, std::span<const dou
   DeviceBuffer<float> d_z(zf.data(), std::max<size_t>(zf.size(), 1));
   DeviceBuffer<double> d_sigma(&state.sigma, 1);
   DeviceBuffer<int32_t> d_div(2);
-  check(abcs_ida_step_state(ctx(), g.rows, g.cols, g.block, set.counts.get(), nullptr, set.y.get(),
-                            static_cast<int64_t>(y.size()), 1, &cfg, d_x.get(), d_z.get(), d_sigma.get(),
-                            state.iteration + 1, d_div.get(), nullptr));
+  const int32_t zero2[2] = {0, 0};
+  d_div.upload(zero2, 2);
+  check(abcs_recon_step_state(ctx(), g.rows, g.cols, g.block, set.counts.get(), nullptr, set.y.get(),
+                              static_cast<int64_t>(y.size()), 1, &cfg, d_x.get(), d_z.get(), d_sigma.get(),
+                              state.iteration, d_div.get(), nullptr));
   state.x = detail::to_f64(d_x.download(xf.size()));
   state.z = detail::to_f64(d_z.download(zf.size()));
   state.sigma = d_sigma.download(1)[0];
   ++state.iteration;
   const std::vector<int32_t> div = d_div.download(2);
   if (div[0] > 0) diverged(div[0], div[1]);
+}
+
+}  // namespace
+
+void ista_step(ReconState& state, const SensingOperator& op, std::span<const double> y, double lambda) {
+  device_step(state, op, y, recon_config(ReconMethod::Ista, 1, 2.0, lambda, 42, DenoiserSpec{}));
+}
+
+void amp_step(ReconState& state, const SensingOperator& op, std::span<const double> y, double lambda) {
+  device_step(state, op, y, recon_config(ReconMethod::Amp, 1, 2.0, lambda, 42, DenoiserSpec{}));
+}
+
+void damp_step(ReconState& state, const SensingOperator& op, std::span<const double> y, const DenoiserSpec& denoiser,
+               ReconMethod variant, double damping, uint64_t seed) {  // recon.cpp:170-197
+  if (variant != ReconMethod::Damp && variant != ReconMethod::DampD && variant != ReconMethod::Ida)
+    throw std::invalid_argument("damp_step: variant must be damp, dampd or ida");
+  if (damping < 1.0) throw std::invalid_argument("damping factor D_F must be >= 1");
+  device_step(state, op, y, recon_config(variant, 1, damping, 1.0, seed, denoiser));
 }
 
 ReconResult reconstruct(const MeasurementSet& ms, const ReconConfig& cfg, const PixelImage* reference) {
@@ -198,20 +215,17 @@ ReconResult reconstruct(const MeasurementSet& ms, const ReconConfig& cfg, const 
     }
     return result;
   }
-  if (cfg.method != ReconMethod::Ida)
-    throw UnsupportedError(std::string("method ") + recon_method_name(cfg.method) +
-                           " is not on the device path (IDCT and IDA are)");
   const SensingOperator op = SensingOperator::from(ms);
   if (static_cast<long long>(ms.coeffs.size()) != op.measurements())
     throw std::invalid_argument("init_state: measurement vector length mismatch");
-  const abcs_ida_config c = ida_config(cfg.denoiser, cfg.iterations, cfg.damping);
+  const abcs_recon_config c = recon_config(cfg.method, cfg.iterations, cfg.damping, cfg.lambda, cfg.seed, cfg.denoiser);
   DeviceSet set(op, ms.coeffs);
   DeviceBuffer<float> d_out(op.field_size());
   DeviceBuffer<double> d_trace(static_cast<size_t>(cfg.iterations + 1) * 4);
   DeviceBuffer<int32_t> d_div(2);
   DeviceBuffer<uint8_t> d_ref(std::max<size_t>(ref_u8.size(), 1));
   d_ref.upload(ref_u8.data(), ref_u8.size());
-  check(abcs_ida_batch(ctx(), g.rows, g.cols, g.block, set.counts.get(), nullptr, set.y.get(),
+  check(abcs_reconstruct_batch(ctx(), g.rows, g.cols, g.block, set.counts.get(), nullptr, set.y.get(),
                        static_cast<int64_t>(ms.coeffs.size()), 1, &c, reference ? d_ref.get() : nullptr,
                        static_cast<int64_t>(ref_u8.size()), g.cropped_width(), d_out.get(), op.field_size(),
                        g.cropped_width(), d_trace.get(), d_div.get(), nullptr));
@@ -229,17 +243,31 @@ ReconResult reconstruct(const MeasurementSet& ms, const ReconConfig& cfg, const 
 PixelImage denoise(const DenoiserSpec& spec, const PixelImage& field, double sigma) {  // denoise.cpp:96-109
   if (sigma < 0) throw std::invalid_argument("denoise: sigma must be >= 0");
   if (spec.name == "identity") return field;
-  if (spec.name == "blur") throw UnsupportedError("the blur denoiser is not on the device path");
-  if (spec.name != "dct_threshold") throw std::invalid_argument("unknown denoiser: '" + spec.name + "'");
+  const abcs_recon_config c = recon_config(ReconMethod::Damp, 1, 2.0, 1.0, 42, spec);  // throws on unknown names
   const std::vector<float> f = detail::to_f32(field.data);
   DeviceBuffer<float> d_in(f.data(), f.size());
   DeviceBuffer<float> d_out(f.size());
-  check(abcs_denoise_dct_batch(ctx(), d_in.get(), field.height, field.width,
-                               static_cast<int64_t>(field.height) * field.width, 1, &sigma, spec.param("k", 2.7),
-                               static_cast<int32_t>(spec.param("block", 8.0)), d_out.get(), nullptr));
+  check(abcs_denoise_batch(ctx(), d_in.get(), field.height, field.width,
+                           static_cast<int64_t>(field.height) * field.width, 1, &sigma, &c, d_out.get(), nullptr));
   PixelImage out(field.height, field.width);
   out.data = detail::to_f64(d_out.download(f.size()));
   return out;
+}
+
+}  // namespace abcs
+
+namespace abcs {
+
+double divergence(const DenoiserSpec& spec, const PixelImage& field, double sigma, double epsilon,
+                  uint64_t seed) {  // denoise.cpp:111-128
+  if (epsilon <= 0) throw std::invalid_argument("divergence: epsilon must be > 0");
+  const abcs_recon_config c = recon_config(ReconMethod::Damp, 1, 2.0, 1.0, seed, spec);
+  const std::vector<float> f = detail::to_f32(field.data);
+  DeviceBuffer<float> d_in(f.data(), f.size());
+  DeviceBuffer<double> d_div(1);
+  check(abcs_divergence_batch(ctx(), d_in.get(), field.height, field.width, 1, &sigma, &epsilon, seed, &c,
+                              d_div.get(), nullptr));
+  return d_div.download(1)[0];
 }
 
 }  // namespace abcs

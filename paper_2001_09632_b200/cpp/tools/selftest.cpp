@@ -114,11 +114,32 @@ int main() {
     expect(false, "non-integer pixels rejected");
   } catch (const std::invalid_argument&) {
   }
+  {  // the rest of the family: AMP, DAMP (divergence probe), blur-denoised IDA
+    SensingConfig cfg;
+    cfg.block = 16;
+    cfg.algorithm = Algorithm::BBV;
+    cfg.set_cr("1/4");
+    const MeasurementSet ms = sense(img, cfg);
+    for (ReconMethod m : {ReconMethod::Amp, ReconMethod::Damp, ReconMethod::DampD, ReconMethod::Ida}) {
+      ReconConfig rc;
+      rc.method = m;
+      rc.iterations = 2;
+      rc.lambda = 0.5;
+      if (m == ReconMethod::Ida) rc.denoiser.name = "blur";
+      const ReconResult r = reconstruct(ms, rc);
+      expect(r.trace.size() == 3, "family trace rows");
+    }
+    DenoiserSpec blur;
+    blur.name = "blur";
+    const PixelImage b = denoise(blur, img, 50.0);
+    expect(b.height == img.height && std::isfinite(divergence(blur, img, 50.0, 0.25, 7)), "blur + divergence");
+  }
   try {
-    ReconConfig amp;
-    amp.method = ReconMethod::Amp;
-    reconstruct(sense(img, full), amp);
-    expect(false, "Amp is outside the device path");
+    ReconConfig bad;
+    bad.method = ReconMethod::Ida;
+    bad.denoiser.params["block"] = 16;
+    reconstruct(sense(img, full), bad);
+    expect(false, "dct_threshold block 16 is outside the device path");
   } catch (const UnsupportedError&) {
   }
   const std::vector<int> alloc = largest_remainder_allocate({3, 1, 0, 2}, 5, {4, 4, 4, 4});

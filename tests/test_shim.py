@@ -33,6 +33,11 @@ SIGNATURES = [
     "abcs::SensingConfig::validate() const",
     "abcs::make_grid(int, int, int)",
     "abcs::zigzag_order(int)",
+    "abcs::ista_step(abcs::ReconState&, abcs::SensingOperator const&, std::span<double const, 18446744073709551615ul>, "
+    "double)",
+    "abcs::amp_step(abcs::ReconState&, abcs::SensingOperator const&, std::span<double const, 18446744073709551615ul>, "
+    "double)",
+    "abcs::divergence(abcs::DenoiserSpec const&, abcs::PixelImage const&, double, double, unsigned long)",
     "abcs::write_measurement_set(abcs::MeasurementSet const&, std::filesystem::__cxx11::path const&)",
     "abcs::read_measurement_set(std::filesystem::__cxx11::path const&)",
 ]
