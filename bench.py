@@ -388,6 +388,14 @@ def run_ours(args, world, rank, local):
         except Exception as e:
             metrics = {"error": repr(e)[:200]}
 
+    # the rest of the reconstruction family on the cfg4 batch
+    family = None
+    if rank == 0:
+        try:
+            family = family_bench(p, torch)
+        except Exception as e:
+            family = {"error": repr(e)[:200]}
+
     # the other BASELINE configs (parity-test workloads, not bench lines): device throughput and
     # algorithmic-bytes roofline fraction of sense+decode (and IDA) on this rank's GPU
     configs = None
@@ -428,6 +436,7 @@ def run_ours(args, world, rank, local):
             "ida": ida,
             "container": container,
             "metrics": metrics,
+            "recon_family": family,
             "configs": configs,
             "clocks": clk,
             "cpu_baseline": cpu,
@@ -495,6 +504,30 @@ def metrics_bench(p, torch, refs, dec, hbm):
             "mse_psnr_ms": round(ms_p, 4), "mse_psnr_frac": round(5 * px / ms_p / 1e6 / hbm, 4),
             "ssim_ms": round(ms_s, 4), "ssim_mp_s": round(px / ms_s / 1e3, 1),
             "ssim_note": "fp64 11x11 Gaussian statistics in the reference's operation order (FP64-pipe bound)"}
+
+
+def family_bench(p, torch):
+    """image-iterations/s of ISTA, AMP, DAMP (dct_threshold, with the Monte-Carlo divergence) and IDA
+    with the blur denoiser on cfg4's batch (64 x 512^2, BBV 0.3), 10 iterations each."""
+    c = CFG4
+    imgs = p.synth_images(p.SynthSpec(c["H"], c["W"], c["ellipses"], c["sigma"], c["seed"]), 0, c["n"])
+    b = p.sense_batch(imgs, p.SensingConfig(c["B"], c["num"], c["den"], p.Algorithm.BBV))
+    out = torch.empty((c["n"], c["H"], c["W"]), dtype=torch.float32, device=imgs.device)
+    res = {}
+    for name, rc in (("ista", p.ReconConfig(p.ReconMethod.Ista, 10, 2.0, p.DenoiserSpec(), 0.05)),
+                     ("amp", p.ReconConfig(p.ReconMethod.Amp, 10, 2.0, p.DenoiserSpec(), 1.0)),
+                     ("damp_dct", p.ReconConfig(p.ReconMethod.Damp, 10)),
+                     ("ida_blur", p.ReconConfig(p.ReconMethod.Ida, 10, 2.0, p.DenoiserSpec("blur")))):
+        p.recon_batch(b, rc, out=out, trace=False, check=False)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        p.recon_batch(b, rc, out=out, trace=False, check=False)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        res[name] = {"ms_per_batch": round(ms, 3), "it_s": round(c["n"] * 10 / ms * 1e3, 1)}
+    return {"workload": "cfg4 batch: 64 x 512^2, BBV 0.3, 10 iterations", **res}
 
 
 SWEEP = [  # (name, H, W, n, B, num, den, algorithm, ellipses, sigma, seed, video, ida_iterations)
