@@ -160,8 +160,13 @@ sense16_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
   constexpr int kWbuf = 256;
   __shared__ float s_buf[kM16Warps][2][kWbuf];
+  __shared__ uint2 s_btab[kWeights ? 8 * 32 : 1];  // stage-2 basis B pairs (fill_btab16), weights pass only
   Frag16 f;
   load_frag16(f);
+  if constexpr (kWeights) {  // (measured: a win for the weights pass, a loss for the fused decode pass)
+    if (threadIdx.x < 32) fill_btab16(f, s_btab);
+    __syncthreads();
+  }
   // The forward runs transposed (Y^T = C X^T C^T): D slot s holds Y[dslot_col(s)][dslot_row(s)].
   uint32_t rank_d[8];
   float thr_hi[kWeights ? 8 : 1], thr_lo[kWeights ? 8 : 1];
@@ -205,6 +210,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       u8_bfragT_il(st + 256, bx[1]);
       Acc16 Y[2];  // Y^T of each block
       if constexpr (kLowCols) dct16_fwd_exact_x2_lo(f, bx, Y);
+      else if constexpr (kWeights) dct16_fwd_exact_x2_tab(f, s_btab, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
       if constexpr (kWeights) {

@@ -107,6 +107,40 @@ __device__ __forceinline__ Acc16 stage2(const Acc16& S, const uint32_t (&bh)[2][
   return R;
 }
 
+// Stage 2 with the basis B pairs read from a shared table (lane-minor, conflict-free LDS.64):
+// tab[(2j + {0 hi, 1 lo}) * 32 + lane]. Saves the register moves that pair non-adjacent A-quad
+// registers into B operands.
+__device__ __forceinline__ Acc16 stage2_tab(const Acc16& S, const uint2* tab) {
+  const int lane = threadIdx.x & 31;
+  uint32_t ah[4], al[4];
+  split2(S.v[0][0], S.v[0][1], ah[0], al[0]);
+  split2(S.v[0][2], S.v[0][3], ah[1], al[1]);
+  split2(S.v[1][0], S.v[1][1], ah[2], al[2]);
+  split2(S.v[1][2], S.v[1][3], ah[3], al[3]);
+  Acc16 R;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const uint2 bh = tab[(2 * j) * 32 + lane], bl = tab[(2 * j + 1) * 32 + lane];
+    R.v[j][0] = R.v[j][1] = R.v[j][2] = R.v[j][3] = 0.f;
+    mma16816(R.v[j], al, bh.x, bh.y);
+    mma16816(R.v[j], ah, bl.x, bl.y);
+    mma16816(R.v[j], ah, bh.x, bh.y);
+  }
+  return R;
+}
+
+// Fill a 8 x 32 uint2 table: rows 0-3 forward stage-2 pairs (C^T as B), rows 4-7 inverse (C as B).
+__device__ __forceinline__ void fill_btab16(const Frag16& f, uint2* tab) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    tab[(2 * j) * 32 + lane] = make_uint2(f.cbh[j][0], f.cbh[j][1]);
+    tab[(2 * j + 1) * 32 + lane] = make_uint2(f.cbl[j][0], f.cbl[j][1]);
+    tab[(4 + 2 * j) * 32 + lane] = make_uint2(f.tbh[j][0], f.tbh[j][1]);
+    tab[(4 + 2 * j + 1) * 32 + lane] = make_uint2(f.tbl[j][0], f.tbl[j][1]);
+  }
+}
+
 // Forward DCT of an exact-fp16 block given as B fragments bx[j][0..1] (n-tile j):
 //   T = C X (stage 1), Y = T C^T (stage 2). Returns Y in D-fragment layout.
 __device__ __forceinline__ Acc16 dct16_fwd_exact(const Frag16& f, const uint32_t (&bx)[2][2]) {
@@ -137,6 +171,26 @@ __device__ __forceinline__ void dct16_fwd_exact_x2(const Frag16& f, const uint32
     for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.ch, bx[q][j][0], bx[q][j][1]);
 #pragma unroll
   for (int q = 0; q < 2; ++q) Y[q] = stage2(T[q], f.cbh, f.cbl);
+}
+
+// dct16_fwd_exact_x2 with stage-2 B pairs from the shared table (fill_btab16)
+__device__ __forceinline__ void dct16_fwd_exact_x2_tab(const Frag16& f, const uint2* tab, const uint32_t (&bx)[2][2][2],
+                                                       Acc16 (&Y)[2]) {
+  Acc16 T[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) T[q].v[j][0] = T[q].v[j][1] = T[q].v[j][2] = T[q].v[j][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.cl, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) mma16816(T[q].v[j], f.ch, bx[q][j][0], bx[q][j][1]);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) Y[q] = stage2_tab(T[q], tab);
 }
 
 // Same, computing only rows 0..7 and columns 0..7 of Y^T (n-tile 0, A rows g): enough when
@@ -250,6 +304,24 @@ __device__ __forceinline__ void u8_bfragT_il(const uint8_t* blk, uint32_t (&bx)[
     bx[j][0] = u8sel_to_h2(w, 0x4140);
     bx[j][1] = u8sel_to_h2(w, 0x4342);
   }
+}
+
+// dct16_inv_from_yt with stage-2 B pairs from the shared table (rows 4-7)
+__device__ __forceinline__ Acc16 dct16_inv_from_yt_tab(const Frag16& f, const uint2* tab, const Acc16& Yt) {
+  uint32_t bh[2][2], bl[2][2];
+  split2(Yt.v[0][0], Yt.v[0][1], bh[0][0], bl[0][0]);
+  split2(Yt.v[1][0], Yt.v[1][1], bh[0][1], bl[0][1]);
+  split2(Yt.v[0][2], Yt.v[0][3], bh[1][0], bl[1][0]);
+  split2(Yt.v[1][2], Yt.v[1][3], bh[1][1], bl[1][1]);
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.th, bl[j][0], bl[j][1]);
+    mma16816(T.v[j], f.tl, bh[j][0], bh[j][1]);
+    mma16816(T.v[j], f.th, bh[j][0], bh[j][1]);
+  }
+  return stage2_tab(T, tab + 4 * 32);
 }
 
 // B fragments of X^T (for the transposed forward) from a u8 block in smem with a
