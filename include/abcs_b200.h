@@ -294,6 +294,17 @@ int abcs_quality_batch(abcs_ctx* ctx, const uint8_t* d_ref, int64_t ref_stride, 
                        int32_t width, int32_t n_images, double* d_mse, double* d_psnr, double* d_ssim,
                        void* stream);
 
+/* thb / thi (metrics.cpp:126-225): full-sensing oracle decodes of u8 images. Keep the
+ * M = floor(C_R N) largest-|coefficient| entries per block with balanced counts (global = 0,
+ * THB) or across the image (global = 1, THI), ties to the lower zigzag index then block,
+ * and invert. fp64 transforms in the reference's operation order: counts and images are
+ * bit-identical to the reference. d_counts: n*n_blocks i32; d_out: f64 (cropped grid). */
+int abcs_threshold_decode_batch(abcs_ctx* ctx, const abcs_sensing_config* cfg,
+                                const uint8_t* d_images, int64_t image_stride, int32_t pitch,
+                                int32_t height, int32_t width, int32_t n_images, int32_t global,
+                                int32_t* d_counts, double* d_out, int64_t out_stride, int32_t out_pitch,
+                                void* stream);
+
 /* ---- .abcs v1 measurement container (container.cpp:58-149) ------------------
  * Layout (little-endian, packed): "ABCS" | version u16 = 1 | H u32 | W u32 | B u16 |
  * algorithm u8 | C_R num u32 | C_R den u32 | threshold f64 | n_B u32 | counts u16[n_B] |

@@ -338,6 +338,18 @@ class Reference:
                                           float(dblock), sigma_scale, C.byref(out)))
         return out.value
 
+    def threshold_decode(self, img, B, num, den, global_):
+        """abcs::thb (global_=False) / abcs::thi -> (decoded image, counts)."""
+        a = _u8(img)
+        rows, cols = a.shape[0] // B, a.shape[1] // B
+        out = np.zeros((rows * B, cols * B))
+        counts = np.zeros(rows * cols, np.int32)
+        self.lib.ref_threshold_decode.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_int, P, P]
+        self._err(self.lib.ref_threshold_decode(a.ctypes.data_as(P), a.shape[0], a.shape[1], B, num, den,
+                                                1 if global_ else 0, out.ctypes.data_as(P),
+                                                counts.ctypes.data_as(P)))
+        return out, counts
+
     def mt19937_64(self, seed, n):
         out = np.zeros(n, np.uint64)
         self.lib.ref_mt19937_64.argtypes = [C.c_ulonglong, C.c_longlong, P]

@@ -192,6 +192,17 @@ void ref_mt19937_64(unsigned long long seed, long long n, unsigned long long* ou
   for (long long i = 0; i < n; ++i) out[i] = rng();
 }
 
+// abcs::thb / abcs::thi (metrics.cpp:219-225) -> decoded image (cropped) and per-block counts.
+int ref_threshold_decode(const uint8_t* px, int h, int w, int block, uint32_t num, uint32_t den, int global,
+                         double* out, int* counts) {
+  return guarded([&] {
+    const abcs::SensingConfig cfg = make_cfg(block, num, den, 0, 0, 0.0);
+    const abcs::ThresholdDecode r = global ? abcs::thi(to_image(px, h, w), cfg) : abcs::thb(to_image(px, h, w), cfg);
+    std::memcpy(out, r.image.data.data(), r.image.data.size() * sizeof(double));
+    std::memcpy(counts, r.counts.data(), r.counts.size() * sizeof(int));
+  });
+}
+
 // abcs::quality (metrics.cpp:118-125) of two images given as doubles.
 int ref_quality(const double* a, const double* b, int h, int w, double* mse, double* psnr, double* ssim) {
   return guarded([&] {

@@ -113,6 +113,8 @@ SIGNATURES = {
     "abcs_denoise_batch": (C.c_int, [P, P, I32, I32, I64, I32, P, C.POINTER(ReconConfigC), P, P]),
     "abcs_divergence_batch": (C.c_int, [P, P, I32, I32, I32, P, P, U64, C.POINTER(ReconConfigC), P, P]),
     "abcs_rademacher_probe": (C.c_int, [P, U64, I64, P, P]),
+    "abcs_threshold_decode_batch": (C.c_int, [P, C.POINTER(SensingConfigC), P, I64, I32, I32, I32, I32, I32, P, P,
+                                              I64, I32, P]),
     "abcs_container_size": (I64, [C.POINTER(SensePlanC)]),
     "abcs_container_pack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, P, P, I32, P, I64, P]),
     "abcs_container_unpack_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, P, P, P, P, P]),

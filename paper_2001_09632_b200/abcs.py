@@ -1028,6 +1028,49 @@ def ssim(ref, test) -> float:
     return float(quality_batch(r, t, ("ssim",))["ssim"][0])
 
 
+# ---- THB / THI full-sensing oracles (metrics.hpp:27-38, metrics.cpp:126-225) ------------
+@dataclass
+class ThresholdDecode:
+    image: np.ndarray  # float64, cropped grid
+    counts: np.ndarray  # int32 retained coefficients per block
+
+
+def threshold_decode_batch(images, cfg: SensingConfig, global_: bool):
+    """thb (global_=False) / thi (global_=True) for (n, H, W) uint8 CUDA images:
+    (decoded (n, Hc, Wc) float64 tensor, counts (n, n_blocks) int32 tensor), bit-identical to the reference."""
+    torch = _torch()
+    cfg.validate()
+    n, H, W = images.shape
+    g = make_grid(H, W, cfg.block)
+    dev = images.device
+    im = images.contiguous()
+    out = torch.empty((n, g.cropped_height(), g.cropped_width()), dtype=torch.float64, device=dev)
+    counts = torch.empty((n, g.count()), dtype=torch.int32, device=dev)
+    c = cfg._c()
+    _check(_lib.load().abcs_threshold_decode_batch(Context.get(dev.index).handle, C.byref(c), im.data_ptr(), H * W,
+                                                   W, H, W, n, 1 if global_ else 0, counts.data_ptr(),
+                                                   out.data_ptr(), out.stride(0), out.stride(1), _stream_ptr(torch)))
+    return out, counts
+
+
+def _threshold(img, cfg: SensingConfig, global_: bool) -> ThresholdDecode:
+    torch = _torch()
+    a = _as_u8_image(img)
+    t = torch.from_numpy(a).to(torch.device("cuda", torch.cuda.current_device()))[None]
+    out, counts = threshold_decode_batch(t, cfg, global_)
+    return ThresholdDecode(out[0].cpu().numpy(), counts[0].cpu().numpy())
+
+
+def thb(img, cfg: SensingConfig) -> ThresholdDecode:
+    """abcs::thb: per-block top-|c| with balanced counts (metrics.cpp:178-193)."""
+    return _threshold(img, cfg, False)
+
+
+def thi(img, cfg: SensingConfig) -> ThresholdDecode:
+    """abcs::thi: image-wide top-|c| (metrics.cpp:162-177)."""
+    return _threshold(img, cfg, True)
+
+
 # ---- .abcs v1 container (container.hpp:8-14, container.cpp:58-149) --------------------
 def container_size(plan: SensePlanC) -> int:
     return int(_lib.load().abcs_container_size(C.byref(plan)))

@@ -85,6 +85,9 @@ int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch,
                 int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr);
 int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
                 int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s);
+int launch_threshold_decode(Ctx* ctx, int block, const uint8_t* imgs, int64_t img_stride, int pitch, int rows, int cols,
+                            int n, int64_t m_target, bool global, int* counts, double* out, int64_t out_stride,
+                            int out_pitch, cudaStream_t s);
 // reconstruction family (recon.cu)
 int launch_soft_threshold(Ctx* ctx, const float* pseudo, float* x, int64_t N, int n, const double* sigma,
                           double lambda, unsigned long long* active, cudaStream_t s);

@@ -138,6 +138,17 @@ def main_family():
                            ref.divergence(field, 80.0, 0.5, 12345, denoiser=1, sigma_scale=25.0)])
     for seed in (0, 42, 0x9E3779B97F4A7C15):
         out[f"mt_{seed:x}"] = ref.mt19937_64(seed, 2000)
+    # THB / THI (metrics.cpp:126-225): (H, W, B, num, den) incl. a ragged crop and a flat image (all-zero AC ties)
+    for i, (H, W, B, num, den, seed) in enumerate([(64, 80, 16, 1, 4, 51), (56, 48, 8, 1, 5, 52),
+                                                   (100, 90, 16, 3, 10, 53), (64, 64, 32, 1, 2, 54)]):
+        im = p.synth_images_host(p.SynthSpec(H, W, 12, 5.0, seed), 0, 1)[0]
+        out[f"th{i}_img"], out[f"th{i}_cfg"] = im, np.array([B, num, den])
+        for g in (0, 1):
+            out[f"th{i}_x{g}"], out[f"th{i}_c{g}"] = ref.threshold_decode(im, B, num, den, bool(g))
+    flat = np.full((32, 32), 77, np.uint8)
+    out["thflat_img"] = flat
+    for g in (0, 1):
+        out[f"thflat_x{g}"], out[f"thflat_c{g}"] = ref.threshold_decode(flat, 16, 1, 2, bool(g))
     np.savez_compressed(os.path.join(HERE, "family_cases.npz"), **out)
 
 

@@ -128,3 +128,21 @@ def test_family_errors(p, z):
     big = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 1, 4, 0.0, z["counts"], z["coeffs"].astype(np.float32) * 1e7)
     with pytest.raises(p.DivergenceError):
         p.reconstruct(big, p.ReconConfig(p.ReconMethod.Ista, 3, 2.0, p.DenoiserSpec(), 0.05))
+
+
+@pytest.mark.gpu
+def test_thb_thi_bit_exact(p, torch, z):
+    """THB / THI oracles (metrics.cpp:126-225): counts and decoded images bit-identical."""
+    cases = [(k[:-4], z[k]) for k in z.files if k.startswith("th") and k.endswith("_img")]
+    assert len(cases) == 5
+    for name, img in cases:
+        B, num, den = z[f"{name}_cfg"] if f"{name}_cfg" in z.files else (16, 1, 2)
+        cfg = p.SensingConfig(int(B), int(num), int(den))
+        for g, fn in ((0, p.thb), (1, p.thi)):
+            r = fn(img, cfg)
+            assert np.array_equal(r.counts, z[f"{name}_c{g}"]), (name, g)
+            assert np.array_equal(r.image, z[f"{name}_x{g}"]), (name, g, np.max(np.abs(r.image - z[f"{name}_x{g}"])))
+    imgs = torch.from_numpy(np.stack([z["th0_img"]] * 3)).cuda()    # batched == single, per image
+    out, counts = p.threshold_decode_batch(imgs, p.SensingConfig(16, 1, 4), True)
+    assert all(np.array_equal(counts[i].cpu().numpy(), z["th0_c1"]) for i in range(3))
+    assert np.array_equal(out[2].cpu().numpy(), z["th0_x1"])
