@@ -396,6 +396,26 @@ def run_ours(args, world, rank, local):
         except Exception as e:
             family = {"error": repr(e)[:200]}
 
+    # THB / THI oracle decodes (fp64, bit-exact) on 64 of the cfg2 images at subrate 0.3
+    oracles = None
+    if rank == 0:
+        try:
+            oracles = {}
+            sub = imgs[:64]
+            for name, glob in (("thb", False), ("thi", True)):
+                p.threshold_decode_batch(sub, cfgs[1], glob)
+                torch.cuda.synchronize()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record()
+                p.threshold_decode_batch(sub, cfgs[1], glob)
+                s1.record()
+                torch.cuda.synchronize()
+                ms_o = s0.elapsed_time(s1)
+                oracles[name] = {"ms": round(ms_o, 3), "MP_s": round(64 * CFG2["H"] * CFG2["W"] / ms_o / 1e3, 1)}
+            oracles["workload"] = "64 x 512^2, DD 3/10 budget, fp64 transforms (bit-exact oracle baselines)"
+        except Exception as e:
+            oracles = {"error": repr(e)[:200]}
+
     # the other BASELINE configs (parity-test workloads, not bench lines): device throughput and
     # algorithmic-bytes roofline fraction of sense+decode (and IDA) on this rank's GPU
     configs = None
@@ -437,6 +457,7 @@ def run_ours(args, world, rank, local):
             "container": container,
             "metrics": metrics,
             "recon_family": family,
+            "threshold_oracles": oracles,
             "configs": configs,
             "clocks": clk,
             "cpu_baseline": cpu,
