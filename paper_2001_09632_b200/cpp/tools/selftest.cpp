@@ -6,6 +6,7 @@
 
 #include <abcs/b200.hpp>
 #include <abcs/container.hpp>
+#include <abcs/metrics.hpp>
 #include <abcs/recon.hpp>
 #include <algorithm>
 #include <cmath>
@@ -97,6 +98,20 @@ int main() {
                back.threshold == ms.threshold && back.algorithm == ms.algorithm,
            "container round trip");
     std::filesystem::remove(path);
+  }
+
+  {  // metrics and THB/THI (metrics.cpp:63-225)
+    SensingConfig cfg;
+    cfg.block = 16;
+    cfg.set_cr("1/4");
+    const ThresholdDecode tb = thb(img, cfg), ti = thi(img, cfg);
+    long long kb = 0, ki = 0;
+    for (int c : tb.counts) kb += c;
+    for (int c : ti.counts) ki += c;
+    const long long M = cfg.target_measurements(make_grid(img.height, img.width, 16).pixel_count());
+    expect(kb == M && ki == M, "thb/thi keep M coefficients");
+    const QualityReport qb = quality(crop_to_grid(img, make_grid(img.height, img.width, 16)), ti.image);
+    expect(qb.psnr_db > 20 && qb.ssim > 0.5 && qb.ssim <= 1.0 && qb.mse > 0, "quality of the THI decode");
   }
 
   // reference error behaviour

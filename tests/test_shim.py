@@ -40,6 +40,10 @@ SIGNATURES = [
     "abcs::divergence(abcs::DenoiserSpec const&, abcs::PixelImage const&, double, double, unsigned long)",
     "abcs::write_measurement_set(abcs::MeasurementSet const&, std::filesystem::__cxx11::path const&)",
     "abcs::read_measurement_set(std::filesystem::__cxx11::path const&)",
+    "abcs::quality(abcs::PixelImage const&, abcs::PixelImage const&)",
+    "abcs::ssim(abcs::PixelImage const&, abcs::PixelImage const&)",
+    "abcs::thb(abcs::PixelImage const&, abcs::SensingConfig const&)",
+    "abcs::thi(abcs::PixelImage const&, abcs::SensingConfig const&)",
 ]
 
 
