@@ -35,6 +35,9 @@ constexpr int kMP = 72;          // smem row pitch (floats): 72 = 8 mod 32 -> co
 struct IdaMmaSmem {
   float in[kMIn * kMP];   // field window; reused as per-warp y/z staging in the block phase
   float acc[kMIn * kMP];  // denoiser accumulator over the window (region at +4, +4), then x
+  Frag16Tab f16;          // B = 16 fragments (block phase / init), filled by warp 0 at kernel start
+  int meta_cnt[64];       // the region's sensing blocks (row-major): counts and image-relative offsets,
+  int meta_off[64];       // fetched at kernel start so the block phase does not wait on them
   double red[4][kMWarps];
   unsigned long long bad[2];
   double mine[4];
@@ -42,7 +45,18 @@ struct IdaMmaSmem {
 static_assert(kMWarps * 512 <= kMIn * kMP, "staging buffers fit in the window");
 constexpr int kMOff = 4 * kMP + 4;  // region pixel (0, 0) inside acc
 
-// field[R0-4 .. R0+68) x [C0-4 .. C0+68) -> s.in (zeros outside the image).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 16-byte async copy global -> shared; src_bytes = 0 zero-fills (out-of-image window parts)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// field[R0-4 .. R0+68) x [C0-4 .. C0+68) -> s.in (zeros outside the image). The vector path
+// only issues async copies; the caller waits (cp_async_wait_all + barrier) before reading.
 template <bool kVec>
 __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t pitch, int R0, int C0, int H, int W,
                                             float* in) {
@@ -50,9 +64,8 @@ __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t
     for (int i = threadIdx.x; i < kMIn * (kMIn / 4); i += kMThreads) {
       const int r = i / (kMIn / 4), c4 = i % (kMIn / 4);
       const int gr = R0 - 4 + r, gc = C0 - 4 + 4 * c4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr >= 0 && gr < H && gc >= 0 && gc < W) v = __ldg(reinterpret_cast<const float4*>(f + (int64_t)gr * pitch + gc));
-      *reinterpret_cast<float4*>(in + r * kMP + 4 * c4) = v;
+      const bool ok = gr >= 0 && gr < H && gc >= 0 && gc < W;
+      cp_async16(in + r * kMP + 4 * c4, ok ? f + (int64_t)gr * pitch + gc : f, ok ? 16 : 0);
     }
   } else {
     for (int i = threadIdx.x; i < kMIn * kMIn; i += kMThreads) {
@@ -68,58 +81,57 @@ __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t
 // is the identity (the DC pass-through, denoise.cpp:76).
 __device__ __forceinline__ float soft(float c, float t) { return c - fminf(fmaxf(c, -t), t); }
 
-// One parity phase of the tile grid: tiles (PA + 2a, PB + 2b) are disjoint; the
-// phase's tiles are taken two at a time (consecutive in row-major order) per MMA.
-template <int PA, int PB, bool kInterior, int NP>
-__device__ __forceinline__ void denoise_pairs(const float* in, float* acc, const Frag8& f, int R0, int C0, int H, int W,
-                                              float thr, float thr_dc, const int (&p)[NP]) {
-  constexpr int NA = PA ? 8 : 9, NB = PB ? 8 : 9, NT = NA * NB;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  int o1[NP], o2[NP];
-  bool v1[NP], v2[NP];
-  float Y[NP][4], X[NP][4];
-#pragma unroll
-  for (int u = 0; u < NP; ++u) {
-    const int k1 = 2 * p[u], k2 = (2 * p[u] + 1 < NT) ? 2 * p[u] + 1 : 2 * p[u];  // odd count: last tile alone
-    const int ti1 = PA + 2 * (k1 / NB), tj1 = PB + 2 * (k1 % NB);
-    const int ti2 = PA + 2 * (k2 / NB), tj2 = PB + 2 * (k2 % NB);
-    o1[u] = (4 * ti1 + g) * kMP + 4 * tj1 + 2 * t;
-    o2[u] = (4 * ti2 + g) * kMP + 4 * tj2 + 2 * t;
-    v1[u] = true;
-    v2[u] = k2 != k1;
-    if (!kInterior) {  // tile origins must lie on the image's origin grid (denoise.cpp:57-62)
-      v1[u] = (unsigned)(R0 - 4 + 4 * ti1) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj1) <= (unsigned)(W - 8);
-      v2[u] = v2[u] && (unsigned)(R0 - 4 + 4 * ti2) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj2) <= (unsigned)(W - 8);
+// The tile pairs of each parity phase: tiles (PA + 2a, PB + 2b) are disjoint; the phase's
+// tiles are taken two at a time (consecutive in row-major order) per warp step. Per pair:
+// x = window offsets of the two tile origins (lo16, hi16; an odd last tile repeats the first),
+// y = tile codes ti << 8 | tj (lo16, hi16; 0xffff: no second tile).
+constexpr int kPairsMax = 41;
+struct DenoisePairs {
+  uint2 e[4][kPairsMax];
+};
+constexpr DenoisePairs make_denoise_pairs() {
+  DenoisePairs d{};
+  for (int ph = 0; ph < 4; ++ph) {
+    const int PA = ph >> 1, PB = ph & 1, NA = PA ? 8 : 9, NB = PB ? 8 : 9, NT = NA * NB;
+    for (int p = 0; p < kPairsMax; ++p) {
+      const int k1 = 2 * p < NT ? 2 * p : 0, k2 = 2 * p + 1 < NT ? 2 * p + 1 : k1;
+      const int ti1 = PA + 2 * (k1 / NB), tj1 = PB + 2 * (k1 % NB), ti2 = PA + 2 * (k2 / NB), tj2 = PB + 2 * (k2 % NB);
+      const unsigned o1 = 4 * ti1 * kMP + 4 * tj1, o2 = 4 * ti2 * kMP + 4 * tj2;
+      const unsigned c1 = (unsigned)(ti1 << 8 | tj1), c2 = k2 != k1 ? (unsigned)(ti2 << 8 | tj2) : 0xffffu;
+      d.e[ph][p] = uint2{o1 | o2 << 16, c1 | c2 << 16};
     }
-    const float2 p0 = *reinterpret_cast<const float2*>(in + o1[u]);
-    const float2 p1 = *reinterpret_cast<const float2*>(in + o2[u]);
-    dct8x2_fwdT(f, p0, p1, Y[u]);
   }
-#pragma unroll
-  for (int u = 0; u < NP; ++u) {
-    // Y^T slots: 0/1 -> tile 1 (row g, cols 2t, 2t+1), 2/3 -> tile 2; DC = slots 0/2 of lane 0
-    Y[u][0] = soft(Y[u][0], thr_dc);
-    Y[u][1] = soft(Y[u][1], thr);
-    Y[u][2] = soft(Y[u][2], thr_dc);
-    Y[u][3] = soft(Y[u][3], thr);
-    dct8x2_inv_from_yt(f, Y[u], X[u]);
+  return d;
+}
+__constant__ DenoisePairs kDenoisePairs = make_denoise_pairs();
+
+// One tile pair of phase PH (PH = 2 PA + PB) per warp step.
+template <int PH, bool kInterior>
+__device__ __forceinline__ void denoise_pair(const float* in, float* acc, const Frag8& f, int lane_off, int R0, int C0,
+                                             int H, int W, float thr, float thr_dc, int p) {
+  const uint2 e = kDenoisePairs.e[PH][p];
+  const int o1 = (int)(e.x & 0xffffu) + lane_off, o2 = (int)(e.x >> 16) + lane_off;
+  bool v1 = true, v2 = (e.y >> 16) != 0xffffu;
+  if (!kInterior) {  // tile origins must lie on the image's origin grid (denoise.cpp:57-62)
+    const int ti1 = (e.y >> 8) & 0xff, tj1 = e.y & 0xff, ti2 = e.y >> 24, tj2 = (e.y >> 16) & 0xff;
+    v1 = (unsigned)(R0 - 4 + 4 * ti1) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj1) <= (unsigned)(W - 8);
+    v2 = v2 && (unsigned)(R0 - 4 + 4 * ti2) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj2) <= (unsigned)(W - 8);
   }
-#pragma unroll
-  for (int u = 0; u < NP; ++u) {
-    if (v1[u]) {
-      float2* d = reinterpret_cast<float2*>(acc + o1[u]);
-      float2 v = *d;
-      v.x += X[u][0];
-      v.y += X[u][1];
-      *d = v;
-    }
-    if (v2[u]) {
-      float2* d = reinterpret_cast<float2*>(acc + o2[u]);
-      float2 v = *d;
-      v.x += X[u][2];
-      v.y += X[u][3];
-      *d = v;
-    }
+  float Y[4], X[4];
+  dct8x2_fwdT(f, *reinterpret_cast<const float2*>(in + o1), *reinterpret_cast<const float2*>(in + o2), Y);
+  // Y^T slots: 0/1 -> tile 1 (row g, cols 2t, 2t+1), 2/3 -> tile 2; DC = slots 0/2 of lane 0
+  Y[0] = soft(Y[0], thr_dc);
+  Y[1] = soft(Y[1], thr);
+  Y[2] = soft(Y[2], thr_dc);
+  Y[3] = soft(Y[3], thr);
+  dct8x2_inv_from_yt(f, Y, X);
+  if (v1) {
+    float2* d = reinterpret_cast<float2*>(acc + o1);
+    *d = fadd2(*d, make_float2(X[0], X[1]));
+  }
+  if (v2) {
+    float2* d = reinterpret_cast<float2*>(acc + o2);
+    *d = fadd2(*d, make_float2(X[2], X[3]));
   }
 }
 
@@ -127,12 +139,12 @@ template <int PA, int PB, bool kInterior>
 __device__ __forceinline__ void denoise_phase(const float* in, float* acc, const Frag8& f, int R0, int C0, int H, int W,
                                               float thr, float thr_dc) {
   constexpr int NA = PA ? 8 : 9, NB = PB ? 8 : 9, NPAIR = (NA * NB + 1) / 2;
-  const int warp = threadIdx.x >> 5;
+  static_assert(NPAIR <= kPairsMax, "pair table");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane_off = (lane >> 2) * kMP + 2 * (lane & 3);
 #pragma unroll 1
-  for (int p = warp; p < NPAIR; p += kMWarps) {  // (two pairs per warp in flight measured slower: registers)
-    const int pp[1] = {p};
-    denoise_pairs<PA, PB, kInterior, 1>(in, acc, f, R0, C0, H, W, thr, thr_dc, pp);
-  }
+  for (int p = warp; p < NPAIR; p += kMWarps)  // (two pairs per warp in flight measured slower: registers)
+    denoise_pair<2 * PA + PB, kInterior>(in, acc, f, lane_off, R0, C0, H, W, thr, thr_dc, p);
   __syncthreads();
 }
 
@@ -153,6 +165,7 @@ __device__ void denoise_region_mma(const float* in, float* acc, int R0, int C0, 
   Frag8 f;
   load_frag8(f);
   const float thr_dc = lane == 0 ? 0.f : thr;
+  cp_async_wait_all();
   __syncthreads();
   if (R0 >= 4 && C0 >= 4 && R0 + kMR + 4 <= H && C0 + kMR + 4 <= W) denoise_phases<true>(in, acc, f, R0, C0, H, W, thr, thr_dc);
   else denoise_phases<false>(in, acc, f, R0, C0, H, W, thr, thr_dc);
@@ -217,17 +230,37 @@ __device__ __forceinline__ void store_out(const IdaParams& P, int img, int gr, i
   }
 }
 
-// Stage cnt values of y (and z) of one block into smem; returns after __syncwarp.
-__device__ __forceinline__ void stage_yz(const IdaParams& P, int64_t off, int cnt, float* yb, float* zb, bool need_z,
-                                        IdaLaneSums& S) {
-  const int lane = threadIdx.x & 31;
-  for (int k = lane; k < cnt; k += 32) {
-    const float yv = __ldg(P.y + off + k);
-    yb[k] = yv;
-    if (P.is_init) S.y += (double)yv * (double)yv;
-    if (need_z) zb[k] = P.z[off + k];
+// Issue the async staging of cnt values of y (and z) of one block into smem (per warp).
+__device__ __forceinline__ void stage_yz_async(const IdaParams& P, int64_t off, int cnt, float* yb, float* zb,
+                                              bool need_z) {
+  for (int k = threadIdx.x & 31; k < cnt; k += 32) {
+    cp_async4(yb + k, P.y + off + k);
+    if (need_z) cp_async4(zb + k, P.z + off + k);
   }
+}
+// Wait for the warp's staging; ||y||^2 for the init step (recon.cpp:128) from the staged copy.
+__device__ __forceinline__ void stage_yz_wait(const IdaParams& P, int cnt, const float* yb, IdaLaneSums& S) {
+  cp_async_wait_all();
   __syncwarp();
+  if (P.is_init)
+    for (int k = threadIdx.x & 31; k < cnt; k += 32) S.y += (double)yb[k] * (double)yb[k];
+}
+
+// The region's sensing blocks (kMR / B)^2, row-major: count (-1 outside the grid) and offset.
+template <int B>
+__device__ __forceinline__ void fetch_meta(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s) {
+  constexpr int PB = kMR / B;
+  for (int bi = threadIdx.x; bi < PB * PB; bi += kMThreads) {
+    const int gbr = R0 / B + bi / PB, gbc = C0 / B + bi % PB;
+    int cnt = -1, off = 0;
+    if (gbr < P.rows && gbc < P.cols) {
+      const int64_t bidx = (int64_t)img * P.rows * P.cols + (int64_t)gbr * P.cols + gbc;
+      cnt = P.counts[bidx];
+      off = P.offsets[bidx];
+    }
+    s.meta_cnt[bi] = cnt;
+    s.meta_off[bi] = off;
+  }
 }
 
 __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax, float zo, unsigned long long gi,
@@ -242,8 +275,6 @@ __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax
 // init: acc <- A* y (the warm start x0, recon.cpp:119-131)
 __device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  Frag16 f;
-  load_frag16(f);
   uint32_t rank[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) rank[q] = zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)];
@@ -263,7 +294,7 @@ __device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem
     Acc16 Yt;
 #pragma unroll
     for (int q = 0; q < 8; ++q) Yt.v[q >> 2][q & 3] = (int)rank[q] < cnt ? yb[rank[q]] : 0.f;
-    const Acc16 X = dct16_inv_from_yt(f, Yt);
+    const Acc16 X = dct16_inv_from_yt_t(s.f16, Yt);
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -277,22 +308,19 @@ __device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem
 __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s, IdaLaneSums& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
-  Frag16 f;
-  load_frag16(f);
-  uint32_t rank[8];
+  uint32_t rk[2] = {0u, 0u};  // zigzag ranks of the lane's 8 slots, one byte each
 #pragma unroll
-  for (int q = 0; q < 8; ++q) rank[q] = zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)];
+  for (int q = 0; q < 8; ++q) rk[q >> 2] |= zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)] << (8 * (q & 3));
   float* yb = s.in + warp * 512;
   float* zb = yb + 256;
   const bool last = P.pseudo_out == nullptr;
   for (int bi = warp; bi < 16; bi += kMWarps) {
-    const int gbr = R0 / 16 + bi / 4, gbc = C0 / 16 + bi % 4;
-    if (gbr >= P.rows || gbc >= P.cols) continue;  // warp-uniform
+    const int cnt = s.meta_cnt[bi];
+    if (cnt < 0) continue;  // outside the block grid (warp-uniform)
     const int lr0 = (bi / 4) * 16, lc0 = (bi % 4) * 16;
-    const int64_t bidx = (int64_t)img * P.rows * P.cols + (int64_t)gbr * P.cols + gbc;
-    const int cnt = P.counts[bidx];
-    const int32_t boff = P.offsets[bidx];
+    const int32_t boff = s.meta_off[bi];
     const int64_t off = (int64_t)img * P.y_stride + boff;
+    stage_yz_async(P, off, cnt, yb, zb, !P.is_init);  // lands while the forward transform runs
     if (lane == 0) S.cnt += (double)cnt;
     float xv[2][4];
 #pragma unroll
@@ -305,12 +333,12 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMm
       xv[j][2] = b.x;
       xv[j][3] = b.y;
     }
-    const Acc16 Yt = dct16_fwd_f32(f, xv);  // (A x)^T in slot layout
-    stage_yz(P, off, cnt, yb, zb, !P.is_init, S);
+    const Acc16 Yt = dct16_fwd_f32_t(s.f16, xv);  // (A x)^T in slot layout
+    stage_yz_wait(P, cnt, yb, S);
     Acc16 Zm;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int r = (int)rank[q];
+      const int r = (int)((rk[q >> 2] >> (8 * (q & 3))) & 0xffu);
       float zn = 0.f;
       if (r < cnt) {
         zn = z_update(P, yb[r], Yt.v[q >> 2][q & 3], P.is_init ? 0.f : zb[r], (unsigned long long)(boff + r), S,
@@ -322,7 +350,7 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMm
     __syncwarp();
     for (int k = lane; k < cnt; k += 32) P.z[off + k] = zb[k];
     Acc16 Az;
-    if (!last) Az = dct16_inv_from_yt(f, Zm);
+    if (!last) Az = dct16_inv_from_yt_t(s.f16, Zm);
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -390,27 +418,25 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMma
   const bool last = P.pseudo_out == nullptr;
   for (int pi = warp; pi < 32; pi += kMWarps) {
     const int br = pi / 4, bc = 2 * (pi % 4);
-    const int gbr = R0 / 8 + br, gbc0 = C0 / 8 + bc;
-    if (gbr >= P.rows || gbc0 >= P.cols) continue;  // warp-uniform
-    const bool has1 = gbc0 + 1 < P.cols;
-    int cnt[2] = {0, 0};
-    int32_t boff[2] = {0, 0};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (q == 1 && !has1) break;
-      const int64_t bidx = (int64_t)img * P.rows * P.cols + (int64_t)gbr * P.cols + gbc0 + q;
-      cnt[q] = P.counts[bidx];
-      boff[q] = P.offsets[bidx];
-    }
+    const int bi0 = br * 8 + bc;
+    if (s.meta_cnt[bi0] < 0) continue;  // outside the block grid (warp-uniform)
+    const bool has1 = s.meta_cnt[bi0 + 1] >= 0;
+    const int cnt[2] = {s.meta_cnt[bi0], has1 ? s.meta_cnt[bi0 + 1] : 0};
+    const int32_t boff[2] = {s.meta_off[bi0], has1 ? s.meta_off[bi0 + 1] : 0};
+    const int64_t ibase = (int64_t)img * P.y_stride;
+    stage_yz_async(P, ibase + boff[0], cnt[0], yb, zb, !P.is_init);
+    stage_yz_async(P, ibase + boff[1], cnt[1], yb + 64, zb + 64, !P.is_init);
     if (lane == 0) S.cnt += (double)(cnt[0] + cnt[1]);
     const int lr = 8 * br + g, lc = 8 * bc + 2 * t;
     const float2 x0 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc);
     const float2 x1 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc + 8);
     float Yt[4];
     dct8x2_fwdT(f, x0, x1, Yt);
-    const int64_t ibase = (int64_t)img * P.y_stride;
-    stage_yz(P, ibase + boff[0], cnt[0], yb, zb, !P.is_init, S);
-    stage_yz(P, ibase + boff[1], cnt[1], yb + 64, zb + 64, !P.is_init, S);
+    cp_async_wait_all();
+    __syncwarp();
+    if (P.is_init)  // ||y||^2 (recon.cpp:128), block 0 then block 1 as staged
+      for (int q = 0; q < 2; ++q)
+        for (int k = lane; k < cnt[q]; k += 32) S.y += (double)yb[64 * q + k] * (double)yb[64 * q + k];
     float Zm[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -479,6 +505,9 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
   __shared__ __align__(16) IdaMmaSmem s;
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
+  fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
+  if (B == 16 && threadIdx.x < 32) fill_frag16_tab(s.f16);
+  if (B == 16 && P.is_init && P.warm) __syncthreads();  // init_x16 reads the table right away
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
       for (int i = threadIdx.x; i < kMIn * kMP / 4; i += kMThreads)

@@ -33,12 +33,23 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
+// {a, b} - {c, d} in one packed FADD2 (sm_100: two fp32 lanes per instruction, each RN as FADD)
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n sub.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0,%1}, rd;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 // {a, b} -> hi = fp16(a,b), lo = fp16(a - hi, b - hi)
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(a, b);
   const float2 hf = __half22float2(h);
   hi = h2u(h);
-  lo = h2u(__floats2half2_rn(a - hf.x, b - hf.y));
+  const float2 r = fsub2(make_float2(a, b), hf);
+  lo = h2u(__floats2half2_rn(r.x, r.y));
 }
 
 // two u8 values (zero-extended) -> exact fp16 pair {lo, hi}
@@ -281,6 +292,69 @@ __device__ __forceinline__ Acc16 dct16_inv_from_yt(const Frag16& f, const Acc16&
 
 // A 16-byte block row with its bytes reordered to [0,1,8,9 | 2,3,10,11 | 4,5,12,13 | 6,7,14,15]:
 // word t then holds exactly the two byte pairs lane (g, t) needs (see u8_bfragT_il).
+// The B = 16 fragments as a shared table (register-lean kernels): per lane the A quads
+// ch, cl, th, tl and the stage-2 B pairs of fill_btab16. Filled by one warp.
+struct Frag16Tab {
+  uint4 a[4][32];
+  uint2 b[8][32];
+};
+__device__ __forceinline__ void fill_frag16_tab(Frag16Tab& T) {
+  const int lane = threadIdx.x & 31;
+  Frag16 f;
+  load_frag16(f);
+  T.a[0][lane] = make_uint4(f.ch[0], f.ch[1], f.ch[2], f.ch[3]);
+  T.a[1][lane] = make_uint4(f.cl[0], f.cl[1], f.cl[2], f.cl[3]);
+  T.a[2][lane] = make_uint4(f.th[0], f.th[1], f.th[2], f.th[3]);
+  T.a[3][lane] = make_uint4(f.tl[0], f.tl[1], f.tl[2], f.tl[3]);
+  fill_btab16(f, &T.b[0][0]);
+}
+__device__ __forceinline__ void quad(uint4 q, uint32_t (&a)[4]) {
+  a[0] = q.x;
+  a[1] = q.y;
+  a[2] = q.z;
+  a[3] = q.w;
+}
+// dct16_fwd_f32 with the fragments read from the table at the point of use.
+__device__ __forceinline__ Acc16 dct16_fwd_f32_t(const Frag16Tab& F, const float (&xv)[2][4]) {
+  const int lane = threadIdx.x & 31;
+  uint32_t ch[4], cl[4];
+  quad(F.a[0][lane], ch);
+  quad(F.a[1][lane], cl);
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    uint32_t h0, l0, h1, l1;
+    split2(xv[j][0], xv[j][1], h0, l0);
+    split2(xv[j][2], xv[j][3], h1, l1);
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], ch, l0, l1);
+    mma16816(T.v[j], cl, h0, h1);
+    mma16816(T.v[j], ch, h0, h1);
+  }
+  return stage2_tab(T, &F.b[0][0]);
+}
+// dct16_inv_from_yt with the fragments read from the table at the point of use.
+__device__ __forceinline__ Acc16 dct16_inv_from_yt_t(const Frag16Tab& F, const Acc16& Yt) {
+  const int lane = threadIdx.x & 31;
+  uint32_t bh[2][2], bl[2][2];
+  split2(Yt.v[0][0], Yt.v[0][1], bh[0][0], bl[0][0]);
+  split2(Yt.v[1][0], Yt.v[1][1], bh[0][1], bl[0][1]);
+  split2(Yt.v[0][2], Yt.v[0][3], bh[1][0], bl[1][0]);
+  split2(Yt.v[1][2], Yt.v[1][3], bh[1][1], bl[1][1]);
+  uint32_t th[4], tl[4];
+  quad(F.a[2][lane], th);
+  quad(F.a[3][lane], tl);
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], th, bl[j][0], bl[j][1]);
+    mma16816(T.v[j], tl, bh[j][0], bh[j][1]);
+    mma16816(T.v[j], th, bh[j][0], bh[j][1]);
+  }
+  return stage2_tab(T, &F.b[4][0]);
+}
+
 __device__ __forceinline__ uint4 interleave_row16(uint4 v) {
   return make_uint4(__byte_perm(v.x, v.z, 0x5410), __byte_perm(v.x, v.z, 0x7632), __byte_perm(v.y, v.w, 0x5410),
                     __byte_perm(v.y, v.w, 0x7632));
@@ -340,12 +414,18 @@ __device__ __forceinline__ void u8_bfragT(const uint8_t* blk, uint32_t (&bx)[2][
 }
 
 // ---------------------------------------------------------------------------
-// 8x8 transforms, two blocks per warp-MMA. Stage 1 uses m16n8k16 with the block-
-// diagonal A = diag(M, M) (so the two 8x8 operands stacked in B never mix), stage 2
-// uses m16n8k8 whose A fragment is the stage-1 accumulator. As for B = 16 the
-// forward runs transposed (Y^T = C8 P^T C8^T) so its accumulator pairs are the
-// inverse's stage-1 B fragments. Slot layout of the 16x8 results: rows g / g+8 =
-// row g of block 0 / block 1, columns 2t, 2t+1.
+// 8x8 transforms, two blocks per warp step. The forward runs transposed
+// (Y^T = C8 P^T C8^T, as for B = 16) so its accumulator pairs are the inverse's
+// stage-1 B fragments. Slot layout of the 16x8 results: rows g / g+8 = row g of
+// block 0 / block 1, columns 2t, 2t+1.
+//
+// Stage 1 (per block, no block-diagonal padding): one m16n8k16 with
+//   A = [Mh Mh; Ml Ml] (the basis hi/lo split over the two row halves),
+//   B = [Ph^T; Pl^T]   (the operand's hi/lo split over the two k halves),
+// so rows g and g+8 of D are Mh*P and Ml*P; their sum (one FADD2) is M*P to ~fp32
+// accuracy, and the two blocks' MMAs are independent. For exact (u8) operands
+// one m16n8k8 with A = [Mh; Ml] suffices. Stage 2 uses m16n8k8 whose A fragment
+// is the stage-1 result of both blocks (rows g: block 0, g+8: block 1).
 __device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
@@ -353,57 +433,69 @@ __device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1,
       : "r"(a0), "r"(a1), "r"(b0));
 }
 
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n add.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0,%1}, rd;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 struct Frag8 {
-  uint32_t ah[4], al[4];  // diag(C8, C8) as A: {p, 0, 0, p}, p = {C8[g][2t], C8[g][2t+1]}  (== C8^T as B)
-  uint32_t th[4], tl[4];  // diag(C8^T, C8^T) as A: p = {C8[2t][g], C8[2t+1][g]}            (== C8 as B)
+  uint32_t ch, cl;  // {C8[g][2t], C8[g][2t+1]} hi/lo: C8 rows as A (forward stage 1) == C8^T as B (stage 2)
+  uint32_t th, tl;  // {C8[2t][g], C8[2t+1][g]} hi/lo: C8^T rows as A (inverse stage 1) == C8 as B
 };
 
 __device__ __forceinline__ void load_frag8(Frag8& f) {
   const double* C = basis_dev<8>();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  uint32_t h, l;
-  split2((float)C[g * 8 + 2 * t], (float)C[g * 8 + 2 * t + 1], h, l);
-  f.ah[0] = f.ah[3] = h;
-  f.al[0] = f.al[3] = l;
-  f.ah[1] = f.ah[2] = f.al[1] = f.al[2] = 0u;
-  split2((float)C[(2 * t) * 8 + g], (float)C[(2 * t + 1) * 8 + g], h, l);
-  f.th[0] = f.th[3] = h;
-  f.tl[0] = f.tl[3] = l;
-  f.th[1] = f.th[2] = f.tl[1] = f.tl[2] = 0u;
+  split2((float)C[g * 8 + 2 * t], (float)C[g * 8 + 2 * t + 1], f.ch, f.cl);
+  split2((float)C[(2 * t) * 8 + g], (float)C[(2 * t + 1) * 8 + g], f.th, f.tl);
 }
 
-// Y^T of two 8x8 blocks from fp32 pixel pairs p0 = {P0[g][2t], P0[g][2t+1]},
-// p1 = {P1[g][2t], P1[g][2t+1]} (row-contiguous pairs).
+// M * P^T for one block: A = [Mh Mh; Ml Ml], B = {hi pair, lo pair} of the lane's P[g][2t..2t+1].
+__device__ __forceinline__ float2 stage1_8(uint32_t mh, uint32_t ml, uint32_t bh, uint32_t bl) {
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  const uint32_t a[4] = {mh, ml, mh, ml};
+  mma16816(d, a, bh, bl);
+  return fadd2(make_float2(d[0], d[1]), make_float2(d[2], d[3]));
+}
+
+// The same for an exact fp16 operand pair (u8 pixels).
+__device__ __forceinline__ float2 stage1_8_exact(uint32_t mh, uint32_t ml, uint32_t b) {
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  mma1688(d, mh, ml, b);
+  return fadd2(make_float2(d[0], d[1]), make_float2(d[2], d[3]));
+}
+
+// Stage 2 of both blocks: S (rows g: block 0 pair s0, g+8: block 1 pair s1) times the
+// basis given as the B operand pair (bh, bl).
+__device__ __forceinline__ void stage2_8(float2 s0, float2 s1, uint32_t bh, uint32_t bl, float (&R)[4]) {
+  uint32_t h0, l0, h1, l1;
+  split2(s0.x, s0.y, h0, l0);
+  split2(s1.x, s1.y, h1, l1);
+  R[0] = R[1] = R[2] = R[3] = 0.f;
+  mma1688(R, l0, l1, bh);
+  mma1688(R, h0, h1, bl);
+  mma1688(R, h0, h1, bh);
+}
+
+// Y^T of two fp32 blocks; lane (g, t) holds p0 = P0[g][2t..2t+1], p1 = P1[g][2t..2t+1].
 __device__ __forceinline__ void dct8x2_fwdT(const Frag8& f, float2 p0, float2 p1, float (&Y)[4]) {
   uint32_t h0, l0, h1, l1;
   split2(p0.x, p0.y, h0, l0);
   split2(p1.x, p1.y, h1, l1);
-  float Q[4] = {0.f, 0.f, 0.f, 0.f};
-  mma16816(Q, f.ah, l0, l1);
-  mma16816(Q, f.al, h0, h1);
-  mma16816(Q, f.ah, h0, h1);
-  uint32_t qh0, ql0, qh1, ql1;
-  split2(Q[0], Q[1], qh0, ql0);
-  split2(Q[2], Q[3], qh1, ql1);
-  Y[0] = Y[1] = Y[2] = Y[3] = 0.f;
-  mma1688(Y, ql0, ql1, f.ah[0]);
-  mma1688(Y, qh0, qh1, f.al[0]);
-  mma1688(Y, qh0, qh1, f.ah[0]);
+  const float2 q0 = stage1_8(f.ch, f.cl, h0, l0);
+  const float2 q1 = stage1_8(f.ch, f.cl, h1, l1);
+  stage2_8(q0, q1, f.ch, f.cl, Y);
 }
 
-// Same from exact-fp16 (u8) B fragments b0 = {P0[g][2t..2t+1]}, b1 = {P1[g][2t..2t+1]}: the
-// data needs no split, so stage 1 is hi/lo of the basis only.
+// Y^T of two u8 blocks given as exact fp16 pairs b0 (block 0) and b1 (block 1).
 __device__ __forceinline__ void dct8x2_fwdT_exact(const Frag8& f, uint32_t b0, uint32_t b1, float (&Y)[4]) {
-  float Q[4] = {0.f, 0.f, 0.f, 0.f};
-  mma16816(Q, f.al, b0, b1);
-  mma16816(Q, f.ah, b0, b1);
-  uint32_t qh0, ql0, qh1, ql1;
-  split2(Q[0], Q[1], qh0, ql0);
-  split2(Q[2], Q[3], qh1, ql1);
-  Y[0] = Y[1] = Y[2] = Y[3] = 0.f;
-  mma1688(Y, ql0, ql1, f.ah[0]);
-  mma1688(Y, qh0, qh1, f.al[0]);
-  mma1688(Y, qh0, qh1, f.ah[0]);
+  const float2 q0 = stage1_8_exact(f.ch, f.cl, b0);
+  const float2 q1 = stage1_8_exact(f.ch, f.cl, b1);
+  stage2_8(q0, q1, f.ch, f.cl, Y);
 }
 
 // X = C8^T Y C8 of two blocks given as Y^T in the slot layout (output of dct8x2_fwdT).
@@ -411,17 +503,9 @@ __device__ __forceinline__ void dct8x2_inv_from_yt(const Frag8& f, const float (
   uint32_t h0, l0, h1, l1;
   split2(Yt[0], Yt[1], h0, l0);
   split2(Yt[2], Yt[3], h1, l1);
-  float R[4] = {0.f, 0.f, 0.f, 0.f};
-  mma16816(R, f.th, l0, l1);
-  mma16816(R, f.tl, h0, h1);
-  mma16816(R, f.th, h0, h1);
-  uint32_t rh0, rl0, rh1, rl1;
-  split2(R[0], R[1], rh0, rl0);
-  split2(R[2], R[3], rh1, rl1);
-  X[0] = X[1] = X[2] = X[3] = 0.f;
-  mma1688(X, rl0, rl1, f.th[0]);
-  mma1688(X, rh0, rh1, f.tl[0]);
-  mma1688(X, rh0, rh1, f.th[0]);
+  const float2 r0 = stage1_8(f.th, f.tl, h0, l0);
+  const float2 r1 = stage1_8(f.th, f.tl, h1, l1);
+  stage2_8(r0, r1, f.th, f.tl, X);
 }
 
 // Positions of the D-fragment slots: slot s = 4j + i -> (row, col)
