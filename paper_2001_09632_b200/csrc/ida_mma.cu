@@ -505,6 +505,10 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
   __shared__ __align__(16) IdaMmaSmem s;
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
+  const bool denoise = !P.is_init && !P.x_in;
+  if (denoise)  // window first: its latency overlaps the metadata and table set-up
+    load_window<kVec>(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s.in);
+  const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
   if (B == 16 && threadIdx.x < 32) fill_frag16_tab(s.f16);
   if (B == 16 && P.is_init && P.warm) __syncthreads();  // init_x16 reads the table right away
@@ -528,9 +532,7 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
     }
     __syncthreads();
   } else {
-    const float thr = (float)(P.k * P.sigma_in[img]);
-    load_window<kVec>(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s.in);
-    denoise_region_mma(s.in, s.acc, R0, C0, P.Hc, P.Wc, thr);
+    denoise_region_mma(s.in, s.acc, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
   if (B == 16) block_phase16(P, img, R0, C0, s, S);
