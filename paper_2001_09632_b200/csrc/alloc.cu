@@ -10,13 +10,16 @@
 //   block scan for exact ties, then clamp to caps; capped blocks leave.
 // Finally counts = base + alloc and offsets = exclusive scan of counts.
 #include <cub/block/block_reduce.cuh>
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
+#include <cstdlib>
 
 #include "alloc_keys.h"
 #include "common.cuh"
 #include "internal.h"
 
 namespace abcs_b200 {
+namespace cg = cooperative_groups;
 
 constexpr int kAllocThreads = 1024;
 
@@ -28,8 +31,9 @@ struct AllocScratch {
 };
 
 size_t allocate_scratch_bytes(int32_t n_blocks, int32_t n_vectors) {
-  // radix kernel: 17 B per block; class kernel: 2 u16 per block, padded to 1024-thread spans
-  const size_t per = std::max((size_t)n_blocks * (8 + 4 + 4 + 1), ((size_t)n_blocks + 1024) * 4);
+  // radix kernel: 17 B per block; class kernel: 2 u16 per block, each cluster CTA's range padded
+  // to 1024-thread spans (up to 16 CTAs per image)
+  const size_t per = std::max((size_t)n_blocks * (8 + 4 + 4 + 1), ((size_t)n_blocks + 16 * 1024) * 4);
   return per * (size_t)n_vectors + 256;
 }
 
@@ -280,13 +284,23 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
 // exact RN64 key per DISTINCT weight (DD: <= phase1 + 1 classes; BBV: the
 // distinct boundary variations) instead of one per block. Per round:
 // histogram of active weights -> compacted class table (count, whole, key) ->
-// MSB radix select of the leftover threshold over the classes weighted by
-// their counts -> exact ties resolved by block index (ordered CTA scan) ->
-// clamp. Results are identical to alloc_kernel / the reference.
-// 256 threads; each thread owns a contiguous range of blocks and of weight
-// values so every CTA-wide scan is a single BlockScan. Per-block state (weight,
-// allocation) lives in shared memory when it fits, else in global scratch.
-constexpr int kClassThreads = 1024;  // one CTA per weight vector: small batches need wide CTAs
+// threshold of the leftover units over the classes weighted by their counts
+// (rank mode for few classes, else an MSB radix select) -> exact ties resolved
+// by block index (ordered scan) -> clamp. Results are identical to alloc_kernel
+// / the reference.
+//
+// A weight vector (image) is owned by a thread-block CLUSTER of cs CTAs
+// (cs = 1 .. 16, chosen by the launcher so small batches of large images still
+// fill the GPU). CTA r of the cluster owns the contiguous block range
+// [nb r / cs, nb (r + 1) / cs); within a CTA each thread owns a contiguous
+// sub-range, so "ties to the lower index" is one ordered scan: thread order
+// inside the CTA, rank order across the cluster. The round's cross-CTA terms go
+// through distributed shared memory: the active-weight histogram and (T,
+// active) after barrier A, the tie counts of lower ranks after barrier C, and
+// (taken, still open) after barrier D; the class table and the threshold are
+// recomputed identically in every CTA from the cluster-wide histogram.
+constexpr int kClassThreads = 1024;
+constexpr int kMaxCluster = 16;
 static_assert(kClassThreads <= 1024, "allocate_scratch_bytes pads spans by 1024");
 
 template <typename T>
@@ -295,15 +309,16 @@ struct Arr {
   __device__ __forceinline__ T& operator[](int i) const { return p[i]; }
 };
 
-// entries per per-block array: ceil(nb / threads) * threads (thread-strided layout)
-__host__ __device__ __forceinline__ int class_span(int nb) {
-  return (nb + kClassThreads - 1) / kClassThreads * kClassThreads;
+// entries per per-block array of a CTA owning nbl blocks (thread-strided layout)
+__host__ __device__ __forceinline__ int class_span(int nbl) {
+  return (nbl + kClassThreads - 1) / kClassThreads * kClassThreads;
 }
+__host__ __device__ __forceinline__ int cluster_lo(int nb, int cs, int r) { return (int)((int64_t)nb * r / cs); }
 
-size_t class_smem_bytes(int wmax, int n_blocks, bool arrays_in_smem) {
+size_t class_smem_bytes(int wmax, int n_blocks, int cs, bool arrays_in_smem) {
   const size_t ncls = (size_t)std::min(n_blocks, wmax + 1);
-  size_t b = 4 * (size_t)(wmax + 1) + ncls * (8 + 4 + 4 + 1) + 64;
-  if (arrays_in_smem) b += (size_t)class_span(n_blocks) * 4 + 16;
+  size_t b = 8 * (size_t)(wmax + 1) + ncls * (8 + 4 + 4 + 1) + 64;
+  if (arrays_in_smem) b += (size_t)class_span((n_blocks + cs - 1) / cs) * 4 + 16;
   return b;
 }
 
@@ -321,12 +336,19 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   __shared__ unsigned int hist8[256];
   __shared__ long long sh_ll[4];
   __shared__ int sh_int[4];
+  __shared__ long long pub[6];  // published to the cluster: 0/1 (T, active) | 2 ties | 3/4 (taken, open) | 5 misc
+  __shared__ long long agg[2];  // cluster aggregates read back by warp 0
   extern __shared__ __align__(16) unsigned char dyn[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks(), rk = (int)cluster.block_rank();
   const int ncls_cap = min(nb, wmax + 1);
   unsigned char* p = dyn;
   uint64_t* ckey = reinterpret_cast<uint64_t*>(p);
   p += 8 * (size_t)ncls_cap;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);  // this CTA's active-weight histogram (read cluster-wide)
+  p += 4 * (size_t)(wmax + 1);
+  // the cluster's histogram, then weight -> class index (a cluster of one uses hist in place)
+  uint32_t* ghist = cs == 1 ? hist : reinterpret_cast<uint32_t*>(p);
   p += 4 * (size_t)(wmax + 1);
   uint32_t* ccnt = reinterpret_cast<uint32_t*>(p);
   p += 4 * (size_t)ncls_cap;
@@ -334,40 +356,93 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   p += 4 * (size_t)ncls_cap;
   uint8_t* cflag = p;
   p += ncls_cap;
-  const int v = blockIdx.x, tid = threadIdx.x;
+  const int v = blockIdx.x / cs, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = cluster_lo(nb, cs, rk), nbl = cluster_lo(nb, cs, rk + 1) - lo;
   Arr<uint16_t> wv, av;  // weight and allocation per block
   // per-block state laid out thread-strided (thread t's k-th block at k * kClassThreads + t) so
-  // the warps' loads coalesce while each thread still walks its blocks in index order
-  const int span = class_span(nb);
+  // the warps' accesses coalesce while each thread still walks its blocks in index order
+  const int span = class_span(nbl);
   if constexpr (kSmemArrays) {
     uint16_t* q = reinterpret_cast<uint16_t*>(dyn + ((p - dyn + 15) & ~15));
     wv.p = q;
     av.p = q + span;
   } else {
-    wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)v * 2 * span;
+    const int span_max = class_span((nb + cs - 1) / cs);
+    wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)blockIdx.x * 2 * span_max;
     av.p = wv.p + span;
   }
-  const uint32_t* w = weights + (int64_t)v * nb;
-  const int per_b = (nb + kClassThreads - 1) / kClassThreads;  // contiguous block range per thread
-  const int b0 = min(nb, tid * per_b), b1 = min(nb, b0 + per_b);
+  const uint32_t* w = weights + (int64_t)v * nb + lo;
+  const int per_b = (nbl + kClassThreads - 1) / kClassThreads;  // contiguous block range per thread
+  const int b0 = min(nbl, tid * per_b), b1 = min(nbl, b0 + per_b);
   const int per_c = (wmax + 1 + kClassThreads - 1) / kClassThreads;
   const int c0 = min(wmax + 1, tid * per_c), c1 = min(wmax + 1, c0 + per_c);
-  if (tid == 0) sh_int[3] = 0;
-  __syncthreads();
-  for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
-    const uint32_t wi = w[i];
-    if (wi > (uint32_t)wmax) sh_int[3] = 1;  // caller's weight bound violated
-    wv[ph] = (uint16_t)min(wi, (uint32_t)wmax);
-    av[ph] = 0;
-  }
   if (budget < 0 || (unsigned long long)budget > (unsigned long long)cap * (unsigned long long)nb || cap < 0 ||
-      cap > 65535) {
-    if (tid == 0 && status) status[v] = ABCS_ERR_INVALID_ARGUMENT;
+      cap > 65535) {  // the same decision in every CTA of the cluster (before any cluster barrier)
+    if (rk == 0 && tid == 0 && status) status[v] = ABCS_ERR_INVALID_ARGUMENT;
     return;
   }
+  // cluster barrier (a CTA barrier for a cluster of one)
+  auto csync = [&]() {
+    if (cs == 1) __syncthreads();
+    else cluster.sync();
+  };
+  // sum over the cluster's ranks < upto of pub[slot0] (and pub[slot1]) -> agg[0..1]; after csync
+  auto cluster_sum2 = [&](int slot0, int slot1, int upto) {
+    if (warp == 0) {
+      long long a = 0, b = 0;
+      if (lane < upto) {
+        a = cs == 1 ? pub[slot0] : *cluster.map_shared_rank(&pub[slot0], lane);
+        if (slot1 >= 0) b = cs == 1 ? pub[slot1] : *cluster.map_shared_rank(&pub[slot1], lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (lane == 0) {
+        agg[0] = a;
+        agg[1] = b;
+      }
+    }
+    __syncthreads();
+  };
+  // weights: coalesced loads, scattered into the owners' thread-strided slots
+  if (tid == 0) sh_int[3] = 0;
   __syncthreads();
+  if constexpr (kSmemArrays) {
+    for (int j = tid; j < nbl; j += kClassThreads) {
+      const uint32_t wi = w[j];
+      if (wi > (uint32_t)wmax) sh_int[3] = 1;  // caller's weight bound violated
+      const int owner = j / per_b, ph = (j - owner * per_b) * kClassThreads + owner;
+      wv[ph] = (uint16_t)min(wi, (uint32_t)wmax);
+      av[ph] = 0;
+    }
+  } else {  // global state: keep its accesses coalesced, read the weights per thread range
+    int i = b0, ph = tid;
+    if (((uintptr_t)(w + b0) & 15) == 0)  // 16-byte loads of 4 weights
+      for (; i + 4 <= b1; i += 4, ph += 4 * kClassThreads) {
+        const uint4 q = *reinterpret_cast<const uint4*>(w + i);
+        const uint32_t wq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (wq[e] > (uint32_t)wmax) sh_int[3] = 1;
+          wv[ph + e * kClassThreads] = (uint16_t)min(wq[e], (uint32_t)wmax);
+          av[ph + e * kClassThreads] = 0;
+        }
+      }
+    for (; i < b1; ++i, ph += kClassThreads) {
+      const uint32_t wi = w[i];
+      if (wi > (uint32_t)wmax) sh_int[3] = 1;
+      wv[ph] = (uint16_t)min(wi, (uint32_t)wmax);
+      av[ph] = 0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) pub[5] = sh_int[3];
+  csync();
+  cluster_sum2(5, -1, cs);
   long long remaining = budget;
-  int st = sh_int[3] ? ABCS_ERR_LOGIC : ABCS_OK;
+  int st = agg[0] ? ABCS_ERR_LOGIC : ABCS_OK;
   int round = 0;
   while (remaining > 0 && st == ABCS_OK) {
     if (++round > nb + 1) {
@@ -382,31 +457,38 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
       const bool act = i < b1 && (int)av[ph] < cap;
       const int wi = act ? (int)wv[ph] : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, wi);
-      if (act && (__ffs(peers) - 1) == (tid & 31)) atomicAdd(&hist[wi], (unsigned)__popc(peers));
+      if (act && (__ffs(peers) - 1) == lane) atomicAdd(&hist[wi], (unsigned)__popc(peers));
       if (act) {
         tw += (unsigned)wi;
         na += 1;
       }
     }
-    const unsigned long long T0 = Reduce64(tmp.r).Sum(tw);
+    const unsigned long long T0l = Reduce64(tmp.r).Sum(tw);
     __syncthreads();
-    const unsigned long long n_active = Reduce64(tmp.r).Sum(na);
+    const unsigned long long nal = Reduce64(tmp.r).Sum(na);
     if (tid == 0) {
-      sh_ll[0] = (long long)T0;
-      sh_ll[1] = (long long)n_active;
+      pub[0] = (long long)T0l;
+      pub[1] = (long long)nal;
     }
-    __syncthreads();
-    const bool uniform = sh_ll[0] == 0;
-    const uint64_t T = uniform ? (uint64_t)sh_ll[1] : (uint64_t)sh_ll[0];
-    const long long n_act = sh_ll[1];
+    csync();  // A: pub[0..1] and every CTA's hist complete
+    if (cs > 1)
+      for (int c = c0; c < c1; ++c) {
+        uint32_t h = 0;
+        for (int q = 0; q < cs; ++q) h += cluster.map_shared_rank(hist, q)[c];
+        ghist[c] = h;
+      }
+    cluster_sum2(0, 1, cs);  // (ends with __syncthreads: ghist complete)
+    const bool uniform = agg[0] == 0;
+    const uint64_t T = uniform ? (uint64_t)agg[1] : (uint64_t)agg[0];
+    const long long n_act = agg[1];
     // compact the nonempty classes (ordered by weight) and compute their shares
     int mine = 0;
-    for (int c = c0; c < c1; ++c) mine += hist[c] ? 1 : 0;
+    for (int c = c0; c < c1; ++c) mine += ghist[c] ? 1 : 0;
     int id, ncls;
     ScanI(tmp.s).ExclusiveSum(mine, id, ncls);
     unsigned long long handed = 0;
     for (int c = c0; c < c1; ++c) {
-      const uint32_t h = hist[c];
+      const uint32_t h = ghist[c];
       if (!h) continue;
       const int k = id++;
       ccnt[k] = h;
@@ -415,7 +497,7 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
       cwhole[k] = (uint32_t)sh.whole;
       ckey[k] = sh.key;
       cflag[k] = (uint8_t)sh.flag;
-      hist[c] = (uint32_t)k;
+      ghist[c] = (uint32_t)k;
       handed += (unsigned long long)h * sh.whole;
     }
     __syncthreads();
@@ -486,7 +568,6 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
         }
         __syncthreads();
         if (tid < 32) {
-          const int lane = tid;
           const int per = (nbins + 31) / 32;
           unsigned local = 0;
           for (int q = 0; q < per; ++q) {
@@ -548,22 +629,25 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
       if (kk != prefix) return kk > prefix ? 1 : 0;
       return (int)cflag[k] > flag_sel ? 1 : ((int)cflag[k] == flag_sel ? 2 : 0);
     };
-    int tie_base = 0;
-    if (!sel_all && !none && !all_equal_taken) {
+    long long tie_base = 0;
+    if (!sel_all && !none && !all_equal_taken) {  // the same decision in every CTA
       int ties = 0;
       for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads)
-        if ((int)av[ph] < cap && cls_rel((int)hist[wv[ph]]) == 2) ++ties;
-      int tot;
-      ScanI(tmp.s).ExclusiveSum(ties, tie_base, tot);
-      __syncthreads();
+        if ((int)av[ph] < cap && cls_rel((int)ghist[wv[ph]]) == 2) ++ties;
+      int tb, tot;
+      ScanI(tmp.s).ExclusiveSum(ties, tb, tot);
+      if (tid == 0) pub[2] = tot;
+      csync();                 // C: tie counts of every rank published
+      cluster_sum2(2, -1, rk);  // ties of the lower ranks (lower block indices)
+      tie_base = tb + agg[0];
     }
     unsigned long long taken_sum = 0, still = 0;
     for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
       if ((int)av[ph] >= cap) continue;
-      const int k = (int)hist[wv[ph]];
+      const int k = (int)ghist[wv[ph]];
       const int rel = cls_rel(k);
       bool sel = rel == 1;
-      if (rel == 2) sel = all_equal_taken || (long long)(tie_base++) < need;
+      if (rel == 2) sel = all_equal_taken || (tie_base++) < need;
       const long long give = (long long)cwhole[k] + (sel ? 1 : 0);
       const long long room = (long long)cap - av[ph];
       const long long taken = give < room ? give : room;  // sensing.cpp:162-171
@@ -575,26 +659,87 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     __syncthreads();
     const unsigned long long st_open = Reduce64(tmp.r).Sum(still);
     if (tid == 0) {
-      sh_ll[0] = (long long)tk;
-      sh_ll[1] = (long long)st_open;
+      pub[3] = (long long)tk;
+      pub[4] = (long long)st_open;
     }
-    __syncthreads();
-    remaining -= sh_ll[0];
-    if (remaining > 0 && sh_ll[1] == 0) st = ABCS_ERR_LOGIC;  // capacity exhausted
+    csync();  // D
+    cluster_sum2(3, 4, cs);
+    remaining -= agg[0];
+    if (remaining > 0 && agg[1] == 0) st = ABCS_ERR_LOGIC;  // capacity exhausted
     __syncthreads();
   }
-  // counts = base + allocation, offsets = exclusive scan (contiguous ranges: one scan)
+  // counts = base + allocation, offsets = exclusive scan over the image (this CTA's range
+  // after the lower ranks'); written coalesced: warp w walks its threads' contiguous ranges
+  // in index order with a running warp scan
   int mine = 0;
   for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) mine += base + (int)av[ph];
   int ex, total;
   ScanI(tmp.s).ExclusiveSum(mine, ex, total);
-  for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
-    const int c = base + (int)av[ph];
-    counts[(int64_t)v * nb + i] = (uint16_t)c;
-    if (offsets) offsets[(int64_t)v * nb + i] = ex;
-    ex += c;
+  if (tid == 0) pub[5] = total;
+  csync();  // E
+  cluster_sum2(5, -1, rk);
+  uint16_t* cnt_out = counts + (int64_t)v * nb + lo;
+  int32_t* off_out = offsets ? offsets + (int64_t)v * nb + lo : nullptr;
+  if constexpr (!kSmemArrays) {  // global state: per thread range, 16-byte stores where aligned
+    ex += (int)agg[0];
+    int i = b0, ph = tid;
+    if (((uintptr_t)(cnt_out + b0) & 15) == 0 && (!off_out || ((uintptr_t)(off_out + b0) & 15) == 0))
+      for (; i + 8 <= b1; i += 8, ph += 8 * kClassThreads) {
+        int c[8], o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          c[e] = base + (int)av[ph + e * kClassThreads];
+          o[e] = ex;
+          ex += c[e];
+        }
+        *reinterpret_cast<uint4*>(cnt_out + i) =
+            make_uint4((uint32_t)c[0] | (uint32_t)c[1] << 16, (uint32_t)c[2] | (uint32_t)c[3] << 16,
+                       (uint32_t)c[4] | (uint32_t)c[5] << 16, (uint32_t)c[6] | (uint32_t)c[7] << 16);
+        if (off_out) {
+          *reinterpret_cast<int4*>(off_out + i) = make_int4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<int4*>(off_out + i + 4) = make_int4(o[4], o[5], o[6], o[7]);
+        }
+      }
+    for (; i < b1; ++i, ph += kClassThreads) {
+      const int c = base + (int)av[ph];
+      cnt_out[i] = (uint16_t)c;
+      if (off_out) off_out[i] = ex;
+      ex += c;
+    }
   }
-  if (tid == 0 && status) status[v] = st;
+  int run = __shfl_sync(0xffffffffu, ex, 0) + (int)agg[0];  // prefix at block warp * 32 * per_b
+  const int wbase = warp * 32 * per_b;
+  for (int j = 0; j < (kSmemArrays ? per_b : 0); ++j) {
+    const int idx = wbase + j * 32 + lane;
+    int c = 0;
+    if (idx < nbl) {
+      const int owner = idx / per_b;
+      c = base + (int)av[(idx - owner * per_b) * kClassThreads + owner];
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (idx < nbl) {
+      cnt_out[idx] = (uint16_t)c;
+      if (off_out) off_out[idx] = run + incl - c;
+    }
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (rk == 0 && tid == 0 && status) status[v] = st;
+  if (cs > 1) cluster.sync();  // F: no CTA leaves while a peer may still read its shared memory
+}
+
+// Cluster size for n_vectors images of n_blocks: split an image over more CTAs only while the
+// batch stays within half the SMs (cluster barriers cost more than they save beyond that; cfg5
+// measured 0.45 / 0.27 / 0.09 / 0.12 / 0.14 ms at 1 / 2 / 4 / 8 / 16) and CTAs keep >= 2048 blocks.
+static int class_cluster_size(const Ctx* ctx, int32_t n_blocks, int32_t n_vectors) {
+  int cs = 1;
+  while (2 * cs <= kMaxCluster && (int64_t)n_vectors * cs * 2 <= ctx->sm_count / 2 && n_blocks / (cs * 2) >= 2048)
+    cs *= 2;
+  return cs;
 }
 
 int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
@@ -604,27 +749,45 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
   if (!caps && wmax >= 0 && wmax < 65536 && cap <= 65535) {
     static bool attr_set = false;
     if (!attr_set) {
-      cudaFuncSetAttribute(alloc_class_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(alloc_class_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      for (auto k : {alloc_class_kernel<true>, alloc_class_kernel<false>}) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
       attr_set = true;
     }
-    uint32_t* gscr = reinterpret_cast<uint32_t*>(scratch);  // n_vectors * n_blocks * 2 u16
-    const size_t smem_in = class_smem_bytes(wmax, n_blocks, true);
-    const size_t smem_out = class_smem_bytes(wmax, n_blocks, false);
-    const int kt = ktimer_begin(ctx, s, "alloc_class");
-    if (smem_in <= 100 * 1024) {  // keep 2 CTAs (2048 threads) per SM
-      alloc_class_kernel<true><<<n_vectors, kClassThreads, smem_in, s>>>(weights, n_blocks, wmax, budget, cap, base,
-                                                                         counts, offsets, status, gscr);
-    } else if (smem_out <= 200 * 1024) {
-      alloc_class_kernel<false><<<n_vectors, kClassThreads, smem_out, s>>>(weights, n_blocks, wmax, budget, cap,
-                                                                           base, counts, offsets, status, gscr);
-    } else {
-      ktimer_end(ctx, s, -1);
-      goto generic;
+    const char* env = getenv("ABCS_ALLOC_CLUSTER");  // tuning override (power of two <= 16)
+    const int cs = env ? std::max(1, std::min(kMaxCluster, atoi(env))) : class_cluster_size(ctx, n_blocks, n_vectors);
+    uint32_t* gscr = reinterpret_cast<uint32_t*>(scratch);  // n_vectors * n_blocks * 2 u16 (+ padding)
+    const size_t smem_in = class_smem_bytes(wmax, n_blocks, cs, true);
+    const size_t smem_out = class_smem_bytes(wmax, n_blocks, cs, false);
+    bool in_smem;
+    if (smem_in <= 100 * 1024) in_smem = true;  // keep 2 CTAs (2048 threads) per SM
+    else if (smem_out <= 200 * 1024) in_smem = false;
+    else goto generic;
+    {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3((unsigned)(n_vectors * cs));
+      lc.blockDim = dim3(kClassThreads);
+      lc.dynamicSmemBytes = in_smem ? smem_in : smem_out;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      const int kt = ktimer_begin(ctx, s, "alloc_class");
+      const cudaError_t e =
+          in_smem ? cudaLaunchKernelEx(&lc, alloc_class_kernel<true>, weights, (int)n_blocks, (int)wmax, budget,
+                                       (int)cap, (int)base, counts, offsets, status, gscr)
+                  : cudaLaunchKernelEx(&lc, alloc_class_kernel<false>, weights, (int)n_blocks, (int)wmax, budget,
+                                       (int)cap, (int)base, counts, offsets, status, gscr);
+      ktimer_end(ctx, s, kt);
+      ctx->launches++;
+      if (e != cudaSuccess) return cuda_status(e, "allocate(class) launch");
+      return cuda_status(cudaGetLastError(), "allocate(class) launch");
     }
-    ktimer_end(ctx, s, kt);
-    ctx->launches++;
-    return cuda_status(cudaGetLastError(), "allocate(class) launch");
   }
 generic:
   AllocScratch scr;

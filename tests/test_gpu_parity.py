@@ -215,6 +215,27 @@ def test_allocator_adversarial_and_large(p, checker, rng):
         p.largest_remainder_allocate([1, 2], 10, [1, 1])
 
 
+@pytest.mark.parametrize("H,W,B,num,den,algo", [(1536, 1536, 16, 3, 10, 2), (1000, 1480, 16, 1, 4, 1),
+                                                  (1080, 1920, 8, 1, 5, 1)])
+def test_class_allocator_cluster_sizes(p, torch, checker, H, W, B, num, den, algo):
+    """The weight-class allocator split over 1..16 CTAs of a cluster: bit-identical counts
+    (ties to the lower index across CTA ranges) and equal to the reference."""
+    imgs = synth(H, W, n=3, seed=H + W + algo, video=(B == 8))
+    got = {}
+    try:
+        for cs in (1, 2, 4, 8, 16):
+            os.environ["ABCS_ALLOC_CLUSTER"] = str(cs)
+            b = sense_dev(p, torch, imgs, B, num, den, algo)
+            got[cs] = (b.counts.cpu().numpy().view(np.uint16).copy(), b.offsets.cpu().numpy().copy())
+    finally:
+        os.environ.pop("ABCS_ALLOC_CLUSTER", None)
+    for cs in (2, 4, 8, 16):
+        assert np.array_equal(got[cs][0], got[1][0]), cs
+        assert np.array_equal(got[cs][1], got[1][1]), cs
+    want = checker.sense(imgs[1], B, num, den, algo)
+    assert np.array_equal(got[16][0][1].astype(np.int64), want["counts"].astype(np.int64))
+
+
 # ---- decode / operators -------------------------------------------------------------------
 def test_decode_golden(p):
     z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
