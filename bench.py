@@ -253,14 +253,28 @@ def run_ours(args, world, rank, local):
     nsub = len(SUBRATES)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nsub + 1)] for _ in range(args.steps)]
 
-    def step(evs):
-        # sense (DD phase 1 + allocation + zigzag gather) and decode_idct, fused over the payload
+    def step_independent(evs):
+        # one subrate at a time: sense (DD phase 1 + allocation + zigzag gather) and decode_idct,
+        # fused over the payload
         for j, (c, pl, b) in enumerate(zip(cfgs, plans, batches)):
             if evs and j == 0:
                 evs[0].record(stream)
             p.sense_decode_batch(imgs, c, pl, out=b, image_out=outs[j])
             if evs:
                 evs[j + 1].record(stream)
+
+    def step_sweep(evs):
+        # the subrate sweep in one call: DD phase 1 of the 3 subrates from one forward transform
+        # per block, then per subrate its own fixup, allocation, payload and decode (outputs
+        # identical to step_independent: tests/test_gpu_parity.py::test_sense_decode_sweep_*)
+        if evs:
+            evs[0].record(stream)
+        p.sense_decode_sweep(imgs, cfgs, outs=batches, image_outs=outs)
+        if evs:
+            for e in evs[1:]:
+                e.record(stream)
+
+    step = step_independent if args.independent else step_sweep
 
     for _ in range(args.warmup):
         step(None)
@@ -297,8 +311,23 @@ def run_ours(args, world, rank, local):
     ctx.set_pipeline_streams(3)
     ser_step_ms = ser0.elapsed_time(ser1) / args.steps
     clk = clocks.stop() if clocks else None
+    # the per-subrate path (one sense_decode_batch per subrate), timed the same way: its
+    # per-subrate phases give the pipeline roofline, and its rate is reported beside the sweep
+    ev_ind = [[torch.cuda.Event(enable_timing=True) for _ in range(nsub + 1)] for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        step_independent(None)
+    torch.cuda.synchronize()
     barrier(world)
-    sub_ms = [sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps for j in range(nsub)]
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0.record(stream)
+    for k in range(args.steps):
+        step_independent(ev_ind[k])
+    i1.record(stream)
+    torch.cuda.synchronize()
+    ind_ms_max = max_over_ranks(i0.elapsed_time(i1), world, dev)
+    barrier(world)
+    sub_ms = [sum(ev_ind[k][j].elapsed_time(ev_ind[k][j + 1]) for k in range(args.steps)) / args.steps
+              for j in range(nsub)]
     ms = start.elapsed_time(end)
     ms_max = max_over_ranks(ms, world, dev)
     ms_step = ms_max / args.steps
@@ -313,6 +342,7 @@ def run_ours(args, world, rank, local):
     alg_bytes = {  # per step (all subrates)
         "sense16_gather_decode": sum(n * (N + 4 * K + 6 * nB + 4 * N) for K in Ks),  # u8 in, payload+counts/offsets, f32 out
         "sense16_weights": nsub * n * (N + 4 * nB),                                    # u8 in, n_i out
+        "sense16_weights_sweep": n * (N + nsub * 4 * nB),                              # u8 in once, n_i per subrate
         "alloc_cta": nsub * n * (4 * nB + 6 * nB),                                     # n_i in, counts+offsets out
     }
     kt = {k: v for k, v in ktimes.items()}
@@ -449,7 +479,14 @@ def run_ours(args, world, rank, local):
             "roofline": roof,
             "kernels": kernels,
             "serialised_ms_per_step": round(ser_step_ms, 3),
-            "pipeline_roofline": {"what": "whole fused step vs its algorithmic bytes (SURVEY 8d)",
+            "step_api": ("one sense_decode_batch per subrate" if args.independent else
+                         "sense_decode_sweep (abcs_sense_decode_sweep_batch): shared DD phase-1 transform"),
+            "independent_subrates": {"what": "the same step as one sense_decode_batch call per subrate",
+                                     "value": round(aggregate_rate(px_step * args.steps, world, ind_ms_max / 1e3)
+                                                    / 1e6, 1), "unit": "MP/s",
+                                     "ms_per_step": round(ind_ms_max / args.steps, 3)},
+            "pipeline_roofline": {"what": "whole step vs its algorithmic bytes (SURVEY 8d), per subrate on the "
+                                          "independent path",
                                   "achieved": round(pipe_ach, 1), "frac": round(pipe_ach / hbm, 4), "phases": per_j},
             "e2e": {"value": round(e2e_value, 1), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "abcs_sense_decode_host (pinned host buffers)"},
@@ -653,6 +690,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-config-sweep", action="store_true", help="skip the cfg1/3/4/5 device sweep")
+    ap.add_argument("--independent", action="store_true",
+                    help="time one sense_decode_batch per subrate instead of the sweep call")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:

@@ -203,6 +203,20 @@ int abcs_sense_decode_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const ui
                             int32_t* d_offsets, float* d_payload, float* d_side, float* d_out,
                             int64_t out_stride, int32_t out_pitch, void* stream);
 
+/* A subrate sweep: abcs_sense_decode_batch of the same images under n_plans
+ * plans (the reference's bench runs sense() per --crs entry on each image,
+ * tools/abcs_main.cpp:215-260). Every pointer argument indexed by plan is a
+ * HOST array of n_plans device pointers (d_offsets / d_side may be NULL or hold
+ * NULLs). When 2..4 plans are DD with B = 16 on the same geometry, DD phase 1
+ * of all of them comes from one forward transform per block; each plan still
+ * gets its own exact fixup, allocation, payload and decode, identical to
+ * separate abcs_sense_decode_batch calls. Otherwise the plans run one by one. */
+int abcs_sense_decode_sweep_batch(abcs_ctx* ctx, const abcs_sense_plan* plans, int32_t n_plans,
+                                  const uint8_t* d_images, int64_t image_stride, int32_t pitch,
+                                  int32_t n_images, uint16_t* const* d_counts, int32_t* const* d_offsets,
+                                  float* const* d_payload, float* const* d_side, float* const* d_out,
+                                  int64_t out_stride, int32_t out_pitch, void* stream);
+
 /* Phase-1 weights only (bbv_measure variation / DD significance counts n_i),
  * u32 per block — exposes the pre-measurement of sensing.cpp:266-294 / :341-358. */
 int abcs_sense_weights_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_images,

@@ -9,6 +9,6 @@ from .abcs import (Algorithm, AllocationPlan, BbvParams, BlockGrid, BudgetSummar
                    ReconConfig, ReconMethod, ReconResult, SensingConfig, SensingOperator, SynthSpec, TraceRow,
                    UnsupportedError, allocate_bbv, bbv_measure, dd_threshold, decode_batch, decode_idct, denoise,
                    ida_batch, largest_remainder_allocate, make_grid, measurement_budget, reconstruct, sense,
-                   sense_batch, sense_decode_batch, sense_dd, sense_plan, sense_zz, synth_images, synth_images_host, zigzag_order)
+                   sense_batch, sense_decode_batch, sense_decode_sweep, sense_dd, sense_plan, sense_zz, synth_images, synth_images_host, zigzag_order)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -98,6 +98,8 @@ SIGNATURES = {
     "abcs_synth_generate_host": (C.c_int, [C.POINTER(SynthSpecC), I64, I32, P]),
     "abcs_sense_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P, P, P]),
     "abcs_sense_decode_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P, P, P, I64, I32, P]),
+    "abcs_sense_decode_sweep_batch": (C.c_int, [P, C.POINTER(SensePlanC), I32, P, I64, I32, I32, P, P, P, P, P, I64,
+                                                I32, P]),
     "abcs_sense_weights_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P]),
     "abcs_allocate_batch": (C.c_int, [P, P, I32, I32, I64, P, I32, I32, P, P, P, P]),
     "abcs_decode_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, P, I64, I32, P, P, P]),

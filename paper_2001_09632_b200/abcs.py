@@ -416,6 +416,47 @@ def sense_decode_batch(images, cfg: SensingConfig, plan: Optional[SensePlanC] = 
     return out, image_out
 
 
+def sense_decode_sweep(images, cfgs, outs=None, image_outs=None):
+    """sense_decode_batch of the same (n, H, W) uint8 CUDA images under each config of cfgs
+    (a subrate sweep, as the reference bench's --crs loop, tools/abcs_main.cpp:215-260).
+    DD B=16 sweeps share DD phase 1's forward transform; each config's outputs are identical
+    to its own sense_decode_batch call. Returns [(MeasurementBatch, decoded images)]."""
+    torch = _torch()
+    if images.dtype != torch.uint8 or images.dim() != 3 or not images.is_cuda:
+        raise ValueError("images must be a (n, H, W) uint8 CUDA tensor")
+    cfgs = list(cfgs)
+    if not cfgs:
+        return []
+    n, H, W = images.shape
+    dev = images.device
+    plans = [sense_plan(c, H, W) for c in cfgs]
+    Hc, Wc = plans[0].rows * plans[0].block, plans[0].cols * plans[0].block
+    if any(q.rows * q.block != Hc or q.cols * q.block != Wc for q in plans):
+        raise ValueError("sweep configs must crop the images to the same grid")
+    if outs is None:
+        outs = []
+        for c, q in zip(cfgs, plans):
+            K, S, NB = q.coeffs_per_image, q.side_per_image, q.n_blocks
+            outs.append(MeasurementBatch(
+                plan=q, cfg=c,
+                counts=torch.empty((n, NB), dtype=torch.uint16, device=dev),
+                offsets=torch.empty((n, NB), dtype=torch.int32, device=dev),
+                payload=torch.empty((n, max(K, 1)), dtype=torch.float32, device=dev)[:, :K],
+                side=torch.empty((n, S), dtype=torch.float32, device=dev) if S > 0 else None))
+    if image_outs is None:
+        image_outs = [torch.empty((n, Hc, Wc), dtype=torch.float32, device=dev) for _ in cfgs]
+    images = images.contiguous()
+    m = len(cfgs)
+    parr = (SensePlanC * m)(*plans)
+    arr = lambda xs: (C.c_void_p * m)(*[_ptr(x) for x in xs])  # noqa: E731
+    ctx = Context.get(dev.index)
+    _check(_lib.load().abcs_sense_decode_sweep_batch(
+        ctx.handle, parr, m, images.data_ptr(), H * W, W, n, arr([o.counts for o in outs]),
+        arr([o.offsets for o in outs]), arr([o.payload for o in outs]), arr([o.side for o in outs]),
+        arr(image_outs), Hc * Wc, Wc, _stream_ptr(torch)))
+    return list(zip(outs, image_outs))
+
+
 def decode_batch(batch: MeasurementBatch, out=None):
     """decode_idct on every set of the batch -> (n, Hc, Wc) float32 CUDA tensor."""
     torch = _torch()

@@ -289,7 +289,84 @@ static int sense_chunked(Ctx* ctx, const abcs_sense_plan* p, const uint8_t* d_im
   return ABCS_OK;
 }
 
-// ---- per-kernel timing -----------------------------------------------------------------
+// ---- subrate sweep (abcs_main.cpp:215-260: sense() of one image per --crs entry) ---------
+// DD plans of B = 16 on the same geometry share DD phase 1's forward transform: one
+// launch_sense16_sweep computes every plan's significance counts, then each plan gets its
+// own fp64 fixup, allocation, payload and decode -- the same outputs as separate calls.
+static bool sweep_shared(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, int32_t n) {
+  if (np < 2 || np > 4) return false;
+  for (int j = 0; j < np; ++j) {
+    const abcs_sense_plan& q = plans[j];
+    if (q.algorithm_used != ABCS_ALGO_DD || q.block != 16 || q.rows != plans[0].rows || q.cols != plans[0].cols ||
+        q.height != plans[0].height || q.width != plans[0].width)
+      return false;
+    if (!fused_alloc_supported(ctx, q.rows, q.cols, n, q.dd_phase1) || !mma16_supported(q.rows, q.cols, n)) return false;
+  }
+  return true;
+}
+
+static size_t sweep_scratch_bytes(const abcs_sense_plan* plans, int32_t np, int32_t n, int32_t* const* d_offsets) {
+  size_t b = 0;
+  for (int j = 0; j < np; ++j) {
+    const int64_t nbt = (int64_t)n * plans[j].n_blocks;
+    b += (d_offsets && d_offsets[j] ? 0 : align_up(nbt * 4, 256)) + align_up(nbt * 4, 256) +
+         align_up(sense_fix_words(nbt) * 4, 256);
+  }
+  return b;
+}
+
+static int sweep_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, const uint8_t* d_images,
+                      int64_t image_stride, int32_t pitch, int32_t n, int64_t first, uint16_t* const* d_counts,
+                      int32_t* const* d_offsets, float* const* d_payload, float* const* d_out, int64_t out_stride,
+                      int32_t out_pitch, char* scr, cudaStream_t s) {
+  if (n == 0) return ABCS_OK;
+  const abcs_sense_plan& p0 = plans[0];
+  int32_t* offs[4];
+  uint32_t* weights[4];
+  uint32_t* fix[4];
+  int phase1[4];
+  double T[4];
+  for (int j = 0; j < np; ++j) {
+    const int64_t nbt = (int64_t)n * plans[j].n_blocks;
+    if (d_offsets && d_offsets[j]) {
+      offs[j] = d_offsets[j] + first * plans[j].n_blocks;
+    } else {
+      offs[j] = reinterpret_cast<int32_t*>(scr);
+      scr += align_up(nbt * 4, 256);
+    }
+    weights[j] = reinterpret_cast<uint32_t*>(scr);
+    scr += align_up(nbt * 4, 256);
+    fix[j] = reinterpret_cast<uint32_t*>(scr);
+    scr += align_up(sense_fix_words(nbt) * 4, 256);
+    phase1[j] = plans[j].dd_phase1;
+    T[j] = plans[j].threshold;
+  }
+  const uint8_t* imgs = d_images + first * image_stride;
+  int st = launch_sense16_sweep(ctx, np, p0.rows, p0.cols, n, imgs, image_stride, pitch, phase1, T, weights, fix, s);
+  if (st) return st;
+  for (int j = 0; j < np; ++j) {
+    const abcs_sense_plan& q = plans[j];
+    uint16_t* counts = d_counts[j] + first * q.n_blocks;
+    FusedAlloc fa;
+    fa.runs_done = nullptr;
+    fa.status = nullptr;
+    fa.counts = counts;
+    fa.offsets = offs[j];
+    fa.budget = q.alloc_budget;
+    fa.cap = q.cap;
+    fa.base = q.count_base;
+    fa.wmax = q.dd_phase1;
+    st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa, s);
+    if (st) return st;
+    st = launch_sense16(ctx, 3, q.rows, q.cols, n, imgs, image_stride, pitch, 0, 0.0, nullptr, counts, offs[j],
+                        d_payload[j] + first * q.coeffs_per_image, q.coeffs_per_image, d_out[j] + first * out_stride,
+                        out_stride, out_pitch, s);
+    if (st) return st;
+  }
+  return ABCS_OK;
+}
+
+// ---- per-kernel timing -----------------------------------------------------------------// ---- per-kernel timing -----------------------------------------------------------------
 static cudaEvent_t take_event(Ctx* ctx) {
   if (ctx->kpool_used == ctx->kpool.size()) {
     cudaEvent_t e;
@@ -343,6 +420,68 @@ int abcs_sense_decode_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return sense_chunked(ctx, p, d_images, image_stride, pitch, n, d_counts, d_offsets, d_payload, d_side, s, d_out,
                        out_stride, out_pitch);
+}
+
+int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans,
+                                  const uint8_t* d_images, int64_t image_stride, int32_t pitch, int32_t n,
+                                  uint16_t* const* d_counts, int32_t* const* d_offsets, float* const* d_payload,
+                                  float* const* d_side, float* const* d_out, int64_t out_stride, int32_t out_pitch,
+                                  void* stream) {
+  CHECK_CTX(c);
+  if (!plans || n_plans < 1 || !d_counts || !d_payload || !d_out)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int j = 0; j < n_plans; ++j) {
+    int st = sense_validate(&plans[j], d_images, image_stride, pitch, n, d_counts[j], d_payload[j],
+                            d_side ? d_side[j] : nullptr);
+    if (st) return st;
+    const int Wc = plans[j].cols * plans[j].block, Hc = plans[j].rows * plans[j].block;
+    if (!d_out[j] || out_pitch < Wc || out_stride < (int64_t)out_pitch * (Hc - 1) + Wc)
+      return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch/stride smaller than the image");
+  }
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool aligned_out = out_pitch % 2 == 0 && out_stride % 2 == 0;
+  bool out_ok = aligned_out;
+  for (int j = 0; j < n_plans; ++j) out_ok = out_ok && ((uintptr_t)d_out[j] % 8) == 0;
+  if (!out_ok || !sweep_shared(ctx, plans, n_plans, n)) {  // no shared transform: one plan at a time
+    for (int j = 0; j < n_plans; ++j) {
+      const int st = sense_chunked(ctx, &plans[j], d_images, image_stride, pitch, n, d_counts[j],
+                                   d_offsets ? d_offsets[j] : nullptr, d_payload[j], d_side ? d_side[j] : nullptr,
+                                   s, d_out[j], out_stride, out_pitch);
+      if (st) return st;
+    }
+    return ABCS_OK;
+  }
+  // chunks of the batch on the pipe streams, as sense_chunked
+  const int nchunks = std::max(1, std::min<int>(ctx->pipe_streams, n / 64));
+  const int chunk = (n + nchunks - 1) / nchunks;
+  const size_t per = align_up(sweep_scratch_bytes(plans, n_plans, chunk, d_offsets), 256);
+  int st;
+  char* scr = static_cast<char*>(ctx_scratch(ctx, per * nchunks, s, &st));
+  if (st) return st;
+  if (nchunks == 1)
+    return sweep_impl(ctx, plans, n_plans, d_images, image_stride, pitch, n, 0, d_counts, d_offsets, d_payload,
+                      d_out, out_stride, out_pitch, scr, s);
+  if (!ctx->ev_fork) {
+    cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    for (auto& e : ctx->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  cudaError_t e = cudaEventRecord(ctx->ev_fork, s);
+  if (e != cudaSuccess) return cuda_status(e, "fork");
+  for (int k = 0; k < nchunks; ++k) {
+    const int first = k * chunk, cnt = std::min(chunk, n - first);
+    cudaStream_t cs = ctx->pipe[k];
+    cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
+    st = sweep_impl(ctx, plans, n_plans, d_images, image_stride, pitch, cnt, first, d_counts, d_offsets, d_payload,
+                    d_out, out_stride, out_pitch, scr + per * k, cs);
+    if (st) return st;
+    e = cudaEventRecord(ctx->ev_join[k], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_join[k], 0);
+    if (e != cudaSuccess) return cuda_status(e, "join");
+  }
+  return ABCS_OK;
 }
 
 int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,

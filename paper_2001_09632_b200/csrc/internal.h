@@ -134,6 +134,11 @@ struct FusedAlloc {
 };
 bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax);
 // mode 1: DD weights; 2: payload; 3: payload + fused decode
+int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
+                         int pitch, const int* phase1, const double* T, uint32_t* const* weights,
+                         uint32_t* const* fix_scratch, cudaStream_t s);
+int launch_alloc_cta(Ctx* ctx, int rows, int cols, int n, const uint32_t* weights, const FusedAlloc& fa,
+                     cudaStream_t s);
 int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,
                    int phase1, double T, uint32_t* weights, const uint16_t* counts, const int32_t* offsets,
                    float* payload, int64_t payload_stride, float* out, int64_t out_stride, int out_pitch,

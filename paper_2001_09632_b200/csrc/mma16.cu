@@ -142,7 +142,16 @@ struct Sense16Args {
   float* out;
   int64_t out_stride;
   int out_pitch;
+  // subrate sweep (kSweep): DD phase 1 of up to kMaxSweep plans from one transform
+  int n_sw;
+  int sw_phase1[4];
+  float sw_hi[4], sw_lo[4];
+  uint32_t* sw_weights[4];
+  uint32_t* sw_fix_list[4];
+  uint32_t* sw_fix_count[4];
+  uint8_t* sw_fix_flag[4];
 };
+constexpr int kMaxSweep = 4;
 
 __device__ __forceinline__ void run_pos(const Grid16& G, uint32_t r, uint32_t& img, int& br, int& bc_first,
                                         int& nblk) {
@@ -154,7 +163,7 @@ __device__ __forceinline__ void run_pos(const Grid16& G, uint32_t r, uint32_t& i
   nblk = min(32, G.cols - bc_first);
 }
 
-template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false>
+template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false, bool kSweep = false>
 __global__ void __launch_bounds__(kM16Threads, 3)
 sense16_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
@@ -173,10 +182,19 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
-    if constexpr (kWeights) {
+    if constexpr (kWeights && !kSweep) {
       const bool in = (int)rank_d[s] < A.phase1;
       thr_hi[s] = in ? A.Tf + A.band : INFINITY;
       thr_lo[s] = in ? A.Tf - A.band : INFINITY;
+    }
+  }
+  uint32_t in_sw[kSweep ? kMaxSweep : 1];  // sweep: bit s set iff slot s is in plan j's prefix
+  if constexpr (kSweep) {
+#pragma unroll
+    for (int j = 0; j < kMaxSweep; ++j) {
+      in_sw[j] = 0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) in_sw[j] |= (j < A.n_sw && (int)rank_d[s] < A.sw_phase1[j]) ? 1u << s : 0u;
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -213,7 +231,55 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       else if constexpr (kWeights) dct16_fwd_exact_x2_tab(f, s_btab, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
-      if constexpr (kWeights) {
+      if constexpr (kSweep) {
+        // the same phase-1 test for each plan of the sweep (prefix phase1_j, band around T_j);
+        // the plans' warp counts travel packed (10 bits each) through one reduction and one vote
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !two) break;
+          uint32_t packed = 0;
+          bool nr = false;
+#pragma unroll
+          for (int j = 0; j < kMaxSweep; ++j) {
+            if (j >= A.n_sw) break;
+            const float hi_t = A.sw_hi[j], lo_t = A.sw_lo[j];
+            const int smax = A.sw_phase1[j] <= 36 ? 2 : 8;  // a prefix of <= 36 lies in slots 0-1 (kLowCols)
+            uint32_t hb = 0, lb = 0;  // per slot: |Y| >= T + band, |Y| > T - band
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              if (s >= smax) break;
+              const float a = fabsf(Y[q].v[s >> 2][s & 3]);
+              hb |= a >= hi_t ? 1u << s : 0u;
+              lb |= a > lo_t ? 1u << s : 0u;
+            }
+            hb &= in_sw[j];  // slots inside plan j's zigzag prefix
+            packed += (uint32_t)__popc(hb) << (10 * j);
+            nr |= (lb & ~hb & in_sw[j]) != 0u;
+          }
+          const uint32_t sig = __reduce_add_sync(0xffffffffu, packed);
+          if (__any_sync(0xffffffffu, nr)) {  // rare: record each plan's near-threshold coefficients
+#pragma unroll 1
+            for (int j = 0; j < A.n_sw; ++j) {
+              const int ph1 = A.sw_phase1[j];
+              const float hi_t = A.sw_hi[j], lo_t = A.sw_lo[j];
+              bool mine = false;
+              for (int s = 0; s < 8; ++s) {
+                const float a = fabsf(Y[q].v[s >> 2][s & 3]);
+                if ((int)rank_d[s] < ph1 && !(a >= hi_t) && a > lo_t) {
+                  mine = true;
+                  const uint32_t e = atomicAdd(A.sw_fix_count[j], 1u);
+                  if (e < A.fix_cap) {
+                    A.sw_fix_list[j][2 * e] = bidx0 + q;
+                    A.sw_fix_list[j][2 * e + 1] = (uint32_t)(dslot_col(s) * 16 + dslot_row(s));
+                  }
+                }
+              }
+              if (mine) A.sw_fix_flag[j][bidx0 + q] = 1;
+            }
+          }
+          if (lane < A.n_sw) A.sw_weights[lane][bidx0 + q] = (sig >> (10 * lane)) & 1023u;
+        }
+      } else if constexpr (kWeights) {
         // phase-1 test in registers: slot s is in the prefix iff rank_d[s] < phase1 (thresholds
         // pre-masked to +inf outside it); counts reduce across the warp. A coefficient within the
         // MMA error band of T is neither counted nor dropped: dd_fixup16_kernel decides it in fp64.
@@ -679,6 +745,66 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
   }
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "sense16 launch");
+}
+
+// DD phase 1 of n_sw plans (same geometry, prefixes phase1[j], thresholds T[j]) from one
+// forward transform per block; then the fp64 fixup of each plan's near-threshold list.
+int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
+                         int pitch, const int* phase1, const double* T, uint32_t* const* weights,
+                         uint32_t* const* fix_scratch, cudaStream_t s) {
+  if (n_sw < 1 || n_sw > kMaxSweep) return set_error(ABCS_ERR_LOGIC, "sense16 sweep: 1..4 plans");
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_units == 0) return ABCS_OK;
+  Sense16Args A{};
+  A.imgs = imgs;
+  A.img_stride = img_stride;
+  A.pitch = pitch;
+  A.aligned = ((uintptr_t)imgs % 16 == 0) && (img_stride % 16 == 0) && (pitch % 16 == 0);
+  const int64_t nbt = (int64_t)G.nb * n;
+  A.fix_cap = (uint32_t)(nbt * 2);
+  A.n_sw = n_sw;
+  for (int j = 0; j < n_sw; ++j) {
+    const float Tf = (float)T[j];
+    const float band = (float)(1e-2 + fabs(T[j] - (double)Tf));  // as launch_sense16
+    A.sw_phase1[j] = phase1[j];
+    A.sw_hi[j] = Tf + band;
+    A.sw_lo[j] = Tf - band;
+    A.sw_weights[j] = weights[j];
+    A.sw_fix_count[j] = fix_scratch[j];
+    A.sw_fix_list[j] = fix_scratch[j] + 4;
+    A.sw_fix_flag[j] = reinterpret_cast<uint8_t*>(fix_scratch[j] + 4 + 2 * (int64_t)A.fix_cap);
+    cudaError_t e = cudaMemsetAsync(A.sw_fix_count[j], 0, 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(A.sw_fix_flag[j], 0, (size_t)nbt, s);
+    if (e != cudaSuccess) return cuda_status(e, "fixup reset");
+  }
+  int kt = ktimer_begin(ctx, s, "sense16_weights_sweep");
+  sense16_kernel<true, false, false, false, true><<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, A);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e, "sense16 sweep launch");
+  for (int j = 0; j < n_sw; ++j) {
+    kt = ktimer_begin(ctx, s, "dd_fixup16");
+    dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1[j], T[j],
+                                                             A.sw_fix_list[j], A.sw_fix_count[j], A.fix_cap,
+                                                             A.sw_fix_flag[j], G.nb * (uint32_t)n, weights[j]);
+    ktimer_end(ctx, s, kt);
+    ctx->launches++;
+  }
+  return cuda_status(cudaGetLastError(), "dd fixup launch");
+}
+
+// The per-image allocation of a DD plan (alloc_cta_kernel) from weights already computed.
+int launch_alloc_cta(Ctx* ctx, int rows, int cols, int n, const uint32_t* weights, const FusedAlloc& fa,
+                     cudaStream_t s) {
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_units == 0) return ABCS_OK;
+  const int kt = ktimer_begin(ctx, s, "alloc_cta");
+  alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa.wmax, fa.budget, fa.cap, fa.base,
+                                                             fa.counts, fa.offsets, fa.status);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "alloc_cta launch");
 }
 
 int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts, const int32_t* offsets,

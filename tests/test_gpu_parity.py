@@ -273,6 +273,33 @@ def test_fused_sense_decode_equals_decode_of_payload(p, torch, case):
     assert torch.equal(x, p.decode_batch(ref))
 
 
+@pytest.mark.parametrize("n,cfgs", [
+    (200, [(16, 1, 10, 2), (16, 3, 10, 2), (16, 1, 2, 2)]),   # cfg2 sweep: shared DD phase 1, 3 chunks
+    (5, [(16, 1, 4, 2), (16, 3, 10, 1), (16, 1, 2, 0)]),      # mixed algorithms: one plan at a time
+])
+def test_sense_decode_sweep_equals_separate_calls(p, torch, n, cfgs):
+    """sense_decode_sweep: every plan's counts, offsets, payload and pixels equal its own
+    sense_decode_batch call bit for bit (the shared transform changes nothing)."""
+    imgs = torch.from_numpy(synth(512, 512, n=n, seed=77 + n)).cuda()
+    cs = [p.SensingConfig(B, num, den, p.Algorithm(a)) for B, num, den, a in cfgs]
+    got = p.sense_decode_sweep(imgs, cs)
+    for c, (b, x) in zip(cs, got):
+        rb, rx = p.sense_decode_batch(imgs, c)
+        assert torch.equal(b.counts.view(torch.int16), rb.counts.view(torch.int16))
+        assert torch.equal(b.offsets, rb.offsets)
+        assert torch.equal(b.payload, rb.payload)
+        assert torch.equal(x, rx)
+
+
+def test_sense_decode_sweep_reference_counts(p, torch, checker):
+    imgs = synth(512, 512, n=2, seed=5)
+    cs = [p.SensingConfig(16, 1, 10, p.Algorithm.DD), p.SensingConfig(16, 1, 2, p.Algorithm.DD)]
+    got = p.sense_decode_sweep(torch.from_numpy(imgs).cuda(), cs)
+    for (b, _), (num, den) in zip(got, [(1, 10), (1, 2)]):
+        for i in range(2):
+            assert_sense_equal(b, i, checker.sense(imgs[i], 16, num, den, 2), 16)
+
+
 def test_decode_format_errors(p):
     ms = p.MeasurementSet(32, 32, 16, p.Algorithm.ZZ, 1, 4, 0.0, np.array([3, 3, 3, 3], np.uint16),
                           np.zeros(11, np.float32))
