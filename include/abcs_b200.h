@@ -223,6 +223,39 @@ int abcs_sense_weights_batch(abcs_ctx* ctx, const abcs_sense_plan* plan, const u
                              int64_t image_stride, int32_t pitch, int32_t n_images,
                              uint32_t* d_weights, float* d_side, void* stream);
 
+/* apply_plan's gather (sensing.cpp:192-227, 386-403) from given counts and
+ * offsets, fused with decode_idct (recon.cpp:109-117) when d_out is non-NULL:
+ * the payload pass of a sense whose allocation was made elsewhere (a sharded
+ * image: each shard gathers its block rows into its slice of the payload). */
+int abcs_gather_decode_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
+                             const uint8_t* d_images, int64_t image_stride, int32_t pitch,
+                             int32_t n_images, const uint16_t* d_counts, const int32_t* d_offsets,
+                             float* d_payload, int64_t payload_stride, float* d_out, int64_t out_stride,
+                             int32_t out_pitch, void* stream);
+
+/* largest_remainder_allocate (sensing.cpp:110-177) of ONE weight vector split
+ * into shards (contiguous block ranges in block order) held by different
+ * devices/processes. The caller drives the rounds and the collectives between
+ * the phases (paper_2001_09632_b200/sharded.py):
+ *   phase 0: load d_weights (n_blocks, u32) into d_scratch; d_out[0] = 1 if a
+ *            weight exceeds wmax.
+ *   phase 1: d_out[0..wmax] = active-weight histogram, d_out[wmax+1] = sum of
+ *            active weights, d_out[wmax+2] = active blocks   -> sum over shards.
+ *   phase 2: d_in = that sum, remaining = units left: the round's class table
+ *            and threshold (identical on every shard); d_out[0] = the shard's
+ *            exact-tie blocks                                 -> prefix over shards.
+ *   phase 3: prefix = tie blocks of the lower shards: apply and clamp;
+ *            d_out[0] = units taken, d_out[1] = blocks still open -> sum.
+ *   phase 4: prefix = the shard's offset in the image's payload:
+ *            d_counts = base + allocation, d_offsets (nullable); d_out[0] = total.
+ * d_scratch: abcs_allocate_shard_scratch_bytes(n_blocks, wmax) bytes, kept
+ * across the phases; d_out: wmax + 3 int64. */
+size_t abcs_allocate_shard_scratch_bytes(int32_t n_blocks, int32_t wmax);
+int abcs_allocate_shard_step(abcs_ctx* ctx, int32_t phase, const uint32_t* d_weights, int32_t n_blocks,
+                             int32_t wmax, int32_t cap, int32_t base, void* d_scratch, int64_t* d_out,
+                             const int64_t* d_in, int64_t remaining, int64_t prefix, uint16_t* d_counts,
+                             int32_t* d_offsets, void* stream);
+
 /* largest_remainder_allocate (sensing.cpp:110-177) for n independent weight
  * vectors of n_blocks integer weights; caps per block (nullable -> uniform
  * `cap`). counts = base + allocation (u16), offsets = exclusive scan (nullable).

@@ -299,7 +299,201 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
 // active) after barrier A, the tie counts of lower ranks after barrier C, and
 // (taken, still open) after barrier D; the class table and the threshold are
 // recomputed identically in every CTA from the cluster-wide histogram.
+// ---- one round's class table and leftover threshold (shared by the cluster and the
+// distributed allocators; every thread of the CTA calls it and gets the same result) ------
 constexpr int kClassThreads = 1024;
+using Reduce64C = cub::BlockReduce<unsigned long long, kClassThreads>;
+using ScanIC = cub::BlockScan<int, kClassThreads>;
+struct ClassShared {
+  union {
+    typename Reduce64C::TempStorage r;
+    typename ScanIC::TempStorage s;
+  } tmp;
+  unsigned int hist8[256];
+  long long sh_ll[4];
+  int sh_int[4];
+};
+struct ClassSel {  // the round's selection: units by class rank, exact ties by block index
+  long long need;  // tie-group units still to hand out (to the lowest indices)
+  unsigned long long prefix;
+  uint64_t thr_key;
+  int ncls, passes, flag_sel, thr_flag;
+  int sel_all, none, rank_mode, all_equal_taken;
+};
+
+// gh[c] (c in this thread's weight range [c0, c1)) = active blocks of weight c in the whole
+// vector; on return gh[c] = the class index of weight c, and ccnt/cwhole/ckey/cflag hold the
+// class table (ordered by weight).
+__device__ ClassSel class_round_select(ClassShared& sm, uint32_t* gh, int c0, int c1, long long remaining,
+                                       uint64_t T, bool uniform, long long n_act, uint32_t* ccnt, uint32_t* cwhole,
+                                       uint64_t* ckey, uint8_t* cflag) {
+  using Reduce64 = Reduce64C;
+  using ScanI = ScanIC;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // compact the nonempty classes (ordered by weight) and compute their shares
+  int mine = 0;
+  for (int c = c0; c < c1; ++c) mine += gh[c] ? 1 : 0;
+  int id, ncls;
+  ScanI(sm.tmp.s).ExclusiveSum(mine, id, ncls);
+  unsigned long long handed = 0;
+  for (int c = c0; c < c1; ++c) {
+    const uint32_t h = gh[c];
+    if (!h) continue;
+    const int k = id++;
+    ccnt[k] = h;
+    const ak_u128 P = (ak_u128)(uint64_t)remaining * (uniform ? 1u : (uint32_t)c);
+    const ak_share sh = ak_compute(P, T);  // sensing.cpp:144-148
+    cwhole[k] = (uint32_t)sh.whole;
+    ckey[k] = sh.key;
+    cflag[k] = (uint8_t)sh.flag;
+    gh[c] = (uint32_t)k;
+    handed += (unsigned long long)h * sh.whole;
+  }
+  __syncthreads();
+  const unsigned long long hsum = Reduce64(sm.tmp.r).Sum(handed);
+  if (tid == 0) sm.sh_ll[2] = (long long)hsum;
+  __syncthreads();
+  const long long leftover = remaining - sm.sh_ll[2];
+  // leftover units -> largest fractions, ties to the lower index (sensing.cpp:150-158)
+  const bool sel_all = leftover > 0 && leftover >= n_act;
+  const bool none = leftover <= 0;
+  unsigned long long prefix = 0;
+  int passes = 0, flag_sel = -1;
+  bool all_equal_taken = false;
+  long long need = leftover;
+  bool rank_mode = false;
+  uint64_t thr_key = 0;
+  int thr_flag = 0;
+  if (!sel_all && !none && ncls <= 512) {
+    // few classes: each class counts the blocks ranking strictly above it and tied with it
+    // (a power-of-two group of tpc threads per class splits the scan; shuffle-reduced)
+    rank_mode = true;
+    int tpc = 1;
+    while (tpc < 32 && 2 * tpc * ncls <= kClassThreads) tpc *= 2;
+    const int cls = tid / tpc, sub = tid & (tpc - 1);
+    int above = 0, eqc = 0;
+    uint64_t kk = 0;
+    int fk = 0;
+    if (cls < ncls) {
+      kk = ckey[cls];
+      fk = cflag[cls];
+#pragma unroll 4
+      for (int j = sub; j < ncls; j += tpc) {
+        const uint64_t kj = ckey[j];
+        const int fj = cflag[j];
+        const int cj = (int)ccnt[j];
+        above += (kj > kk || (kj == kk && fj > fk)) ? cj : 0;
+        eqc += (kj == kk && fj == fk) ? cj : 0;
+      }
+    }
+    for (int o = 1; o < tpc; o <<= 1) {
+      above += __shfl_xor_sync(0xffffffffu, above, o);
+      eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
+    }
+    if (cls < ncls && sub == 0 && above < need && need <= (long long)above + eqc) {  // the threshold tie group
+      sm.sh_ll[3] = above;
+      sm.sh_int[2] = eqc;
+      sm.sh_int[1] = fk;
+      sm.sh_ll[2] = (long long)kk;
+    }
+    __syncthreads();
+    need -= sm.sh_ll[3];
+    all_equal_taken = need == (long long)sm.sh_int[2];
+    thr_key = (uint64_t)sm.sh_ll[2];
+    thr_flag = sm.sh_int[1];
+    __syncthreads();
+  } else if (!sel_all && !none) {
+    for (int pass = 0; pass < 9; ++pass) {
+      const int nbins = pass < 8 ? 256 : 2;
+      if (tid < 256) sm.hist8[tid] = 0;
+      __syncthreads();
+      const int shift_hi = 64 - 8 * pass;
+      for (int k = tid; k < ncls; k += kClassThreads) {
+        const uint64_t kk = ckey[k];
+        const bool match = (pass == 0) ? true : (pass < 8 ? ((kk >> shift_hi) == prefix) : (kk == prefix));
+        if (!match) continue;
+        const unsigned d = pass < 8 ? (unsigned)((kk >> (56 - 8 * pass)) & 0xffu) : (unsigned)cflag[k];
+        atomicAdd(&sm.hist8[d], ccnt[k]);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const int per = (nbins + 31) / 32;
+        unsigned local = 0;
+        for (int q = 0; q < per; ++q) {
+          const int d = nbins - 1 - (lane * per + q);
+          if (d >= 0) local += sm.hist8[d];
+        }
+        unsigned incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const unsigned excl = incl - local;
+        const bool hit = ((long long)excl < need) && ((long long)incl >= need);
+        const unsigned ball = __ballot_sync(0xffffffffu, hit);
+        const int src = __ffs(ball) - 1;
+        if (lane == src) {
+          unsigned cum = excl;
+          for (int q = 0; q < per; ++q) {
+            const int d = nbins - 1 - (lane * per + q);
+            if (d < 0) break;
+            if ((long long)cum + sm.hist8[d] >= need) {
+              sm.sh_int[1] = d;
+              sm.sh_int[2] = (int)sm.hist8[d];
+              sm.sh_ll[3] = (long long)cum;
+              break;
+            }
+            cum += sm.hist8[d];
+          }
+        }
+      }
+      __syncthreads();
+      const int g = sm.sh_int[1];
+      const int eq = sm.sh_int[2];
+      need -= sm.sh_ll[3];
+      if (pass < 8) prefix = (prefix << 8) | (unsigned long long)g;
+      else flag_sel = g;
+      passes = pass + 1;
+      __syncthreads();
+      if (eq == need) {
+        all_equal_taken = true;
+        break;
+      }
+    }
+  }
+  ClassSel S;
+  S.need = need;
+  S.prefix = prefix;
+  S.thr_key = thr_key;
+  S.ncls = ncls;
+  S.passes = passes;
+  S.flag_sel = flag_sel;
+  S.thr_flag = thr_flag;
+  S.sel_all = sel_all;
+  S.none = none;
+  S.rank_mode = rank_mode;
+  S.all_equal_taken = all_equal_taken;
+  return S;
+}
+
+// Class k's relation to the threshold: 1 = above it, 2 = in the exact-tie group, 0 = below.
+__device__ __forceinline__ int class_rel(const ClassSel& S, int k, const uint64_t* ckey, const uint8_t* cflag) {
+  if (S.sel_all) return 1;
+  if (S.none) return 0;
+  const uint64_t kk = ckey[k];
+  if (S.rank_mode) {
+    if (kk != S.thr_key) return kk > S.thr_key ? 1 : 0;
+    return (int)cflag[k] > S.thr_flag ? 1 : ((int)cflag[k] == S.thr_flag ? 2 : 0);
+  }
+  if (S.passes <= 8) {
+    const int sh = 64 - 8 * S.passes;
+    const unsigned long long top = sh >= 64 ? 0ull : (kk >> sh);
+    return top > S.prefix ? 1 : (top == S.prefix ? 2 : 0);
+  }
+  if (kk != S.prefix) return kk > S.prefix ? 1 : 0;
+  return (int)cflag[k] > S.flag_sel ? 1 : ((int)cflag[k] == S.flag_sel ? 2 : 0);
+}
+
 constexpr int kMaxCluster = 16;
 static_assert(kClassThreads <= 1024, "allocate_scratch_bytes pads spans by 1024");
 
@@ -327,15 +521,11 @@ __global__ void __launch_bounds__(kClassThreads)
 alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64_t budget, int cap, int base,
                    uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status,
                    uint32_t* __restrict__ gscratch) {
-  using Reduce64 = cub::BlockReduce<unsigned long long, kClassThreads>;
-  using ScanI = cub::BlockScan<int, kClassThreads>;
-  __shared__ union {
-    typename Reduce64::TempStorage r;
-    typename ScanI::TempStorage s;
-  } tmp;
-  __shared__ unsigned int hist8[256];
-  __shared__ long long sh_ll[4];
-  __shared__ int sh_int[4];
+  using Reduce64 = Reduce64C;
+  using ScanI = ScanIC;
+  __shared__ ClassShared sm;
+  auto& tmp = sm.tmp;
+  auto& sh_int = sm.sh_int;
   __shared__ long long pub[6];  // published to the cluster: 0/1 (T, active) | 2 ties | 3/4 (taken, open) | 5 misc
   __shared__ long long agg[2];  // cluster aggregates read back by warp 0
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -481,154 +671,10 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     const bool uniform = agg[0] == 0;
     const uint64_t T = uniform ? (uint64_t)agg[1] : (uint64_t)agg[0];
     const long long n_act = agg[1];
-    // compact the nonempty classes (ordered by weight) and compute their shares
-    int mine = 0;
-    for (int c = c0; c < c1; ++c) mine += ghist[c] ? 1 : 0;
-    int id, ncls;
-    ScanI(tmp.s).ExclusiveSum(mine, id, ncls);
-    unsigned long long handed = 0;
-    for (int c = c0; c < c1; ++c) {
-      const uint32_t h = ghist[c];
-      if (!h) continue;
-      const int k = id++;
-      ccnt[k] = h;
-      const ak_u128 P = (ak_u128)(uint64_t)remaining * (uniform ? 1u : (uint32_t)c);
-      const ak_share sh = ak_compute(P, T);  // sensing.cpp:144-148
-      cwhole[k] = (uint32_t)sh.whole;
-      ckey[k] = sh.key;
-      cflag[k] = (uint8_t)sh.flag;
-      ghist[c] = (uint32_t)k;
-      handed += (unsigned long long)h * sh.whole;
-    }
-    __syncthreads();
-    const unsigned long long hsum = Reduce64(tmp.r).Sum(handed);
-    if (tid == 0) sh_ll[2] = (long long)hsum;
-    __syncthreads();
-    const long long leftover = remaining - sh_ll[2];
-    // leftover units -> largest fractions, ties to the lower index (sensing.cpp:150-158)
-    const bool sel_all = leftover > 0 && leftover >= n_act;
-    const bool none = leftover <= 0;
-    unsigned long long prefix = 0;
-    int passes = 0, flag_sel = -1;
-    bool all_equal_taken = false;
-    long long need = leftover;
-    bool rank_mode = false;
-    uint64_t thr_key = 0;
-    int thr_flag = 0;
-    if (!sel_all && !none && ncls <= 512) {
-      // few classes: each class counts the blocks ranking strictly above it and tied with it
-      // (a power-of-two group of tpc threads per class splits the scan; shuffle-reduced)
-      rank_mode = true;
-      int tpc = 1;
-      while (tpc < 32 && 2 * tpc * ncls <= kClassThreads) tpc *= 2;
-      const int cls = tid / tpc, sub = tid & (tpc - 1);
-      int above = 0, eqc = 0;
-      uint64_t kk = 0;
-      int fk = 0;
-      if (cls < ncls) {
-        kk = ckey[cls];
-        fk = cflag[cls];
-#pragma unroll 4
-        for (int j = sub; j < ncls; j += tpc) {
-          const uint64_t kj = ckey[j];
-          const int fj = cflag[j];
-          const int cj = (int)ccnt[j];
-          above += (kj > kk || (kj == kk && fj > fk)) ? cj : 0;
-          eqc += (kj == kk && fj == fk) ? cj : 0;
-        }
-      }
-      for (int o = 1; o < tpc; o <<= 1) {
-        above += __shfl_xor_sync(0xffffffffu, above, o);
-        eqc += __shfl_xor_sync(0xffffffffu, eqc, o);
-      }
-      if (cls < ncls && sub == 0 && above < need && need <= (long long)above + eqc) {  // the threshold tie group
-        sh_ll[3] = above;
-        sh_int[2] = eqc;
-        sh_int[1] = fk;
-        sh_ll[2] = (long long)kk;
-      }
-      __syncthreads();
-      need -= sh_ll[3];
-      all_equal_taken = need == (long long)sh_int[2];
-      thr_key = (uint64_t)sh_ll[2];
-      thr_flag = sh_int[1];
-      __syncthreads();
-    } else if (!sel_all && !none) {
-      for (int pass = 0; pass < 9; ++pass) {
-        const int nbins = pass < 8 ? 256 : 2;
-        if (tid < 256) hist8[tid] = 0;
-        __syncthreads();
-        const int shift_hi = 64 - 8 * pass;
-        for (int k = tid; k < ncls; k += kClassThreads) {
-          const uint64_t kk = ckey[k];
-          const bool match = (pass == 0) ? true : (pass < 8 ? ((kk >> shift_hi) == prefix) : (kk == prefix));
-          if (!match) continue;
-          const unsigned d = pass < 8 ? (unsigned)((kk >> (56 - 8 * pass)) & 0xffu) : (unsigned)cflag[k];
-          atomicAdd(&hist8[d], ccnt[k]);
-        }
-        __syncthreads();
-        if (tid < 32) {
-          const int per = (nbins + 31) / 32;
-          unsigned local = 0;
-          for (int q = 0; q < per; ++q) {
-            const int d = nbins - 1 - (lane * per + q);
-            if (d >= 0) local += hist8[d];
-          }
-          unsigned incl = local;
-          for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          const unsigned excl = incl - local;
-          const bool hit = ((long long)excl < need) && ((long long)incl >= need);
-          const unsigned ball = __ballot_sync(0xffffffffu, hit);
-          const int src = __ffs(ball) - 1;
-          if (lane == src) {
-            unsigned cum = excl;
-            for (int q = 0; q < per; ++q) {
-              const int d = nbins - 1 - (lane * per + q);
-              if (d < 0) break;
-              if ((long long)cum + hist8[d] >= need) {
-                sh_int[1] = d;
-                sh_int[2] = (int)hist8[d];
-                sh_ll[3] = (long long)cum;
-                break;
-              }
-              cum += hist8[d];
-            }
-          }
-        }
-        __syncthreads();
-        const int g = sh_int[1];
-        const int eq = sh_int[2];
-        need -= sh_ll[3];
-        if (pass < 8) prefix = (prefix << 8) | (unsigned long long)g;
-        else flag_sel = g;
-        passes = pass + 1;
-        __syncthreads();
-        if (eq == need) {
-          all_equal_taken = true;
-          break;
-        }
-      }
-    }
-    // classify: 1 = above the threshold, 2 = in the exact-tie group
-    auto cls_rel = [&](int k) -> int {
-      if (sel_all) return 1;
-      if (none) return 0;
-      const uint64_t kk = ckey[k];
-      if (rank_mode) {
-        if (kk != thr_key) return kk > thr_key ? 1 : 0;
-        return (int)cflag[k] > thr_flag ? 1 : ((int)cflag[k] == thr_flag ? 2 : 0);
-      }
-      if (passes <= 8) {
-        const int sh = 64 - 8 * passes;
-        const unsigned long long top = sh >= 64 ? 0ull : (kk >> sh);
-        return top > prefix ? 1 : (top == prefix ? 2 : 0);
-      }
-      if (kk != prefix) return kk > prefix ? 1 : 0;
-      return (int)cflag[k] > flag_sel ? 1 : ((int)cflag[k] == flag_sel ? 2 : 0);
-    };
+    const ClassSel S = class_round_select(sm, ghist, c0, c1, remaining, T, uniform, n_act, ccnt, cwhole, ckey, cflag);
+    auto cls_rel = [&](int k) -> int { return class_rel(S, k, ckey, cflag); };
+    const bool sel_all = S.sel_all, none = S.none, all_equal_taken = S.all_equal_taken;
+    long long need = S.need;
     long long tie_base = 0;
     if (!sel_all && !none && !all_equal_taken) {  // the same decision in every CTA
       int ties = 0;
@@ -806,6 +852,197 @@ generic:
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "allocate launch");
+}
+
+// ---------------------------------------------------------------------------
+// Sharded allocation: one weight vector (image) split over shards held by different
+// GPUs / processes (intra-image sharding). Shard s owns the contiguous
+// block range its caller assigns (shards in block order). The round structure is the
+// cluster allocator's, with each exchange point turned into a kernel boundary and a
+// host collective: (1) active-weight histogram + (sum w, active) -> all-reduce,
+// (2) class table + threshold from the global histogram (identical on every shard) and
+// the shard's tie-group count -> exclusive prefix over shards, (3) apply + clamp ->
+// all-reduce of (taken, still open), (4) counts and offsets with the shard's global
+// offset prefix. One 1024-thread CTA per shard; state persists in global scratch.
+struct ShardState {
+  ClassSel sel;
+  long long remaining;
+};
+
+struct ShardArgs {
+  const uint32_t* weights;  // the shard's weights (nbl)
+  int nbl, wmax, cap, base;
+  uint16_t* wv;  // thread-strided per-block state, class_span(nbl) entries each
+  uint16_t* av;
+  uint32_t* gh;  // wmax + 1: global histogram -> class index
+  uint32_t* ccnt;
+  uint32_t* cwhole;
+  uint64_t* ckey;
+  uint8_t* cflag;
+  ShardState* state;
+  long long* out;        // phase outputs (phase 1: wmax + 3 values)
+  const long long* in;   // phase 2: the all-reduced phase-1 output
+  long long remaining;   // phase 2
+  long long prefix;      // phase 3: tie-group blocks in lower shards; phase 4: offset of the shard
+  uint16_t* counts;      // phase 4
+  int32_t* offsets;      // phase 4 (nullable)
+};
+
+size_t shard_scratch_bytes(int32_t n_blocks, int32_t wmax) {
+  const size_t span = (size_t)class_span(n_blocks);
+  const size_t nc = (size_t)wmax + 1;
+  return 256 + sizeof(ShardState) + 2 * span * 2 + nc * (4 + 4 + 4 + 8 + 1) + 8 * (nc + 3) + 64;
+}
+
+__global__ void __launch_bounds__(kClassThreads) alloc_shard_kernel(int phase, ShardArgs A) {
+  using Reduce64 = Reduce64C;
+  using ScanI = ScanIC;
+  __shared__ ClassShared sm;
+  extern __shared__ __align__(16) unsigned int shist[];  // phase 1: wmax + 1 bins
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int per_b = (A.nbl + kClassThreads - 1) / kClassThreads;
+  const int b0 = min(A.nbl, tid * per_b), b1 = min(A.nbl, b0 + per_b);
+  const int per_c = (A.wmax + 1 + kClassThreads - 1) / kClassThreads;
+  const int c0 = min(A.wmax + 1, tid * per_c), c1 = min(A.wmax + 1, c0 + per_c);
+  Arr<uint16_t> wv{A.wv}, av{A.av};
+  if (phase == 0) {  // load: weights -> state; out[0] = weight bound violated
+    unsigned bad = 0;
+    for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
+      const uint32_t wi = A.weights[i];
+      bad |= wi > (uint32_t)A.wmax ? 1u : 0u;
+      wv[ph] = (uint16_t)min(wi, (uint32_t)A.wmax);
+      av[ph] = 0;
+    }
+    const unsigned long long b = Reduce64(sm.tmp.r).Sum(bad);
+    if (tid == 0) A.out[0] = (long long)b;
+  } else if (phase == 1) {  // local histogram of active weights, sum of weights, active count
+    for (int c = tid; c <= A.wmax; c += kClassThreads) shist[c] = 0;
+    __syncthreads();
+    unsigned long long tw = 0, na = 0;
+    for (int k = 0; k < per_b; ++k) {
+      const int i = b0 + k, ph = k * kClassThreads + tid;
+      const bool act = i < b1 && (int)av[ph] < A.cap;
+      const int wi = act ? (int)wv[ph] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, wi);
+      if (act && (__ffs(peers) - 1) == lane) atomicAdd(&shist[wi], (unsigned)__popc(peers));
+      if (act) {
+        tw += (unsigned)wi;
+        na += 1;
+      }
+    }
+    const unsigned long long T0 = Reduce64(sm.tmp.r).Sum(tw);
+    __syncthreads();
+    const unsigned long long n_act = Reduce64(sm.tmp.r).Sum(na);
+    for (int c = tid; c <= A.wmax; c += kClassThreads) A.out[c] = shist[c];
+    if (tid == 0) {
+      A.out[A.wmax + 1] = (long long)T0;
+      A.out[A.wmax + 2] = (long long)n_act;
+    }
+  } else if (phase == 2) {  // class table + threshold from the global histogram; local tie count
+    for (int c = c0; c < c1; ++c) A.gh[c] = (uint32_t)A.in[c];
+    const long long T0 = A.in[A.wmax + 1], n_act = A.in[A.wmax + 2];
+    const bool uniform = T0 == 0;
+    const uint64_t T = uniform ? (uint64_t)n_act : (uint64_t)T0;
+    __syncthreads();
+    const ClassSel S =
+        class_round_select(sm, A.gh, c0, c1, A.remaining, T, uniform, n_act, A.ccnt, A.cwhole, A.ckey, A.cflag);
+    __syncthreads();  // the class table and gh map complete
+    int ties = 0;
+    if (!S.sel_all && !S.none && !S.all_equal_taken)
+      for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads)
+        if ((int)av[ph] < A.cap && class_rel(S, (int)A.gh[wv[ph]], A.ckey, A.cflag) == 2) ++ties;
+    const unsigned long long tt = Reduce64(sm.tmp.r).Sum((unsigned long long)ties);
+    if (tid == 0) {
+      A.state->sel = S;
+      A.state->remaining = A.remaining;
+      A.out[0] = (long long)tt;
+    }
+  } else if (phase == 3) {  // apply with the tie ranks of the lower shards; out = (taken, still open)
+    const ClassSel S = A.state->sel;
+    long long tie_base = 0;
+    if (!S.sel_all && !S.none && !S.all_equal_taken) {
+      int ties = 0;
+      for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads)
+        if ((int)av[ph] < A.cap && class_rel(S, (int)A.gh[wv[ph]], A.ckey, A.cflag) == 2) ++ties;
+      int tb, tot;
+      ScanI(sm.tmp.s).ExclusiveSum(ties, tb, tot);
+      __syncthreads();
+      tie_base = tb + A.prefix;
+    }
+    unsigned long long taken_sum = 0, still = 0;
+    for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
+      if ((int)av[ph] >= A.cap) continue;
+      const int k = (int)A.gh[wv[ph]];
+      const int rel = class_rel(S, k, A.ckey, A.cflag);
+      bool sel = rel == 1;
+      if (rel == 2) sel = S.all_equal_taken || (tie_base++) < S.need;
+      const long long give = (long long)A.cwhole[k] + (sel ? 1 : 0);
+      const long long room = (long long)A.cap - av[ph];
+      const long long taken = give < room ? give : room;  // sensing.cpp:162-171
+      av[ph] = (uint16_t)(av[ph] + taken);
+      taken_sum += (unsigned long long)taken;
+      if ((int)av[ph] < A.cap) still += 1;
+    }
+    const unsigned long long tk = Reduce64(sm.tmp.r).Sum(taken_sum);
+    __syncthreads();
+    const unsigned long long st_open = Reduce64(sm.tmp.r).Sum(still);
+    if (tid == 0) {
+      A.out[0] = (long long)tk;
+      A.out[1] = (long long)st_open;
+    }
+  } else {  // phase 4: counts = base + allocation; offsets from the shard's global offset
+    int mine = 0;
+    for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) mine += A.base + (int)av[ph];
+    int ex, total;
+    ScanI(sm.tmp.s).ExclusiveSum(mine, ex, total);
+    long long run = ex + A.prefix;
+    for (int i = b0, ph = tid; i < b1; ++i, ph += kClassThreads) {
+      const int c = A.base + (int)av[ph];
+      A.counts[i] = (uint16_t)c;
+      if (A.offsets) A.offsets[i] = (int32_t)run;
+      run += c;
+    }
+    if (tid == 0) A.out[0] = total;
+  }
+}
+
+int launch_alloc_shard(Ctx* ctx, int phase, const uint32_t* weights, int32_t n_blocks, int32_t wmax, int32_t cap,
+                       int32_t base, void* scratch, long long* out, const long long* in, long long remaining,
+                       long long prefix, uint16_t* counts, int32_t* offsets, cudaStream_t s) {
+  ShardArgs A{};
+  char* p = reinterpret_cast<char*>(scratch);
+  auto take = [&](size_t bytes) {
+    char* q = p;
+    p += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  const size_t span = (size_t)class_span(n_blocks), nc = (size_t)wmax + 1;
+  A.state = reinterpret_cast<ShardState*>(take(sizeof(ShardState)));
+  A.wv = reinterpret_cast<uint16_t*>(take(span * 2));
+  A.av = reinterpret_cast<uint16_t*>(take(span * 2));
+  A.ckey = reinterpret_cast<uint64_t*>(take(nc * 8));
+  A.gh = reinterpret_cast<uint32_t*>(take(nc * 4));
+  A.ccnt = reinterpret_cast<uint32_t*>(take(nc * 4));
+  A.cwhole = reinterpret_cast<uint32_t*>(take(nc * 4));
+  A.cflag = reinterpret_cast<uint8_t*>(take(nc));
+  A.weights = weights;
+  A.nbl = n_blocks;
+  A.wmax = wmax;
+  A.cap = cap;
+  A.base = base;
+  A.out = out;
+  A.in = in;
+  A.remaining = remaining;
+  A.prefix = prefix;
+  A.counts = counts;
+  A.offsets = offsets;
+  const size_t dyn = phase == 1 ? nc * 4 : 0;
+  if (dyn > 48 * 1024) cudaFuncSetAttribute(alloc_shard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  const int kt = ktimer_begin(ctx, s, "alloc_shard");
+  alloc_shard_kernel<<<1, kClassThreads, dyn, s>>>(phase, A);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "alloc_shard launch");
 }
 
 }  // namespace abcs_b200

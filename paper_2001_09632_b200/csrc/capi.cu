@@ -500,6 +500,56 @@ int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks
                          scr, s);
 }
 
+size_t abcs_allocate_shard_scratch_bytes(int32_t n_blocks, int32_t wmax) {
+  if (n_blocks < 0 || wmax < 0 || wmax > 65535) return 0;
+  return shard_scratch_bytes(n_blocks, wmax);
+}
+
+int abcs_allocate_shard_step(abcs_ctx* c, int32_t phase, const uint32_t* d_weights, int32_t n_blocks, int32_t wmax,
+                             int32_t cap, int32_t base, void* d_scratch, int64_t* d_out, const int64_t* d_in,
+                             int64_t remaining, int64_t prefix, uint16_t* d_counts, int32_t* d_offsets,
+                             void* stream) {
+  CHECK_CTX(c);
+  if (phase < 0 || phase > 4 || n_blocks < 0 || wmax < 0 || wmax > 65535 || cap < 0 || cap > 65535 || !d_scratch ||
+      !d_out || (phase == 0 && n_blocks > 0 && !d_weights) || (phase == 2 && !d_in) || (phase == 4 && !d_counts))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_alloc_shard(ctx, phase, d_weights, n_blocks, wmax, cap, base, d_scratch,
+                            reinterpret_cast<long long*>(d_out), reinterpret_cast<const long long*>(d_in), remaining,
+                            prefix, d_counts, d_offsets, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int abcs_gather_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint8_t* d_images,
+                             int64_t image_stride, int32_t pitch, int32_t n, const uint16_t* d_counts,
+                             const int32_t* d_offsets, float* d_payload, int64_t payload_stride, float* d_out,
+                             int64_t out_stride, int32_t out_pitch, void* stream) {
+  CHECK_CTX(c);
+  if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_images || !d_counts || !d_offsets || !d_payload)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!block_supported(block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+  if (pitch < cols * block || image_stride < (int64_t)pitch * (rows * block - 1) + cols * block)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "image pitch/stride smaller than the image");
+  if (d_out && (out_pitch < cols * block || out_stride < (int64_t)out_pitch * (rows * block - 1) + cols * block))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "output pitch/stride smaller than the image");
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool vec_out = d_out && out_pitch % 2 == 0 && out_stride % 2 == 0 && ((uintptr_t)d_out % 8) == 0;
+  if (vec_out && block == 16 && mma16_supported(rows, cols, n))
+    return launch_sense16(ctx, 3, rows, cols, n, d_images, image_stride, pitch, 0, 0.0, nullptr, d_counts, d_offsets,
+                          d_payload, payload_stride, d_out, out_stride, out_pitch, s);
+  if (vec_out && block == 8 && mma16_supported(rows, cols, n))
+    return launch_sense8(ctx, true, true, rows, cols, n, d_images, image_stride, pitch, d_counts, d_offsets,
+                         d_payload, payload_stride, d_out, out_stride, out_pitch, s);
+  int st = launch_gather(ctx, rows, cols, block, d_images, nullptr, image_stride, pitch, n, d_counts, d_offsets,
+                         d_payload, payload_stride, s);
+  if (st || !d_out) return st;
+  return launch_decode(ctx, rows, cols, block, d_counts, d_offsets, d_payload, payload_stride, n, d_out, out_stride,
+                       out_pitch, s);
+}
+
 int abcs_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
                       const int32_t* d_offsets, const float* d_payload, int64_t payload_stride, int32_t n,
                       float* d_out, int64_t out_stride, int32_t out_pitch, const int64_t* d_payload_len,

@@ -60,6 +60,10 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
                     int64_t budget, const int32_t* caps, int32_t cap, int32_t base, uint16_t* counts,
                     int32_t* offsets, int32_t* status, void* scratch, cudaStream_t s, int32_t wmax = -1);
 size_t allocate_scratch_bytes(int32_t n_blocks, int32_t n_vectors);
+size_t shard_scratch_bytes(int32_t n_blocks, int32_t wmax);
+int launch_alloc_shard(Ctx* ctx, int phase, const uint32_t* weights, int32_t n_blocks, int32_t wmax, int32_t cap,
+                       int32_t base, void* scratch, long long* out, const long long* in, long long remaining,
+                       long long prefix, uint16_t* counts, int32_t* offsets, cudaStream_t s);
 int launch_zz_counts(Ctx* ctx, const abcs_sense_plan& p, int32_t n, uint16_t* counts, int32_t* offsets,
                      cudaStream_t s);
 int launch_gather(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint8_t* imgs,

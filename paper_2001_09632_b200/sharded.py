@@ -1,0 +1,221 @@
+"""Intra-image sharding: one image's block rows split over GPUs (last tier).
+
+The batch path shards whole images and needs no collective. An image too large for one GPU, or a
+single image that should use several, is split into horizontal strips of whole block rows
+(shards, in block order). Everything of `sense` + `decode_idct` is per block, except the
+allocation (largest_remainder_allocate, sensing.cpp:110-177), which ranks all blocks of the image.
+That is the path's only exchange. Per allocation round:
+
+    phase 1  active-weight histogram, sum of weights, active count   -> all-reduce (sum)
+    phase 2  class table + threshold from the global histogram (identical everywhere);
+             the shard's exact-tie blocks                           -> all-gather (prefix)
+    phase 3  apply + clamp with the lower shards' tie count          -> all-reduce (taken, open)
+
+followed by one all-gather of the shard totals for the payload offsets. The phases are the
+device kernels behind `abcs_allocate_shard_step` (csrc/alloc.cu), so every shard's counts and
+payload are bit-identical to the single-GPU sense of the whole image
+(tests/test_sharded.py).
+
+A process may hold several shards (`ShardComm(n_local)`): their collectives are summed locally
+before the torch.distributed collective across processes (one rank per GPU, NCCL), so the
+same code runs as 1 process x k shards on one GPU (the GPU tests) or as k ranks x 1 shard.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .abcs import (Algorithm, Context, LogicError, SensingConfig, UnsupportedError, _check, _ptr, _stream_ptr,
+                   _torch, sense_plan)
+
+
+class ShardComm:
+    """Collectives over the shards of one image: n_local shards in this process, the same number
+    in every rank of torch.distributed (if initialised with world size > 1); rank r holds global
+    shards [r * n_local, (r + 1) * n_local)."""
+
+    def __init__(self, n_local: int = 1, device=None, group=None):
+        torch = _torch_any()
+        self.n_local = int(n_local)
+        self.group = group
+        dist = torch.distributed
+        self.dist = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        self.world = dist.get_world_size(group) if self.dist else 1
+        self.rank = dist.get_rank(group) if self.dist else 0
+        self.device = device
+
+    @property
+    def n_shards(self) -> int:
+        return self.world * self.n_local
+
+    @property
+    def first(self) -> int:
+        return self.rank * self.n_local
+
+    def allreduce(self, parts):
+        """Elementwise sum of one int64 tensor per local shard over all shards."""
+        acc = parts[0].clone()
+        for t in parts[1:]:
+            acc += t
+        if self.dist:
+            _torch_any().distributed.all_reduce(acc, group=self.group)
+        return acc
+
+    def allgather(self, vals: Sequence[int]) -> List[int]:
+        """One integer per local shard -> the list over all shards in global order."""
+        if not self.dist:
+            return [int(v) for v in vals]
+        torch = _torch_any()
+        t = torch.tensor([int(v) for v in vals], dtype=torch.int64, device=self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        torch.distributed.all_gather(out, t, group=self.group)
+        return [int(x) for o in out for x in o.tolist()]
+
+
+def _torch_any():
+    import torch
+    return torch
+
+
+class DeviceShard:
+    """One shard's allocation state on the device (abcs_allocate_shard_step)."""
+
+    def __init__(self, weights, wmax: int, cap: int, base: int):
+        torch = _torch()
+        self.w = weights.contiguous()
+        self.nb = int(self.w.numel())
+        self.wmax, self.cap, self.base = int(wmax), int(cap), int(base)
+        lib = _lib.load()
+        dev = self.w.device
+        nbytes = lib.abcs_allocate_shard_scratch_bytes(self.nb, self.wmax)
+        if nbytes == 0:
+            raise ValueError("bad shard geometry")
+        self.scratch = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+        self.out = torch.zeros(self.wmax + 3, dtype=torch.int64, device=dev)
+        self.ctx = Context.get(dev.index)
+
+    def phase(self, k: int, inp=None, remaining: int = 0, prefix: int = 0, counts=None, offsets=None):
+        torch = _torch()
+        _check(_lib.load().abcs_allocate_shard_step(
+            self.ctx.handle, k, _ptr(self.w), self.nb, self.wmax, self.cap, self.base, self.scratch.data_ptr(),
+            self.out.data_ptr(), _ptr(inp), int(remaining), int(prefix), _ptr(counts), _ptr(offsets),
+            _stream_ptr(torch)))
+        return self.out
+
+
+def allocate_sharded(shards: Sequence, comm: ShardComm, budget: int, counts: Sequence, offsets: Sequence):
+    """largest_remainder_allocate of one weight vector held as `shards` (this process's
+    DeviceShard-like objects, in global order) -> counts[i] (u16) and offsets[i] (int32, global
+    payload offsets; entries may be None) of each local shard. Returns the local shard totals."""
+    nb_total = sum(comm.allgather([s.nb for s in shards]))
+    cap = shards[0].cap
+    if budget < 0 or budget > cap * nb_total or cap < 0 or cap > 65535:
+        raise ValueError("allocate: budget exceeds the capacity of the blocks")
+    bad = comm.allreduce([s.phase(0)[:1] for s in shards])
+    if int(bad[0]):
+        raise LogicError("allocate: a weight exceeds the declared bound")
+    remaining = int(budget)
+    taken_local = [0] * len(shards)
+    rounds = 0
+    while remaining > 0:
+        rounds += 1
+        if rounds > nb_total + 1:
+            raise LogicError("allocate: no progress")
+        hist = comm.allreduce([s.phase(1) for s in shards])            # exchange 1
+        ties = comm.allgather([int(s.phase(2, inp=hist, remaining=remaining)[0]) for s in shards])  # exchange 2
+        parts = []
+        for j, s in enumerate(shards):
+            g = comm.first + j
+            out = s.phase(3, prefix=sum(ties[:g]))[:2].clone()
+            taken_local[j] += int(out[0])
+            parts.append(out)
+        tk = comm.allreduce(parts)                                      # exchange 3
+        remaining -= int(tk[0])
+        if remaining > 0 and int(tk[1]) == 0:
+            raise LogicError("allocate: capacity exhausted before budget placed")
+    totals_local = [s.base * s.nb + t for s, t in zip(shards, taken_local)]
+    totals = comm.allgather(totals_local)                               # payload offsets
+    for j, s in enumerate(shards):
+        g = comm.first + j
+        s.phase(4, prefix=sum(totals[:g]), counts=counts[j], offsets=offsets[j])
+    return totals_local
+
+
+@dataclass
+class ShardSense:
+    """One shard's sense + decode: block rows [row0, row0 + rows) of the image."""
+    row0: int
+    rows: int
+    counts: object        # (rows * cols,) uint16, the image's counts of these blocks
+    offsets: object       # (rows * cols,) int32, offsets into the image's payload
+    payload_offset: int   # where this shard's payload slice starts in the image's payload
+    payload: object       # (its total,) float32: the image's payload[payload_offset : + total]
+    decoded: Optional[object]  # (rows * B, cols * B) float32
+
+
+def split_rows(rows: int, n_shards: int) -> List[int]:
+    """Block-row starts of n_shards balanced strips (the last entry is `rows`)."""
+    return [rows * k // n_shards for k in range(n_shards + 1)]
+
+
+def sense_decode_sharded(strips: Sequence, row0s: Sequence[int], cfg: SensingConfig, height: int, width: int,
+                         comm: ShardComm, decode: bool = True) -> List[ShardSense]:
+    """sense (+ decode_idct) of one height x width image whose block rows are split over shards.
+    strips[j]: this process's shard j as a (rows_j * B, W) uint8 CUDA tensor holding block rows
+    [row0s[j], row0s[j] + rows_j) of the image; shards in global order across ranks. DD and ZZ
+    sensing are supported (BBV needs its neighbours' boundary rows: UnsupportedError)."""
+    torch = _torch()
+    plan = sense_plan(cfg, height, width)
+    B, cols = plan.block, plan.cols
+    if plan.algorithm_used == Algorithm.BBV:
+        raise UnsupportedError("sharded sense: BBV needs the neighbouring shards' boundary rows")
+    if plan.algorithm_used not in (Algorithm.DD, Algorithm.ZZ):
+        raise UnsupportedError("sharded sense: unsupported algorithm")
+    lib = _lib.load()
+    shards, counts, offsets, strip_plans = [], [], [], []
+    for strip, r0 in zip(strips, row0s):
+        if strip.dtype != torch.uint8 or strip.dim() != 2 or not strip.is_cuda or strip.shape[1] != width:
+            raise ValueError("strips must be (rows * B, W) uint8 CUDA tensors")
+        rows = strip.shape[0] // B
+        sp = _lib.SensePlanC.from_buffer_copy(plan)  # the image's plan on the strip's block rows
+        sp.rows, sp.height, sp.n_blocks = rows, rows * B, rows * cols
+        strip_plans.append((sp, r0, rows))
+        dev = strip.device
+        counts.append(torch.empty(rows * cols, dtype=torch.uint16, device=dev))
+        offsets.append(torch.empty(rows * cols, dtype=torch.int32, device=dev))
+        if plan.algorithm_used == Algorithm.DD:
+            w = torch.empty(rows * cols, dtype=torch.int32, device=dev)
+            _check(lib.abcs_sense_weights_batch(Context.get(dev.index).handle, C.byref(sp), strip.data_ptr(),
+                                                strip.numel(), width, 1, w.data_ptr(), None, _stream_ptr(torch)))
+            shards.append(DeviceShard(w, plan.dd_phase1, plan.cap, plan.count_base))
+    if plan.algorithm_used == Algorithm.DD:
+        totals_local = allocate_sharded(shards, comm, plan.alloc_budget, counts, offsets)
+    else:  # ZZ: floor(M / n_B) per block, +1 for the first M mod n_B blocks (sensing.cpp:181-190)
+        totals_local = []
+        for c, o, (sp, r0, rows) in zip(counts, offsets, strip_plans):
+            g = np.arange(r0 * cols, (r0 + rows) * cols, dtype=np.int64)
+            cnt = np.minimum(plan.zz_per_block + (g < plan.zz_extra), B * B).astype(np.uint16)
+            c.copy_(torch.from_numpy(cnt.view(np.int16)).view(torch.uint16))
+            totals_local.append(int(cnt.sum(dtype=np.int64)))
+        totals = comm.allgather(totals_local)
+        for j, (c, o) in enumerate(zip(counts, offsets)):
+            pre = sum(totals[:comm.first + j])
+            cnt = c.view(torch.int16).to(torch.int64) & 0xFFFF
+            o.copy_((torch.cumsum(cnt, 0) - cnt + pre).to(torch.int32))
+    out = []
+    for strip, c, o, tot, (sp, r0, rows) in zip(strips, counts, offsets, totals_local, strip_plans):
+        dev = strip.device
+        pay = torch.empty(max(tot, 1), dtype=torch.float32, device=dev)[:tot]
+        pre = int(o[0]) if rows * cols else 0
+        local_off = o - pre
+        dec = torch.empty((rows * B, cols * B), dtype=torch.float32, device=dev) if decode else None
+        _check(lib.abcs_gather_decode_batch(Context.get(dev.index).handle, rows, cols, B, strip.data_ptr(),
+                                            strip.numel(), width, 1, _ptr(c), local_off.data_ptr(), _ptr(pay),
+                                            max(tot, 1), _ptr(dec), rows * B * cols * B, cols * B,
+                                            _stream_ptr(torch)))
+        out.append(ShardSense(r0, rows, c, o, pre, pay, dec))
+    return out

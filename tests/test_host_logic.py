@@ -20,7 +20,7 @@ HEADER = os.path.join(ROOT, "include", "abcs_b200.h")
 
 def test_library_exports_every_header_symbol():
     text = open(HEADER).read()
-    declared = set(re.findall(r"^\s*(?:int|double|int64_t|const char\*)\s+(abcs_\w+)\s*\(", text, re.M))
+    declared = set(re.findall(r"^\s*(?:int|double|int64_t|size_t|const char\*)\s+(abcs_\w+)\s*\(", text, re.M))
     assert len(declared) >= 18
     lib = _lib.load()
     for name in declared:
