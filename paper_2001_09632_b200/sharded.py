@@ -76,6 +76,35 @@ class ShardComm:
         return [int(x) for o in out for x in o.tolist()]
 
 
+    def halo(self, fields, rows: int):
+        """fields: one (h_j, W) tensor per local shard (global order). Returns per local shard
+        (above, below): the last `rows` rows of the previous shard and the first `rows` of the
+        next (None at the image's top / bottom). Across ranks: paired send/recv with rank +- 1."""
+        n = len(fields)
+        above = [fields[j - 1][-rows:] if j > 0 else None for j in range(n)]
+        below = [fields[j + 1][:rows] if j + 1 < n else None for j in range(n)]
+        if self.dist:
+            torch = _torch_any()
+            dist = torch.distributed
+            ops, bufs = [], {}
+            if self.rank > 0:
+                bufs["up"] = torch.empty_like(fields[0][:rows])
+                ops.append(dist.P2POp(dist.isend, fields[0][:rows].contiguous(), self.rank - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, bufs["up"], self.rank - 1, self.group))
+            if self.rank + 1 < self.world:
+                bufs["down"] = torch.empty_like(fields[-1][-rows:])
+                ops.append(dist.P2POp(dist.isend, fields[-1][-rows:].contiguous(), self.rank + 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, bufs["down"], self.rank + 1, self.group))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+            if "up" in bufs:
+                above[0] = bufs["up"]
+            if "down" in bufs:
+                below[-1] = bufs["down"]
+        return list(zip(above, below))
+
+
 def _torch_any():
     import torch
     return torch
@@ -219,3 +248,72 @@ def sense_decode_sharded(strips: Sequence, row0s: Sequence[int], cfg: SensingCon
                                             _stream_ptr(torch)))
         out.append(ShardSense(r0, rows, c, o, pre, pay, dec))
     return out
+
+
+def ida_sharded(parts: Sequence[ShardSense], width: int, block: int, comm: ShardComm, iterations: int = 10,
+                damping: float = 2.0, k: float = 2.7):
+    """reconstruct() with method Ida (recon.cpp:199-259, dct_threshold denoiser) of one image
+    whose block rows are split over shards: `parts` are this process's ShardSense results of
+    sense_decode_sharded (global order). Per iteration the exchanges are the 4-row halo of the
+    pseudo field (denoiser tiles at stride 4 straddle the strip boundaries) and the all-reduce
+    of ||z||^2 for sigma = ||z|| / sqrt(M) (recon.cpp:81-93); divergence is agreed by all shards.
+    Returns this process's clamped estimate strips."""
+    torch = _torch()
+    lib = _lib.load()
+    B = block
+    Wc = (width // B) * B
+    cols = Wc // B
+    geo = []
+    for r in parts:
+        dev = r.counts.device
+        ctx = Context.get(dev.index).handle
+        off = (r.offsets - r.payload_offset).contiguous()
+        geo.append((ctx, r.rows, r.counts, off, r.payload.contiguous(), dev))
+    st = _stream_ptr(torch)
+
+    def adjoint(g, v):  # A* v: the strip's IDCT of its prefixes (operators.cpp:51-76)
+        ctx, rows, cnt, off, y, dev = g
+        out = torch.empty((rows * B, Wc), dtype=torch.float32, device=dev)
+        _check(lib.abcs_decode_batch(ctx, rows, cols, B, _ptr(cnt), _ptr(off), _ptr(v), max(v.numel(), 1), 1,
+                                     out.data_ptr(), out.numel(), Wc, None, None, st))
+        return out
+
+    def forward(g, x):  # A x (operators.cpp:23-48)
+        ctx, rows, cnt, off, y, dev = g
+        out = torch.empty(y.numel(), dtype=torch.float32, device=dev)
+        _check(lib.abcs_forward_batch(ctx, rows, cols, B, _ptr(cnt), _ptr(off), x.data_ptr(), x.numel(), Wc, 1,
+                                      _ptr(out), max(out.numel(), 1), st))
+        return out
+
+    def gsum(vals):  # fp64 sum over all shards
+        return float(comm.allreduce([torch.tensor([v], dtype=torch.float64, device=g[5])
+                                     for v, g in zip(vals, geo)])[0])
+
+    M = float(sum(comm.allgather([g[4].numel() for g in geo])))
+    if M <= 0:
+        raise ValueError("reconstruct: no measurements")
+    # warm start (recon.cpp:119-131): x0 = A* y, z0 = y - A x0, sigma0 = ||y|| / sqrt(M)
+    xs = [adjoint(g, g[4]) for g in geo]
+    zs = [g[4] - forward(g, x) for g, x in zip(geo, xs)]
+    sigma = (gsum([float(torch.sum(g[4].double() ** 2)) for g in geo]) / M) ** 0.5
+    ons = 1.0 / damping
+    for it in range(1, iterations + 1):
+        pseudo = [x + adjoint(g, z) for g, x, z in zip(geo, xs, zs)]       # recon.cpp:75-79
+        new_x = []
+        for (above, below), ps, g in zip(comm.halo(pseudo, 4), pseudo, geo):
+            ext = torch.cat([t for t in (above, ps, below) if t is not None]).contiguous()
+            den = torch.empty_like(ext)
+            sig = (C.c_double * 1)(sigma)
+            _check(lib.abcs_denoise_dct_batch(g[0], ext.data_ptr(), ext.shape[0], Wc, ext.numel(), 1, sig, k, 8,
+                                              den.data_ptr(), st))
+            top = 0 if above is None else above.shape[0]
+            new_x.append(den[top:top + ps.shape[0]])
+        xs = new_x
+        zs = [(g[4] - forward(g, x)) + ons * z for g, x, z in zip(geo, xs, zs)]  # finish_step, recon.cpp:81-93
+        sigma = (gsum([float(torch.sum(z.double() ** 2)) for z in zs]) / M) ** 0.5
+        bad = gsum([float((~torch.isfinite(x)).any() | (x.abs() > 1e6).any() | (~torch.isfinite(z)).any())
+                    for x, z in zip(xs, zs)])
+        if bad:
+            from .abcs import DivergenceError
+            raise DivergenceError(f"reconstruct: diverged at iteration {it}", it)
+    return [x.clamp(0.0, 255.0) for x in xs]                               # recon.cpp:255-257
