@@ -227,8 +227,17 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       u8_bfragT_il(st, bx[0]);
       u8_bfragT_il(st + 256, bx[1]);
       Acc16 Y[2];  // Y^T of each block
+      // payload pass: when both blocks keep <= 36 coefficients their zigzag prefixes lie in the
+      // top-left 8x8 (slots 0/1), so the low-quadrant transforms suffice (warp-uniform choice)
+      bool lo_pair = false;
+      if constexpr (kPayload && !kWeights) {
+        const int c0 = __shfl_sync(0xffffffffu, my_cnt, 2 * p);
+        const int c1 = two ? __shfl_sync(0xffffffffu, my_cnt, (2 * p + 1) & 31) : 0;
+        lo_pair = c0 <= 36 && c1 <= 36;
+      }
       if constexpr (kLowCols) dct16_fwd_exact_x2_lo(f, bx, Y);
       else if constexpr (kWeights) dct16_fwd_exact_x2_tab(f, s_btab, bx, Y);
+      else if (lo_pair) dct16_fwd_exact_x2_lo(f, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
       if constexpr (kSweep) {
@@ -324,7 +333,8 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll
           for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int s = 0; s < 8; ++s) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+            for (int s = 0; s < 8; ++s)
+              if (s < 2 || !lo_pair) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
           __syncwarp();
           // the pair's prefixes are adjacent in the payload (offset1 = offset0 + cnt0): one
           // coalesced copy of cnt0 + cnt1 values, two loads in flight per iteration
@@ -349,7 +359,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
             Acc16 Ym;  // zero the coefficients outside the block's zigzag prefix
 #pragma unroll
             for (int s = 0; s < 8; ++s) Ym.v[s >> 2][s & 3] = (int)rank_d[s] < cnt[q] ? Y[q].v[s >> 2][s & 3] : 0.f;
-            const Acc16 X = dct16_inv_from_yt(f, Ym);
+            const Acc16 X = lo_pair ? dct16_inv_from_yt_lo(f, Ym) : dct16_inv_from_yt(f, Ym);
             store_dfrag(A.out + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
                         A.out_pitch, X);
           }

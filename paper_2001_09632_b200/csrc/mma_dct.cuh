@@ -355,6 +355,33 @@ __device__ __forceinline__ Acc16 dct16_inv_from_yt_t(const Frag16Tab& F, const A
   return stage2_tab(T, &F.b[4][0]);
 }
 
+// dct16_inv_from_yt for a Y^T supported on its top-left 8x8 (slots 0/1 only: zigzag ranks
+// < 36): stage 1's second n-tile is zero and stage 2's k-range 8..15 is zero, so 9 of the 12
+// MMAs and 4 of the 8 splits remain. Bit-identical to dct16_inv_from_yt on such input (the
+// skipped terms are exact zeros).
+__device__ __forceinline__ Acc16 dct16_inv_from_yt_lo(const Frag16& f, const Acc16& Yt) {
+  uint32_t bh0, bl0;
+  split2(Yt.v[0][0], Yt.v[0][1], bh0, bl0);
+  Acc16 T;
+  T.v[0][0] = T.v[0][1] = T.v[0][2] = T.v[0][3] = 0.f;
+  mma16816(T.v[0], f.th, bl0, 0u);
+  mma16816(T.v[0], f.tl, bh0, 0u);
+  mma16816(T.v[0], f.th, bh0, 0u);
+  uint32_t ah[4], al[4];
+  split2(T.v[0][0], T.v[0][1], ah[0], al[0]);
+  split2(T.v[0][2], T.v[0][3], ah[1], al[1]);
+  ah[2] = al[2] = ah[3] = al[3] = 0u;
+  Acc16 R;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    R.v[j][0] = R.v[j][1] = R.v[j][2] = R.v[j][3] = 0.f;
+    mma16816(R.v[j], al, f.tbh[j][0], f.tbh[j][1]);
+    mma16816(R.v[j], ah, f.tbl[j][0], f.tbl[j][1]);
+    mma16816(R.v[j], ah, f.tbh[j][0], f.tbh[j][1]);
+  }
+  return R;
+}
+
 __device__ __forceinline__ uint4 interleave_row16(uint4 v) {
   return make_uint4(__byte_perm(v.x, v.z, 0x5410), __byte_perm(v.x, v.z, 0x7632), __byte_perm(v.y, v.w, 0x5410),
                     __byte_perm(v.y, v.w, 0x7632));
