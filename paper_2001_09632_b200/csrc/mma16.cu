@@ -594,7 +594,7 @@ sense8_kernel(Grid16 G, Sense16Args A) {
         for (int k = lane; k < qtot; k += 32) zb[k] = __ldg(src + k);
         __syncwarp();
       }
-#pragma unroll 1
+#pragma unroll
       for (int pp = 0; pp < 4; ++pp) {
         const int b = qb + 2 * pp;
         if (b >= nblk) break;
