@@ -178,7 +178,8 @@ CPU_TARGET_CORE_S = 20.0  # bounded CPU sample: ~10-30 s of CPU work (core-secon
 def calibrated_count(checker, imgs, threads, cap):
     """Images per CPU sample so one sample is ~CPU_TARGET_CORE_S core-seconds (a multiple of threads)."""
     n0 = min(len(imgs), threads)
-    sec, _ = cpu_sample(checker, imgs[:n0], threads)  # also the warm-up
+    cpu_sample(checker, imgs[:n0], threads)  # warm-up (thread start, page-in)
+    sec, _ = cpu_sample(checker, imgs[:n0], threads)
     per_img = sec * min(threads, n0) / n0  # core-seconds per image (all subrates)
     n = int(CPU_TARGET_CORE_S / max(per_img, 1e-6))
     n = max(threads, (n // threads) * threads)
