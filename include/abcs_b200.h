@@ -233,6 +233,15 @@ int abcs_gather_decode_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t 
                              float* d_payload, int64_t payload_stride, float* d_out, int64_t out_stride,
                              int32_t out_pitch, void* stream);
 
+/* bbv_measure (sensing.cpp:239-296) of one shard strip of an image: plan = the image's plan
+ * with rows / height / n_blocks of the strip. has_below != 0: the strip is not the image's
+ * bottom, and d_strip holds one more pixel row (the next strip's first) after its last block
+ * row, which the bottom-side probes of that row read; side values then follow the image's
+ * block-major order for these blocks (no bottom values). */
+int abcs_bbv_weights_strip(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* d_strip,
+                           int64_t strip_stride, int32_t pitch, int32_t has_below, uint32_t* d_weights,
+                           float* d_side, void* stream);
+
 /* largest_remainder_allocate (sensing.cpp:110-177) of ONE weight vector split
  * into shards (contiguous block ranges in block order) held by different
  * devices/processes. The caller drives the rounds and the collectives between

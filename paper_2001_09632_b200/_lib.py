@@ -98,6 +98,7 @@ SIGNATURES = {
     "abcs_synth_generate_host": (C.c_int, [C.POINTER(SynthSpecC), I64, I32, P]),
     "abcs_sense_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P, P, P]),
     "abcs_sense_decode_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P, P, P, I64, I32, P]),
+    "abcs_bbv_weights_strip": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P]),
     "abcs_gather_decode_batch": (C.c_int, [P, I32, I32, I32, P, I64, I32, I32, P, P, P, I64, P, I64, I32, P]),
     "abcs_allocate_shard_scratch_bytes": (C.c_size_t, [I32, I32]),
     "abcs_allocate_shard_step": (C.c_int, [P, I32, P, I32, I32, I32, I32, P, P, P, I64, I64, P, P, P]),

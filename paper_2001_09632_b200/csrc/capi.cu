@@ -161,6 +161,17 @@ int abcs_sense_weights_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_
   return launch_sense_weights(ctx, *p, d_images, image_stride, pitch, n, d_weights, d_side, s, fix);
 }
 
+int abcs_bbv_weights_strip(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_strip, int64_t strip_stride,
+                           int32_t pitch, int32_t has_below, uint32_t* d_weights, float* d_side, void* stream) {
+  CHECK_CTX(c);
+  if (!p || !d_strip || !d_weights || p->algorithm_used != ABCS_ALGO_BBV)
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bbv strip weights: bad arguments");
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  return launch_sense_weights(ctx, *p, d_strip, strip_stride, pitch, 1, d_weights, d_side,
+                              reinterpret_cast<cudaStream_t>(stream), nullptr, has_below != 0);
+}
+
 }  // extern "C"
 
 namespace abcs_b200 {

@@ -53,7 +53,7 @@ int cuda_status(cudaError_t e, const char* what);
 // Kernel launchers (return abcs_status).
 int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs, int64_t img_stride,
                          int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s,
-                         uint32_t* fix_scratch = nullptr);
+                         uint32_t* fix_scratch = nullptr, bool bbv_below = false);
 // u32 words of fixup scratch launch_sense_weights needs (count + one entry per block)
 inline size_t sense_fix_words(int64_t n_blocks_total) { return (size_t)n_blocks_total * 5 + 8; }
 int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t n_vectors,

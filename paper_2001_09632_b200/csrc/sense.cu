@@ -101,7 +101,9 @@ dd_weights_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitc
 __global__ void __launch_bounds__(256)
 bbv_weights_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch, int rows, int cols,
                    int n, int B, int L, int offset, int per_side, int valid, uint32_t* __restrict__ weights,
-                   float* __restrict__ side, int64_t side_stride) {
+                   float* __restrict__ side, int64_t side_stride, bool below) {
+  // below: the block rows continue under this field (a shard strip whose buffer holds the next
+  // strip's first pixel row after its last block row), so its last block row is not the image's
   const int64_t nb = (int64_t)rows * cols;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)n * nb) return;
@@ -109,9 +111,9 @@ bbv_weights_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pit
   const int bi = (int)(gid % nb), br = bi / cols, bc = bi % cols;
   const uint8_t* im = imgs + img * img_stride;
   const int r0 = br * B, c0 = bc * B;
-  const int bottom = (br + 1 < rows) ? r0 + B : r0 + B - 1;
+  const bool last_row = (br + 1 == rows) && !below, last_col = (bc + 1 == cols);
+  const int bottom = last_row ? r0 + B - 1 : r0 + B;
   const int right = (bc + 1 < cols) ? c0 + B : c0 + B - 1;
-  const bool last_row = (br + 1 == rows), last_col = (bc + 1 == cols);
   float* out = nullptr;
   if (side) {
     out = side + img * side_stride +
@@ -190,7 +192,7 @@ static bool aligned_rows(const void* base, int64_t img_stride_bytes, int64_t pit
 
 int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs, int64_t img_stride,
                          int32_t pitch, int32_t n, uint32_t* weights, float* side, cudaStream_t s,
-                         uint32_t* fix_scratch) {
+                         uint32_t* fix_scratch, bool bbv_below) {
   const int64_t total = (int64_t)n * p.n_blocks;
   if (total == 0) return ABCS_OK;
   if (p.algorithm_used == ABCS_ALGO_BBV) {
@@ -199,7 +201,8 @@ int launch_sense_weights(Ctx* ctx, const abcs_sense_plan& p, const uint8_t* imgs
     const int kt = ktimer_begin(ctx, s, "bbv_weights");
     bbv_weights_kernel<<<(unsigned)grid, threads, 0, s>>>(imgs, img_stride, pitch, p.rows, p.cols, n, p.block,
                                                           (int)p.bbv_stride, p.bbv_offset, p.bbv_per_side,
-                                                          p.bbv_valid_probes, weights, side, p.side_per_image);
+                                                          p.bbv_valid_probes, weights, side, p.side_per_image,
+                                                          bbv_below);
     ktimer_end(ctx, s, kt);
   } else if (p.algorithm_used == ABCS_ALGO_DD && p.block == 16 && mma16_supported(p.rows, p.cols, n)) {
     return launch_sense16(ctx, 1, p.rows, p.cols, n, imgs, img_stride, pitch, p.dd_phase1, p.threshold, weights,

@@ -184,6 +184,8 @@ class ShardSense:
     payload_offset: int   # where this shard's payload slice starts in the image's payload
     payload: object       # (its total,) float32: the image's payload[payload_offset : + total]
     decoded: Optional[object]  # (rows * B, cols * B) float32
+    side: Optional[object] = None  # BBV: this shard's boundary values, side[side_offset : + len]
+    side_offset: int = 0
 
 
 def split_rows(rows: int, n_shards: int) -> List[int]:
@@ -195,17 +197,18 @@ def sense_decode_sharded(strips: Sequence, row0s: Sequence[int], cfg: SensingCon
                          comm: ShardComm, decode: bool = True) -> List[ShardSense]:
     """sense (+ decode_idct) of one height x width image whose block rows are split over shards.
     strips[j]: this process's shard j as a (rows_j * B, W) uint8 CUDA tensor holding block rows
-    [row0s[j], row0s[j] + rows_j) of the image; shards in global order across ranks. DD and ZZ
-    sensing are supported (BBV needs its neighbours' boundary rows: UnsupportedError)."""
+    [row0s[j], row0s[j] + rows_j) of the image; shards in global order across ranks. DD, BBV and
+    ZZ sensing (after the reference's fallbacks) are supported; BBV's bottom-side probes of a
+    strip's last block row read the next strip's first pixel row (a 1-row halo exchange)."""
     torch = _torch()
     plan = sense_plan(cfg, height, width)
     B, cols = plan.block, plan.cols
-    if plan.algorithm_used == Algorithm.BBV:
-        raise UnsupportedError("sharded sense: BBV needs the neighbouring shards' boundary rows")
-    if plan.algorithm_used not in (Algorithm.DD, Algorithm.ZZ):
+    if plan.algorithm_used not in (Algorithm.DD, Algorithm.ZZ, Algorithm.BBV):
         raise UnsupportedError("sharded sense: unsupported algorithm")
     lib = _lib.load()
-    shards, counts, offsets, strip_plans = [], [], [], []
+    rows_total = plan.rows
+    below_rows = comm.halo(list(strips), 1) if plan.algorithm_used == Algorithm.BBV else None
+    shards, counts, offsets, strip_plans, sides = [], [], [], [], []
     for strip, r0 in zip(strips, row0s):
         if strip.dtype != torch.uint8 or strip.dim() != 2 or not strip.is_cuda or strip.shape[1] != width:
             raise ValueError("strips must be (rows * B, W) uint8 CUDA tensors")
@@ -221,7 +224,22 @@ def sense_decode_sharded(strips: Sequence, row0s: Sequence[int], cfg: SensingCon
             _check(lib.abcs_sense_weights_batch(Context.get(dev.index).handle, C.byref(sp), strip.data_ptr(),
                                                 strip.numel(), width, 1, w.data_ptr(), None, _stream_ptr(torch)))
             shards.append(DeviceShard(w, plan.dd_phase1, plan.cap, plan.count_base))
-    if plan.algorithm_used == Algorithm.DD:
+        elif plan.algorithm_used == Algorithm.BBV:
+            # side values of these blocks: valid probes x (top, left per block; right per block row;
+            # bottom per block of the image's last block row), contiguous in block-major order
+            valid = plan.bbv_valid_probes
+            last = r0 + rows == rows_total
+            n_side = valid * (2 * rows * cols + rows + (cols if last else 0))
+            side = torch.empty(max(n_side, 1), dtype=torch.float32, device=dev)[:n_side]
+            below = below_rows[len(sides)][1]
+            ext = strip if last else torch.cat([strip, below[:1]]).contiguous()
+            w = torch.empty(rows * cols, dtype=torch.int32, device=dev)
+            _check(lib.abcs_bbv_weights_strip(Context.get(dev.index).handle, C.byref(sp), ext.data_ptr(),
+                                              ext.numel(), width, 0 if last else 1, w.data_ptr(), _ptr(side),
+                                              _stream_ptr(torch)))
+            sides.append((side, valid * (2 * r0 * cols + r0)))
+            shards.append(DeviceShard(w, 4 * valid * 255, plan.cap, plan.count_base))
+    if plan.algorithm_used in (Algorithm.DD, Algorithm.BBV):
         totals_local = allocate_sharded(shards, comm, plan.alloc_budget, counts, offsets)
     else:  # ZZ: floor(M / n_B) per block, +1 for the first M mod n_B blocks (sensing.cpp:181-190)
         totals_local = []
@@ -246,7 +264,8 @@ def sense_decode_sharded(strips: Sequence, row0s: Sequence[int], cfg: SensingCon
                                             strip.numel(), width, 1, _ptr(c), local_off.data_ptr(), _ptr(pay),
                                             max(tot, 1), _ptr(dec), rows * B * cols * B, cols * B,
                                             _stream_ptr(torch)))
-        out.append(ShardSense(r0, rows, c, o, pre, pay, dec))
+        sd, so = sides[len(out)] if sides else (None, 0)
+        out.append(ShardSense(r0, rows, c, o, pre, pay, dec, sd, so))
     return out
 
 

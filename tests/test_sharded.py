@@ -266,7 +266,7 @@ def test_sharded_sense_decode_equals_whole_image(H, W, num, den, k):
 
 
 @pytest.mark.gpu
-def test_sharded_sense_zz_and_bbv():
+def test_sharded_sense_zz():
     import torch
 
     import paper_2001_09632_b200 as p
@@ -279,8 +279,34 @@ def test_sharded_sense_zz_and_bbv():
     res = sense_decode_sharded(strips, cuts[:-1], cfg, 512, 768, ShardComm(3))
     assert torch.equal(torch.cat([r.counts.view(torch.int16) for r in res]), b.counts[0].view(torch.int16))
     assert torch.equal(torch.cat([r.decoded for r in res]), x[0])
-    with pytest.raises(p.UnsupportedError):
-        sense_decode_sharded(strips, cuts[:-1], p.SensingConfig(16, 1, 4, p.Algorithm.BBV), 512, 768, ShardComm(3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("H,W,B,num,den,k", [(1024, 1024, 16, 3, 10, 3), (1080, 1920, 8, 1, 5, 4),
+                                             (1000, 1480, 16, 1, 4, 2)])
+def test_sharded_sense_bbv(H, W, B, num, den, k):
+    """BBV on strips (bottom probes read the next strip's first row): weights, side values,
+    counts, payload and decoded rows equal the whole-image sense."""
+    import torch
+
+    import paper_2001_09632_b200 as p
+    from paper_2001_09632_b200.sharded import ShardComm, sense_decode_sharded, split_rows
+    img = p.synth_images(p.SynthSpec(H, W, 25, 5.0, 13), 0, 1)
+    cfg = p.SensingConfig(B, num, den, p.Algorithm.BBV)
+    b, x = p.sense_decode_batch(img, cfg)
+    assert b.plan.algorithm_used == p.Algorithm.BBV
+    cuts = split_rows(b.plan.rows, k)
+    strips = [img[0, cuts[j] * B:cuts[j + 1] * B].contiguous() for j in range(k)]
+    res = sense_decode_sharded(strips, cuts[:-1], cfg, H, W, ShardComm(k))
+    cols = b.plan.cols
+    for j, r in enumerate(res):
+        sl = slice(cuts[j] * cols, cuts[j + 1] * cols)
+        assert torch.equal(r.counts.view(torch.int16), b.counts[0, sl].view(torch.int16)), j
+        assert torch.equal(r.offsets, b.offsets[0, sl]), j
+        assert torch.equal(r.payload, b.payload[0, r.payload_offset:r.payload_offset + r.payload.numel()]), j
+        assert torch.equal(r.side, b.side[0, r.side_offset:r.side_offset + r.side.numel()]), j
+        assert torch.equal(r.decoded, x[0, cuts[j] * B:cuts[j + 1] * B]), j
+    assert sum(r.side.numel() for r in res) == b.side.shape[1]
 
 
 @pytest.mark.gpu
