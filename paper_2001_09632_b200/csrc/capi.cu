@@ -88,6 +88,11 @@ int abcs_ctx_destroy(abcs_ctx* c) {
   cudaDeviceSynchronize();
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->pipe_buf) cudaFree(ctx->pipe_buf);
+  for (int k = 0; k < 3; ++k) {
+    if (ctx->side[k]) cudaStreamDestroy(ctx->side[k]);
+    for (auto& e : ctx->ev_side[k])
+      if (e) cudaEventDestroy(e);
+  }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   for (auto& e : ctx->ev_join)
     if (e) cudaEventDestroy(e);
@@ -329,7 +334,7 @@ static size_t sweep_scratch_bytes(const abcs_sense_plan* plans, int32_t np, int3
 static int sweep_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, const uint8_t* d_images,
                       int64_t image_stride, int32_t pitch, int32_t n, int64_t first, uint16_t* const* d_counts,
                       int32_t* const* d_offsets, float* const* d_payload, float* const* d_out, int64_t out_stride,
-                      int32_t out_pitch, char* scr, cudaStream_t s) {
+                      int32_t out_pitch, char* scr, cudaStream_t s, int lane) {
   if (n == 0) return ABCS_OK;
   const abcs_sense_plan& p0 = plans[0];
   int32_t* offs[4];
@@ -355,19 +360,54 @@ static int sweep_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, const 
   const uint8_t* imgs = d_images + first * image_stride;
   int st = launch_sense16_sweep(ctx, np, p0.rows, p0.cols, n, imgs, image_stride, pitch, phase1, T, weights, fix, s);
   if (st) return st;
-  for (int j = 0; j < np; ++j) {
+  auto fa_of = [&](int j) {
     const abcs_sense_plan& q = plans[j];
-    uint16_t* counts = d_counts[j] + first * q.n_blocks;
     FusedAlloc fa;
     fa.runs_done = nullptr;
     fa.status = nullptr;
-    fa.counts = counts;
+    fa.counts = d_counts[j] + first * q.n_blocks;
     fa.offsets = offs[j];
     fa.budget = q.alloc_budget;
     fa.cap = q.cap;
     fa.base = q.count_base;
     fa.wmax = q.dd_phase1;
-    st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa, s);
+    return fa;
+  };
+  // the later plans' allocations (latency-bound, one CTA per image) run on a side stream,
+  // under the earlier plans' payload passes (not when the ctx is set to serialise: 1 pipe stream)
+  if (ctx->pipe_streams <= 1) {
+    for (int j = 0; j < np; ++j) {
+      const abcs_sense_plan& q = plans[j];
+      st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa_of(j), s);
+      if (st) return st;
+      st = launch_sense16(ctx, 3, q.rows, q.cols, n, imgs, image_stride, pitch, 0, 0.0, nullptr,
+                          d_counts[j] + first * q.n_blocks, offs[j], d_payload[j] + first * q.coeffs_per_image,
+                          q.coeffs_per_image, d_out[j] + first * out_stride, out_stride, out_pitch, s);
+      if (st) return st;
+    }
+    return ABCS_OK;
+  }
+  cudaStream_t side = ctx->side[lane];
+  if (!side) {
+    cudaStreamCreateWithFlags(&ctx->side[lane], cudaStreamNonBlocking);
+    for (auto& e : ctx->ev_side[lane]) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    side = ctx->side[lane];
+  }
+  cudaError_t e = cudaEventRecord(ctx->ev_side[lane][0], s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_side[lane][0], 0);
+  if (e != cudaSuccess) return cuda_status(e, "sweep fork");
+  for (int j = 1; j < np; ++j) {
+    const abcs_sense_plan& q = plans[j];
+    st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa_of(j), side);
+    if (st) return st;
+    e = cudaEventRecord(ctx->ev_side[lane][j], side);
+    if (e != cudaSuccess) return cuda_status(e, "sweep event");
+  }
+  for (int j = 0; j < np; ++j) {
+    const abcs_sense_plan& q = plans[j];
+    uint16_t* counts = d_counts[j] + first * q.n_blocks;
+    if (j == 0) st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa_of(j), s);
+    else st = cuda_status(cudaStreamWaitEvent(s, ctx->ev_side[lane][j], 0), "sweep join");
     if (st) return st;
     st = launch_sense16(ctx, 3, q.rows, q.cols, n, imgs, image_stride, pitch, 0, 0.0, nullptr, counts, offs[j],
                         d_payload[j] + first * q.coeffs_per_image, q.coeffs_per_image, d_out[j] + first * out_stride,
@@ -474,7 +514,7 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
   if (st) return st;
   if (nchunks == 1)
     return sweep_impl(ctx, plans, n_plans, d_images, image_stride, pitch, n, 0, d_counts, d_offsets, d_payload,
-                      d_out, out_stride, out_pitch, scr, s);
+                      d_out, out_stride, out_pitch, scr, s, 0);
   if (!ctx->ev_fork) {
     cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
     for (auto& e : ctx->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -486,7 +526,7 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
     cudaStream_t cs = ctx->pipe[k];
     cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
     st = sweep_impl(ctx, plans, n_plans, d_images, image_stride, pitch, cnt, first, d_counts, d_offsets, d_payload,
-                    d_out, out_stride, out_pitch, scr + per * k, cs);
+                    d_out, out_stride, out_pitch, scr + per * k, cs, k);
     if (st) return st;
     e = cudaEventRecord(ctx->ev_join[k], cs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_join[k], 0);

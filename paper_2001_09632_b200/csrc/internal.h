@@ -27,6 +27,9 @@ struct Ctx {
   int64_t launches = 0;
   void* pipe_buf = nullptr;  // abcs_sense_decode_host slot buffers
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  // sweep: per pipe lane, a side stream for the allocations of the later plans
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_side[3][5] = {};
   size_t pipe_bytes = 0;
   // opt-in per-kernel CUDA-event timing (abcs_ctx_kernel_timing): events recorded on the
   // launching stream around each hot kernel, drained by abcs_ctx_kernel_times
