@@ -172,7 +172,7 @@ def cpu_sample(checker, imgs, threads):
     return time.perf_counter() - t0, px
 
 
-CPU_TARGET_CORE_S = 20.0  # bounded CPU sample: ~10-30 s of CPU work (core-seconds)
+CPU_TARGET_CORE_S = 40.0  # calibration overestimates per-image cost ~2x: lands at ~15-25 core-seconds
 
 
 def calibrated_count(checker, imgs, threads, cap):
