@@ -236,6 +236,24 @@ def test_class_allocator_cluster_sizes(p, torch, checker, H, W, B, num, den, alg
     assert np.array_equal(got[16][0][1].astype(np.int64), want["counts"].astype(np.int64))
 
 
+def test_class_allocator_cluster_global_state(p, torch, checker):
+    """A 4096^2 image at cluster sizes 1 and 2: the per-block state no longer fits shared memory
+    and lives in global scratch (alloc_class_kernel<false>), split across the cluster's CTAs."""
+    imgs = p.synth_images(p.SynthSpec(4096, 4096, 200, 8.0, 5), 0, 2)
+    cfg = p.SensingConfig(16, 1, 4, p.Algorithm.DD)
+    got = {}
+    try:
+        for cs in (1, 2):
+            os.environ["ABCS_ALLOC_CLUSTER"] = str(cs)
+            b = p.sense_batch(imgs, cfg)
+            got[cs] = (b.counts.cpu().numpy().view(np.uint16).copy(), b.offsets.cpu().numpy().copy())
+    finally:
+        os.environ.pop("ABCS_ALLOC_CLUSTER", None)
+    assert np.array_equal(got[1][0], got[2][0]) and np.array_equal(got[1][1], got[2][1])
+    b = p.sense_batch(imgs, cfg)  # the launcher's own choice
+    assert np.array_equal(b.counts.cpu().numpy().view(np.uint16), got[1][0])
+
+
 # ---- decode / operators -------------------------------------------------------------------
 def test_decode_golden(p):
     z = np.load(os.path.join(ROOT, "tests", "golden", "recon_case.npz"))
