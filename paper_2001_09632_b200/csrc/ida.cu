@@ -563,17 +563,6 @@ int launch_ida_state(Ctx* ctx, bool init, int32_t rows, int32_t cols, int32_t bl
 // ---- every iterative method (recon.cpp:133-259) -------------------------------------------
 namespace {
 
-// splitmix-style probe seed per iteration (recon.cpp:95-105)
-uint64_t probe_seed_for(uint64_t seed, int iteration) {
-  uint64_t v = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(iteration + 1);
-  v ^= v >> 30;
-  v *= 0xBF58476D1CE4E5B9ull;
-  v ^= v >> 27;
-  v *= 0x94D049BB133111EBull;
-  v ^= v >> 31;
-  return v;
-}
-
 struct ReconScratch {
   IdaLayout L;          // block-phase reductions; L.pseudo[0] = pseudo field, L.pseudo[1] = new estimate
   float* perturbed;     // DAMP: pseudo + eps * probe
@@ -642,7 +631,9 @@ int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t bl
   auto al = [](size_t v) { return (v + 255) / 256 * 256; };
   const size_t fld = al((size_t)n * N * 4);
   const size_t parts = divergence_partials(ctx, N, n);
-  size_t need = base + 3 * fld + al((size_t)N * 4) + 6 * al((size_t)n * 8) + al(parts * 8) + al((size_t)n * 4) +
+  const int steps = one_step ? 1 : cfg.iterations;
+  const size_t probe_bytes = al((size_t)N * 4 * (damp ? steps : 1));  // every iteration's probe
+  size_t need = base + 3 * fld + probe_bytes + 6 * al((size_t)n * 8) + al(parts * 8) + al((size_t)n * 4) +
                 al((size_t)n * rows * cols * 4);
   if (!one_step) need += fld + al((size_t)n * y_stride * 4) + al((size_t)n * 8);
   int st;
@@ -659,7 +650,7 @@ int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t bl
   R.perturbed = reinterpret_cast<float*>(take(fld));
   R.moved = reinterpret_cast<float*>(take(fld));
   R.tmp = reinterpret_cast<float*>(take(fld));
-  R.probe = reinterpret_cast<float*>(take(al((size_t)N * 4)));
+  R.probe = reinterpret_cast<float*>(take(probe_bytes));
   R.thr = reinterpret_cast<double*>(take(al((size_t)n * 8)));
   R.eps = reinterpret_cast<double*>(take(al((size_t)n * 8)));
   R.onsager = reinterpret_cast<double*>(take(al((size_t)n * 8)));
@@ -712,7 +703,10 @@ int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t bl
     launch_one(ctx, block, G, P, s);
     it = 0;
   }
-  const int steps = one_step ? 1 : cfg.iterations;
+  if (damp) {  // the probes depend only on (seed, iteration): all of them in one launch up front
+    st = launch_probes(ctx, cfg.seed, it, steps, N, R.probe, s);
+    if (st) return st;
+  }
   for (int t = 0; t < steps; ++t) {
     // pseudo_data (recon.cpp:75-79): P = A* z + x
     float* pseudo = R.L.pseudo[0];
@@ -736,11 +730,11 @@ int launch_recon(Ctx* ctx, bool one_step, int32_t rows, int32_t cols, int32_t bl
       st = run_denoiser(ctx, cfg, pseudo, xn, R.tmp, (int)G.Hc, (int)G.Wc, n, R.sigma, R.thr, s);
       if (st) return st;
       if (damp) {
-        st = launch_probe(ctx, probe_seed_for(cfg.seed, it), N, R.probe, s);
-        if (!st) st = launch_divergence_prep(ctx, pseudo, R.probe, N, n, R.maxbits, R.perturbed, R.eps, s);
+        const float* probe = R.probe + (int64_t)t * N;
+        st = launch_divergence_prep(ctx, pseudo, probe, N, n, R.maxbits, R.perturbed, R.eps, s);
         if (!st) st = run_denoiser(ctx, cfg, R.perturbed, R.moved, R.tmp, (int)G.Hc, (int)G.Wc, n, R.sigma, R.thr, s);
         if (!st)
-          st = launch_damp_onsager(ctx, R.probe, R.moved, xn, N, n, R.eps, Mimg,
+          st = launch_damp_onsager(ctx, probe, R.moved, xn, N, n, R.eps, Mimg,
                                    cfg.method == ABCS_RECON_DAMPD ? cfg.damping : 1.0, R.partials, R.onsager, s);
         if (st) return st;
         onsager_img = R.onsager;

@@ -105,6 +105,8 @@ int launch_amp_onsager(Ctx* ctx, const unsigned long long* active, int n, const 
 int launch_blur(Ctx* ctx, const float* in, float* tmp, float* out, int H, int W, int n, const double* sigma_dev,
                 double scale, int rmax, double* wscratch, int* rscratch, cudaStream_t s);
 int launch_probe(Ctx* ctx, uint64_t seed, int64_t N, float* probe, cudaStream_t s);
+// the probes of iterations it0 .. it0 + count - 1 (seeds as probe_seed_for) at probes + k * N
+int launch_probes(Ctx* ctx, uint64_t seed, int it0, int count, int64_t N, float* probes, cudaStream_t s);
 int launch_divergence_prep(Ctx* ctx, const float* pseudo, const float* probe, int64_t N, int n, unsigned* maxbits,
                            float* perturbed, double* eps, cudaStream_t s);
 int launch_damp_onsager(Ctx* ctx, const float* probe, const float* moved, const float* base, int64_t N, int n,

@@ -64,12 +64,31 @@ __global__ void absmax_kernel(const float* __restrict__ p, int64_t N, unsigned* 
   if ((threadIdx.x & 31) == 0) atomicMax(maxbits + img, m);
 }
 
-// std::mt19937_64 (seed) -> probe[i] = (out_i & 1) ? +1 : -1 for i < N. One CTA of 320 threads.
-__global__ void __launch_bounds__(320) mt19937_64_probe_kernel(uint64_t seed, int64_t N, float* __restrict__ probe) {
+// splitmix-style probe seed of an iteration (recon.cpp:95-105)
+__device__ __forceinline__ uint64_t probe_seed_dev(uint64_t seed, int iteration) {
+  uint64_t v = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(iteration + 1);
+  v ^= v >> 30;
+  v *= 0xBF58476D1CE4E5B9ull;
+  v ^= v >> 27;
+  v *= 0x94D049BB133111EBull;
+  v ^= v >> 31;
+  return v;
+}
+
+// std::mt19937_64 (seed) -> probe[i] = (out_i & 1) ? +1 : -1 for i < N. One CTA of 320 threads
+// per probe: with it0 >= 0, CTA b writes the probe of iteration it0 + b (seed derived from
+// `seed` as the reference does per damp_step) at probe + b * N, so a whole reconstruction's
+// probes come from one launch; with it0 < 0 one CTA uses `seed` itself.
+__global__ void __launch_bounds__(320)
+mt19937_64_probe_kernel(uint64_t seed, int it0, int64_t N, float* __restrict__ probe) {
   constexpr int kN = 312, kM = 156;
   constexpr uint64_t kA = 0xB5026F5AA96619E9ull, kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull;
   __shared__ uint64_t mt[kN];
   const int t = threadIdx.x;
+  if (it0 >= 0) {
+    seed = probe_seed_dev(seed, it0 + (int)blockIdx.x);
+    probe += (int64_t)blockIdx.x * N;
+  }
   if (t == 0) {  // seeding is sequential (mt[i] depends on mt[i-1])
     mt[0] = seed;
     for (int i = 1; i < kN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
@@ -250,7 +269,15 @@ int launch_blur(Ctx* ctx, const float* in, float* tmp, float* out, int H, int W,
 
 int launch_probe(Ctx* ctx, uint64_t seed, int64_t N, float* probe, cudaStream_t s) {
   const int kt = ktimer_begin(ctx, s, "mt19937_64_probe");
-  mt19937_64_probe_kernel<<<1, 320, 0, s>>>(seed, N, probe);
+  mt19937_64_probe_kernel<<<1, 320, 0, s>>>(seed, -1, N, probe);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "probe launch");
+}
+
+int launch_probes(Ctx* ctx, uint64_t seed, int it0, int count, int64_t N, float* probes, cudaStream_t s) {
+  const int kt = ktimer_begin(ctx, s, "mt19937_64_probe");
+  mt19937_64_probe_kernel<<<(unsigned)count, 320, 0, s>>>(seed, it0, N, probes);
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "probe launch");
