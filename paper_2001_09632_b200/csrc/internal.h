@@ -143,6 +143,10 @@ struct FusedAlloc {
 };
 bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax);
 // mode 1: DD weights; 2: payload; 3: payload + fused decode
+bool umma16_enabled();
+int launch_sense16_umma(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
+                        int pitch, const uint16_t* counts, const int32_t* offsets, float* payload,
+                        int64_t payload_stride, float* out, int64_t out_stride, int out_pitch, cudaStream_t s);
 int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
                          int pitch, const int* phase1, const double* T, uint32_t* const* weights,
                          uint32_t* const* fix_scratch, cudaStream_t s);

@@ -742,11 +742,17 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
       }
       break;
     case 2:
+      if (umma16_enabled())
+        return launch_sense16_umma(ctx, 2, rows, cols, n, imgs, img_stride, pitch, counts, offsets, payload,
+                                   payload_stride, nullptr, 0, 0, s);
       kt = ktimer_begin(ctx, s, "sense16_gather");
       sense16_kernel<false, true, false><<<grid, kM16Threads, 0, s>>>(G, A);
       ktimer_end(ctx, s, kt);
       break;
     case 3:
+      if (umma16_enabled())
+        return launch_sense16_umma(ctx, 3, rows, cols, n, imgs, img_stride, pitch, counts, offsets, payload,
+                                   payload_stride, out, out_stride, out_pitch, s);
       kt = ktimer_begin(ctx, s, "sense16_gather_decode");
       sense16_kernel<false, true, true><<<grid, kM16Threads, 0, s>>>(G, A);
       ktimer_end(ctx, s, kt);
@@ -823,6 +829,9 @@ int launch_decode16(Ctx* ctx, int rows, int cols, int n, const uint16_t* counts,
   const Grid16 G = make_grid16(rows, cols, n);
   const uint32_t total = G.nb * (uint32_t)n;
   if (total == 0) return ABCS_OK;
+  if (umma16_enabled())
+    return launch_sense16_umma(ctx, 4, rows, cols, n, nullptr, 0, 0, counts, offsets, const_cast<float*>(payload),
+                               payload_stride, out, out_stride, out_pitch, s);
   const int kt = ktimer_begin(ctx, s, "decode16");
   decode16_kernel<<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, total, counts, offsets, payload,
                                                                       payload_stride, out, out_stride, out_pitch);

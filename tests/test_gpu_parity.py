@@ -318,6 +318,33 @@ def test_sense_decode_sweep_reference_counts(p, torch, checker):
             assert_sense_equal(b, i, checker.sense(imgs[i], 16, num, den, 2), 16)
 
 
+@pytest.mark.parametrize("H,W,num,den,algo", [(512, 512, 3, 10, 2), (480, 1000, 1, 4, 1), (256, 256, 1, 2, 0)])
+def test_umma_path_parity(p, torch, checker, H, W, num, den, algo):
+    """The opt-in tcgen05 (UMMA/TMEM) gather + decode path (ABCS_UMMA=1): counts unchanged,
+    payload and pixels within the parity bars of the reference, fused decode == decode of its
+    payload, and within 2e-4 of the mma.sync path."""
+    imgs_np = synth(H, W, n=3, seed=H + W + algo)
+    imgs = torch.from_numpy(imgs_np).cuda()
+    cfg = p.SensingConfig(16, num, den, p.Algorithm(algo))
+    base_b, base_x = p.sense_decode_batch(imgs, cfg)
+    try:
+        os.environ["ABCS_UMMA"] = "1"
+        b, x = p.sense_decode_batch(imgs, cfg)
+        g = p.sense_batch(imgs, cfg)
+        d = p.decode_batch(b)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("ABCS_UMMA", None)
+    assert torch.equal(b.counts.view(torch.int16), base_b.counts.view(torch.int16))
+    assert torch.equal(g.payload, b.payload) and torch.equal(d, x)
+    assert float((x - base_x).abs().max()) <= 2e-4
+    for i in range(3):
+        want = checker.sense(imgs_np[i], 16, num, den, algo)
+        ref = checker.decode(b.plan.rows, b.plan.cols, 16, want["counts"], want["coeffs"])
+        assert np.max(np.abs(x[i].cpu().numpy() - ref)) <= PIXEL_TOL
+        assert np.max(np.abs(b.payload[i].cpu().numpy() - want["coeffs"])) <= 1e-2
+
+
 def test_decode_format_errors(p):
     ms = p.MeasurementSet(32, 32, 16, p.Algorithm.ZZ, 1, 4, 0.0, np.array([3, 3, 3, 3], np.uint16),
                           np.zeros(11, np.float32))
