@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 #include <cstdlib>
+#include <type_traits>
 
 #include "alloc_keys.h"
 #include "common.cuh"
@@ -516,7 +517,9 @@ size_t class_smem_bytes(int wmax, int n_blocks, int cs, bool arrays_in_smem) {
   return b;
 }
 
-template <bool kSmemArrays>
+// kSmemArrays: weights and allocations in shared memory; else weights in global scratch and
+// allocations in shared memory as u8 (kAv8, caps <= 255) or in global scratch as u16.
+template <bool kSmemArrays, bool kAv8 = false>
 __global__ void __launch_bounds__(kClassThreads)
 alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64_t budget, int cap, int base,
                    uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status,
@@ -548,18 +551,21 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
   p += ncls_cap;
   const int v = blockIdx.x / cs, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = cluster_lo(nb, cs, rk), nbl = cluster_lo(nb, cs, rk + 1) - lo;
-  Arr<uint16_t> wv, av;  // weight and allocation per block
+  using AvT = typename std::conditional<kAv8, uint8_t, uint16_t>::type;
+  Arr<uint16_t> wv;  // weight and allocation per block
+  Arr<AvT> av;
   // per-block state laid out thread-strided (thread t's k-th block at k * kClassThreads + t) so
   // the warps' accesses coalesce while each thread still walks its blocks in index order
   const int span = class_span(nbl);
   if constexpr (kSmemArrays) {
     uint16_t* q = reinterpret_cast<uint16_t*>(dyn + ((p - dyn + 15) & ~15));
     wv.p = q;
-    av.p = q + span;
+    av.p = reinterpret_cast<AvT*>(q + span);
   } else {
     const int span_max = class_span((nb + cs - 1) / cs);
     wv.p = reinterpret_cast<uint16_t*>(gscratch) + (int64_t)blockIdx.x * 2 * span_max;
-    av.p = wv.p + span;
+    if constexpr (kAv8) av.p = reinterpret_cast<AvT*>(dyn + ((p - dyn + 15) & ~15));
+    else av.p = reinterpret_cast<AvT*>(wv.p + span);
   }
   const uint32_t* w = weights + (int64_t)v * nb + lo;
   const int per_b = (nbl + kClassThreads - 1) / kClassThreads;  // contiguous block range per thread
@@ -697,7 +703,7 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
       const long long give = (long long)cwhole[k] + (sel ? 1 : 0);
       const long long room = (long long)cap - av[ph];
       const long long taken = give < room ? give : room;  // sensing.cpp:162-171
-      av[ph] = (uint16_t)(av[ph] + taken);
+      av[ph] = (AvT)(av[ph] + taken);
       taken_sum += (unsigned long long)taken;
       if ((int)av[ph] < cap) still += 1;
     }
@@ -795,7 +801,7 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
   if (!caps && wmax >= 0 && wmax < 65536 && cap <= 65535) {
     static bool attr_set = false;
     if (!attr_set) {
-      for (auto k : {alloc_class_kernel<true>, alloc_class_kernel<false>}) {
+      for (auto k : {alloc_class_kernel<true>, alloc_class_kernel<false>, alloc_class_kernel<false, true>}) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       }
@@ -806,15 +812,19 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
     uint32_t* gscr = reinterpret_cast<uint32_t*>(scratch);  // n_vectors * n_blocks * 2 u16 (+ padding)
     const size_t smem_in = class_smem_bytes(wmax, n_blocks, cs, true);
     const size_t smem_out = class_smem_bytes(wmax, n_blocks, cs, false);
-    bool in_smem;
+    // u8 allocations in shared memory beside global weights (caps <= 255)
+    const size_t smem_av8 = smem_out + (size_t)class_span((n_blocks + cs - 1) / cs) + 16;
+    bool in_smem, av8 = false;
     if (smem_in <= 100 * 1024) in_smem = true;  // keep 2 CTAs (2048 threads) per SM
-    else if (smem_out <= 200 * 1024) in_smem = false;
-    else goto generic;
+    else if (smem_out <= 200 * 1024) {
+      in_smem = false;
+      av8 = cap <= 255 && smem_av8 <= 100 * 1024;
+    } else goto generic;
     {
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3((unsigned)(n_vectors * cs));
       lc.blockDim = dim3(kClassThreads);
-      lc.dynamicSmemBytes = in_smem ? smem_in : smem_out;
+      lc.dynamicSmemBytes = in_smem ? smem_in : av8 ? smem_av8 : smem_out;
       lc.stream = s;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -827,6 +837,8 @@ int launch_allocate(Ctx* ctx, const uint32_t* weights, int32_t n_blocks, int32_t
       const cudaError_t e =
           in_smem ? cudaLaunchKernelEx(&lc, alloc_class_kernel<true>, weights, (int)n_blocks, (int)wmax, budget,
                                        (int)cap, (int)base, counts, offsets, status, gscr)
+          : av8   ? cudaLaunchKernelEx(&lc, alloc_class_kernel<false, true>, weights, (int)n_blocks, (int)wmax,
+                                       budget, (int)cap, (int)base, counts, offsets, status, gscr)
                   : cudaLaunchKernelEx(&lc, alloc_class_kernel<false>, weights, (int)n_blocks, (int)wmax, budget,
                                        (int)cap, (int)base, counts, offsets, status, gscr);
       ktimer_end(ctx, s, kt);
