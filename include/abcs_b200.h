@@ -433,6 +433,14 @@ int abcs_synth_generate(abcs_ctx* ctx, const abcs_synth_spec* spec, int64_t firs
  * f32 host pixels out (cropped), with H2D / kernels / D2H overlapped in chunks
  * on the ctx's streams. h_images/h_out should be pinned for full PCIe rate.
  * Optional host outputs: counts (n*n_blocks) and payload (n*K). Blocks until done. */
+/* The subrate sweep end to end from host buffers: each chunk of images is uploaded once and
+ * sensed + decoded under every plan (abcs_sense_decode_sweep_batch), and each plan's decoded
+ * pixels go to h_out[j] (HOST array of n_plans pinned host pointers), chunks pipelined over
+ * the ctx's streams as abcs_sense_decode_host. Plans share the image size. */
+int abcs_sense_decode_sweep_host(abcs_ctx* ctx, const abcs_sense_plan* plans, int32_t n_plans,
+                                 const uint8_t* h_images, int32_t n_images, float* const* h_out,
+                                 int32_t chunk_images);
+
 int abcs_sense_decode_host(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* h_images,
                            int32_t n_images, float* h_out, uint16_t* h_counts, float* h_payload,
                            int32_t chunk_images);

@@ -1026,6 +1026,108 @@ int abcs_synth_generate(abcs_ctx* c, const abcs_synth_spec* spec, int64_t first_
 // stream owns one slot of device buffers, so chunk i's copies overlap the other
 // streams' kernels. Inputs/outputs are host buffers (pinned for full PCIe
 // rate); the slot buffers are cached in the ctx across calls.
+int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
+                                 int32_t n, float* const* h_out, int32_t chunk) {
+  CHECK_CTX(c);
+  if (!plans || n_plans < 1 || n_plans > 4 || n < 0 || (n > 0 && (!h_images || !h_out)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int j = 0; j < n_plans; ++j) {
+    if (!block_supported(plans[j].block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+    if (plans[j].height != plans[0].height || plans[j].width != plans[0].width || !h_out[j])
+      return set_error(ABCS_ERR_INVALID_ARGUMENT, "sweep plans must share the image size");
+  }
+  if (n == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  if (chunk <= 0) chunk = 16;
+  if (chunk > n) chunk = n;
+  constexpr int kSlots = 3;
+  const abcs_sense_plan& p0 = plans[0];
+  const int64_t px_in = (int64_t)p0.height * p0.width;
+  // per slot: the images once; per plan counts, offsets, payload, side, pixels; the sweep scratch
+  size_t b_plan[4], per_slot = align_up(chunk * px_in, 256);
+  int64_t px_out[4];
+  for (int j = 0; j < n_plans; ++j) {
+    const abcs_sense_plan& q = plans[j];
+    px_out[j] = (int64_t)q.rows * q.block * q.cols * q.block;
+    b_plan[j] = align_up(chunk * q.n_blocks * 2, 256) + align_up(chunk * q.n_blocks * 4, 256) +
+                align_up(chunk * q.coeffs_per_image * 4 + 4, 256) + align_up(chunk * q.side_per_image * 4 + 4, 256) +
+                align_up(chunk * px_out[j] * 4, 256);
+    per_slot += b_plan[j];
+  }
+  const bool shared = sweep_shared(ctx, plans, n_plans, chunk);
+  size_t b_scr = 0;
+  if (shared) {
+    b_scr = align_up(sweep_scratch_bytes(plans, n_plans, chunk, nullptr), 256);
+  } else {
+    for (int j = 0; j < n_plans; ++j) b_scr = std::max(b_scr, align_up(sense_scratch_bytes(&plans[j], chunk, true), 256));
+  }
+  per_slot += b_scr;
+  if (per_slot * kSlots > ctx->pipe_bytes) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && ctx->pipe_buf) e = cudaFree(ctx->pipe_buf);
+    if (e != cudaSuccess) return cuda_status(e, "pipeline realloc");
+    ctx->pipe_buf = nullptr;
+    ctx->pipe_bytes = 0;
+    e = cudaMalloc(&ctx->pipe_buf, per_slot * kSlots);
+    if (e != cudaSuccess) return cuda_status(e, "pipeline alloc");
+    ctx->pipe_bytes = per_slot * kSlots;
+  }
+  const int saved_streams = ctx->pipe_streams;
+  ctx->pipe_streams = 1;  // each slot's sweep runs serialised on its own stream; the slots overlap
+  int st = ABCS_OK;
+  const int nchunks = (n + chunk - 1) / chunk;
+  for (int ci = 0; ci < nchunks && st == ABCS_OK; ++ci) {
+    const int k = ci % kSlots;
+    char* base = static_cast<char*>(ctx->pipe_buf) + per_slot * k;
+    uint8_t* img = reinterpret_cast<uint8_t*>(base);
+    char* q = base + align_up(chunk * px_in, 256);
+    uint16_t* counts[4];
+    int32_t* offsets[4];
+    float *payload[4], *side[4], *out[4];
+    for (int j = 0; j < n_plans; ++j) {
+      const abcs_sense_plan& pl = plans[j];
+      counts[j] = reinterpret_cast<uint16_t*>(q);
+      q += align_up(chunk * pl.n_blocks * 2, 256);
+      offsets[j] = reinterpret_cast<int32_t*>(q);
+      q += align_up(chunk * pl.n_blocks * 4, 256);
+      payload[j] = reinterpret_cast<float*>(q);
+      q += align_up(chunk * pl.coeffs_per_image * 4 + 4, 256);
+      side[j] = reinterpret_cast<float*>(q);
+      q += align_up(chunk * pl.side_per_image * 4 + 4, 256);
+      out[j] = reinterpret_cast<float*>(q);
+      q += align_up(chunk * px_out[j] * 4, 256);
+    }
+    char* scr = q;
+    const int first = ci * chunk;
+    const int cnt = std::min(chunk, n - first);
+    cudaStream_t s = ctx->pipe[k];
+    cudaError_t e = cudaMemcpyAsync(img, h_images + first * px_in, cnt * px_in, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      st = cuda_status(e, "h2d");
+      break;
+    }
+    if (shared) {
+      st = sweep_impl(ctx, plans, n_plans, img, px_in, p0.width, cnt, 0, counts, offsets, payload, out,
+                      px_out[0], plans[0].cols * plans[0].block, scr, s, k);
+    } else {
+      for (int j = 0; j < n_plans && st == ABCS_OK; ++j)
+        st = sense_impl(ctx, &plans[j], img, px_in, p0.width, cnt, counts[j], offsets[j], payload[j], side[j], scr, s,
+                        out[j], px_out[j], plans[j].cols * plans[j].block);
+    }
+    if (st) break;
+    for (int j = 0; j < n_plans && e == cudaSuccess; ++j)
+      e = cudaMemcpyAsync(h_out[j] + first * px_out[j], out[j], cnt * px_out[j] * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) st = cuda_status(e, "d2h");
+  }
+  for (auto& s : ctx->pipe) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (st == ABCS_OK && e != cudaSuccess) st = cuda_status(e, "pipeline sync");
+  }
+  ctx->pipe_streams = saved_streams;
+  return st;
+}
+
 int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* h_images, int32_t n, float* h_out,
                            uint16_t* h_counts, float* h_payload, int32_t chunk) {
   CHECK_CTX(c);

@@ -309,6 +309,23 @@ def test_sense_decode_sweep_equals_separate_calls(p, torch, n, cfgs):
         assert torch.equal(x, rx)
 
 
+def test_sense_decode_sweep_host(p, torch):
+    """abcs_sense_decode_sweep_host (chunks uploaded once, every plan decoded back to host
+    buffers) gives the device sweep's pixels."""
+    import ctypes as C
+    n = 150
+    imgs = synth(512, 512, n=n, seed=31)
+    cfgs = [p.SensingConfig(16, num, den, p.Algorithm.DD) for num, den in ((1, 10), (3, 10), (1, 2))]
+    want = p.sense_decode_sweep(torch.from_numpy(imgs).cuda(), cfgs)
+    plans = (p._lib.SensePlanC * 3)(*[p.sense_plan(c, 512, 512) for c in cfgs])
+    outs = [np.empty((n, 512, 512), np.float32) for _ in cfgs]
+    arr = (C.c_void_p * 3)(*[o.ctypes.data for o in outs])
+    st = p._lib.load().abcs_sense_decode_sweep_host(p.Context.get().handle, plans, 3, imgs.ctypes.data, n, arr, 64)
+    assert st == 0, p._lib.last_error()
+    for (b, x), o in zip(want, outs):
+        assert np.array_equal(o, x.cpu().numpy())
+
+
 def test_sense_decode_sweep_reference_counts(p, torch, checker):
     imgs = synth(512, 512, n=2, seed=5)
     cs = [p.SensingConfig(16, 1, 10, p.Algorithm.DD), p.SensingConfig(16, 1, 2, p.Algorithm.DD)]
