@@ -106,7 +106,10 @@ constexpr DenoisePairs make_denoise_pairs() {
 __constant__ DenoisePairs kDenoisePairs = make_denoise_pairs();
 
 // One tile pair of phase PH (PH = 2 PA + PB) per warp step.
-template <int PH, bool kInterior>
+// kDcSkip: a tile pair whose AC coefficients all threshold to zero takes its DC / 8 directly
+// (the inverse of a DC-only block) instead of the inverse transform; used by the IDA step, not by
+// the standalone denoiser that DAMP's Monte-Carlo divergence differentiates.
+template <int PH, bool kInterior, bool kDcSkip>
 __device__ __forceinline__ void denoise_pair(const float* in, float* acc, const Frag8& f, int lane_off, int R0, int C0,
                                              int H, int W, float thr, float thr_dc, int p) {
   const uint2 e = kDenoisePairs.e[PH][p];
@@ -124,7 +127,14 @@ __device__ __forceinline__ void denoise_pair(const float* in, float* acc, const 
   Y[1] = soft(Y[1], thr);
   Y[2] = soft(Y[2], thr_dc);
   Y[3] = soft(Y[3], thr);
-  dct8x2_inv_from_yt(f, Y, X);
+  const bool ac = !kDcSkip || Y[1] != 0.f || Y[3] != 0.f || (thr_dc != 0.f && (Y[0] != 0.f || Y[2] != 0.f));
+  if (!kDcSkip || __any_sync(0xffffffffu, ac)) {
+    dct8x2_inv_from_yt(f, Y, X);
+  } else {  // every AC coefficient of both tiles thresholded away: each tile is its DC / 8
+    const float d1 = __shfl_sync(0xffffffffu, Y[0], 0) * 0.125f, d2 = __shfl_sync(0xffffffffu, Y[2], 0) * 0.125f;
+    X[0] = X[1] = d1;
+    X[2] = X[3] = d2;
+  }
   if (v1) {
     float2* d = reinterpret_cast<float2*>(acc + o1);
     *d = fadd2(*d, make_float2(X[0], X[1]));
@@ -135,7 +145,7 @@ __device__ __forceinline__ void denoise_pair(const float* in, float* acc, const 
   }
 }
 
-template <int PA, int PB, bool kInterior>
+template <int PA, int PB, bool kInterior, bool kDcSkip>
 __device__ __forceinline__ void denoise_phase(const float* in, float* acc, const Frag8& f, int R0, int C0, int H, int W,
                                               float thr, float thr_dc) {
   constexpr int NA = PA ? 8 : 9, NB = PB ? 8 : 9, NPAIR = (NA * NB + 1) / 2;
@@ -144,21 +154,22 @@ __device__ __forceinline__ void denoise_phase(const float* in, float* acc, const
   const int lane_off = (lane >> 2) * kMP + 2 * (lane & 3);
 #pragma unroll 1
   for (int p = warp; p < NPAIR; p += kMWarps)  // (two pairs per warp in flight measured slower: registers)
-    denoise_pair<2 * PA + PB, kInterior>(in, acc, f, lane_off, R0, C0, H, W, thr, thr_dc, p);
+    denoise_pair<2 * PA + PB, kInterior, kDcSkip>(in, acc, f, lane_off, R0, C0, H, W, thr, thr_dc, p);
   __syncthreads();
 }
 
-template <bool kInterior>
+template <bool kInterior, bool kDcSkip>
 __device__ __forceinline__ void denoise_phases(const float* in, float* acc, const Frag8& f, int R0, int C0, int H,
                                                int W, float thr, float thr_dc) {
-  denoise_phase<0, 0, kInterior>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<0, 1, kInterior>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<1, 0, kInterior>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<1, 1, kInterior>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  denoise_phase<0, 0, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  denoise_phase<0, 1, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  denoise_phase<1, 0, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  denoise_phase<1, 1, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
 }
 
 // dct_soft_threshold of the window into acc, normalised on the region (denoise.cpp:90).
 // Expects the window loaded; ends with __syncthreads.
+template <bool kDcSkip>
 __device__ void denoise_region_mma(const float* in, float* acc, int R0, int C0, int H, int W, float thr) {
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kMIn * kMP / 4; i += kMThreads) reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -167,8 +178,10 @@ __device__ void denoise_region_mma(const float* in, float* acc, int R0, int C0, 
   const float thr_dc = lane == 0 ? 0.f : thr;
   cp_async_wait_all();
   __syncthreads();
-  if (R0 >= 4 && C0 >= 4 && R0 + kMR + 4 <= H && C0 + kMR + 4 <= W) denoise_phases<true>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  else denoise_phases<false>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  if (R0 >= 4 && C0 >= 4 && R0 + kMR + 4 <= H && C0 + kMR + 4 <= W)
+    denoise_phases<true, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
+  else
+    denoise_phases<false, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
   // weights: valid tile origins covering the pixel per axis (1 or 2 each) -> exact power-of-two scale;
   // the 4 pixels of a float4 share their 4-aligned column group
   for (int i = tid; i < kMR * kMR / 4; i += kMThreads) {
@@ -532,7 +545,7 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
     }
     __syncthreads();
   } else {
-    denoise_region_mma(s.in, s.acc, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
+    denoise_region_mma<true>(s.in, s.acc, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
   if (B == 16) block_phase16(P, img, R0, C0, s, S);
@@ -549,7 +562,7 @@ denoise_mma_kernel(const float* __restrict__ field, int H, int W, int64_t stride
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / regions_x) * kMR, C0 = (region % regions_x) * kMR;
   load_window<kVec>(field + (int64_t)img * stride, W, R0, C0, H, W, s.in);
-  denoise_region_mma(s.in, s.acc, R0, C0, H, W, (float)thr[img]);
+  denoise_region_mma<false>(s.in, s.acc, R0, C0, H, W, (float)thr[img]);
   for (int i = threadIdx.x; i < kMR * kMR; i += kMThreads) {
     const int r = i / kMR, c = i % kMR;
     if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s.acc[kMOff + r * kMP + c];
