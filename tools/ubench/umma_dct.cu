@@ -205,7 +205,8 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(umma_dct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = std::min(n_strips, sms * 8);
+  const int per_sm = argc > 3 ? atoi(argv[3]) : 8;  // CTAs per SM (1: the chain latency alone)
+  const int grid = std::min(n_strips, sms * per_sm);
   umma_dct_kernel<<<grid, 128, smem>>>(d_img, W, n_strips, d_basis, d_out, 1);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -235,7 +236,8 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(z);
   float ms;
   cudaEventElapsedTime(&ms, a, z);
-  printf("%d strips x %d reps: %.3f ms -> %.1f M blocks/s (%s)\n", n_strips, reps, ms,
-         (double)n_strips * 8 * reps / ms / 1e3, cudaGetErrorString(cudaGetLastError()));
+  printf("%d strips x %d reps, %d CTAs/SM: %.3f ms -> %.1f M blocks/s, %.2f us per strip per CTA (%s)\n", n_strips,
+         reps, per_sm, ms, (double)n_strips * 8 * reps / ms / 1e3, ms * 1e3 * grid / ((double)n_strips * reps),
+         cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
