@@ -413,6 +413,7 @@ def test_ida_golden(p):
 
 
 IDA_CASES = [  # (H, W, B, num, den, algo, iters)
+    (512, 512, 16, 3, 10, 1, 10),    # cfg4 (full image size and iteration count)
     (128, 128, 16, 3, 10, 1, 10),    # cfg4 shape
     (256, 256, 16, 1, 4, 2, 5),      # cfg5 shape
     (96, 160, 8, 1, 5, 1, 3),        # B = 8
