@@ -341,7 +341,9 @@ def run_ours(args, world, rank, local):
     Ks = [pl.coeffs_per_image for pl in plans]
     nB = plans[0].n_blocks
     alg_bytes = {  # per step (all subrates)
-        "sense16_gather_decode": sum(n * (N + 4 * K + 6 * nB + 4 * N) for K in Ks),  # u8 in, payload+counts/offsets, f32 out
+        # u8 in (once per step for the sweep's single multi-plan pass), payload+counts/offsets, f32 out
+        "sense16_gather_decode": (0 if args.independent else -(nsub - 1) * n * N)
+        + sum(n * (N + 4 * K + 6 * nB + 4 * N) for K in Ks),
         "sense16_weights": nsub * n * (N + 4 * nB),                                    # u8 in, n_i out
         "sense16_weights_sweep": n * (N + nsub * 4 * nB),                              # u8 in once, n_i per subrate
         "alloc_cta": nsub * n * (4 * nB + 6 * nB),                                     # n_i in, counts+offsets out

@@ -147,6 +147,10 @@ bool umma16_enabled();
 int launch_sense16_umma(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
                         int pitch, const uint16_t* counts, const int32_t* offsets, float* payload,
                         int64_t payload_stride, float* out, int64_t out_stride, int out_pitch, cudaStream_t s);
+int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
+                         int pitch, const uint16_t* const* counts, const int32_t* const* offsets,
+                         float* const* payload, const int64_t* payload_stride, float* const* out, int64_t out_stride,
+                         int out_pitch, cudaStream_t s);
 int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
                          int pitch, const int* phase1, const double* T, uint32_t* const* weights,
                          uint32_t* const* fix_scratch, cudaStream_t s);

@@ -763,6 +763,143 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
   return cuda_status(cudaGetLastError(), "sense16 launch");
 }
 
+// The sweep's payload passes in one: each block's forward transform (and its u8 read) is
+// computed once and serves every plan (its zigzag prefix to that plan's payload, its masked
+// inverse to that plan's decoded image). Per plan the arithmetic is sense16_kernel<0,1,1>'s, so
+// the outputs are bit-identical to the per-plan launches.
+struct MultiArgs {
+  const uint8_t* imgs;
+  int64_t img_stride;
+  int pitch;
+  bool aligned;
+  int np;
+  const uint16_t* counts[kMaxSweep];
+  const int32_t* offsets[kMaxSweep];
+  float* payload[kMaxSweep];
+  int64_t payload_stride[kMaxSweep];
+  float* out[kMaxSweep];
+  int64_t out_stride;
+  int out_pitch;
+};
+
+__global__ void __launch_bounds__(kM16Threads, 3) sense16_multi_kernel(Grid16 G, MultiArgs A) {
+  __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
+  constexpr int kWbuf = 256;
+  __shared__ float s_buf[kM16Warps][2][kWbuf];
+  Frag16 f;
+  load_frag16(f);
+  uint32_t rank_d[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* st = s_stage[warp];
+  float* zb0 = &s_buf[warp][0][0];
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < G.total_runs; r += nwarps) {
+    uint32_t img;
+    int br, bcf, nblk;
+    run_pos(G, r, img, br, bcf, nblk);
+    const uint32_t bidx_first = img * G.nb + (uint32_t)(br * G.cols + bcf);
+    int my_cnt[kMaxSweep], my_off[kMaxSweep];
+#pragma unroll
+    for (int j = 0; j < kMaxSweep; ++j) {
+      my_cnt[j] = 0;
+      my_off[j] = 0;
+      if (j < A.np && lane < nblk) {
+        my_cnt[j] = A.counts[j][bidx_first + lane];
+        my_off[j] = A.offsets[j][bidx_first + lane];
+      }
+    }
+    uint4 nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bcf, A.aligned);
+    for (int p = 0; 2 * p < nblk; ++p) {
+      const int bc0 = bcf + 2 * p;
+      const bool two = 2 * p + 1 < nblk;
+      __syncwarp();
+      reinterpret_cast<uint4*>(st)[lane] = interleave_row16(nxt);
+      __syncwarp();
+      if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
+      uint32_t bx[2][2][2];
+      u8_bfragT_il(st, bx[0]);
+      u8_bfragT_il(st + 256, bx[1]);
+      int cnt[kMaxSweep][2];
+      bool lo_all = true;
+#pragma unroll
+      for (int j = 0; j < kMaxSweep; ++j) {
+        cnt[j][0] = __shfl_sync(0xffffffffu, my_cnt[j], 2 * p);
+        cnt[j][1] = two ? __shfl_sync(0xffffffffu, my_cnt[j], (2 * p + 1) & 31) : 0;
+        if (j < A.np) lo_all = lo_all && cnt[j][0] <= 36 && cnt[j][1] <= 36;
+      }
+      Acc16 Y[2];
+      if (lo_all) dct16_fwd_exact_x2_lo(f, bx, Y);
+      else dct16_fwd_exact_x2(f, bx, Y);
+      // zigzag-ordered copy of both blocks (every plan's prefix is a prefix of it)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < 2 || !lo_all) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+      __syncwarp();
+#pragma unroll 1
+      for (int j = 0; j < A.np; ++j) {
+        const int32_t o0 = __shfl_sync(0xffffffffu, my_off[j], 2 * p);
+        float* dst = A.payload[j] + (int64_t)img * A.payload_stride[j] + o0;
+        const int c0 = cnt[j][0], c1 = cnt[j][1], total = c0 + c1, skip = kWbuf - c0;
+#pragma unroll 1
+        for (int k = lane; k < total; k += 64) {
+          const int k2 = k + 32;
+          const float v0 = zb0[k < c0 ? k : k + skip];
+          float v1 = 0.f;
+          if (k2 < total) v1 = zb0[k2 < c0 ? k2 : k2 + skip];
+          dst[k] = v0;
+          if (k2 < total) dst[k2] = v1;
+        }
+        const bool lo_j = c0 <= 36 && c1 <= 36;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !two) break;
+          const int cq = q ? c1 : c0;
+          Acc16 Ym;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) Ym.v[s >> 2][s & 3] = (int)rank_d[s] < cq ? Y[q].v[s >> 2][s & 3] : 0.f;
+          const Acc16 X = lo_j ? dct16_inv_from_yt_lo(f, Ym) : dct16_inv_from_yt(f, Ym);
+          store_dfrag(A.out[j] + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
+                      A.out_pitch, X);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
+                         int pitch, const uint16_t* const* counts, const int32_t* const* offsets,
+                         float* const* payload, const int64_t* payload_stride, float* const* out, int64_t out_stride,
+                         int out_pitch, cudaStream_t s) {
+  if (np < 1 || np > kMaxSweep) return set_error(ABCS_ERR_LOGIC, "sense16 multi: 1..4 plans");
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_units == 0) return ABCS_OK;
+  MultiArgs A{};
+  A.imgs = imgs;
+  A.img_stride = img_stride;
+  A.pitch = pitch;
+  A.aligned = ((uintptr_t)imgs % 16 == 0) && (img_stride % 16 == 0) && (pitch % 16 == 0);
+  A.np = np;
+  for (int j = 0; j < np; ++j) {
+    A.counts[j] = counts[j];
+    A.offsets[j] = offsets[j];
+    A.payload[j] = payload[j];
+    A.payload_stride[j] = payload_stride[j];
+    A.out[j] = out[j];
+  }
+  A.out_stride = out_stride;
+  A.out_pitch = out_pitch;
+  const int kt = ktimer_begin(ctx, s, "sense16_gather_decode");
+  sense16_multi_kernel<<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, A);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "sense16 multi launch");
+}
+
 // DD phase 1 of n_sw plans (same geometry, prefixes phase1[j], thresholds T[j]) from one
 // forward transform per block; then the fp64 fixup of each plan's near-threshold list.
 int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
