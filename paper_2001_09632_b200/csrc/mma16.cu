@@ -782,7 +782,7 @@ struct MultiArgs {
   int out_pitch;
 };
 
-__global__ void __launch_bounds__(kM16Threads, 3) sense16_multi_kernel(Grid16 G, MultiArgs A) {
+__global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G, MultiArgs A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
   constexpr int kWbuf = 256;
   __shared__ float s_buf[kM16Warps][2][kWbuf];
@@ -894,7 +894,7 @@ int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint
   A.out_stride = out_stride;
   A.out_pitch = out_pitch;
   const int kt = ktimer_begin(ctx, s, "sense16_gather_decode");
-  sense16_multi_kernel<<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, A);
+  sense16_multi_kernel<<<grid_for(ctx, G.total_runs, 2), kM16Threads, 0, s>>>(G, A);
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "sense16 multi launch");
