@@ -411,6 +411,25 @@ def run_ours(args, world, rank, local):
     h2d = (len(SUBRATES) if args.independent else 1) * n * N
     d2h = len(SUBRATES) * n * N * 4
 
+    # the reference bench's own step (abcs_main.cpp:226-258): sense + decode every image under
+    # every subrate, then psnr/ssim per cell; only the cells (mse, psnr, ssim: f64) come back
+    cells = [torch.empty((nsub, n), dtype=torch.float64, pin_memory=True) for _ in range(3)]
+    cell_times = []
+    for it in range(1 + max(1, min(args.steps, 3))):
+        barrier(world)
+        t0 = time.perf_counter()
+        st = lib.abcs_bench_cells_host(ctx.handle, parr, nsub, h_in.data_ptr(), n, *[c.data_ptr() for c in cells], 64)
+        if st != 0:
+            raise RuntimeError(p._lib.last_error())
+        dt = time.perf_counter() - t0
+        if it > 0:
+            cell_times.append(dt)
+    cells_s = max_over_ranks(float(np.mean(cell_times)), world, dev)
+    e2e_cells = {"value": round(aggregate_rate(px_step, world, cells_s) / 1e6, 1), "unit": "MP/s",
+                 "h2d_bytes_per_step": n * N, "d2h_bytes_per_step": 3 * nsub * n * 8,
+                 "api": "abcs_bench_cells_host (the reference bench step: mse/psnr/ssim cells back, pinned host images in)",
+                 "mean_psnr_db": [round(float(x), 3) for x in cells[1].mean(dim=1)]}
+
     # secondary: cfg4 IDA (64 x 512^2, BBV 0.3, 10 iterations)
     ida = run_ida(p, torch, local, rank, hbm, world, dev)
 
@@ -504,6 +523,7 @@ def run_ours(args, world, rank, local):
                     "d2h_bytes_per_step": d2h,
                     "api": ("abcs_sense_decode_host per subrate" if args.independent else
                             "abcs_sense_decode_sweep_host") + " (pinned host buffers)"},
+            "e2e_bench_cells": e2e_cells,
             "ida": ida,
             "container": container,
             "metrics": metrics,

@@ -441,6 +441,15 @@ int abcs_sense_decode_sweep_host(abcs_ctx* ctx, const abcs_sense_plan* plans, in
                                  const uint8_t* h_images, int32_t n_images, float* const* h_out,
                                  int32_t chunk_images);
 
+/* The reference bench step (tools/abcs_main.cpp:226-258, `abcs bench`) from host buffers:
+ * sense + decode_idct every image under every plan, then mse, psnr and ssim of each decoded
+ * image against the input cropped to the block grid (metrics.cpp:63-125). Only the cells come
+ * back: h_mse/h_psnr/h_ssim (each nullable, not all null) hold n_plans*n_images f64, plan-major
+ * (cell [j*n_images + i]). Chunks pipelined as abcs_sense_decode_sweep_host. */
+int abcs_bench_cells_host(abcs_ctx* ctx, const abcs_sense_plan* plans, int32_t n_plans,
+                          const uint8_t* h_images, int32_t n_images, double* h_mse, double* h_psnr,
+                          double* h_ssim, int32_t chunk_images);
+
 int abcs_sense_decode_host(abcs_ctx* ctx, const abcs_sense_plan* plan, const uint8_t* h_images,
                            int32_t n_images, float* h_out, uint16_t* h_counts, float* h_payload,
                            int32_t chunk_images);

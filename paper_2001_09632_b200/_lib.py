@@ -134,6 +134,7 @@ SIGNATURES = {
     "abcs_synth_generate": (C.c_int, [P, C.POINTER(SynthSpecC), I64, I32, P, I64, P]),
     "abcs_sense_decode_host": (C.c_int, [P, C.POINTER(SensePlanC), P, I32, P, P, P, I32]),
     "abcs_sense_decode_sweep_host": (C.c_int, [P, C.POINTER(SensePlanC), I32, P, I32, P, I32]),
+    "abcs_bench_cells_host": (C.c_int, [P, C.POINTER(SensePlanC), I32, P, I32, P, P, P, I32]),
 }
 
 _lib = None

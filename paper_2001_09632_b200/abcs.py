@@ -457,6 +457,27 @@ def sense_decode_sweep(images, cfgs, outs=None, image_outs=None):
     return list(zip(outs, image_outs))
 
 
+def bench_cells_host(images, cfgs, device=0, chunk=64, ssim=True):
+    """The reference bench step (tools/abcs_main.cpp:226-258) from HOST images: sense + IDCT
+    decode under each config, then mse/psnr/ssim of every decoded image against the input
+    cropped to the block grid (metrics.cpp:63-125). images: (n, H, W) uint8 CPU tensor (pin it
+    for full PCIe rate). Only the cells come back: dict of (len(cfgs), n) float64 tensors."""
+    torch = _torch()
+    if images.dtype != torch.uint8 or images.dim() != 3 or images.is_cuda:
+        raise ValueError("images must be a (n, H, W) uint8 CPU tensor")
+    cfgs = list(cfgs)
+    n, H, W = images.shape
+    plans = [sense_plan(c, H, W) for c in cfgs]
+    m = len(plans)
+    images = images.contiguous()
+    cells = {k: torch.empty((m, n), dtype=torch.float64) for k in (("mse", "psnr", "ssim") if ssim else ("mse", "psnr"))}
+    ctx = Context.get(device)
+    _check(_lib.load().abcs_bench_cells_host(
+        ctx.handle, (SensePlanC * m)(*plans), m, images.data_ptr(), n, cells["mse"].data_ptr(),
+        cells["psnr"].data_ptr(), cells["ssim"].data_ptr() if ssim else None, chunk))
+    return cells
+
+
 def decode_batch(batch: MeasurementBatch, out=None):
     """decode_idct on every set of the batch -> (n, Hc, Wc) float32 CUDA tensor."""
     torch = _torch()

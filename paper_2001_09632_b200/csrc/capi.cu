@@ -1066,23 +1066,17 @@ int abcs_synth_generate(abcs_ctx* c, const abcs_synth_spec* spec, int64_t first_
 // stream owns one slot of device buffers, so chunk i's copies overlap the other
 // streams' kernels. Inputs/outputs are host buffers (pinned for full PCIe
 // rate); the slot buffers are cached in the ctx across calls.
-int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
-                                 int32_t n, float* const* h_out, int32_t chunk) {
-  CHECK_CTX(c);
-  if (!plans || n_plans < 1 || n_plans > 4 || n < 0 || (n > 0 && (!h_images || !h_out)))
-    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
-  for (int j = 0; j < n_plans; ++j) {
-    if (!block_supported(plans[j].block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
-    if (plans[j].height != plans[0].height || plans[j].width != plans[0].width || !h_out[j])
-      return set_error(ABCS_ERR_INVALID_ARGUMENT, "sweep plans must share the image size");
-  }
+// The host-buffer sweep. h_out (per plan decoded pixels) and/or h_cells (mse, psnr, ssim per
+// plan and image: the bench cells of abcs_main.cpp:226-258) come back to the host.
+static int sweep_host_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
+                           int32_t n, float* const* h_out, double* const* h_cells, int32_t chunk) {
   if (n == 0) return ABCS_OK;
-  Ctx* ctx = reinterpret_cast<Ctx*>(c);
   cudaSetDevice(ctx->device);
   if (chunk <= 0) chunk = 16;
   if (chunk > n) chunk = n;
   constexpr int kSlots = 3;
   const abcs_sense_plan& p0 = plans[0];
+  const bool want_px = h_out != nullptr, want_cells = h_cells != nullptr;
   const int64_t px_in = (int64_t)p0.height * p0.width;
   // per slot: the images once; per plan counts, offsets, payload, side, pixels; the sweep scratch
   size_t b_plan[4], per_slot = align_up(chunk * px_in, 256);
@@ -1095,6 +1089,15 @@ int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int3
                 align_up(chunk * px_out[j] * 4, 256);
     per_slot += b_plan[j];
   }
+  // cells plus the metric kernels' partial sums: each slot owns its own (the slots run concurrently)
+  size_t b_mpart = 0;
+  for (int j = 0; j < n_plans && want_cells; ++j) {
+    const int h = plans[j].rows * plans[j].block, w = plans[j].cols * plans[j].block;
+    b_mpart = std::max(b_mpart, align_up(std::max(psnr_scratch_bytes(h, chunk),
+                                                  h_cells[2] ? ssim_scratch_bytes(h, w, chunk) : 0), 256));
+  }
+  const size_t b_cells = want_cells ? align_up(3 * n_plans * chunk * sizeof(double), 256) + b_mpart : 0;
+  per_slot += b_cells;
   const bool shared = sweep_shared(ctx, plans, n_plans, chunk);
   size_t b_scr = 0;
   if (shared) {
@@ -1138,6 +1141,8 @@ int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int3
       out[j] = reinterpret_cast<float*>(q);
       q += align_up(chunk * px_out[j] * 4, 256);
     }
+    double* cells = reinterpret_cast<double*>(q);  // [plan][mse, psnr, ssim][chunk]
+    q += b_cells;
     char* scr = q;
     const int first = ci * chunk;
     const int cnt = std::min(chunk, n - first);
@@ -1156,8 +1161,24 @@ int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int3
                         out[j], px_out[j], plans[j].cols * plans[j].block);
     }
     if (st) break;
-    for (int j = 0; j < n_plans && e == cudaSuccess; ++j)
+    void* mpart = reinterpret_cast<char*>(cells) + align_up(3 * n_plans * chunk * sizeof(double), 256);
+    for (int j = 0; j < n_plans && want_cells && st == ABCS_OK; ++j) {
+      // psnr/ssim against the image cropped to the block grid (abcs_main.cpp:230, 254-255)
+      const abcs_sense_plan& pl = plans[j];
+      const int h = pl.rows * pl.block, w = pl.cols * pl.block;
+      double* cj = cells + 3 * j * chunk;
+      st = launch_psnr(ctx, img, px_in, p0.width, out[j], px_out[j], w, h, w, cnt, cj + chunk, s, cj, mpart);
+      if (st == ABCS_OK && h_cells[2])
+        st = launch_ssim(ctx, img, px_in, p0.width, out[j], px_out[j], w, h, w, cnt, cj + 2 * chunk, s, mpart);
+    }
+    if (st) break;
+    for (int j = 0; j < n_plans && want_px && e == cudaSuccess; ++j)
       e = cudaMemcpyAsync(h_out[j] + first * px_out[j], out[j], cnt * px_out[j] * 4, cudaMemcpyDeviceToHost, s);
+    for (int j = 0; j < n_plans && want_cells && e == cudaSuccess; ++j)
+      for (int m = 0; m < 3 && e == cudaSuccess; ++m)
+        if (h_cells[m])
+          e = cudaMemcpyAsync(h_cells[m] + (int64_t)j * n + first, cells + (3 * j + m) * chunk, cnt * sizeof(double),
+                              cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) st = cuda_status(e, "d2h");
   }
   for (auto& s : ctx->pipe) {
@@ -1166,6 +1187,38 @@ int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int3
   }
   ctx->pipe_streams = saved_streams;
   return st;
+}
+
+static int sweep_host_check(const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images, int32_t n,
+                            bool have_out) {
+  if (!plans || n_plans < 1 || n_plans > 4 || n < 0 || (n > 0 && (!h_images || !have_out)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int j = 0; j < n_plans; ++j) {
+    if (!block_supported(plans[j].block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");
+    if (plans[j].height != plans[0].height || plans[j].width != plans[0].width)
+      return set_error(ABCS_ERR_INVALID_ARGUMENT, "sweep plans must share the image size");
+  }
+  return ABCS_OK;
+}
+
+int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
+                                 int32_t n, float* const* h_out, int32_t chunk) {
+  CHECK_CTX(c);
+  if (int st = sweep_host_check(plans, n_plans, h_images, n, h_out != nullptr)) return st;
+  for (int j = 0; j < n_plans && n > 0; ++j)
+    if (!h_out[j]) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null output for a plan");
+  return sweep_host_impl(reinterpret_cast<Ctx*>(c), plans, n_plans, h_images, n, h_out, nullptr, chunk);
+}
+
+int abcs_bench_cells_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
+                          int32_t n, double* h_mse, double* h_psnr, double* h_ssim, int32_t chunk) {
+  CHECK_CTX(c);
+  if (int st = sweep_host_check(plans, n_plans, h_images, n, h_mse || h_psnr || h_ssim)) return st;
+  for (int j = 0; j < n_plans && h_ssim; ++j)
+    if (plans[j].rows * plans[j].block < 11 || plans[j].cols * plans[j].block < 11)
+      return set_error(ABCS_ERR_INVALID_ARGUMENT, "ssim: images smaller than the 11x11 window");
+  double* const cells[3] = {h_mse, h_psnr, h_ssim};
+  return sweep_host_impl(reinterpret_cast<Ctx*>(c), plans, n_plans, h_images, n, nullptr, cells, chunk);
 }
 
 int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* h_images, int32_t n, float* h_out,

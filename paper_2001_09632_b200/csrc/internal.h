@@ -89,9 +89,12 @@ struct IdaParams;
 int ida_mma_region();
 void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s);
 int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr);
+                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr,
+                void* scratch = nullptr);
 int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s);
+                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s, void* scratch = nullptr);
+size_t psnr_scratch_bytes(int h, int n);
+size_t ssim_scratch_bytes(int h, int w, int n);
 int launch_threshold_decode(Ctx* ctx, int block, const uint8_t* imgs, int64_t img_stride, int pitch, int rows, int cols,
                             int n, int64_t m_target, bool global, int* counts, double* out, int64_t out_stride,
                             int out_pitch, cudaStream_t s);

@@ -153,12 +153,21 @@ __global__ void ssim_fold_kernel(const double* __restrict__ partials, int tiles,
   ssim[i] = s / windows;
 }
 
-int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s) {
+size_t ssim_scratch_bytes(int h, int w, int n) {
   const int Hv = h - kSsimWin + 1, Wv = w - kSsimWin + 1;
   const int tx = (Wv + kSsimTC - 1) / kSsimTC, ty = (Hv + kSsimTR - 1) / kSsimTR;
-  int st;
-  double* partials = static_cast<double*>(ctx_scratch(ctx, (size_t)n * tx * ty * 8, s, &st));
+  return (size_t)n * tx * ty * 8;
+}
+
+size_t psnr_scratch_bytes(int h, int n) { return (size_t)n * ((h + kMetricRowsPerCta - 1) / kMetricRowsPerCta) * 8; }
+
+int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
+                int img_pitch, int h, int w, int n, double* ssim, cudaStream_t s, void* scratch) {
+  const int Hv = h - kSsimWin + 1, Wv = w - kSsimWin + 1;
+  const int tx = (Wv + kSsimTC - 1) / kSsimTC, ty = (Hv + kSsimTR - 1) / kSsimTR;
+  int st = ABCS_OK;
+  // concurrent callers (the host pipeline's slots) pass their own scratch
+  double* partials = static_cast<double*>(scratch ? scratch : ctx_scratch(ctx, ssim_scratch_bytes(h, w, n), s, &st));
   if (st) return st;
   const SsimKernel kw = ssim_kernel_weights();
   const int kt = ktimer_begin(ctx, s, "ssim");
@@ -177,10 +186,10 @@ int launch_ssim(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch,
 }
 
 int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
-                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse) {
+                int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse, void* scratch) {
   const int parts = (h + kMetricRowsPerCta - 1) / kMetricRowsPerCta;
-  int st;
-  double* partials = static_cast<double*>(ctx_scratch(ctx, (size_t)n * parts * 8, s, &st));
+  int st = ABCS_OK;
+  double* partials = static_cast<double*>(scratch ? scratch : ctx_scratch(ctx, psnr_scratch_bytes(h, n), s, &st));
   if (st) return st;
   for (int done = 0; done < n;) {
     const int cnt = std::min(n - done, 65535);

@@ -326,6 +326,33 @@ def test_sense_decode_sweep_host(p, torch):
         assert np.array_equal(o, x.cpu().numpy())
 
 
+@pytest.mark.parametrize("H,W,n,chunk", [(512, 512, 70, 32), (100, 90, 5, 2)])
+def test_bench_cells_host(p, torch, checker, H, W, n, chunk):
+    """abcs_bench_cells_host (the reference bench step, abcs_main.cpp:226-258, from host
+    buffers): each cell equals quality_batch of the device sweep's decoded image, and the
+    oracle's psnr/ssim of the reference decode within the parity bars."""
+    imgs = synth(H, W, n=n, seed=H + n)
+    cfgs = [p.SensingConfig(16, num, den, p.Algorithm.DD) for num, den in ((1, 10), (3, 10), (1, 2))]
+    t = torch.from_numpy(imgs)
+    cells = p.bench_cells_host(t.pin_memory(), cfgs, chunk=chunk)
+    got = p.sense_decode_sweep(t.cuda(), cfgs)
+    for j, (b, x) in enumerate(got):
+        q = p.quality_batch(t.cuda(), x)
+        for k in ("mse", "psnr", "ssim"):
+            assert torch.equal(cells[k][j], q[k].cpu()), (j, k)
+    Hc, Wc = got[0][1].shape[1:]
+    for i in (0, n - 1):
+        crop = imgs[i, :Hc, :Wc]
+        for j, (num, den) in enumerate(((1, 10), (3, 10), (1, 2))):
+            want = checker.sense(imgs[i], 16, num, den, 2)
+            ref = checker.decode(want["rows"], want["cols"], 16, want["counts"], want["coeffs"])
+            _, ps, ss = checker.quality(crop, ref)
+            assert abs(float(cells["psnr"][j, i]) - ps) <= PSNR_TOL
+            assert abs(float(cells["ssim"][j, i]) - ss) <= 1e-5
+    with pytest.raises(Exception):
+        p.bench_cells_host(t.cuda(), cfgs)
+
+
 def test_sense_decode_sweep_reference_counts(p, torch, checker):
     imgs = synth(512, 512, n=2, seed=5)
     cs = [p.SensingConfig(16, 1, 10, p.Algorithm.DD), p.SensingConfig(16, 1, 2, p.Algorithm.DD)]
