@@ -595,7 +595,7 @@ def metrics_bench(p, torch, refs, dec, hbm):
     return {"workload": f"{n} x 512^2 decoded (DD 3/10) vs sources",
             "mse_psnr_ms": round(ms_p, 4), "mse_psnr_frac": round(5 * px / ms_p / 1e6 / hbm, 4),
             "ssim_ms": round(ms_s, 4), "ssim_mp_s": round(px / ms_s / 1e3, 1),
-            "ssim_note": "fp64 11x11 Gaussian statistics in the reference's operation order (FP64-pipe bound)"}
+            "ssim_note": "fp64 11x11 Gaussian statistics, taps in the reference's order with DFMA (FP64-bound)"}
 
 
 def family_bench(p, torch):
