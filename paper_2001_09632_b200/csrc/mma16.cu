@@ -782,6 +782,10 @@ struct MultiArgs {
   int out_pitch;
 };
 
+__device__ __forceinline__ int pick4(const int (&a)[kMaxSweep], int j) {
+  return j == 0 ? a[0] : j == 1 ? a[1] : j == 2 ? a[2] : a[3];
+}
+
 __global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G, MultiArgs A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
   constexpr int kWbuf = 256;
@@ -821,13 +825,13 @@ __global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G,
       uint32_t bx[2][2][2];
       u8_bfragT_il(st, bx[0]);
       u8_bfragT_il(st + 256, bx[1]);
-      int cnt[kMaxSweep][2];
+      int cnt0[kMaxSweep], cnt1[kMaxSweep];
       bool lo_all = true;
 #pragma unroll
       for (int j = 0; j < kMaxSweep; ++j) {
-        cnt[j][0] = __shfl_sync(0xffffffffu, my_cnt[j], 2 * p);
-        cnt[j][1] = two ? __shfl_sync(0xffffffffu, my_cnt[j], (2 * p + 1) & 31) : 0;
-        if (j < A.np) lo_all = lo_all && cnt[j][0] <= 36 && cnt[j][1] <= 36;
+        cnt0[j] = __shfl_sync(0xffffffffu, my_cnt[j], 2 * p);
+        cnt1[j] = two ? __shfl_sync(0xffffffffu, my_cnt[j], (2 * p + 1) & 31) : 0;
+        if (j < A.np) lo_all = lo_all && cnt0[j] <= 36 && cnt1[j] <= 36;
       }
       Acc16 Y[2];
       if (lo_all) dct16_fwd_exact_x2_lo(f, bx, Y);
@@ -841,9 +845,10 @@ __global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G,
       __syncwarp();
 #pragma unroll 1
       for (int j = 0; j < A.np; ++j) {
-        const int32_t o0 = __shfl_sync(0xffffffffu, my_off[j], 2 * p);
+        // register arrays picked by a select chain: a dynamic index would put them in local memory
+        const int32_t o0 = __shfl_sync(0xffffffffu, pick4(my_off, j), 2 * p);
         float* dst = A.payload[j] + (int64_t)img * A.payload_stride[j] + o0;
-        const int c0 = cnt[j][0], c1 = cnt[j][1], total = c0 + c1, skip = kWbuf - c0;
+        const int c0 = pick4(cnt0, j), c1 = pick4(cnt1, j), total = c0 + c1, skip = kWbuf - c0;
 #pragma unroll 1
         for (int k = lane; k < total; k += 64) {
           const int k2 = k + 32;
