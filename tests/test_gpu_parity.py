@@ -326,7 +326,7 @@ def test_sense_decode_sweep_host(p, torch):
         assert np.array_equal(o, x.cpu().numpy())
 
 
-@pytest.mark.parametrize("H,W,n,chunk", [(512, 512, 70, 32), (100, 90, 5, 2)])
+@pytest.mark.parametrize("H,W,n,chunk", [(512, 512, 70, 32), (256, 256, 96, 4), (100, 90, 5, 2)])
 def test_bench_cells_host(p, torch, checker, H, W, n, chunk):
     """abcs_bench_cells_host (the reference bench step, abcs_main.cpp:226-258, from host
     buffers): each cell equals quality_batch of the device sweep's decoded image, and the
