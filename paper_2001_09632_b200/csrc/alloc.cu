@@ -52,7 +52,6 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
   } tmp;
   __shared__ unsigned int hist[256];
   __shared__ long long sh_ll[4];
-  __shared__ unsigned long long sh_prefix;
   __shared__ int sh_int[4];
 
   const int v = blockIdx.x, tid = threadIdx.x;
