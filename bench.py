@@ -667,6 +667,26 @@ def config_sweep(p, torch, hbm):
     return out
 
 
+# Naive separable-DCT FLOP per pixel per IDA iteration: the 8x8 denoiser
+# at 4x tile overlap (256) plus the B=16 block phase's forward and inverse transforms and the
+# elementwise updates (~138). The kernel runs them on the tensor cores (fp16 hi/lo split), so
+# this is the reference's arithmetic expressed against the fp32 pipe it would otherwise use.
+IDA_NAIVE_FLOP_PER_PX = 394
+
+
+def ida_compute_view(pixels, avg_ms):
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz, src = float(json.load(f)["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
+    except (OSError, KeyError, ValueError):
+        mhz, src = 1965.0, "B200 boost clock (fallback)"
+    peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # fp32 FMA lanes x 2 FLOP x clock
+    ach = pixels * IDA_NAIVE_FLOP_PER_PX / (avg_ms / 1e3) / 1e12
+    return {"bound": "fp32-equivalent arithmetic (kernel is issue-bound)", "naive_flop_per_px": IDA_NAIVE_FLOP_PER_PX,
+            "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+            "peak_source": "148 SMs x 128 fp32 lanes x 2 x " + src}
+
+
 def run_ida(p, torch, local, rank, hbm, world, dev):
     c = CFG4
     spec = p.SynthSpec(c["H"], c["W"], c["ellipses"], c["sigma"], c["seed"])
@@ -706,7 +726,8 @@ def run_ida(p, torch, local, rank, hbm, world, dev):
                      "peak": hbm, "unit": "GB/s", "frac": round(a_k / hbm, 4), "avg_launch_ms": round(avg, 4),
                      "algorithmic_bytes_per_launch": int(per_iter),
                      "traffic": round(tr["dram_bytes_per_image"] * c["n"]) if tr else None,
-                     "share_of_batch": round(total_ms / reps / ms, 4)}
+                     "share_of_batch": round(total_ms / reps / ms, 4),
+                     "compute_view": ida_compute_view(c["n"] * N, avg)}
     return {"metric": "IDA image-iterations/s (cfg4: 64 x 512^2, BBV 0.3, 10 it, dct_threshold)",
             "value": round(world * c["n"] * c["iters"] / (ms / 1e3), 1), "unit": "it/s",
             "mp_it_per_s": round(world * c["n"] * c["iters"] * N / (ms / 1e3) / 1e6, 1),
