@@ -116,8 +116,8 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        if args.impl == "ours":
+        backend = "nccl" if args.impl == "ours" and not args.dry_run else "gloo"
+        if backend == "nccl":
             import torch
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
@@ -186,14 +186,20 @@ def calibrated_count(checker, imgs, threads, cap):
     return min(n, cap)
 
 
-def sample_images(n):
-    import paper_2001_09632_b200 as p
-    return p.synth_images_host(p.SynthSpec(CFG2["H"], CFG2["W"], CFG2["ellipses"], CFG2["sigma"], CFG2["seed"]), 0, n)
+def oracle_module():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as o
+    return o
+
+
+def sample_images(n, c=CFG2, first=0, video=False):
+    """BASELINE inputs for the CPU arms from the oracle library's copy of the seeded generator
+    (oracle/synth_inputs.c): the reference arm never loads the product library."""
+    return oracle_module().synth_images(c["H"], c["W"], c["ellipses"], c["sigma"], c["seed"], first, n, video)
 
 
 def get_checker():
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as o
+    o = oracle_module()
     if o.Reference.available():
         return o.Reference(), "reference"
     return o.CPort(), "port"
@@ -228,6 +234,54 @@ def run_reference(args, world, rank):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+CPU_CONFIGS = [  # (key, H, W, B, num, den, algo(1 BBV, 2 DD), ellipses, sigma, seed, video, ida_iterations)
+    ("cfg1", 256, 256, 16, 1, 4, 1, 20, 5.0, 1, False, 0),
+    ("cfg3", 1080, 1920, 8, 1, 5, 1, 20, 5.0, 3, True, 0),
+    ("cfg4", 512, 512, 16, 3, 10, 1, 20, 5.0, 4, False, 10),
+    ("cfg5", 4096, 4096, 16, 1, 4, 2, 200, 8.0, 5, False, 5),
+]
+
+
+def cpu_config_baselines(threads):
+    """The reference library (oracle/_ref) timed on this host beside every other BASELINE config:
+    sense + decode_idct MP/s, and for cfg4/cfg5 the IDA loop (recon.cpp:225-257) in image-iterations/s.
+    Each phase runs over `threads` images on `threads` host threads (the reference is reentrant);
+    cfg1 is one image on one core, median of 5 (tools/abcs_main.cpp:42-52). cfg5's IDA runs one
+    iteration per image and is extrapolated per iteration as t(Ida, 1) - t(Idct) (the warm-start
+    init is one decode plus one forward, about one Idct reconstruct)."""
+    o = oracle_module()
+    if not o.Reference.available():
+        return {"unavailable": "oracle/_ref not built"}
+    res = {}
+    for key, H, W, B, num, den, algo, ell, sig, seed, video, iters in CPU_CONFIGS:
+        spec = dict(H=H, W=W, ellipses=ell, sigma=sig, seed=seed)
+        if key == "cfg1":
+            imgs = sample_images(1, spec)
+            runs = sorted(sum(o.reference_bench_phases(imgs, B, num, den, algo, 0, 1, 1)) for _ in range(5))
+            t = runs[2]
+            res[key] = {"sense_decode_ms": round(t * 1e3, 3), "MP_s": round(H * W / t / 1e6, 3), "cores": 1,
+                        "sample": "1 image, median of 5 (sense + decode_idct)"}
+            continue
+        n = threads * (4 if key in ("cfg3", "cfg4") else 1)
+        imgs = sample_images(n, spec, video=video)
+        ts, td = o.reference_bench_phases(imgs, B, num, den, algo, 0, 1, threads)
+        row = {"MP_s": round(n * H * W / (ts + td) / 1e6, 3), "sense_s": round(ts, 3), "decode_s": round(td, 3),
+               "cores": threads, "sample": f"{n} images (seed {seed}) over {threads} host threads"}
+        if iters:
+            it_run = iters if key == "cfg4" else 1
+            _, ti = o.reference_bench_phases(imgs, B, num, den, algo, 5, it_run, threads)
+            if key == "cfg4":
+                row["ida_it_s"] = round(n * iters / ti, 2)
+                row["ida_sample"] = f"{n} images x {iters} iterations incl. warm-start init"
+            else:
+                step = max(ti - td, 1e-9)
+                row["ida_it_s"] = round(n / step, 3)
+                row["ida_sample"] = (f"{n} images x 1 iteration; per-iteration time = t(Ida,1) - t(Idct) = "
+                                     f"{step:.2f} s wall (extrapolated to {iters} iterations)")
+        res[key] = row
+    return res
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -487,7 +541,7 @@ def run_ours(args, world, rank, local):
             configs = {"error": repr(e)[:200]}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         checker, kind = get_checker()
         threads = host_cores()
         ns = calibrated_count(checker, imgs[:threads].cpu().numpy(), threads, cap=imgs.shape[0])
@@ -496,12 +550,26 @@ def run_ours(args, world, rank, local):
         cpu = {"value": round(pxs / sec / 1e6, 3), "unit": "MP/s", "cores": threads, "kind": kind,
                "sample": f"{ns} of this rank's cfg2 images x subrates {{0.1,0.3,0.5}} "
                          f"({sec:.2f} s wall, ~{sec * threads:.0f} core-s)"}
+        if kind == "reference":
+            try:
+                cpb = cpu_config_baselines(threads)
+            except Exception as e:
+                cpb = {"error": repr(e)[:200]}
+            cpu["configs"] = cpb
+            if isinstance(configs, dict):  # each config's device row gets the reference beside it
+                for name, row in configs.items():
+                    k = name.split()[0]
+                    if isinstance(row, dict) and k in cpb:
+                        row["cpu_reference"] = cpb[k]
+            if isinstance(ida, dict) and "cfg4" in cpb and "ida_it_s" in cpb["cfg4"]:
+                ida["cpu_reference"] = {"value": cpb["cfg4"]["ida_it_s"], "unit": "it/s", "cores": threads,
+                                        "kind": "reference", "sample": cpb["cfg4"]["ida_sample"]}
 
     if rank == 0:
         line = {
             "metric": "megapixels/s for ABCS sense+reconstruct", "value": round(value, 1), "unit": "MP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp16 hi/lo operands, fp32 accumulate)", "data": "synthetic",
             "config": {"workload": "cfg2: 1024 x 512x512 u8 per GPU, DD-ABCS B=16, subrate sweep {0.1,0.3,0.5}, "
                                    "IDCT reconstruction (BASELINE configs[1])",
                        "global_batch": world * n, "l2": "inputs+outputs >> L2 (no flush needed)",
@@ -737,6 +805,44 @@ def run_ida(p, torch, local, rank, hbm, world, dev):
             "kernel_roofline": step_roof}
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` without torchrun: one process per GPU on this node, RANK / LOCAL_RANK /
+    WORLD_SIZE / MASTER_* set as torch.distributed.run would set them; rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rcs = [pr.wait() for pr in procs]
+    return max(rcs, key=abs)
+
+
+def run_dry(args, world, rank):
+    """--dry-run: the multi-rank plumbing without device work (CPU, gloo): each rank takes its shard
+    of the global image indices, 'times' a stand-in step, and rank 0 prints the aggregate line."""
+    import torch
+    first, n = shard(rank, CFG2["n"])
+    barrier(world)
+    t0 = time.perf_counter()
+    sample_images(1, dict(CFG2, H=64, W=64), first=first)  # a token of per-rank work on its own indices
+    sec = max_over_ranks(time.perf_counter() - t0, world)
+    firsts = [None] * world
+    if world > 1:
+        torch.distributed.all_gather_object(firsts, (first, n))
+    else:
+        firsts = [(first, n)]
+    if rank == 0:
+        px = len(SUBRATES) * n * CFG2["H"] * CFG2["W"]
+        print(json.dumps({"metric": "megapixels/s for ABCS sense+reconstruct", "dry_run": True, "n_gpus": world,
+                          "value": round(aggregate_rate(px, world, sec) / 1e6, 3), "unit": "MP/s",
+                          "shards": firsts, "scaling": "weak"}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -747,9 +853,14 @@ def main():
     ap.add_argument("--no-config-sweep", action="store_true", help="skip the cfg1/3/4/5 device sweep")
     ap.add_argument("--independent", action="store_true",
                     help="time one sense_decode_batch per subrate instead of the sweep call")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (no device work; gloo)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return spawn_ranks(args)
     world, rank, local = dist_setup(args)
     try:
+        if args.dry_run:
+            return run_dry(args, world, rank)
         if args.impl == "reference":
             return run_reference(args, world, rank)
         return run_ours(args, world, rank, local)

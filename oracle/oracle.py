@@ -461,6 +461,38 @@ class Reference:
                                                        iters, threads, None if out is None else out.ctypes.data_as(P)))
 
 
+def synth_images(height, width, ellipses, sigma, seed, first, n, video=False, threads=None):
+    """The BASELINE seeded inputs (csrc/synth_gen.h host path compiled into the oracle library by
+    oracle/synth_inputs.c): the same bytes as the product's generator, without loading it."""
+    lib = _load(PORT_SO)
+    lib.o_synth_images.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_int32,
+                                   C.c_int64, C.c_int32, P, C.c_int32]
+    out = np.empty((n, height, width), dtype=np.uint8)
+    if threads is None:
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    st = lib.o_synth_images(height, width, ellipses, float(sigma), seed, int(bool(video)), first, n,
+                            out.ctypes.data_as(P), threads)
+    if st != 0:
+        raise OracleError(st, "o_synth_images failed")
+    return out
+
+
+def reference_bench_phases(imgs, block, num, den, algo, method, iters, threads):
+    """Wall seconds (sense, reconstruct) of the reference library over a batch on `threads` host
+    threads (ref_bench_phases in ref_capi.cpp). method: 0 Idct, 5 Ida (recon.hpp:15)."""
+    lib = C.CDLL(REF_SO)
+    lib.ref_bench_phases.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, P, P]
+    a = np.ascontiguousarray(imgs, dtype=np.uint8)
+    n, H, W = a.shape
+    ts, tr = C.c_double(0.0), C.c_double(0.0)
+    st = lib.ref_bench_phases(a.ctypes.data_as(P), n, H, W, block, num, den, algo, method, iters, threads,
+                              C.byref(ts), C.byref(tr))
+    if st != 0:
+        raise OracleError(st, "ref_bench_phases failed")
+    return ts.value, tr.value
+
+
 def best_available():
     """The reference library when it was built here, else the C port."""
     return Reference() if Reference.available() else CPort()

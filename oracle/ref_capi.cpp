@@ -8,6 +8,7 @@
 // through ctypes. Nothing here re-implements reference logic; each entry point
 // forwards to the reference API named in its comment.
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -457,6 +458,48 @@ int ref_sense_reconstruct_batch(const uint8_t* imgs, int n, int h, int w, int bl
     for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
     for (auto& th : pool) th.join();
   }
+  return status.load();
+}
+
+// The reference bench's per-cell work (tools/abcs_main.cpp:234-251) split into its two timed
+// phases over a batch: abcs::sense of every image, then abcs::reconstruct of every measurement set
+// (Idct, or Ida with `iters` iterations and the default dct_threshold denoiser, recon.cpp:199-259),
+// each phase spread over `threads` host threads on disjoint images (the reference is reentrant).
+// Wall seconds of each phase are returned; the payloads are not copied out.
+int ref_bench_phases(const uint8_t* imgs, int n, int h, int w, int block, uint32_t num, uint32_t den, int algo,
+                     int method, int iters, int threads, double* sense_sec, double* recon_sec) {
+  std::vector<abcs::MeasurementSet> sets(static_cast<size_t>(n));
+  std::atomic<int> status{OK};
+  const long long hw = static_cast<long long>(h) * w;
+  auto run = [&](auto&& body) {
+    std::atomic<int> next{0};
+    auto worker = [&] {
+      for (;;) {
+        const int i = next.fetch_add(1);
+        if (i >= n || status.load() != OK) return;
+        const int st = guarded([&] { body(i); });
+        if (st != OK) status.store(st);
+      }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    if (threads <= 1) {
+      worker();
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+      for (auto& th : pool) th.join();
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const auto cfg = make_cfg(block, num, den, algo, 0, 0.0);
+  const double ts = run([&](int i) { sets[i] = abcs::sense(to_image(imgs + i * hw, h, w), cfg); });
+  if (status.load() != OK) return status.load();
+  abcs::ReconConfig rc;
+  rc.method = static_cast<abcs::ReconMethod>(method);
+  rc.iterations = iters;
+  const double tr = run([&](int i) { (void)abcs::reconstruct(sets[i], rc); });
+  if (sense_sec) *sense_sec = ts;
+  if (recon_sec) *recon_sec = tr;
   return status.load();
 }
 

@@ -13,7 +13,8 @@
 // reference's long-double `frac` does. A plain rational floor/remainder port
 // disagrees with the reference on ~0.3% of adversarial vectors;
 // this one is checked against the reference on adversarial and realistic
-// vectors by tests/test_alloc_keys.py (host build of this same header).
+// vectors by tests/native/alloc_keys_check.c (host build of this same header, run from
+// tests/test_host_logic.py).
 #pragma once
 #include <stdint.h>
 

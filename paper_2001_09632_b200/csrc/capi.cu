@@ -457,7 +457,7 @@ static int sweep_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, const 
   return ABCS_OK;
 }
 
-// ---- per-kernel timing -----------------------------------------------------------------// ---- per-kernel timing -----------------------------------------------------------------
+// ---- per-kernel timing -----------------------------------------------------------------
 static cudaEvent_t take_event(Ctx* ctx) {
   if (ctx->kpool_used == ctx->kpool.size()) {
     cudaEvent_t e;

@@ -46,6 +46,8 @@ class ShardComm:
         self.dist = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
         self.world = dist.get_world_size(group) if self.dist else 1
         self.rank = dist.get_rank(group) if self.dist else 0
+        if device is None and self.dist and dist.get_backend(group) == "nccl":
+            device = torch.device("cuda", torch.cuda.current_device())  # NCCL collectives need device tensors
         self.device = device
 
     @property

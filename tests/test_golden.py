@@ -46,3 +46,15 @@ def test_recon_case(port):
     assert np.array_equal(tr, z["ida_trace"])
     assert np.array_equal(port.denoise(z["field"], 0.0), z["den0"])
     assert np.array_equal(port.denoise(z["field"], 20.0), z["den20"])
+
+
+def test_oracle_synth_matches_golden_hashes():
+    """The oracle-side input generator (used by bench.py's reference arm, which must not load the
+    product library) produces the pinned bytes."""
+    import hashlib
+    import oracle as o
+    got = {f"{h}x{w}-{e}-{s}-{seed}-{v}": hashlib.sha256(o.synth_images(h, w, e, s, seed, 0, 2, bool(v)).tobytes())
+           .hexdigest() for (h, w, e, s, seed, v) in ((256, 256, 20, 5.0, 1, 0), (64, 64, 200, 8.0, 5, 0),
+                                                      (54, 96, 20, 5.0, 3, 1))}
+    want = dict(line.split() for line in open(os.path.join(G, "synth_hashes.txt")).read().splitlines() if line.strip())
+    assert got == want

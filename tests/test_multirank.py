@@ -56,3 +56,19 @@ def test_two_rank_shards_and_timing(tmp_path):
         assert (first, n) == (r * per_rank, per_rank)
     # whole-job value = units of all ranks / slowest rank's time
     assert bench.aggregate_rate(100.0, world, 1.25) == pytest.approx(160.0)
+
+
+def test_bench_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` without torchrun spawns one process per rank (RANK/WORLD_SIZE set like
+    torch.distributed.run); --dry-run exercises that path over gloo without device work."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=300, env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    assert d["shards"] == [[0, 1024], [1024, 1024]]
