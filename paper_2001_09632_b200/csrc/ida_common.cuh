@@ -49,18 +49,17 @@ struct IdaParams {
 
 // Last CTA of an image folds the region partials (fixed order, so the result
 // is deterministic) into sigma, the trace row and the divergence record.
+// Called by every thread with `mine` written by thread 0 (the only thread that
+// continues): the partial is published with a release RMW on the image's counter,
+// and the CTA whose RMW completes the count acquires every other CTA's partial.
+// No CTA barrier and no sequentially consistent fence: the other threads leave.
 static __device__ void finish_image(const IdaParams& P, int img, int region, const double* mine) {
-  __shared__ bool s_last;
-  if (threadIdx.x == 0) {
-    double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
-    for (int q = 0; q < 4; ++q) part[q] = mine[q];
-    __threadfence();
-    const unsigned prev = atomicAdd(P.counters + img, 1u);
-    s_last = (prev == (unsigned)P.regions_per_img - 1);
-  }
-  __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
-  __threadfence();
+  if (threadIdx.x != 0) return;
+  double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
+  for (int q = 0; q < 4; ++q) part[q] = mine[q];
+  unsigned prev;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(P.counters + img) : "memory");
+  if (prev != (unsigned)P.regions_per_img - 1) return;
   double a[4] = {0.0, 0.0, 0.0, 0.0};
   const volatile double* pp = P.partials + (int64_t)img * P.regions_per_img * 4;
   for (int r = 0; r < P.regions_per_img; ++r)

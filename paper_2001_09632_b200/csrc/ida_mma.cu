@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "ida_common.cuh"
 #include "internal.h"
+#include "dct_pair.cuh"
 #include "mma_dct.cuh"
 
 namespace abcs_b200 {
@@ -38,7 +39,7 @@ struct IdaMmaSmem {
   Frag16Tab f16;          // B = 16 fragments (block phase / init), filled by warp 0 at kernel start
   int meta_cnt[64];       // the region's sensing blocks (row-major): counts and image-relative offsets,
   int meta_off[64];       // fetched at kernel start so the block phase does not wait on them
-  double red[4][kMWarps];
+  double red[4][16];
   unsigned long long bad[2];
   double mine[4];
 };
@@ -57,21 +58,30 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // field[R0-4 .. R0+68) x [C0-4 .. C0+68) -> s.in (zeros outside the image). The vector path
 // only issues async copies; the caller waits (cp_async_wait_all + barrier) before reading.
-template <bool kVec>
+template <bool kVec, int WP = kMP>
 __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t pitch, int R0, int C0, int H, int W,
                                             float* in) {
   if (kVec) {  // W % 4 == 0, 16-byte aligned rows: every float4 is wholly inside or outside
-    for (int i = threadIdx.x; i < kMIn * (kMIn / 4); i += kMThreads) {
-      const int r = i / (kMIn / 4), c4 = i % (kMIn / 4);
+    constexpr int Q = WP / 4;  // float4 per window row
+    const int step = blockDim.x, dr = step / Q, dc = step % Q;
+    int r = threadIdx.x / Q, c4 = threadIdx.x % Q;  // (r, c4) advanced incrementally
+    const float* fb = f + (int64_t)(R0 - 4) * pitch + (C0 - 4);
+    for (; r < kMIn;) {
       const int gr = R0 - 4 + r, gc = C0 - 4 + 4 * c4;
-      const bool ok = gr >= 0 && gr < H && gc >= 0 && gc < W;
-      cp_async16(in + r * kMP + 4 * c4, ok ? f + (int64_t)gr * pitch + gc : f, ok ? 16 : 0);
+      const bool ok = (unsigned)gr < (unsigned)H && (unsigned)gc < (unsigned)W && c4 < kMIn / 4;
+      cp_async16(in + r * WP + 4 * c4, ok ? fb + (int64_t)r * pitch + 4 * c4 : f, ok ? 16 : 0);
+      c4 += dc;
+      r += dr;
+      if (c4 >= Q) {
+        c4 -= Q;
+        ++r;
+      }
     }
   } else {
-    for (int i = threadIdx.x; i < kMIn * kMIn; i += kMThreads) {
-      const int r = i / kMIn, c = i % kMIn;
+    for (int i = threadIdx.x; i < kMIn * WP; i += blockDim.x) {
+      const int r = i / WP, c = i % WP;
       const int gr = R0 - 4 + r, gc = C0 - 4 + c;
-      in[r * kMP + c] = (gr >= 0 && gr < H && gc >= 0 && gc < W) ? __ldg(f + (int64_t)gr * pitch + gc) : 0.f;
+      in[r * WP + c] = (gr >= 0 && gr < H && gc >= 0 && gc < W && c < kMIn) ? __ldg(f + (int64_t)gr * pitch + gc) : 0.f;
     }
   }
 }
@@ -202,6 +212,166 @@ __device__ void denoise_region_mma(const float* in, float* acc, int R0, int C0, 
   __syncthreads();
 }
 
+// ---- fp32 denoiser of the IDA step (dct_soft_threshold, denoise.cpp:52-92) ------------------
+// The 17 x 17 tiles (8 x 8, stride 4) over the 72 x 72 window are transformed separably on the
+// CUDA cores with packed-pair butterflies (dct_pair.cuh), and the separability is used twice:
+//   A. row DCT of every (window row, 8-px segment tj): shared by the two tiles that contain that
+//      row segment (tiles ti and ti - 1), so each row transform is done once, not twice;
+//   B. per tile, column DCT -> soft threshold -> inverse column DCT, summed into S over the two
+//      tiles covering each row (even tile rows store, odd tile rows add: a fixed order);
+//   C. inverse row DCT of S (linearity: the two tiles' contributions to a row segment are summed
+//      before the inverse, halving those transforms), then the two segments covering each pixel
+//      are summed and scaled by 1 / weight (denoise.cpp:90), straight into acc.
+// Vectors are paired across adjacent segments (tj = 2 tp, 2 tp + 1), so every transform is one
+// FFMA2 / FADD2 stream with no transposes. Tiles whose origin is off the image's tile grid get an
+// infinite threshold, so they contribute zero (denoise.cpp:57-62).
+constexpr int kWP = 76;            // window pitch: 72 + 4 zero columns (A reads 12 px from col 8 tp)
+constexpr int kTP = 9;             // segment pairs per row (tj = 17 is a zero dummy)
+constexpr int kRP = kTP * 16 + 4;  // R / S row pitch: [tp][v][2] + 4 (148 = 20 mod 32: conflict-free)
+constexpr int kFThreads = 32 * kTP;  // fused kernel: warp w owns segment pair tp = w through stages A-C
+
+struct IdaF32Smem {
+  union {
+    float in[kMIn * kWP];   // field window (pitch kWP)
+    float acc[kMIn * kMP];  // then x over the region (at kMOff, pitch kMP) for the block phase
+  };
+  union {
+    float RS[kMIn * kRP];      // stage A output R[y][tp][v][tj parity], overwritten in place by stage B's S
+    float stage[kMIn * kRP];   // per-warp y/z staging in the block phase
+  };
+  Frag16Tab f16;
+  int meta_cnt[64];
+  int meta_off[64];
+  double red[4][16];
+  unsigned long long bad[2];
+  double mine[4];
+};
+static_assert(kFThreads / 32 * 512 <= kMIn * kRP, "staging buffers fit");
+static_assert(kMIn * kMP <= kMIn * kWP, "acc fits in the window");
+
+__device__ __forceinline__ bool tile_on_grid(int R0, int C0, int H, int W, int ti, int tj) {
+  return tj <= 16 && (unsigned)(R0 - 4 + 4 * ti) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj) <= (unsigned)(W - 8);
+}
+
+__device__ __forceinline__ void sts2(float* p, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(smem_u32(p)), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float2 lds2(const float* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 shfl2(float2 v, int src) {
+  return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// dct_soft_threshold of the window s.in into s.acc (the 64 x 64 region, pitch kMP at kMOff;
+// acc aliases the window, which is dead once every warp is past stage A).
+// Warp w owns segment pair tp = w (tj = 2w, 2w + 1) through stages A-C, so the stages are
+// ordered by __syncwarp; only stage C's quads shared with the neighbouring pair need the CTA.
+// Expects the window's async copies issued; ends with __syncthreads.
+__device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
+  const int lane = threadIdx.x & 31, tp = threadIdx.x >> 5;
+  cp_async_wait_all();
+  __syncthreads();
+  // A: row DCTs of the window rows y = lane + 32 j (lanes along rows: conflict-free)
+#pragma unroll 1
+  for (int y = lane; y < kMIn; y += 32) {
+    const float* src = s.in + y * kWP + 8 * tp;
+    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4),
+                 c = *reinterpret_cast<const float4*>(src + 8);
+    const float2 x[8] = {make_float2(a.x, b.x), make_float2(a.y, b.y), make_float2(a.z, b.z), make_float2(a.w, b.w),
+                         make_float2(b.x, c.x), make_float2(b.y, c.y), make_float2(b.z, c.z), make_float2(b.w, c.w)};
+    float2 Y[8];
+    dct8_fwd_pair(x, Y);
+    float4* d = reinterpret_cast<float4*>(s.RS + y * kRP + 16 * tp);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_float4(Y[2 * q].x, Y[2 * q].y, Y[2 * q + 1].x, Y[2 * q + 1].y);
+  }
+  __syncwarp();
+  // B: lanes = (coefficient column v, tile tq of a group of 4 consecutive tile rows); per tile:
+  // column DCT, soft threshold, inverse column DCT. A tile's top half (4 rows) plus the bottom
+  // half of the tile above (the lane 8 below, or the carry from the previous group) completes
+  // those S rows, written in place over R (every R row they replace was loaded by both of its
+  // tiles before the warp's first store to it: the loads of a group precede its stores).
+  {
+    const float kInf = __int_as_float(0x7f800000);
+    const int v = lane & 7, tq = lane >> 3;
+    const bool gc0 = (unsigned)(C0 - 4 + 8 * tp) <= (unsigned)(W - 8);
+    const bool gc1 = tp < 8 && (unsigned)(C0 + 8 * tp) <= (unsigned)(W - 8);
+    float2 carry[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll 1
+    for (int g = 0; g < 5; ++g) {
+      const int ti = min(4 * g + tq, 16);  // group 4: tiles 17..19 are repeats of 16, never stored
+      const bool act = 4 * g + tq <= 16;
+      float* col = s.RS + 4 * ti * kRP + 16 * tp + 2 * v;
+      float2 x[8], Y[8], X[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) x[r] = lds2(col + r * kRP);
+      __syncwarp();
+      dct8_fwd_pair(x, Y);
+      const bool gr = (unsigned)(R0 - 4 + 4 * ti) <= (unsigned)(H - 8);
+      const bool g0 = gr && gc0, g1 = gr && gc1;
+      const float t0 = g0 ? thr : kInf, t1 = g1 ? thr : kInf;
+      // the DC (u = 0, v = 0) passes through (denoise.cpp:76)
+      Y[0] = p_soft(Y[0], v == 0 ? (g0 ? 0.f : kInf) : t0, v == 0 ? (g1 ? 0.f : kInf) : t1);
+#pragma unroll
+      for (int u = 1; u < 8; ++u) Y[u] = p_soft(Y[u], t0, t1);
+      dct8_inv_pair(Y, X);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        // lane L takes lane L - 8 (mod 32): the tile above, or (tq = 0) the previous group's last tile
+        const float2 above = shfl2(tq == 3 ? carry[r] : X[4 + r], (lane + 24) & 31);
+        if (act) sts2(col + r * kRP, p_add(X[r], above));
+        carry[r] = X[4 + r];
+      }
+    }
+  }
+  __syncthreads();  // acc (stage C's output) aliases the window; S rows of every pair are complete
+  // C: inverse row DCTs of S over the region rows yr = lane + 32 j.
+  // Output quads (window cols): Q0 = 8tp..+3 (tj0 only), Q1 = 8tp+4..+7 (tj0 + tj1, complete),
+  // Q2 = 8tp+8..+11 (tj1 only). Q0 of pair tp+1 and Q2 of pair tp are the same quad: Q0 is
+  // stored first, Q2 added after a barrier (a fixed order), then scaled by 1 / weight.
+  float4 q2[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int yr = lane + 32 * j;
+    const float4* src = reinterpret_cast<const float4*>(s.RS + (yr + 4) * kRP + 16 * tp);
+    float2 y[8], X[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = src[q];
+      y[2 * q] = make_float2(v.x, v.y);
+      y[2 * q + 1] = make_float2(v.z, v.w);
+    }
+    dct8_inv_pair(y, X);
+    float* row = s.acc + kMOff + yr * kMP - 4;  // indexed by window column
+    if (tp >= 1) *reinterpret_cast<float4*>(row + 8 * tp) = make_float4(X[0].x, X[1].x, X[2].x, X[3].x);
+    if (tp <= 7) {
+      const int br = (R0 + yr) & ~3, bc = C0 + 8 * tp;  // weights: tile origins per axis (1 or 2)
+      const int w = max(((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0)), 1);
+      const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
+      *reinterpret_cast<float4*>(row + 8 * tp + 4) =
+          make_float4((X[4].x + X[0].y) * sc, (X[5].x + X[1].y) * sc, (X[6].x + X[2].y) * sc, (X[7].x + X[3].y) * sc);
+    }
+    q2[j] = make_float4(X[4].y, X[5].y, X[6].y, X[7].y);
+  }
+  __syncthreads();
+  if (tp <= 7) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int yr = lane + 32 * j;
+      const int br = (R0 + yr) & ~3, bc = C0 + 8 * tp + 4;
+      const int w = max(((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0)), 1);
+      const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
+      float4* d = reinterpret_cast<float4*>(s.acc + kMOff + yr * kMP + 8 * tp + 4);
+      const float4 a = *d;
+      *d = make_float4((a.x + q2[j].x) * sc, (a.y + q2[j].y) * sc, (a.z + q2[j].z) * sc, (a.w + q2[j].w) * sc);
+    }
+  }
+  __syncthreads();
+}
+
 struct IdaLaneSums {
   double z = 0.0, sse = 0.0, y = 0.0, cnt = 0.0;
   unsigned long long badx = ~0ull, badz = ~0ull;
@@ -260,10 +430,10 @@ __device__ __forceinline__ void stage_yz_wait(const IdaParams& P, int cnt, const
 }
 
 // The region's sensing blocks (kMR / B)^2, row-major: count (-1 outside the grid) and offset.
-template <int B>
-__device__ __forceinline__ void fetch_meta(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s) {
+template <int B, class Sm>
+__device__ __forceinline__ void fetch_meta(const IdaParams& P, int img, int R0, int C0, Sm& s) {
   constexpr int PB = kMR / B;
-  for (int bi = threadIdx.x; bi < PB * PB; bi += kMThreads) {
+  for (int bi = threadIdx.x; bi < PB * PB; bi += blockDim.x) {
     const int gbr = R0 / B + bi / PB, gbc = C0 / B + bi % PB;
     int cnt = -1, off = 0;
     if (gbr < P.rows && gbc < P.cols) {
@@ -286,13 +456,14 @@ __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax
 
 // ---- B = 16: one sensing block per warp step ---------------------------------------------
 // init: acc <- A* y (the warm start x0, recon.cpp:119-131)
-__device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s) {
+template <class Sm>
+__device__ void init_x16(const IdaParams& P, int img, int R0, int C0, Sm& s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   uint32_t rank[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) rank[q] = zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)];
-  float* yb = s.in + warp * 512;
-  for (int bi = warp; bi < 16; bi += kMWarps) {
+  float* yb = s.stage + warp * 512;
+  for (int bi = warp; bi < 16; bi += (int)(blockDim.x >> 5)) {
     const int gbr = R0 / 16 + bi / 4, gbc = C0 / 16 + bi % 4;
     const int lr0 = (bi / 4) * 16, lc0 = (bi % 4) * 16;
     int cnt = 0;
@@ -318,16 +489,17 @@ __device__ void init_x16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem
   }
 }
 
-__device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s, IdaLaneSums& S) {
+template <class Sm>
+__device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
   uint32_t rk[2] = {0u, 0u};  // zigzag ranks of the lane's 8 slots, one byte each
 #pragma unroll
   for (int q = 0; q < 8; ++q) rk[q >> 2] |= zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)] << (8 * (q & 3));
-  float* yb = s.in + warp * 512;
+  float* yb = s.stage + warp * 512;
   float* zb = yb + 256;
   const bool last = P.pseudo_out == nullptr;
-  for (int bi = warp; bi < 16; bi += kMWarps) {
+  for (int bi = warp; bi < 16; bi += (int)(blockDim.x >> 5)) {
     const int cnt = s.meta_cnt[bi];
     if (cnt < 0) continue;  // outside the block grid (warp-uniform)
     const int lr0 = (bi / 4) * 16, lc0 = (bi % 4) * 16;
@@ -377,16 +549,239 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, IdaMm
   }
 }
 
+// ---- B = 16 block phase on the CUDA cores (recon.cpp:81-93, 75-79; operators.cpp:50-76) ------
+// Thread (b, r) / (b, v) of the region's 16 sensing blocks (threads 0..255; warp 8 stages data):
+//   1. rows:    T[r][.] = DCT16(x[r][.])                 x_checks, trace SSE, last step: x out
+//   2. columns: Y[.][v] = DCT16(T[.][v]); in the zigzag prefix z <- (y - Y) + z / D_F and
+//               W = Y + z, else W = Y;                    V[.][v] = IDCT16(W[.][v])
+//   3. rows:    pseudo[r][.] = IDCT16(V[r][.])  =  x + A* z  (IDCT16 o DCT16 = identity: the full
+//               transform of x is already at hand, so pseudo needs one inverse, not x + a second one)
+// The transposes go through the window buffer (x is dead once every thread holds its row), the
+// region's y / z prefixes are staged in RS by cp.async (issued before stage 1) and z goes back
+// coalesced from there.
+constexpr int kTB = 336;  // per-block transpose tile: 16 rows x pitch 20 (+16: conflict-free between blocks)
+static_assert(16 * kTB <= kMIn * kWP, "transpose tiles fit in the window buffer");
+
+struct RegionRuns {  // the region's payload runs: one per block row (its blocks are consecutive)
+  int row[4];        // region offset of block row j's run (exclusive scan of max(cnt, 0))
+  int total;
+};
+
+__device__ __forceinline__ void region_runs(const int* cnt, RegionRuns& R) {
+  int a = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    if ((b & 3) == 0) R.row[b >> 2] = a;
+    a += max(cnt[b], 0);
+  }
+  R.total = a;
+}
+// region offset of block b's prefix
+__device__ __forceinline__ int region_pre(const int* cnt, int b) {
+  int a = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a += i < b ? max(cnt[i], 0) : 0;
+  return a;
+}
+// run (block row) of region element e, and its start
+__device__ __forceinline__ int run_of(const RegionRuns& R, int e, int& start) {
+  const int j = (e >= R.row[1]) + (e >= R.row[2]) + (e >= R.row[3]);
+  start = j == 0 ? 0 : (j == 1 ? R.row[1] : (j == 2 ? R.row[2] : R.row[3]));
+  return j;
+}
+
+// Issue the async copies of the region's y (and z) prefixes into RS: y at 0, z at 4096.
+__device__ __forceinline__ void stage_region_yz(const IdaParams& P, int img, const IdaF32Smem& s,
+                                                const RegionRuns& R, float* ys, float* zs, bool need_z) {
+  const int64_t ibase = (int64_t)img * P.y_stride;
+  for (int e = threadIdx.x; e < R.total; e += blockDim.x) {
+    int st;
+    const int j = run_of(R, e, st);  // block row of the element
+    const int64_t g = ibase + s.meta_off[4 * j] + (e - st);
+    cp_async4(ys + e, P.y + g);
+    if (need_z) cp_async4(zs + e, P.z + g);
+  }
+}
+
+template <class Sm>
+__device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
+  const int t = threadIdx.x;
+  const bool worker = t < 256;
+  const int b = (t >> 4) & 15, lr = t & 15;  // block of the region (row-major) and row / column
+  const int br = b >> 2, bc = b & 3;
+  const int cnt = s.meta_cnt[b];
+  const bool valid = worker && cnt >= 0;
+  const bool last = P.pseudo_out == nullptr;
+  const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
+  RegionRuns RR;
+  region_runs(s.meta_cnt, RR);
+  float* ys = s.RS;
+  float* zs = s.RS + 4096;
+  stage_region_yz(P, img, s, RR, ys, zs, !P.is_init);
+  // 1. rows of x
+  float xr[16], T[16];
+  if (valid) {
+    const float4* src = reinterpret_cast<const float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = src[q];
+      xr[4 * q] = v.x;
+      xr[4 * q + 1] = v.y;
+      xr[4 * q + 2] = v.z;
+      xr[4 * q + 3] = v.w;
+    }
+    const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) x_checks(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), S);
+    if (last) {  // the estimate itself (recon.cpp:255-257 clamp on reconstruct's final step)
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) store_out(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), make_float2(0.f, 0.f));
+    }
+    abcs_gen::dct16_fwd(xr, T);
+  }
+  __syncthreads();  // every x row is in registers: the window buffer takes the transposes
+  float* tb = s.in + b * kTB;
+  if (valid) {
+#pragma unroll
+    for (int v = 0; v < 16; ++v) tb[v * 20 + lr] = T[v];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // 2. columns: v = lr
+  float W[16];
+  if (valid) {
+    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
+    float Tc[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = src[q];
+      Tc[4 * q] = v.x;
+      Tc[4 * q + 1] = v.y;
+      Tc[4 * q + 2] = v.z;
+      Tc[4 * q + 3] = v.w;
+    }
+    float Y[16];
+    abcs_gen::dct16_fwd(Tc, Y);
+    const unsigned short* rk = zigzag_rank_dev<16>() + lr;
+    const int base = region_pre(s.meta_cnt, b);
+    const int boff = s.meta_off[b];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int k = rk[16 * u];
+      float w = Y[u];
+      if (k < cnt) {
+        const float yv = ys[base + k];
+        if (P.is_init) S.y += (double)yv * (double)yv;  // ||y||^2 (recon.cpp:128)
+        const float zn = z_update(P, yv, Y[u], P.is_init ? 0.f : zs[base + k], (unsigned long long)(boff + k), S, ons);
+        zs[base + k] = zn;
+        w += zn;
+      }
+      W[u] = w;
+    }
+    if (lr == 0) S.cnt += (double)cnt;
+  }
+  __syncthreads();  // all column loads done (tb is rewritten) and z complete in RS
+  // z back to the payload, coalesced (its runs mirror the staging)
+  {
+    const int64_t ibase = (int64_t)img * P.y_stride;
+    for (int e = t; e < RR.total; e += blockDim.x) {
+      int st;
+      const int j = run_of(RR, e, st);
+      P.z[ibase + s.meta_off[4 * j] + (e - st)] = zs[e];
+    }
+  }
+  if (last) return;
+  if (valid) {
+    float V[16];
+    abcs_gen::dct16_inv(W, V);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
+  }
+  __syncthreads();
+  // 3. rows: pseudo = IDCT16 of row r of V
+  if (valid) {
+    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
+    float Vr[16], O[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = src[q];
+      Vr[4 * q] = v.x;
+      Vr[4 * q + 1] = v.y;
+      Vr[4 * q + 2] = v.z;
+      Vr[4 * q + 3] = v.w;
+    }
+    abcs_gen::dct16_inv(Vr, O);
+    float4* dst = reinterpret_cast<float4*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc +
+                                            (int64_t)(R0 + 16 * br + lr) * P.Wc + C0 + 16 * bc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
+  }
+}
+
+// init, warm start: acc <- x0 = A* y (recon.cpp:119-131), the inverse of each block's y prefix
+// (columns then rows through the transpose tiles). Called before block_phase16_f32.
+template <class Sm>
+__device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s) {
+  const int t = threadIdx.x;
+  const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
+  const int cnt = s.meta_cnt[b];
+  const bool valid = t < 256 && cnt >= 0;
+  RegionRuns RR;
+  region_runs(s.meta_cnt, RR);
+  float* ys = s.RS;
+  stage_region_yz(P, img, s, RR, ys, nullptr, false);
+  cp_async_wait_all();
+  __syncthreads();
+  float* tb = s.in + b * kTB;  // acc (in the same buffer) is written only after the last tb read
+  float V[16];
+  if (valid) {
+    float Wc[16];
+    const int base = region_pre(s.meta_cnt, b);
+    const unsigned short* rk = zigzag_rank_dev<16>() + lr;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int k = rk[16 * u];
+      Wc[u] = k < cnt ? ys[base + k] : 0.f;
+    }
+    abcs_gen::dct16_inv(Wc, V);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
+  }
+  __syncthreads();
+  float O[16];
+  if (valid) {
+    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
+    float Vr[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = src[q];
+      Vr[4 * q] = v.x;
+      Vr[4 * q + 1] = v.y;
+      Vr[4 * q + 2] = v.z;
+      Vr[4 * q + 3] = v.w;
+    }
+    abcs_gen::dct16_inv(Vr, O);
+  }
+  __syncthreads();
+  if (valid) {
+    float4* dst = reinterpret_cast<float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
+  }
+  __syncthreads();
+}
+
 // ---- B = 8: two horizontally adjacent sensing blocks per warp step ------------------------
-__device__ void init_x8(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s) {
+template <class Sm>
+__device__ void init_x8(const IdaParams& P, int img, int R0, int C0, Sm& s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   Frag8 f;
   load_frag8(f);
   uint32_t rank[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) rank[e] = zigzag_rank_dev<8>()[(2 * t + e) * 8 + g];  // Y^T[g][2t+e] = Y[2t+e][g]
-  float* yb = s.in + warp * 512;
-  for (int pi = warp; pi < 32; pi += kMWarps) {
+  float* yb = s.stage + warp * 512;
+  for (int pi = warp; pi < 32; pi += (int)(blockDim.x >> 5)) {
     const int br = pi / 4, bc = 2 * (pi % 4);
     const int gbr = R0 / 8 + br;
     int cnt[2] = {0, 0};
@@ -418,7 +813,8 @@ __device__ void init_x8(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem&
   }
 }
 
-__device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMmaSmem& s, IdaLaneSums& S) {
+template <class Sm>
+__device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
   Frag8 f;
@@ -426,10 +822,10 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMma
   uint32_t rank[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) rank[e] = zigzag_rank_dev<8>()[(2 * t + e) * 8 + g];
-  float* yb = s.in + warp * 512;  // [q][64] y, then [q][64] z at +128
+  float* yb = s.stage + warp * 512;  // [q][64] y, then [q][64] z at +128
   float* zb = yb + 128;
   const bool last = P.pseudo_out == nullptr;
-  for (int pi = warp; pi < 32; pi += kMWarps) {
+  for (int pi = warp; pi < 32; pi += (int)(blockDim.x >> 5)) {
     const int br = pi / 4, bc = 2 * (pi % 4);
     const int bi0 = br * 8 + bc;
     if (s.meta_cnt[bi0] < 0) continue;  // outside the block grid (warp-uniform)
@@ -478,7 +874,8 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, IdaMma
 }
 
 // CTA reduction of the lane sums -> mine[4] (+ bad indices) and the per-image fold.
-__device__ void reduce_and_finish(const IdaParams& P, int img, int region, IdaMmaSmem& s, IdaLaneSums& S) {
+template <class Sm>
+__device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s, IdaLaneSums& S) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     s.bad[0] = ~0ull;
@@ -504,7 +901,7 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, IdaMm
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) {
       double a = 0.0;
-      for (int w = 0; w < kMWarps; ++w) a += s.red[q][w];
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += s.red[q][w];
       s.mine[q] = a;
     }
     if (s.bad[0] != ~0ull) atomicMin(P.badx + img, s.bad[0]);
@@ -513,31 +910,31 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, IdaMm
   finish_image(P, img, region, s.mine);
 }
 
-template <int B, bool kVec>
-__global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
-  __shared__ __align__(16) IdaMmaSmem s;
+template <int B>
+__global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P) {
+  extern __shared__ __align__(16) unsigned char ida_smem_raw[];
+  IdaF32Smem& s = *reinterpret_cast<IdaF32Smem*>(ida_smem_raw);
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
   const bool denoise = !P.is_init && !P.x_in;
   if (denoise)  // window first: its latency overlaps the metadata and table set-up
-    load_window<kVec>(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s.in);
+    load_window<true, kWP>(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s.in);
   const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
-  if (B == 16 && threadIdx.x < 32) fill_frag16_tab(s.f16);
-  if (B == 16 && P.is_init && P.warm) __syncthreads();  // init_x16 reads the table right away
+  if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
-      for (int i = threadIdx.x; i < kMIn * kMP / 4; i += kMThreads)
+      for (int i = threadIdx.x; i < kMIn * kMP / 4; i += blockDim.x)
         reinterpret_cast<float4*>(s.acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (B == 16) {
-      init_x16(P, img, R0, C0, s);
+      init_x16_f32(P, img, R0, C0, s);
     } else {
       init_x8(P, img, R0, C0, s);
     }
     __syncthreads();
   } else if (P.x_in) {  // x from another denoiser: load the region
     const float* xs = P.x_in + (int64_t)img * P.Hc * P.Wc;
-    for (int i = threadIdx.x; i < kMR * kMR / 4; i += kMThreads) {
+    for (int i = threadIdx.x; i < kMR * kMR / 4; i += blockDim.x) {
       const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (R0 + r < P.Hc && C0 + c < P.Wc) v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)(R0 + r) * P.Wc + C0 + c));
@@ -545,10 +942,10 @@ __global__ void __launch_bounds__(kMThreads, 4) ida_mma_kernel(IdaParams P) {
     }
     __syncthreads();
   } else {
-    denoise_region_mma<true>(s.in, s.acc, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
+    denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
-  if (B == 16) block_phase16(P, img, R0, C0, s, S);
+  if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
   else block_phase8(P, img, R0, C0, s, S);
   reduce_and_finish(P, img, region, s, S);
 }
@@ -592,10 +989,21 @@ int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t s
 
 int ida_mma_region() { return kMR; }
 
+template <int B>
+static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
+  static bool attr = false;  // > 48 KB of dynamic shared memory: opt in once per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(ida_mma_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(IdaF32Smem));
+    attr = true;
+  }
+  ida_mma_kernel<B><<<grid, kFThreads, sizeof(IdaF32Smem), s>>>(P);
+}
+
 void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s) {
   // pseudo buffers are internal (256-B aligned, Wc % 8 == 0): always the vector window
-  if (block == 16) ida_mma_kernel<16, true><<<grid, kMThreads, 0, s>>>(P);
-  else ida_mma_kernel<8, true><<<grid, kMThreads, 0, s>>>(P);
+  if (block == 16) launch_ida_b<16>(P, grid, s);
+  else launch_ida_b<8>(P, grid, s);
 }
+
 
 }  // namespace abcs_b200

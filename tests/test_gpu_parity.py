@@ -530,11 +530,14 @@ def test_ida_divergence(p):
     ms = p.MeasurementSet(64, 64, 16, p.Algorithm.BBV, 3, 10, 0.0, z["counts"], z["coeffs"] * 1e7)
     with pytest.raises(p.DivergenceError) as e:
         p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=3))
-    assert e.value.iteration == 1
+    assert e.value.iteration == 1   # the reference: "solver diverged (|x| > 1e6) at iteration 1"
     with pytest.raises(ValueError):
         p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=0))
-    with pytest.raises(p.DivergenceError):                     # every method runs on the device now
-        p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Amp, iterations=2))
+    # AMP on the same set does not diverge in the reference (its soft threshold at lambda * sigma
+    # zeroes the estimate); the device path is fp32 end to end, so no fp16 range overflow may
+    # raise a spurious DivergenceError either (recon.cpp:53-73 is the only divergence rule)
+    res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Amp, iterations=2))
+    assert np.all(np.isfinite(res.image)) and np.max(np.abs(res.image)) <= 1e-3
     with pytest.raises(p.UnsupportedError):
         p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, 2, 2.0, p.DenoiserSpec("dct_threshold", {"block": 4})))
 
