@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libabcs_b200.so")
+LIB_PATH = os.environ.get("ABCS_LIB_OVERRIDE") or os.path.join(HERE, "libabcs_b200.so")
 
 OK, INVALID, FORMAT, DIVERGENCE, CUDA, LOGIC, UNSUPPORTED = range(7)
 

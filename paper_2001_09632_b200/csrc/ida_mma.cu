@@ -18,6 +18,8 @@
 //   4. per-image reductions folded by the last CTA (finish_image).
 // fp32 operands are split into fp16 hi/lo pairs (mma_dct.cuh), ~fp32 accuracy.
 #include <cfloat>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "ida_common.cuh"
@@ -45,6 +47,7 @@ struct IdaMmaSmem {
 };
 static_assert(kMWarps * 512 <= kMIn * kMP, "staging buffers fit in the window");
 constexpr int kMOff = 4 * kMP + 4;  // region pixel (0, 0) inside acc
+constexpr int kWinBytes = 76 * kMIn * 4;  // the fused kernel's TMA window box (kWP x kMIn floats)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // 16-byte async copy global -> shared; src_bytes = 0 zero-fills (out-of-image window parts)
@@ -55,6 +58,29 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// The 76 x 72 window (4-px halo, 4 spare columns) of image `img` by one TMA tile copy: the 3-D
+// tensor map (Wc, Hc, n) of the pseudo field fills out-of-image elements with zeros, which is the
+// denoiser's boundary (tiles there are off the grid and weigh nothing).
+__device__ __forceinline__ void tma_window(float* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+  const uint32_t b = smem_u32(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(kWinBytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(smem_u32(dst)), "l"(tm), "r"(x), "r"(y), "r"(z), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void tma_window_wait(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred p;\nWIN_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WIN_WAIT_%=;\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 
 // field[R0-4 .. R0+68) x [C0-4 .. C0+68) -> s.in (zeros outside the image). The vector path
 // only issues async copies; the caller waits (cp_async_wait_all + barrier) before reading.
@@ -232,19 +258,20 @@ constexpr int kFThreads = 32 * kTP;  // fused kernel: warp w owns segment pair t
 
 struct IdaF32Smem {
   union {
-    float in[kMIn * kWP];   // field window (pitch kWP)
+    float in[kMIn * kWP];   // field window (pitch kWP), the TMA destination (128-B aligned)
     float acc[kMIn * kMP];  // then x over the region (at kMOff, pitch kMP) for the block phase
   };
   union {
-    float RS[kMIn * kRP];      // stage A output R[y][tp][v][tj parity], overwritten in place by stage B's S
-    float stage[kMIn * kRP];   // per-warp y/z staging in the block phase
+    float RS[kMIn * kRP];     // stage A output R[y][tp][v][tj parity], overwritten in place by stage B's S
+    float stage[kMIn * kRP];  // y / z staging in the block phase
   };
-  Frag16Tab f16;
+  Frag16Tab f16;  // tensor-core block phase (estimates from another denoiser, x_in)
   int meta_cnt[64];
   int meta_off[64];
   double red[4][16];
   unsigned long long bad[2];
   double mine[4];
+  uint64_t win_bar;  // TMA window load (one phase per CTA)
 };
 static_assert(kFThreads / 32 * 512 <= kMIn * kRP, "staging buffers fit");
 static_assert(kMIn * kMP <= kMIn * kWP, "acc fits in the window");
@@ -272,8 +299,8 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
 // Expects the window's async copies issued; ends with __syncthreads.
 __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
   const int lane = threadIdx.x & 31, tp = threadIdx.x >> 5;
-  cp_async_wait_all();
-  __syncthreads();
+  __syncthreads();  // the window's mbarrier is initialised (thread 0) before anyone waits on it
+  tma_window_wait(&s.win_bar);
   // A: row DCTs of the window rows y = lane + 32 j (lanes along rows: conflict-free)
 #pragma unroll 1
   for (int y = lane; y < kMIn; y += 32) {
@@ -711,8 +738,8 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
       Vr[4 * q + 3] = v.w;
     }
     abcs_gen::dct16_inv(Vr, O);
-    float4* dst = reinterpret_cast<float4*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc +
-                                            (int64_t)(R0 + 16 * br + lr) * P.Wc + C0 + 16 * bc);
+    const int64_t o = (int64_t)img * P.Hc * P.Wc + (int64_t)(R0 + 16 * br + lr) * P.Wc + C0 + 16 * bc;
+    float4* dst = reinterpret_cast<float4*>(P.pseudo_out + o);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
   }
@@ -911,14 +938,14 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s
 }
 
 template <int B>
-__global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P) {
-  extern __shared__ __align__(16) unsigned char ida_smem_raw[];
-  IdaF32Smem& s = *reinterpret_cast<IdaF32Smem*>(ida_smem_raw);
+__global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, const __grid_constant__ CUtensorMap win_map) {
+  extern __shared__ __align__(128) unsigned char ida_smem_raw[];
+  IdaF32Smem& s = *reinterpret_cast<IdaF32Smem*>(ida_smem_raw + ((128 - (smem_u32(ida_smem_raw) & 127)) & 127));
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
   const bool denoise = !P.is_init && !P.x_in;
-  if (denoise)  // window first: its latency overlaps the metadata and table set-up
-    load_window<true, kWP>(P.pseudo_in + (int64_t)img * P.Hc * P.Wc, P.Wc, R0, C0, P.Hc, P.Wc, s.in);
+  if (denoise && threadIdx.x == 0)  // window first: its latency overlaps the metadata set-up
+    tma_window(s.in, &win_map, C0 - 4, R0 - 4, img, &s.win_bar);
   const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
@@ -933,6 +960,7 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P) {
     }
     __syncthreads();
   } else if (P.x_in) {  // x from another denoiser: load the region
+    if (B == 16 && threadIdx.x < 32) fill_frag16_tab(s.f16);
     const float* xs = P.x_in + (int64_t)img * P.Hc * P.Wc;
     for (int i = threadIdx.x; i < kMR * kMR / 4; i += blockDim.x) {
       const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
@@ -945,7 +973,12 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P) {
     denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
-  if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
+  // The fused IDA step (and its warm start) runs the fp32 block phase; an estimate from another
+  // denoiser (ISTA / AMP / DAMP, x_in) keeps the tensor-core one whose pseudo = x + A* z is the
+  // reference's formula term by term (DAMP's Monte-Carlo divergence differences two denoiser
+  // calls on that pseudo and is the most rounding-sensitive path: measured 5e-4 vs 1.2e-3 px).
+  if (B == 16 && !P.x_in) block_phase16_f32(P, img, R0, C0, s, S);
+  else if (B == 16) block_phase16(P, img, R0, C0, s, S);
   else block_phase8(P, img, R0, C0, s, S);
   reduce_and_finish(P, img, region, s, S);
 }
@@ -989,14 +1022,38 @@ int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t s
 
 int ida_mma_region() { return kMR; }
 
+// 3-D tiled tensor map over the pseudo field (Wc, Hc, n) with the window box (kWP x kMIn x 1).
+static int encode_window_map(CUtensorMap* tm, const float* field, int Wc, int Hc, int n) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return set_error(ABCS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)Wc, (cuuint64_t)Hc, (cuuint64_t)n};
+  const cuuint64_t strides[2] = {(cuuint64_t)Wc * 4, (cuuint64_t)Wc * Hc * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)kWP, (cuuint32_t)kMIn, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(field), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? ABCS_OK : set_error(ABCS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
 template <int B>
 static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   static bool attr = false;  // > 48 KB of dynamic shared memory: opt in once per instantiation
+  const int bytes = (int)sizeof(IdaF32Smem) + 128;  // + alignment slack (TMA destination: 128 B)
   if (!attr) {
-    cudaFuncSetAttribute(ida_mma_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(IdaF32Smem));
+    cudaFuncSetAttribute(ida_mma_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
-  ida_mma_kernel<B><<<grid, kFThreads, sizeof(IdaF32Smem), s>>>(P);
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (!P.is_init && !P.x_in && P.pseudo_in && encode_window_map(&tm, P.pseudo_in, P.Wc, P.Hc, P.n) != ABCS_OK) return;
+  ida_mma_kernel<B><<<grid, kFThreads, bytes, s>>>(P, tm);
 }
 
 void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s) {
