@@ -297,9 +297,33 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
 // Warp w owns segment pair tp = w (tj = 2w, 2w + 1) through stages A-C, so the stages are
 // ordered by __syncwarp; only stage C's quads shared with the neighbouring pair need the CTA.
 // Expects the window's async copies issued; ends with __syncthreads.
-__device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
+// The region's y / z prefixes (one run per block row) into L1 while the denoiser runs: the block
+// phase's rank-order accesses to them then hit L1 instead of waiting on L2.
+__device__ __forceinline__ void l1_prefetch_region_yz(const IdaParams& P, int img, const IdaF32Smem& s) {
+  if (!P.y) return;
+  const int t = threadIdx.x;
+  const int j = (t >> 5) & 3, line = t & 31;  // warps 0-3 -> block rows 0-3 of y, warps 4-7 of z
+  if (t >= 256) return;
+  int first = -1, n = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = s.meta_cnt[4 * j + i];
+    if (c >= 0) {
+      if (first < 0) first = s.meta_off[4 * j + i];
+      n += c;
+    }
+  }
+  if (first < 0) return;
+  const float* base = ((t >> 7) ? P.z : P.y) + (int64_t)img * P.y_stride + first;
+  for (int o = line * 32; o < n; o += 32 * 32)
+    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(base + o));
+}
+
+__device__ void denoise_region_f32(const IdaParams& P_, int img_, IdaF32Smem& s, int R0, int C0, int H, int W,
+                                   float thr) {
   const int lane = threadIdx.x & 31, tp = threadIdx.x >> 5;
   __syncthreads();  // the window's mbarrier is initialised (thread 0) before anyone waits on it
+  l1_prefetch_region_yz(P_, img_, s);
   tma_window_wait(&s.win_bar);
   // A: row DCTs of the window rows y = lane + 32 j (lanes along rows: conflict-free)
 #pragma unroll 1
@@ -577,89 +601,66 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, Sm& s
 }
 
 // ---- B = 16 block phase on the CUDA cores (recon.cpp:81-93, 75-79; operators.cpp:50-76) ------
-// Thread (b, r) / (b, v) of the region's 16 sensing blocks (threads 0..255; warp 8 stages data):
-//   1. rows:    T[r][.] = DCT16(x[r][.])                 x_checks, trace SSE, last step: x out
+// Thread (b, r) / (b, v) of the region's 16 sensing blocks (threads 0..255):
+//   1. rows:    T[r][.] = DCT16(x[r][.])                 check_finite, trace SSE, last step: x out
 //   2. columns: Y[.][v] = DCT16(T[.][v]); in the zigzag prefix z <- (y - Y) + z / D_F and
 //               W = Y + z, else W = Y;                    V[.][v] = IDCT16(W[.][v])
 //   3. rows:    pseudo[r][.] = IDCT16(V[r][.])  =  x + A* z  (IDCT16 o DCT16 = identity: the full
 //               transform of x is already at hand, so pseudo needs one inverse, not x + a second one)
-// The transposes go through the window buffer (x is dead once every thread holds its row), the
-// region's y / z prefixes are staged in RS by cp.async (issued before stage 1) and z goes back
-// coalesced from there.
+// The transposes go through the window buffer (x is dead once every thread holds its row). y and z
+// are read where they lie (a block's prefix is one short run, so the column threads' rank-order
+// accesses stay in L1) and z is written back in place.
 constexpr int kTB = 336;  // per-block transpose tile: 16 rows x pitch 20 (+16: conflict-free between blocks)
 static_assert(16 * kTB <= kMIn * kWP, "transpose tiles fit in the window buffer");
 
-struct RegionRuns {  // the region's payload runs: one per block row (its blocks are consecutive)
-  int row[4];        // region offset of block row j's run (exclusive scan of max(cnt, 0))
-  int total;
-};
-
-__device__ __forceinline__ void region_runs(const int* cnt, RegionRuns& R) {
-  int a = 0;
+// check_finite (recon.cpp:56-65) over a thread's 16 x values: the common case is one compare per
+// value; the first offending index (x-major, kind bit as in x_checks) only on the rare path.
+__device__ __forceinline__ void row_checks(const IdaParams& P, int img, int gr, int gc, const float (&x)[16],
+                                           IdaLaneSums& S) {
+  bool bad = false;
 #pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    if ((b & 3) == 0) R.row[b >> 2] = a;
-    a += max(cnt[b], 0);
+  for (int c = 0; c < 16; ++c) bad |= !(fabsf(x[c]) <= 1e6f);
+  if (bad) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) x_checks(P, img, gr, gc + c, make_float2(x[c], x[c + 1]), S);
+  } else if (P.ref) {
+    const uint8_t* rp = P.ref + (int64_t)img * P.ref_stride + (int64_t)gr * P.ref_pitch + gc;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const double d = (double)rp[c] - (double)x[c];
+      S.sse += d * d;
+    }
   }
-  R.total = a;
-}
-// region offset of block b's prefix
-__device__ __forceinline__ int region_pre(const int* cnt, int b) {
-  int a = 0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a += i < b ? max(cnt[i], 0) : 0;
-  return a;
-}
-// run (block row) of region element e, and its start
-__device__ __forceinline__ int run_of(const RegionRuns& R, int e, int& start) {
-  const int j = (e >= R.row[1]) + (e >= R.row[2]) + (e >= R.row[3]);
-  start = j == 0 ? 0 : (j == 1 ? R.row[1] : (j == 2 ? R.row[2] : R.row[3]));
-  return j;
 }
 
-// Issue the async copies of the region's y (and z) prefixes into RS: y at 0, z at 4096.
-__device__ __forceinline__ void stage_region_yz(const IdaParams& P, int img, const IdaF32Smem& s,
-                                                const RegionRuns& R, float* ys, float* zs, bool need_z) {
-  const int64_t ibase = (int64_t)img * P.y_stride;
-  for (int e = threadIdx.x; e < R.total; e += blockDim.x) {
-    int st;
-    const int j = run_of(R, e, st);  // block row of the element
-    const int64_t g = ibase + s.meta_off[4 * j] + (e - st);
-    cp_async4(ys + e, P.y + g);
-    if (need_z) cp_async4(zs + e, P.z + g);
+__device__ __forceinline__ void load_row16(const float* p, float (&v)[16]) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 a = q[i];
+    v[4 * i] = a.x;
+    v[4 * i + 1] = a.y;
+    v[4 * i + 2] = a.z;
+    v[4 * i + 3] = a.w;
   }
 }
 
 template <class Sm>
 __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
   const int t = threadIdx.x;
-  const bool worker = t < 256;
   const int b = (t >> 4) & 15, lr = t & 15;  // block of the region (row-major) and row / column
   const int br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
-  const bool valid = worker && cnt >= 0;
+  const bool valid = t < 256 && cnt >= 0;
   const bool last = P.pseudo_out == nullptr;
   const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
-  RegionRuns RR;
-  region_runs(s.meta_cnt, RR);
-  float* ys = s.RS;
-  float* zs = s.RS + 4096;
-  stage_region_yz(P, img, s, RR, ys, zs, !P.is_init);
+  const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;  // this thread's image row (stages 1, 3)
   // 1. rows of x
-  float xr[16], T[16];
+  float T[16];
   if (valid) {
-    const float4* src = reinterpret_cast<const float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 v = src[q];
-      xr[4 * q] = v.x;
-      xr[4 * q + 1] = v.y;
-      xr[4 * q + 2] = v.z;
-      xr[4 * q + 3] = v.w;
-    }
-    const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;
-#pragma unroll
-    for (int c = 0; c < 16; c += 2) x_checks(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), S);
+    float xr[16];
+    load_row16(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc, xr);
+    row_checks(P, img, gr, gc, xr, S);
     if (last) {  // the estimate itself (recon.cpp:255-257 clamp on reconstruct's final step)
 #pragma unroll
       for (int c = 0; c < 16; c += 2) store_out(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), make_float2(0.f, 0.f));
@@ -672,74 +673,64 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
 #pragma unroll
     for (int v = 0; v < 16; ++v) tb[v * 20 + lr] = T[v];
   }
-  cp_async_wait_all();
   __syncthreads();
   // 2. columns: v = lr
-  float W[16];
+  float Y[16];  // Y, then W = Y + z over the prefix
   if (valid) {
-    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
-    float Tc[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 v = src[q];
-      Tc[4 * q] = v.x;
-      Tc[4 * q + 1] = v.y;
-      Tc[4 * q + 2] = v.z;
-      Tc[4 * q + 3] = v.w;
-    }
-    float Y[16];
-    abcs_gen::dct16_fwd(Tc, Y);
+    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];  // the block's prefix in y / z
     const unsigned short* rk = zigzag_rank_dev<16>() + lr;
-    const int base = region_pre(s.meta_cnt, b);
-    const int boff = s.meta_off[b];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int k = rk[16 * u];
-      float w = Y[u];
-      if (k < cnt) {
-        const float yv = ys[base + k];
-        if (P.is_init) S.y += (double)yv * (double)yv;  // ||y||^2 (recon.cpp:128)
-        const float zn = z_update(P, yv, Y[u], P.is_init ? 0.f : zs[base + k], (unsigned long long)(boff + k), S, ons);
-        zs[base + k] = zn;
-        w += zn;
-      }
-      W[u] = w;
+    {
+      float Tc[16];
+      load_row16(tb + lr * 20, Tc);
+      abcs_gen::dct16_fwd(Tc, Y);
     }
+    float zsq = 0.f, ysq = 0.f;
+    unsigned long long badz = ~0ull;
+#pragma unroll
+    for (int h = 0; h < 16; h += 4) {  // 4 coefficients' prefix loads in flight at a time
+      int k[4];
+      float yv[4], zo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        k[i] = rk[16 * (h + i)];
+        yv[i] = k[i] < cnt ? __ldg(P.y + pb + k[i]) : 0.f;
+        zo[i] = (k[i] < cnt && !P.is_init) ? P.z[pb + k[i]] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (k[i] < cnt) {
+          const float zn = (yv[i] - Y[h + i]) + ons * zo[i];  // finish_step (recon.cpp:86-88)
+          P.z[pb + k[i]] = zn;
+          zsq = fmaf(zn, zn, zsq);
+          ysq = fmaf(yv[i], yv[i], ysq);
+          if (!isfinite(zn)) {
+            const unsigned long long gi = (unsigned long long)(s.meta_off[b] + k[i]);
+            badz = gi < badz ? gi : badz;
+          }
+          Y[h + i] += zn;  // W = Y + z
+        }
+      }
+    }
+    S.z += (double)zsq;
+    if (P.is_init) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
+    S.badz = badz < S.badz ? badz : S.badz;
     if (lr == 0) S.cnt += (double)cnt;
   }
-  __syncthreads();  // all column loads done (tb is rewritten) and z complete in RS
-  // z back to the payload, coalesced (its runs mirror the staging)
-  {
-    const int64_t ibase = (int64_t)img * P.y_stride;
-    for (int e = t; e < RR.total; e += blockDim.x) {
-      int st;
-      const int j = run_of(RR, e, st);
-      P.z[ibase + s.meta_off[4 * j] + (e - st)] = zs[e];
-    }
-  }
   if (last) return;
+  __syncthreads();  // all column loads of tb done: it takes V
   if (valid) {
     float V[16];
-    abcs_gen::dct16_inv(W, V);
+    abcs_gen::dct16_inv(Y, V);
 #pragma unroll
     for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
   }
   __syncthreads();
   // 3. rows: pseudo = IDCT16 of row r of V
   if (valid) {
-    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
     float Vr[16], O[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 v = src[q];
-      Vr[4 * q] = v.x;
-      Vr[4 * q + 1] = v.y;
-      Vr[4 * q + 2] = v.z;
-      Vr[4 * q + 3] = v.w;
-    }
+    load_row16(tb + lr * 20, Vr);
     abcs_gen::dct16_inv(Vr, O);
-    const int64_t o = (int64_t)img * P.Hc * P.Wc + (int64_t)(R0 + 16 * br + lr) * P.Wc + C0 + 16 * bc;
-    float4* dst = reinterpret_cast<float4*>(P.pseudo_out + o);
+    float4* dst = reinterpret_cast<float4*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc + (int64_t)gr * P.Wc + gc);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
   }
@@ -753,22 +744,15 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
   const bool valid = t < 256 && cnt >= 0;
-  RegionRuns RR;
-  region_runs(s.meta_cnt, RR);
-  float* ys = s.RS;
-  stage_region_yz(P, img, s, RR, ys, nullptr, false);
-  cp_async_wait_all();
-  __syncthreads();
   float* tb = s.in + b * kTB;  // acc (in the same buffer) is written only after the last tb read
-  float V[16];
   if (valid) {
-    float Wc[16];
-    const int base = region_pre(s.meta_cnt, b);
+    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];
     const unsigned short* rk = zigzag_rank_dev<16>() + lr;
+    float Wc[16], V[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int k = rk[16 * u];
-      Wc[u] = k < cnt ? ys[base + k] : 0.f;
+      Wc[u] = k < cnt ? __ldg(P.y + pb + k) : 0.f;
     }
     abcs_gen::dct16_inv(Wc, V);
 #pragma unroll
@@ -777,16 +761,8 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   __syncthreads();
   float O[16];
   if (valid) {
-    const float4* src = reinterpret_cast<const float4*>(tb + lr * 20);
     float Vr[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 v = src[q];
-      Vr[4 * q] = v.x;
-      Vr[4 * q + 1] = v.y;
-      Vr[4 * q + 2] = v.z;
-      Vr[4 * q + 3] = v.w;
-    }
+    load_row16(tb + lr * 20, Vr);
     abcs_gen::dct16_inv(Vr, O);
   }
   __syncthreads();
@@ -970,7 +946,7 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, cons
     }
     __syncthreads();
   } else {
-    denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
+    denoise_region_f32(P, img, s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
   // The fused IDA step (and its warm start) runs the fp32 block phase; an estimate from another
