@@ -319,20 +319,24 @@ __device__ __forceinline__ void l1_prefetch_region_yz(const IdaParams& P, int im
     asm volatile("prefetch.global.L1 [%0];\n" ::"l"(base + o));
 }
 
-__device__ void denoise_region_f32(const IdaParams& P_, int img_, IdaF32Smem& s, int R0, int C0, int H, int W,
-                                   float thr) {
+__device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
   const int lane = threadIdx.x & 31, tp = threadIdx.x >> 5;
-  __syncthreads();  // the window's mbarrier is initialised (thread 0) before anyone waits on it
-  l1_prefetch_region_yz(P_, img_, s);
-  tma_window_wait(&s.win_bar);
+  // The field is centred on a per-region constant cen before the transforms and cen is added back
+  // to the output: D(p - cen) = D(p) - cen exactly (the DC passes the threshold and the weights
+  // sum to one), and the smaller magnitudes cut the fp32 rounding of every butterfly stage (DAMP's
+  // Monte-Carlo divergence differences two denoiser calls and feels that rounding).
+  const float cen = 0.25f * (s.in[35 * kWP + 35] + s.in[35 * kWP + 36] + s.in[36 * kWP + 35] + s.in[36 * kWP + 36]);
+  const float2 mc = make_float2(-cen, -cen);
   // A: row DCTs of the window rows y = lane + 32 j (lanes along rows: conflict-free)
 #pragma unroll 1
   for (int y = lane; y < kMIn; y += 32) {
     const float* src = s.in + y * kWP + 8 * tp;
     const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4),
                  c = *reinterpret_cast<const float4*>(src + 8);
-    const float2 x[8] = {make_float2(a.x, b.x), make_float2(a.y, b.y), make_float2(a.z, b.z), make_float2(a.w, b.w),
-                         make_float2(b.x, c.x), make_float2(b.y, c.y), make_float2(b.z, c.z), make_float2(b.w, c.w)};
+    float2 x[8] = {make_float2(a.x, b.x), make_float2(a.y, b.y), make_float2(a.z, b.z), make_float2(a.w, b.w),
+                   make_float2(b.x, c.x), make_float2(b.y, c.y), make_float2(b.z, c.z), make_float2(b.w, c.w)};
+#pragma unroll
+    for (int n = 0; n < 8; ++n) x[n] = p_add(x[n], mc);
     float2 Y[8];
     dct8_fwd_pair(x, Y);
     float4* d = reinterpret_cast<float4*>(s.RS + y * kRP + 16 * tp);
@@ -403,7 +407,8 @@ __device__ void denoise_region_f32(const IdaParams& P_, int img_, IdaF32Smem& s,
       const int w = max(((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0)), 1);
       const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
       *reinterpret_cast<float4*>(row + 8 * tp + 4) =
-          make_float4((X[4].x + X[0].y) * sc, (X[5].x + X[1].y) * sc, (X[6].x + X[2].y) * sc, (X[7].x + X[3].y) * sc);
+          make_float4(fmaf(X[4].x + X[0].y, sc, cen), fmaf(X[5].x + X[1].y, sc, cen), fmaf(X[6].x + X[2].y, sc, cen),
+                      fmaf(X[7].x + X[3].y, sc, cen));
     }
     q2[j] = make_float4(X[4].y, X[5].y, X[6].y, X[7].y);
   }
@@ -417,7 +422,8 @@ __device__ void denoise_region_f32(const IdaParams& P_, int img_, IdaF32Smem& s,
       const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
       float4* d = reinterpret_cast<float4*>(s.acc + kMOff + yr * kMP + 8 * tp + 4);
       const float4 a = *d;
-      *d = make_float4((a.x + q2[j].x) * sc, (a.y + q2[j].y) * sc, (a.z + q2[j].z) * sc, (a.w + q2[j].w) * sc);
+      *d = make_float4(fmaf(a.x + q2[j].x, sc, cen), fmaf(a.y + q2[j].y, sc, cen), fmaf(a.z + q2[j].z, sc, cen),
+                       fmaf(a.w + q2[j].w, sc, cen));
     }
   }
   __syncthreads();
@@ -505,6 +511,29 @@ __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax
   return zn;
 }
 
+
+// Power-of-two rescale keeping the fp16 hi/lo operand split in range (as decode16_kernel): when any
+// of the warp's 8-per-lane values exceeds kIdaSafeMax, scale them all by 2^-e (exact) and return
+// 2^e for the result; warp-uniform, and the common case costs one compare per value.
+constexpr float kIdaSafeMax = 8192.f;
+__device__ __forceinline__ float fp16_range_scale(float (&v)[8]) {
+  bool big = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) big |= !(fabsf(v[i]) <= kIdaSafeMax);
+  if (!__any_sync(0xffffffffu, big)) return 1.f;
+  float mx = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(v[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (!isfinite(mx) || mx <= kIdaSafeMax) return 1.f;  // non-finite: check_finite reports it
+  int e;
+  frexpf(mx / kIdaSafeMax, &e);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = ldexpf(v[i], -e);
+  return ldexpf(1.f, e);
+}
+
 // ---- B = 16: one sensing block per warp step ---------------------------------------------
 // init: acc <- A* y (the warm start x0, recon.cpp:119-131)
 template <class Sm>
@@ -569,7 +598,14 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, Sm& s
       xv[j][2] = b.x;
       xv[j][3] = b.y;
     }
-    const Acc16 Yt = dct16_fwd_f32_t(s.f16, xv);  // (A x)^T in slot layout
+    float xs[8] = {xv[0][0], xv[0][1], xv[0][2], xv[0][3], xv[1][0], xv[1][1], xv[1][2], xv[1][3]};
+    const float xsc = fp16_range_scale(xs);
+    const float xin[2][4] = {{xs[0], xs[1], xs[2], xs[3]}, {xs[4], xs[5], xs[6], xs[7]}};
+    Acc16 Yt = dct16_fwd_f32_t(s.f16, xin);  // (A x)^T in slot layout
+    if (xsc != 1.f) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Yt.v[q >> 2][q & 3] *= xsc;
+    }
     stage_yz_wait(P, cnt, yb, S);
     Acc16 Zm;
 #pragma unroll
@@ -586,7 +622,19 @@ __device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, Sm& s
     __syncwarp();
     for (int k = lane; k < cnt; k += 32) P.z[off + k] = zb[k];
     Acc16 Az;
-    if (!last) Az = dct16_inv_from_yt_t(s.f16, Zm);
+    if (!last) {
+      float zs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) zs[q] = Zm.v[q >> 2][q & 3];
+      const float zsc = fp16_range_scale(zs);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Zm.v[q >> 2][q & 3] = zs[q];
+      Az = dct16_inv_from_yt_t(s.f16, Zm);
+      if (zsc != 1.f) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) Az.v[q >> 2][q & 3] *= zsc;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -946,7 +994,10 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, cons
     }
     __syncthreads();
   } else {
-    denoise_region_f32(P, img, s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
+    __syncthreads();  // the window's mbarrier is initialised (thread 0) before anyone waits on it
+    l1_prefetch_region_yz(P, img, s);
+    tma_window_wait(&s.win_bar);
+    denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
   // The fused IDA step (and its warm start) runs the fp32 block phase; an estimate from another
@@ -959,17 +1010,21 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, cons
   reduce_and_finish(P, img, region, s, S);
 }
 
-// Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109).
+// Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109): the IDA step's fp32
+// denoiser (denoise_region_f32) over 64 x 64 regions, the window by cp.async (any field stride).
 template <bool kVec>
-__global__ void __launch_bounds__(kMThreads, 3)
-denoise_mma_kernel(const float* __restrict__ field, int H, int W, int64_t stride, const double* __restrict__ thr,
+__global__ void __launch_bounds__(kFThreads, 3)
+denoise_f32_kernel(const float* __restrict__ field, int H, int W, int64_t stride, const double* __restrict__ thr,
                    float* __restrict__ out, int regions_x) {
-  __shared__ __align__(16) IdaMmaSmem s;
+  extern __shared__ __align__(128) unsigned char den_smem_raw[];
+  IdaF32Smem& s = *reinterpret_cast<IdaF32Smem*>(den_smem_raw + ((128 - (smem_u32(den_smem_raw) & 127)) & 127));
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / regions_x) * kMR, C0 = (region % regions_x) * kMR;
-  load_window<kVec>(field + (int64_t)img * stride, W, R0, C0, H, W, s.in);
-  denoise_region_mma<false>(s.in, s.acc, R0, C0, H, W, (float)thr[img]);
-  for (int i = threadIdx.x; i < kMR * kMR; i += kMThreads) {
+  load_window<kVec, kWP>(field + (int64_t)img * stride, W, R0, C0, H, W, s.in);
+  cp_async_wait_all();
+  __syncthreads();
+  denoise_region_f32(s, R0, C0, H, W, (float)thr[img]);
+  for (int i = threadIdx.x; i < kMR * kMR; i += blockDim.x) {
     const int r = i / kMR, c = i % kMR;
     if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s.acc[kMOff + r * kMP + c];
   }
@@ -979,16 +1034,23 @@ int launch_denoise(Ctx* ctx, const float* field, int32_t h, int32_t w, int64_t s
                    const double* thresholds_dev, float* out, cudaStream_t s) {
   const int rx = (w + kMR - 1) / kMR, ry = (h + kMR - 1) / kMR;
   const bool vec = (w % 4 == 0) && (stride % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0);
+  const int bytes = (int)sizeof(IdaF32Smem) + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(denoise_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(denoise_f32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr = true;
+  }
   for (int done = 0; done < n;) {
     const int cnt = std::min(n - done, 65535);
     const dim3 grid(rx * ry, cnt);
     const int kt = ktimer_begin(ctx, s, "denoise");
     if (vec)
-      denoise_mma_kernel<true><<<grid, kMThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
-                                                           thresholds_dev + done, out + (int64_t)done * stride, rx);
+      denoise_f32_kernel<true><<<grid, kFThreads, bytes, s>>>(field + (int64_t)done * stride, h, w, stride,
+                                                               thresholds_dev + done, out + (int64_t)done * stride, rx);
     else
-      denoise_mma_kernel<false><<<grid, kMThreads, 0, s>>>(field + (int64_t)done * stride, h, w, stride,
-                                                            thresholds_dev + done, out + (int64_t)done * stride, rx);
+      denoise_f32_kernel<false><<<grid, kFThreads, bytes, s>>>(field + (int64_t)done * stride, h, w, stride,
+                                                                thresholds_dev + done, out + (int64_t)done * stride, rx);
     ktimer_end(ctx, s, kt);
     ctx->launches++;
     done += cnt;
