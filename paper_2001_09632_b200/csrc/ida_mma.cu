@@ -703,16 +703,21 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
   const bool last = P.pseudo_out == nullptr;
   const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
   const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;  // this thread's image row (stages 1, 3)
-  // 1. rows of x
-  float T[16];
+  // 1. rows of x. Each block is centred on its centre pixel cb before the transforms (the transform
+  // of x - cb is that of x less 16 cb at the DC; pseudo gets cb back): smaller magnitudes, less
+  // fp32 rounding in every butterfly stage.
+  float T[16], cb = 0.f;
   if (valid) {
     float xr[16];
     load_row16(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc, xr);
+    cb = s.acc[kMOff + (16 * br + 8) * kMP + 16 * bc + 8];
     row_checks(P, img, gr, gc, xr, S);
     if (last) {  // the estimate itself (recon.cpp:255-257 clamp on reconstruct's final step)
 #pragma unroll
       for (int c = 0; c < 16; c += 2) store_out(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), make_float2(0.f, 0.f));
     }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) xr[c] -= cb;
     abcs_gen::dct16_fwd(xr, T);
   }
   __syncthreads();  // every x row is in registers: the window buffer takes the transposes
@@ -747,7 +752,9 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (k[i] < cnt) {
-          const float zn = (yv[i] - Y[h + i]) + ons * zo[i];  // finish_step (recon.cpp:86-88)
+          // finish_step (recon.cpp:86-88); the centred transform's DC lacks 16 cb (exact)
+          const float ya = (h + i == 0 && lr == 0) ? yv[i] - 16.f * cb : yv[i];
+          const float zn = (ya - Y[h + i]) + ons * zo[i];
           P.z[pb + k[i]] = zn;
           zsq = fmaf(zn, zn, zsq);
           ysq = fmaf(yv[i], yv[i], ysq);
@@ -780,7 +787,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     abcs_gen::dct16_inv(Vr, O);
     float4* dst = reinterpret_cast<float4*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc + (int64_t)gr * P.Wc + gc);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q] + cb, O[4 * q + 1] + cb, O[4 * q + 2] + cb, O[4 * q + 3] + cb);
   }
 }
 
@@ -793,6 +800,7 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   const int cnt = s.meta_cnt[b];
   const bool valid = t < 256 && cnt >= 0;
   float* tb = s.in + b * kTB;  // acc (in the same buffer) is written only after the last tb read
+  float cb = 0.f;
   if (valid) {
     const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];
     const unsigned short* rk = zigzag_rank_dev<16>() + lr;
@@ -802,10 +810,15 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
       const int k = rk[16 * u];
       Wc[u] = k < cnt ? __ldg(P.y + pb + k) : 0.f;
     }
+    if (lr == 0) {  // centre on the block mean y00 / 16: out of the transform, added back after
+      cb = Wc[0] * 0.0625f;
+      Wc[0] = 0.f;
+    }
     abcs_gen::dct16_inv(Wc, V);
 #pragma unroll
     for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
   }
+  cb = __shfl_sync(0xffffffffu, cb, threadIdx.x & 16);  // from the block's column-0 thread
   __syncthreads();
   float O[16];
   if (valid) {
@@ -817,7 +830,7 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   if (valid) {
     float4* dst = reinterpret_cast<float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q], O[4 * q + 1], O[4 * q + 2], O[4 * q + 3]);
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q] + cb, O[4 * q + 1] + cb, O[4 * q + 2] + cb, O[4 * q + 3] + cb);
   }
   __syncthreads();
 }
@@ -984,7 +997,6 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, cons
     }
     __syncthreads();
   } else if (P.x_in) {  // x from another denoiser: load the region
-    if (B == 16 && threadIdx.x < 32) fill_frag16_tab(s.f16);
     const float* xs = P.x_in + (int64_t)img * P.Hc * P.Wc;
     for (int i = threadIdx.x; i < kMR * kMR / 4; i += blockDim.x) {
       const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
@@ -1000,12 +1012,7 @@ __global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, cons
     denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
-  // The fused IDA step (and its warm start) runs the fp32 block phase; an estimate from another
-  // denoiser (ISTA / AMP / DAMP, x_in) keeps the tensor-core one whose pseudo = x + A* z is the
-  // reference's formula term by term (DAMP's Monte-Carlo divergence differences two denoiser
-  // calls on that pseudo and is the most rounding-sensitive path: measured 5e-4 vs 1.2e-3 px).
-  if (B == 16 && !P.x_in) block_phase16_f32(P, img, R0, C0, s, S);
-  else if (B == 16) block_phase16(P, img, R0, C0, s, S);
+  if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
   else block_phase8(P, img, R0, C0, s, S);
   reduce_and_finish(P, img, region, s, S);
 }
