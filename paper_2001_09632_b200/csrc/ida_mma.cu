@@ -29,23 +29,10 @@
 
 namespace abcs_b200 {
 
-constexpr int kMThreads = 256;
-constexpr int kMWarps = kMThreads / 32;
 constexpr int kMR = 64;          // output region side
 constexpr int kMIn = kMR + 8;    // 72: region + 4-px halo each side
 constexpr int kMP = 72;          // smem row pitch (floats): 72 = 8 mod 32 -> conflict-free float2 fragments
 
-struct IdaMmaSmem {
-  float in[kMIn * kMP];   // field window; reused as per-warp y/z staging in the block phase
-  float acc[kMIn * kMP];  // denoiser accumulator over the window (region at +4, +4), then x
-  Frag16Tab f16;          // B = 16 fragments (block phase / init), filled by warp 0 at kernel start
-  int meta_cnt[64];       // the region's sensing blocks (row-major): counts and image-relative offsets,
-  int meta_off[64];       // fetched at kernel start so the block phase does not wait on them
-  double red[4][16];
-  unsigned long long bad[2];
-  double mine[4];
-};
-static_assert(kMWarps * 512 <= kMIn * kMP, "staging buffers fit in the window");
 constexpr int kMOff = 4 * kMP + 4;  // region pixel (0, 0) inside acc
 constexpr int kWinBytes = 76 * kMIn * 4;  // the fused kernel's TMA window box (kWP x kMIn floats)
 
@@ -112,132 +99,6 @@ __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t
   }
 }
 
-// Soft threshold sign(c) * max(|c| - t, 0) as c - clamp(c, -t, t): the same fp32
-// result for every finite c (c -/+ t is exactly |c| - t with c's sign), and t = 0
-// is the identity (the DC pass-through, denoise.cpp:76).
-__device__ __forceinline__ float soft(float c, float t) { return c - fminf(fmaxf(c, -t), t); }
-
-// The tile pairs of each parity phase: tiles (PA + 2a, PB + 2b) are disjoint; the phase's
-// tiles are taken two at a time (consecutive in row-major order) per warp step. Per pair:
-// x = window offsets of the two tile origins (lo16, hi16; an odd last tile repeats the first),
-// y = tile codes ti << 8 | tj (lo16, hi16; 0xffff: no second tile).
-constexpr int kPairsMax = 41;
-struct DenoisePairs {
-  uint2 e[4][kPairsMax];
-};
-constexpr DenoisePairs make_denoise_pairs() {
-  DenoisePairs d{};
-  for (int ph = 0; ph < 4; ++ph) {
-    const int PA = ph >> 1, PB = ph & 1, NA = PA ? 8 : 9, NB = PB ? 8 : 9, NT = NA * NB;
-    for (int p = 0; p < kPairsMax; ++p) {
-      const int k1 = 2 * p < NT ? 2 * p : 0, k2 = 2 * p + 1 < NT ? 2 * p + 1 : k1;
-      const int ti1 = PA + 2 * (k1 / NB), tj1 = PB + 2 * (k1 % NB), ti2 = PA + 2 * (k2 / NB), tj2 = PB + 2 * (k2 % NB);
-      const unsigned o1 = 4 * ti1 * kMP + 4 * tj1, o2 = 4 * ti2 * kMP + 4 * tj2;
-      const unsigned c1 = (unsigned)(ti1 << 8 | tj1), c2 = k2 != k1 ? (unsigned)(ti2 << 8 | tj2) : 0xffffu;
-      d.e[ph][p] = uint2{o1 | o2 << 16, c1 | c2 << 16};
-    }
-  }
-  return d;
-}
-__constant__ DenoisePairs kDenoisePairs = make_denoise_pairs();
-
-// One tile pair of phase PH (PH = 2 PA + PB) per warp step.
-// kDcSkip: a tile pair whose AC coefficients all threshold to zero takes its DC / 8 directly
-// (the inverse of a DC-only block) instead of the inverse transform; used by the IDA step, not by
-// the standalone denoiser that DAMP's Monte-Carlo divergence differentiates.
-template <int PH, bool kInterior, bool kDcSkip>
-__device__ __forceinline__ void denoise_pair(const float* in, float* acc, const Frag8& f, int lane_off, int R0, int C0,
-                                             int H, int W, float thr, float thr_dc, int p) {
-  const uint2 e = kDenoisePairs.e[PH][p];
-  const int o1 = (int)(e.x & 0xffffu) + lane_off, o2 = (int)(e.x >> 16) + lane_off;
-  bool v1 = true, v2 = (e.y >> 16) != 0xffffu;
-  if (!kInterior) {  // tile origins must lie on the image's origin grid (denoise.cpp:57-62)
-    const int ti1 = (e.y >> 8) & 0xff, tj1 = e.y & 0xff, ti2 = e.y >> 24, tj2 = (e.y >> 16) & 0xff;
-    v1 = (unsigned)(R0 - 4 + 4 * ti1) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj1) <= (unsigned)(W - 8);
-    v2 = v2 && (unsigned)(R0 - 4 + 4 * ti2) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj2) <= (unsigned)(W - 8);
-  }
-  float Y[4], X[4];
-  dct8x2_fwdT(f, *reinterpret_cast<const float2*>(in + o1), *reinterpret_cast<const float2*>(in + o2), Y);
-  // Y^T slots: 0/1 -> tile 1 (row g, cols 2t, 2t+1), 2/3 -> tile 2; DC = slots 0/2 of lane 0
-  Y[0] = soft(Y[0], thr_dc);
-  Y[1] = soft(Y[1], thr);
-  Y[2] = soft(Y[2], thr_dc);
-  Y[3] = soft(Y[3], thr);
-  const bool ac = !kDcSkip || Y[1] != 0.f || Y[3] != 0.f || (thr_dc != 0.f && (Y[0] != 0.f || Y[2] != 0.f));
-  if (!kDcSkip || __any_sync(0xffffffffu, ac)) {
-    dct8x2_inv_from_yt(f, Y, X);
-  } else {  // every AC coefficient of both tiles thresholded away: each tile is its DC / 8
-    const float d1 = __shfl_sync(0xffffffffu, Y[0], 0) * 0.125f, d2 = __shfl_sync(0xffffffffu, Y[2], 0) * 0.125f;
-    X[0] = X[1] = d1;
-    X[2] = X[3] = d2;
-  }
-  if (v1) {
-    float2* d = reinterpret_cast<float2*>(acc + o1);
-    *d = fadd2(*d, make_float2(X[0], X[1]));
-  }
-  if (v2) {
-    float2* d = reinterpret_cast<float2*>(acc + o2);
-    *d = fadd2(*d, make_float2(X[2], X[3]));
-  }
-}
-
-template <int PA, int PB, bool kInterior, bool kDcSkip>
-__device__ __forceinline__ void denoise_phase(const float* in, float* acc, const Frag8& f, int R0, int C0, int H, int W,
-                                              float thr, float thr_dc) {
-  constexpr int NA = PA ? 8 : 9, NB = PB ? 8 : 9, NPAIR = (NA * NB + 1) / 2;
-  static_assert(NPAIR <= kPairsMax, "pair table");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lane_off = (lane >> 2) * kMP + 2 * (lane & 3);
-#pragma unroll 1
-  for (int p = warp; p < NPAIR; p += kMWarps)  // (two pairs per warp in flight measured slower: registers)
-    denoise_pair<2 * PA + PB, kInterior, kDcSkip>(in, acc, f, lane_off, R0, C0, H, W, thr, thr_dc, p);
-  __syncthreads();
-}
-
-template <bool kInterior, bool kDcSkip>
-__device__ __forceinline__ void denoise_phases(const float* in, float* acc, const Frag8& f, int R0, int C0, int H,
-                                               int W, float thr, float thr_dc) {
-  denoise_phase<0, 0, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<0, 1, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<1, 0, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  denoise_phase<1, 1, kInterior, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-}
-
-// dct_soft_threshold of the window into acc, normalised on the region (denoise.cpp:90).
-// Expects the window loaded; ends with __syncthreads.
-template <bool kDcSkip>
-__device__ void denoise_region_mma(const float* in, float* acc, int R0, int C0, int H, int W, float thr) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < kMIn * kMP / 4; i += kMThreads) reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  Frag8 f;
-  load_frag8(f);
-  const float thr_dc = lane == 0 ? 0.f : thr;
-  cp_async_wait_all();
-  __syncthreads();
-  if (R0 >= 4 && C0 >= 4 && R0 + kMR + 4 <= H && C0 + kMR + 4 <= W)
-    denoise_phases<true, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  else
-    denoise_phases<false, kDcSkip>(in, acc, f, R0, C0, H, W, thr, thr_dc);
-  // weights: valid tile origins covering the pixel per axis (1 or 2 each) -> exact power-of-two scale;
-  // the 4 pixels of a float4 share their 4-aligned column group
-  for (int i = tid; i < kMR * kMR / 4; i += kMThreads) {
-    const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
-    const int br = (R0 + r) & ~3, bc = C0 + c;
-    const int wr = (br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0);
-    const int wc = (bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0);
-    const int w = wr * wc;
-    const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
-    float4* d = reinterpret_cast<float4*>(acc + kMOff + r * kMP + c);
-    float4 v = *d;
-    v.x *= sc;
-    v.y *= sc;
-    v.z *= sc;
-    v.w *= sc;
-    *d = v;
-  }
-  __syncthreads();
-}
-
 // ---- fp32 denoiser of the IDA step (dct_soft_threshold, denoise.cpp:52-92) ------------------
 // The 17 x 17 tiles (8 x 8, stride 4) over the 72 x 72 window are transformed separably on the
 // CUDA cores with packed-pair butterflies (dct_pair.cuh), and the separability is used twice:
@@ -265,11 +126,10 @@ struct IdaF32Smem {
     float RS[kMIn * kRP];     // stage A output R[y][tp][v][tj parity], overwritten in place by stage B's S
     float stage[kMIn * kRP];  // y / z staging in the block phase
   };
-  Frag16Tab f16;  // tensor-core block phase (estimates from another denoiser, x_in)
   int meta_cnt[64];
   int meta_off[64];
   double red[4][16];
-  unsigned long long bad[2];
+  unsigned int bad[2];
   double mine[4];
   uint64_t win_bar;  // TMA window load (one phase per CTA)
 };
@@ -430,8 +290,9 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
 }
 
 struct IdaLaneSums {
-  double z = 0.0, sse = 0.0, y = 0.0, cnt = 0.0;
-  unsigned long long badx = ~0ull, badz = ~0ull;
+  double z = 0.0, sse = 0.0, y = 0.0;
+  int cnt = 0;
+  unsigned int badx = ~0u, badz = ~0u;  // first offending index (x: index << 1 | kind), < 2^32 per image
 };
 
 // check_finite on x (recon.cpp:56-65) and the trace SSE for one float2 of x at (gr, gc).
@@ -443,7 +304,8 @@ __device__ __forceinline__ void x_checks(const IdaParams& P, int img, int gr, in
     if (!isfinite(xv) || fabsf(xv) > 1e6f) {
       const unsigned long long gi =
           ((unsigned long long)((int64_t)gr * P.Wc + gc + e) << 1) | (isfinite(xv) ? 1ull : 0ull);
-      S.badx = gi < S.badx ? gi : S.badx;
+      const unsigned g32 = (unsigned)min(gi, 0xfffffffeull) | (unsigned)(gi & 1ull);  // kind bit kept
+      S.badx = g32 < S.badx ? g32 : S.badx;
     }
   }
   if (P.ref) {
@@ -507,145 +369,32 @@ __device__ __forceinline__ float z_update(const IdaParams& P, float yv, float ax
                                           IdaLaneSums& S, float onsager) {
   const float zn = (yv - ax) + onsager * zo;  // finish_step (recon.cpp:86-88)
   S.z += (double)zn * (double)zn;
-  if (!isfinite(zn)) S.badz = gi < S.badz ? gi : S.badz;
+  if (!isfinite(zn)) S.badz = (unsigned)gi < S.badz ? (unsigned)gi : S.badz;
   return zn;
 }
 
 
-// Power-of-two rescale keeping the fp16 hi/lo operand split in range (as decode16_kernel): when any
-// of the warp's 8-per-lane values exceeds kIdaSafeMax, scale them all by 2^-e (exact) and return
-// 2^e for the result; warp-uniform, and the common case costs one compare per value.
+
+// Power-of-two rescale keeping the fp16 hi/lo operand split of the B = 8 tensor-core transforms in
+// range (as decode16_kernel): when any of the warp's values exceeds kIdaSafeMax, scale them all by
+// 2^-e (exact) and return 2^e for the result. Warp-uniform; the common case is one compare per value.
 constexpr float kIdaSafeMax = 8192.f;
-__device__ __forceinline__ float fp16_range_scale(float (&v)[8]) {
+__device__ __forceinline__ float fp16_range_scale(float (&v)[4]) {
   bool big = false;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) big |= !(fabsf(v[i]) <= kIdaSafeMax);
+  for (int i = 0; i < 4; ++i) big |= !(fabsf(v[i]) <= kIdaSafeMax);
   if (!__any_sync(0xffffffffu, big)) return 1.f;
   float mx = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(v[i]));
+  for (int i = 0; i < 4; ++i) mx = fmaxf(mx, fabsf(v[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (!isfinite(mx) || mx <= kIdaSafeMax) return 1.f;  // non-finite: check_finite reports it
   int e;
   frexpf(mx / kIdaSafeMax, &e);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = ldexpf(v[i], -e);
+  for (int i = 0; i < 4; ++i) v[i] = ldexpf(v[i], -e);
   return ldexpf(1.f, e);
-}
-
-// ---- B = 16: one sensing block per warp step ---------------------------------------------
-// init: acc <- A* y (the warm start x0, recon.cpp:119-131)
-template <class Sm>
-__device__ void init_x16(const IdaParams& P, int img, int R0, int C0, Sm& s) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  uint32_t rank[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) rank[q] = zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)];
-  float* yb = s.stage + warp * 512;
-  for (int bi = warp; bi < 16; bi += (int)(blockDim.x >> 5)) {
-    const int gbr = R0 / 16 + bi / 4, gbc = C0 / 16 + bi % 4;
-    const int lr0 = (bi / 4) * 16, lc0 = (bi % 4) * 16;
-    int cnt = 0;
-    int64_t off = 0;
-    if (gbr < P.rows && gbc < P.cols) {
-      const int64_t bidx = (int64_t)img * P.rows * P.cols + (int64_t)gbr * P.cols + gbc;
-      cnt = P.counts[bidx];
-      off = (int64_t)img * P.y_stride + P.offsets[bidx];
-    }
-    for (int k = lane; k < cnt; k += 32) yb[k] = __ldg(P.y + off + k);
-    __syncwarp();
-    Acc16 Yt;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) Yt.v[q >> 2][q & 3] = (int)rank[q] < cnt ? yb[rank[q]] : 0.f;
-    const Acc16 X = dct16_inv_from_yt_t(s.f16, Yt);
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        *reinterpret_cast<float2*>(s.acc + kMOff + (lr0 + g + 8 * h) * kMP + lc0 + 8 * j + 2 * t) =
-            make_float2(X.v[j][2 * h], X.v[j][2 * h + 1]);
-    __syncwarp();
-  }
-}
-
-template <class Sm>
-__device__ void block_phase16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const float ons = P.onsager_img ? (float)P.onsager_img[img] : P.onsager;
-  uint32_t rk[2] = {0u, 0u};  // zigzag ranks of the lane's 8 slots, one byte each
-#pragma unroll
-  for (int q = 0; q < 8; ++q) rk[q >> 2] |= zigzag_rank_dev<16>()[dslot_col(q) * 16 + dslot_row(q)] << (8 * (q & 3));
-  float* yb = s.stage + warp * 512;
-  float* zb = yb + 256;
-  const bool last = P.pseudo_out == nullptr;
-  for (int bi = warp; bi < 16; bi += (int)(blockDim.x >> 5)) {
-    const int cnt = s.meta_cnt[bi];
-    if (cnt < 0) continue;  // outside the block grid (warp-uniform)
-    const int lr0 = (bi / 4) * 16, lc0 = (bi % 4) * 16;
-    const int32_t boff = s.meta_off[bi];
-    const int64_t off = (int64_t)img * P.y_stride + boff;
-    stage_yz_async(P, off, cnt, yb, zb, !P.is_init);  // lands while the forward transform runs
-    if (lane == 0) S.cnt += (double)cnt;
-    float xv[2][4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const float* r = s.acc + kMOff + (lr0 + 8 * j + g) * kMP + lc0 + 2 * t;
-      const float2 a = *reinterpret_cast<const float2*>(r);
-      const float2 b = *reinterpret_cast<const float2*>(r + 8);
-      xv[j][0] = a.x;
-      xv[j][1] = a.y;
-      xv[j][2] = b.x;
-      xv[j][3] = b.y;
-    }
-    float xs[8] = {xv[0][0], xv[0][1], xv[0][2], xv[0][3], xv[1][0], xv[1][1], xv[1][2], xv[1][3]};
-    const float xsc = fp16_range_scale(xs);
-    const float xin[2][4] = {{xs[0], xs[1], xs[2], xs[3]}, {xs[4], xs[5], xs[6], xs[7]}};
-    Acc16 Yt = dct16_fwd_f32_t(s.f16, xin);  // (A x)^T in slot layout
-    if (xsc != 1.f) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) Yt.v[q >> 2][q & 3] *= xsc;
-    }
-    stage_yz_wait(P, cnt, yb, S);
-    Acc16 Zm;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int r = (int)((rk[q >> 2] >> (8 * (q & 3))) & 0xffu);
-      float zn = 0.f;
-      if (r < cnt) {
-        zn = z_update(P, yb[r], Yt.v[q >> 2][q & 3], P.is_init ? 0.f : zb[r], (unsigned long long)(boff + r), S,
-                      ons);
-        zb[r] = zn;
-      }
-      Zm.v[q >> 2][q & 3] = zn;
-    }
-    __syncwarp();
-    for (int k = lane; k < cnt; k += 32) P.z[off + k] = zb[k];
-    Acc16 Az;
-    if (!last) {
-      float zs[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) zs[q] = Zm.v[q >> 2][q & 3];
-      const float zsc = fp16_range_scale(zs);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) Zm.v[q >> 2][q & 3] = zs[q];
-      Az = dct16_inv_from_yt_t(s.f16, Zm);
-      if (zsc != 1.f) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) Az.v[q >> 2][q & 3] *= zsc;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int lr = lr0 + g + 8 * h, lc = lc0 + 8 * j + 2 * t;
-        const float2 x = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc);
-        x_checks(P, img, R0 + lr, C0 + lc, x, S);
-        store_out(P, img, R0 + lr, C0 + lc, x, last ? make_float2(0.f, 0.f) : make_float2(Az.v[j][2 * h], Az.v[j][2 * h + 1]));
-      }
-    __syncwarp();
-  }
 }
 
 // ---- B = 16 block phase on the CUDA cores (recon.cpp:81-93, 75-79; operators.cpp:50-76) ------
@@ -738,7 +487,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
       abcs_gen::dct16_fwd(Tc, Y);
     }
     float zsq = 0.f, ysq = 0.f;
-    unsigned long long badz = ~0ull;
+    unsigned int badz = ~0u;
 #pragma unroll
     for (int h = 0; h < 16; h += 4) {  // 4 coefficients' prefix loads in flight at a time
       int k[4];
@@ -759,7 +508,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
           zsq = fmaf(zn, zn, zsq);
           ysq = fmaf(yv[i], yv[i], ysq);
           if (!isfinite(zn)) {
-            const unsigned long long gi = (unsigned long long)(s.meta_off[b] + k[i]);
+            const unsigned int gi = (unsigned)(s.meta_off[b] + k[i]);
             badz = gi < badz ? gi : badz;
           }
           Y[h + i] += zn;  // W = Y + z
@@ -769,7 +518,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     S.z += (double)zsq;
     if (P.is_init) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
     S.badz = badz < S.badz ? badz : S.badz;
-    if (lr == 0) S.cnt += (double)cnt;
+    if (lr == 0) S.cnt += cnt;
   }
   if (last) return;
   __syncthreads();  // all column loads of tb done: it takes V
@@ -869,7 +618,10 @@ __device__ void init_x8(const IdaParams& P, int img, int R0, int C0, Sm& s) {
       Yt[i] = r < cnt[q] ? yb[64 * q + r] : 0.f;
     }
     float X[4];
+    const float ysc = fp16_range_scale(Yt);
     dct8x2_inv_from_yt(f, Yt, X);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) X[i] *= ysc;
     const int lr = 8 * br + g, lc = 8 * bc + 2 * t;
     *reinterpret_cast<float2*>(s.acc + kMOff + lr * kMP + lc) = make_float2(X[0], X[1]);
     *reinterpret_cast<float2*>(s.acc + kMOff + lr * kMP + lc + 8) = make_float2(X[2], X[3]);
@@ -899,12 +651,15 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, Sm& s,
     const int64_t ibase = (int64_t)img * P.y_stride;
     stage_yz_async(P, ibase + boff[0], cnt[0], yb, zb, !P.is_init);
     stage_yz_async(P, ibase + boff[1], cnt[1], yb + 64, zb + 64, !P.is_init);
-    if (lane == 0) S.cnt += (double)(cnt[0] + cnt[1]);
+    if (lane == 0) S.cnt += cnt[0] + cnt[1];
     const int lr = 8 * br + g, lc = 8 * bc + 2 * t;
     const float2 x0 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc);
     const float2 x1 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc + 8);
-    float Yt[4];
-    dct8x2_fwdT(f, x0, x1, Yt);
+    float Yt[4], xs[4] = {x0.x, x0.y, x1.x, x1.y};
+    const float xsc = fp16_range_scale(xs);
+    dct8x2_fwdT(f, make_float2(xs[0], xs[1]), make_float2(xs[2], xs[3]), Yt);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Yt[i] *= xsc;
     cp_async_wait_all();
     __syncwarp();
     if (P.is_init)  // ||y||^2 (recon.cpp:128), block 0 then block 1 as staged
@@ -926,7 +681,12 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, Sm& s,
     for (int k = lane; k < cnt[0]; k += 32) P.z[ibase + boff[0] + k] = zb[k];
     for (int k = lane; k < cnt[1]; k += 32) P.z[ibase + boff[1] + k] = zb[64 + k];
     float Az[4] = {0.f, 0.f, 0.f, 0.f};
-    if (!last) dct8x2_inv_from_yt(f, Zm, Az);
+    if (!last) {
+      const float zsc = fp16_range_scale(Zm);
+      dct8x2_inv_from_yt(f, Zm, Az);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) Az[i] *= zsc;
+    }
     x_checks(P, img, R0 + lr, C0 + lc, x0, S);
     store_out(P, img, R0 + lr, C0 + lc, x0, make_float2(Az[0], Az[1]));
     if (has1) {
@@ -942,8 +702,8 @@ template <class Sm>
 __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s, IdaLaneSums& S) {
   const int tid = threadIdx.x;
   if (tid == 0) {
-    s.bad[0] = ~0ull;
-    s.bad[1] = ~0ull;
+    s.bad[0] = ~0u;
+    s.bad[1] = ~0u;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -957,10 +717,10 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s
     s.red[0][tid >> 5] = S.z;
     s.red[1][tid >> 5] = S.sse;
     s.red[2][tid >> 5] = S.y;
-    s.red[3][tid >> 5] = S.cnt;
+    s.red[3][tid >> 5] = (double)S.cnt;
   }
-  if (S.badx != ~0ull) atomicMin(&s.bad[0], S.badx);
-  if (S.badz != ~0ull) atomicMin(&s.bad[1], S.badz);
+  if (S.badx != ~0u) atomicMin(&s.bad[0], S.badx);
+  if (S.badz != ~0u) atomicMin(&s.bad[1], S.badz);
   __syncthreads();
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) {
@@ -968,8 +728,8 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += s.red[q][w];
       s.mine[q] = a;
     }
-    if (s.bad[0] != ~0ull) atomicMin(P.badx + img, s.bad[0]);
-    if (s.bad[1] != ~0ull) atomicMin(P.badz + img, s.bad[1]);
+    if (s.bad[0] != ~0u) atomicMin(P.badx + img, (unsigned long long)s.bad[0]);
+    if (s.bad[1] != ~0u) atomicMin(P.badz + img, (unsigned long long)s.bad[1]);
   }
   finish_image(P, img, region, s.mine);
 }
