@@ -115,6 +115,9 @@ __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t
 constexpr int kWP = 76;            // window pitch: 72 + 4 zero columns (A reads 12 px from col 8 tp)
 constexpr int kTP = 9;             // segment pairs per row (tj = 17 is a zero dummy)
 constexpr int kRP = kTP * 16 + 4;  // R / S row pitch: [tp][v][2] + 4 (148 = 20 mod 32: conflict-free)
+#ifndef IDA_MINB
+#define IDA_MINB 3
+#endif
 constexpr int kFThreads = 32 * kTP;  // fused kernel: warp w owns segment pair tp = w through stages A-C
 
 struct IdaF32Smem {
@@ -735,7 +738,7 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s
 }
 
 template <int B>
-__global__ void __launch_bounds__(kFThreads, 3) ida_mma_kernel(IdaParams P, const __grid_constant__ CUtensorMap win_map) {
+__global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams P, const __grid_constant__ CUtensorMap win_map) {
   extern __shared__ __align__(128) unsigned char ida_smem_raw[];
   IdaF32Smem& s = *reinterpret_cast<IdaF32Smem*>(ida_smem_raw + ((128 - (smem_u32(ida_smem_raw) & 127)) & 127));
   const int img = blockIdx.y, region = blockIdx.x;

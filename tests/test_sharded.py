@@ -216,8 +216,9 @@ def test_rn64_rounding():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [1, 2, 3, 5])
-def test_device_shard_allocation(k):
-    """The device phases, k shards in one process: equal to the single-GPU allocator."""
+def test_device_shard_allocation(k, checker):
+    """The device phases, k shards in one process: equal to the reference allocator
+    (largest_remainder_allocate, sensing.cpp:110-177) through the oracle."""
     import torch
 
     import paper_2001_09632_b200 as p
@@ -234,17 +235,18 @@ def test_device_shard_allocation(k):
         offs = [torch.empty(s.nb, dtype=torch.int32, device="cuda") for s in shards]
         allocate_sharded(shards, comm, budget, counts, offs)
         got = np.concatenate([c.cpu().numpy().view(np.uint16).astype(np.int64) for c in counts])
-        want = p.largest_remainder_allocate(w.astype(np.float64), budget, np.full(n, cap, np.int32))
-        assert np.array_equal(got, np.asarray(want)), (n, k)
+        want = checker.allocate(w.astype(np.float64), budget, np.full(n, cap, np.int32))
+        assert np.array_equal(got, np.asarray(want, dtype=np.int64)), (n, k)
         assert np.array_equal(np.concatenate([o.cpu().numpy() for o in offs]), np.cumsum(got) - got)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("H,W,num,den,k", [(2048, 2048, 1, 4, 4), (1024, 1536, 3, 10, 3), (1000, 1000, 1, 2, 2),
                                            (512, 512, 1, 4, 1)])
-def test_sharded_sense_decode_equals_whole_image(H, W, num, den, k):
+def test_sharded_sense_decode_equals_whole_image(H, W, num, den, k, checker):
     """DD sense + decode of one image split into k block-row strips: counts, offsets, payload
-    slices and decoded rows equal the single-GPU sense_decode_batch of the whole image."""
+    slices and decoded rows equal the single-GPU sense_decode_batch of the whole image, and the
+    reference (oracle): counts bit-exact, payload within the fp32 bound, pixels within 1e-3."""
     import torch
 
     import paper_2001_09632_b200 as p
@@ -263,6 +265,14 @@ def test_sharded_sense_decode_equals_whole_image(H, W, num, den, k):
         assert torch.equal(r.offsets, b.offsets[0, sl])
         assert torch.equal(r.payload, b.payload[0, r.payload_offset:r.payload_offset + r.payload.numel()])
         assert torch.equal(r.decoded, x[0, cuts[j] * 16:cuts[j + 1] * 16])
+    host = img[0].cpu().numpy()
+    want = checker.sense(host, 16, num, den, 2)
+    got_counts = np.concatenate([r.counts.cpu().numpy().view(np.uint16) for r in res]).astype(np.int64)
+    assert np.array_equal(got_counts, want["counts"].astype(np.int64))
+    got_pay = np.concatenate([r.payload.cpu().numpy() for r in res]).astype(np.float64)
+    assert np.max(np.abs(got_pay - want["coeffs"])) <= 2e-3
+    ref = checker.decode(rows, cols, 16, want["counts"], want["coeffs"])
+    assert np.max(np.abs(torch.cat([r.decoded for r in res]).cpu().numpy() - ref)) <= 1e-3
 
 
 @pytest.mark.gpu
@@ -284,9 +294,9 @@ def test_sharded_sense_zz():
 @pytest.mark.gpu
 @pytest.mark.parametrize("H,W,B,num,den,k", [(1024, 1024, 16, 3, 10, 3), (1080, 1920, 8, 1, 5, 4),
                                              (1000, 1480, 16, 1, 4, 2)])
-def test_sharded_sense_bbv(H, W, B, num, den, k):
+def test_sharded_sense_bbv(H, W, B, num, den, k, checker):
     """BBV on strips (bottom probes read the next strip's first row): weights, side values,
-    counts, payload and decoded rows equal the whole-image sense."""
+    counts, payload and decoded rows equal the whole-image sense and the reference (oracle)."""
     import torch
 
     import paper_2001_09632_b200 as p
@@ -307,13 +317,20 @@ def test_sharded_sense_bbv(H, W, B, num, den, k):
         assert torch.equal(r.side, b.side[0, r.side_offset:r.side_offset + r.side.numel()]), j
         assert torch.equal(r.decoded, x[0, cuts[j] * B:cuts[j + 1] * B]), j
     assert sum(r.side.numel() for r in res) == b.side.shape[1]
+    want = checker.sense(img[0].cpu().numpy(), B, num, den, 1)
+    assert np.array_equal(np.concatenate([r.counts.cpu().numpy().view(np.uint16) for r in res]).astype(np.int64),
+                          want["counts"].astype(np.int64))
+    assert np.array_equal(np.concatenate([r.side.cpu().numpy() for r in res]).astype(np.float64), want["side"])
+    ref = checker.decode(b.plan.rows, cols, B, want["counts"], want["coeffs"])
+    assert np.max(np.abs(torch.cat([r.decoded for r in res]).cpu().numpy() - ref)) <= 1e-3
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("H,W,k", [(1024, 768, 3), (512, 512, 2)])
-def test_sharded_ida_matches_whole_image(H, W, k):
+def test_sharded_ida_matches_whole_image(H, W, k, checker):
     """IDA (dct_threshold) on k block-row strips with halo exchange and sigma all-reduce: the
-    estimate matches the single-GPU reconstruct of the whole image (1e-3 bar, PSNR 0.01 dB)."""
+    estimate matches the reference's reconstruct (oracle) and the single-GPU reconstruct of the
+    whole image (1e-3 bar, PSNR 0.01 dB)."""
     import torch
 
     import paper_2001_09632_b200 as p
@@ -334,3 +351,9 @@ def test_sharded_ida_matches_whole_image(H, W, k):
     ref = img[0].double()
     mse = lambda x: float(((x.double() - ref) ** 2).mean())  # noqa: E731
     assert abs(10 * np.log10(255 ** 2 / mse(got)) - 10 * np.log10(255 ** 2 / mse(whole[0]))) <= 0.01
+    host = img[0].cpu().numpy()
+    want = checker.sense(host, 16, 1, 4, 2)
+    xr, _ = checker.reconstruct_ida(b.plan.rows, b.plan.cols, 16, want["counts"], want["coeffs"], 6, ref=host)
+    assert float(np.max(np.abs(got.cpu().numpy() - xr))) <= 1e-3
+    psnr_ref = 10 * np.log10(255 ** 2 / np.mean((xr - host.astype(np.float64)) ** 2))
+    assert abs(10 * np.log10(255 ** 2 / mse(got)) - psnr_ref) <= 0.01
