@@ -285,6 +285,13 @@ int abcs_decode_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
                       int32_t out_pitch, const int64_t* d_payload_len, int32_t* d_error,
                       void* stream);
 
+/* BlockDct::forward / inverse (dct.cpp:9-79; replaces abcs::BlockDct, abcs::dct2, abcs::idct2 of
+ * dct.hpp:14-31) on n_blocks row-major size x size fp64 blocks in device memory, any size >= 1.
+ * Bit-identical to the reference: its basis expression (glibc cos) and summation order, no FMA.
+ * inverse = 0: pixels -> coefficients; 1: coefficients -> pixels. Synchronizes `stream`. */
+int abcs_block_dct_f64(abcs_ctx* ctx, int32_t size, int32_t inverse, const double* d_in, double* d_out,
+                       int64_t n_blocks, void* stream);
+
 /* SensingOperator::forward (operators.cpp:23-48) on f32 fields. */
 int abcs_forward_batch(abcs_ctx* ctx, int32_t rows, int32_t cols, int32_t block,
                        const uint16_t* d_counts, const int32_t* d_offsets, const float* d_field,

@@ -108,6 +108,7 @@ SIGNATURES = {
     "abcs_allocate_batch": (C.c_int, [P, P, I32, I32, I64, P, I32, I32, P, P, P, P]),
     "abcs_decode_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, P, I64, I32, P, P, P]),
     "abcs_forward_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, I32, P, I64, P]),
+    "abcs_block_dct_f64": (C.c_int, [P, I32, I32, P, P, I64, P]),
     "abcs_denoise_dct_batch": (C.c_int, [P, P, I32, I32, I64, I32, P, D, I32, P, P]),
     "abcs_ida_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, C.POINTER(IdaConfigC),
                                  P, I64, I32, P, I64, I32, P, P, P]),

@@ -478,6 +478,33 @@ def bench_cells_host(images, cfgs, device=0, chunk=64, ssim=True):
     return cells
 
 
+def block_dct_batch(blocks, inverse: bool = False):
+    """BlockDct::forward / inverse (dct.cpp:9-79) on a (n, B, B) float64 device tensor, any B >= 1:
+    fp64, bit-identical to the reference (abcs_block_dct_f64)."""
+    torch = _torch()
+    if blocks.dim() != 3 or blocks.shape[1] != blocks.shape[2] or blocks.dtype != torch.float64:
+        raise ValueError("block_dct_batch: expects (n, B, B) float64")
+    x = blocks.contiguous()
+    out = torch.empty_like(x)
+    _check(_lib.load().abcs_block_dct_f64(Context.get(x.device.index).handle, x.shape[1], 1 if inverse else 0,
+                                          _ptr(x), _ptr(out), x.shape[0], _stream_ptr(torch)))
+    return out
+
+
+def dct2(block, size: int) -> np.ndarray:
+    """abcs::dct2 (dct.hpp:30): one size x size block (row-major values), on the device."""
+    torch = _torch()
+    b = torch.as_tensor(np.asarray(block, np.float64).reshape(1, size, size), device="cuda")
+    return block_dct_batch(b).reshape(-1).cpu().numpy()
+
+
+def idct2(coeffs, size: int) -> np.ndarray:
+    """abcs::idct2 (dct.hpp:31)."""
+    torch = _torch()
+    b = torch.as_tensor(np.asarray(coeffs, np.float64).reshape(1, size, size), device="cuda")
+    return block_dct_batch(b, inverse=True).reshape(-1).cpu().numpy()
+
+
 def decode_batch(batch: MeasurementBatch, out=None):
     """decode_idct on every set of the batch -> (n, Hc, Wc) float32 CUDA tensor."""
     torch = _torch()

@@ -155,6 +155,7 @@ int abcs_ctx_kernel_times(abcs_ctx* c, abcs_kernel_time* out, int32_t capacity, 
 
 int abcs_sense_weights_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
                              int32_t pitch, int32_t n, uint32_t* d_weights, float* d_side, void* stream) {
+  ABCS_NVTX("abcs_sense_weights_batch");
   CHECK_CTX(c);
   if (!p || (!d_images && n > 0) || !d_weights || n < 0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
   Ctx* ctx = reinterpret_cast<Ctx*>(c);
@@ -487,6 +488,7 @@ extern "C" {
 int abcs_sense_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
                      int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
                      float* d_side, void* stream) {
+  ABCS_NVTX("abcs_sense_batch");
   CHECK_CTX(c);
   int st = sense_validate(p, d_images, image_stride, pitch, n, d_counts, d_payload, d_side);
   if (st || n == 0) return st;
@@ -500,6 +502,7 @@ int abcs_sense_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_ima
 int abcs_sense_decode_batch(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* d_images, int64_t image_stride,
                             int32_t pitch, int32_t n, uint16_t* d_counts, int32_t* d_offsets, float* d_payload,
                             float* d_side, float* d_out, int64_t out_stride, int32_t out_pitch, void* stream) {
+  ABCS_NVTX("abcs_sense_decode_batch");
   CHECK_CTX(c);
   int st = sense_validate(p, d_images, image_stride, pitch, n, d_counts, d_payload, d_side);
   if (st || n == 0) return st;
@@ -518,6 +521,7 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
                                   uint16_t* const* d_counts, int32_t* const* d_offsets, float* const* d_payload,
                                   float* const* d_side, float* const* d_out, int64_t out_stride, int32_t out_pitch,
                                   void* stream) {
+  ABCS_NVTX("abcs_sense_decode_sweep_batch");
   CHECK_CTX(c);
   if (!plans || n_plans < 1 || !d_counts || !d_payload || !d_out)
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -578,6 +582,7 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
 int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
                         const int32_t* d_caps, int32_t cap, int32_t base, uint16_t* d_counts, int32_t* d_offsets,
                         int32_t* d_status, void* stream) {
+  ABCS_NVTX("abcs_allocate_batch");
   CHECK_CTX(c);
   if (n_blocks < 0 || n_vectors < 0 || (n_blocks * (int64_t)n_vectors > 0 && (!d_weights || !d_counts)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -615,6 +620,7 @@ int abcs_gather_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t bl
                              int64_t image_stride, int32_t pitch, int32_t n, const uint16_t* d_counts,
                              const int32_t* d_offsets, float* d_payload, int64_t payload_stride, float* d_out,
                              int64_t out_stride, int32_t out_pitch, void* stream) {
+  ABCS_NVTX("abcs_gather_decode_batch");
   CHECK_CTX(c);
   if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_images || !d_counts || !d_offsets || !d_payload)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -645,6 +651,7 @@ int abcs_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, co
                       const int32_t* d_offsets, const float* d_payload, int64_t payload_stride, int32_t n,
                       float* d_out, int64_t out_stride, int32_t out_pitch, const int64_t* d_payload_len,
                       int32_t* d_error, void* stream) {
+  ABCS_NVTX("abcs_decode_batch");
   CHECK_CTX(c);
   if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_out)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -674,6 +681,7 @@ int abcs_decode_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, co
 int abcs_forward_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
                        const int32_t* d_offsets, const float* d_field, int64_t field_stride, int32_t field_pitch,
                        int32_t n, float* d_y, int64_t y_stride, void* stream) {
+  ABCS_NVTX("abcs_forward_batch");
   CHECK_CTX(c);
   if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_field || !d_y)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -697,6 +705,7 @@ int abcs_forward_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, c
 
 int abcs_denoise_dct_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int64_t field_stride,
                            int32_t n, const double* sigma, double k, int32_t block, float* d_out, void* stream) {
+  ABCS_NVTX("abcs_denoise_dct_batch");
   CHECK_CTX(c);
   if (height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_out || !sigma)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -725,6 +734,7 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
                    const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n, const abcs_ida_config* cfg,
                    const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, float* d_out, int64_t out_stride,
                    int32_t out_pitch, double* d_trace, int32_t* d_diverged, void* stream) {
+  ABCS_NVTX("abcs_ida_batch");
   CHECK_CTX(c);
   if (!cfg) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null config");
   // ReconConfig::validate (recon.cpp:39-43)
@@ -786,6 +796,7 @@ static int ida_state_common(abcs_ctx* c, int32_t rows, int32_t cols, int32_t blo
 int abcs_ida_init_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const uint16_t* d_counts,
                         const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n, int32_t warm,
                         float* d_x, float* d_z, double* d_sigma, void* stream) {
+  ABCS_NVTX("abcs_ida_init_state");
   CHECK_CTX(c);
   if (n == 0) return ABCS_OK;
   char* scr;
@@ -802,6 +813,7 @@ int abcs_ida_step_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, 
                         const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n,
                         const abcs_ida_config* cfg, float* d_x, float* d_z, double* d_sigma, int32_t iteration,
                         int32_t* d_diverged, void* stream) {
+  ABCS_NVTX("abcs_ida_step_state");
   CHECK_CTX(c);
   if (!cfg) return set_error(ABCS_ERR_INVALID_ARGUMENT, "null config");
   if (cfg->damping < 1.0) return set_error(ABCS_ERR_INVALID_ARGUMENT, "damping factor D_F must be >= 1");
@@ -853,6 +865,7 @@ int abcs_ssim_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32
 int abcs_quality_batch(abcs_ctx* c, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch, const float* d_img,
                        int64_t img_stride, int32_t img_pitch, int32_t height, int32_t width, int32_t n,
                        double* d_mse, double* d_psnr, double* d_ssim, void* stream) {
+  ABCS_NVTX("abcs_quality_batch");
   CHECK_CTX(c);
   if (height < 1 || width < 1 || n < 0 || ref_pitch < width || img_pitch < width ||
       (n > 0 && (!d_ref || !d_img || (!d_mse && !d_psnr && !d_ssim))))
@@ -901,6 +914,7 @@ int abcs_reconstruct_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t bloc
                            const abcs_recon_config* cfg, const uint8_t* d_ref, int64_t ref_stride, int32_t ref_pitch,
                            float* d_out, int64_t out_stride, int32_t out_pitch, double* d_trace, int32_t* d_diverged,
                            void* stream) {
+  ABCS_NVTX("abcs_reconstruct_batch");
   CHECK_CTX(c);
   if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_out)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -932,6 +946,7 @@ int abcs_recon_step_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block
                           const int32_t* d_offsets, const float* d_y, int64_t y_stride, int32_t n,
                           const abcs_recon_config* cfg, float* d_x, float* d_z, double* d_sigma, int32_t iteration,
                           int32_t* d_diverged, void* stream) {
+  ABCS_NVTX("abcs_recon_step_state");
   CHECK_CTX(c);
   if (rows < 1 || cols < 1 || n < 0 || (n > 0 && (!d_counts || !d_y || !d_x || !d_z || !d_sigma)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -950,6 +965,7 @@ int abcs_recon_step_state(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block
 
 int abcs_denoise_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int64_t field_stride,
                        int32_t n, const double* sigma, const abcs_recon_config* cfg, float* d_out, void* stream) {
+  ABCS_NVTX("abcs_denoise_batch");
   CHECK_CTX(c);
   if (!cfg || height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_out || !sigma)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -990,6 +1006,7 @@ int abcs_rademacher_probe(abcs_ctx* c, uint64_t seed, int64_t n, float* d_probe,
 int abcs_divergence_batch(abcs_ctx* c, const float* d_field, int32_t height, int32_t width, int32_t n,
                           const double* sigma, const double* epsilon, uint64_t seed, const abcs_recon_config* cfg,
                           double* d_div, void* stream) {
+  ABCS_NVTX("abcs_divergence_batch");
   CHECK_CTX(c);
   if (!cfg || height < 1 || width < 1 || n < 0 || (n > 0 && (!d_field || !d_div || !sigma || !epsilon)))
     return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -1203,6 +1220,7 @@ static int sweep_host_check(const abcs_sense_plan* plans, int32_t n_plans, const
 
 int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
                                  int32_t n, float* const* h_out, int32_t chunk) {
+  ABCS_NVTX("abcs_sense_decode_sweep_host");
   CHECK_CTX(c);
   if (int st = sweep_host_check(plans, n_plans, h_images, n, h_out != nullptr)) return st;
   for (int j = 0; j < n_plans && n > 0; ++j)
@@ -1212,6 +1230,7 @@ int abcs_sense_decode_sweep_host(abcs_ctx* c, const abcs_sense_plan* plans, int3
 
 int abcs_bench_cells_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_plans, const uint8_t* h_images,
                           int32_t n, double* h_mse, double* h_psnr, double* h_ssim, int32_t chunk) {
+  ABCS_NVTX("abcs_bench_cells_host");
   CHECK_CTX(c);
   if (int st = sweep_host_check(plans, n_plans, h_images, n, h_mse || h_psnr || h_ssim)) return st;
   for (int j = 0; j < n_plans && h_ssim; ++j)
@@ -1223,6 +1242,7 @@ int abcs_bench_cells_host(abcs_ctx* c, const abcs_sense_plan* plans, int32_t n_p
 
 int abcs_sense_decode_host(abcs_ctx* c, const abcs_sense_plan* p, const uint8_t* h_images, int32_t n, float* h_out,
                            uint16_t* h_counts, float* h_payload, int32_t chunk) {
+  ABCS_NVTX("abcs_sense_decode_host");
   CHECK_CTX(c);
   if (!p || n < 0 || (n > 0 && (!h_images || !h_out))) return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments");
   if (!block_supported(p->block)) return set_error(ABCS_ERR_UNSUPPORTED, "device path supports block sizes 8, 16, 32");

@@ -488,6 +488,7 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
   P.iteration = 0;
   launch_one(ctx, block, G, P, s);
   for (int t = 0; t < cfg.iterations; ++t) {  // damp_step(Ida) x iterations (recon.cpp:236-253)
+    ABCS_NVTX("ida_iteration");
     P.is_init = 0;
     P.onsager = (float)(1.0 / cfg.damping);  // IDA: onsager = 1/D_F (recon.cpp:183-184)
     P.pseudo_in = L.pseudo[t & 1];

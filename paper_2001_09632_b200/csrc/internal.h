@@ -1,6 +1,7 @@
 // Internal declarations shared by the host entry points (capi.cu, plan.cpp)
 // and the kernel translation units.
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <vector>
 #include <cstdint>
 #include <string>
@@ -12,6 +13,16 @@
 #endif
 
 namespace abcs_b200 {
+
+// NVTX range over a host entry point / phase (header-only nvtx3: no link, inert without a tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define ABCS_NVTX(name) ::abcs_b200::NvtxRange abcs_nvtx_range_(name)
+
 
 int set_error(int code, const std::string& msg);
 void clear_error();

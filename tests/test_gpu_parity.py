@@ -731,3 +731,58 @@ def test_host_pipeline_matches_device_path(p, torch):
     b = sense_dev(p, torch, imgs, 16, 3, 10, 2)
     assert np.array_equal(counts, b.counts.cpu().numpy().view(np.uint16))
     assert np.array_equal(out, p.decode_batch(b).cpu().numpy())
+
+
+def test_block_dct_bit_exact(p, torch, checker):
+    """BlockDct::forward / inverse, dct2 / idct2 (dct.cpp:9-79) on the device: fp64 and the
+    reference's order, so every value equals the reference's bits, for any block size."""
+    rng = np.random.default_rng(5)
+    for B in (1, 2, 7, 8, 16, 33):
+        blocks = rng.normal(100.0, 60.0, (5, B, B))
+        blocks[0] = np.round(blocks[0])  # integer pixels, as the sense path sees them
+        fwd = p.block_dct_batch(torch.from_numpy(blocks).cuda()).cpu().numpy()
+        inv = p.block_dct_batch(torch.from_numpy(blocks).cuda(), inverse=True).cpu().numpy()
+        for i in range(5):
+            assert np.array_equal(fwd[i].reshape(-1), checker.dct2(blocks[i], B)), (B, i)
+            assert np.array_equal(inv[i].reshape(-1), checker.idct2(blocks[i], B)), (B, i)
+    assert np.array_equal(p.dct2(blocks[1], 33), checker.dct2(blocks[1], 33))
+    assert np.array_equal(p.idct2(blocks[2], 33), checker.idct2(blocks[2], 33))
+
+
+@pytest.mark.parametrize("cs", ["1", "2", "16"])
+def test_race_free_batch_independence(p, torch, cs):
+    """Race / ordering evidence in place of compute-sanitizer (closed on this GPU pool): every
+    image's results are bit-identical whether it runs alone, first, or last in a batch, and run
+    to run. Covers the cluster allocator at 1/2/16 CTAs (DSMEM + cluster barriers), DD phase 1 +
+    fixup, the multi-plan payload pass, the fused IDA step (TMA window, in-place column stage,
+    acq_rel per-image fold) at B = 16 and 8, and the standalone denoiser."""
+    os.environ["ABCS_ALLOC_CLUSTER"] = cs
+    try:
+        for B, H, W, algo, num, den in ((16, 192, 256, p.Algorithm.BBV, 3, 10), (8, 96, 128, p.Algorithm.BBV, 1, 5),
+                                        (16, 256, 256, p.Algorithm.DD, 1, 4)):
+            imgs = p.synth_images(p.SynthSpec(H, W, 20, 5.0, 31), 0, 7)
+            cfg = p.SensingConfig(B, num, den, algo)
+            rc = p.ReconConfig(p.ReconMethod.Ida, iterations=3)
+            b_all = p.sense_batch(imgs, cfg)
+            x_all, tr_all, _ = p.ida_batch(b_all, rc, reference=imgs)
+            for sl in (slice(0, 1), slice(6, 7), slice(2, 5)):
+                b = p.sense_batch(imgs[sl].contiguous(), cfg)
+                assert torch.equal(b.counts.view(torch.int16), b_all.counts[sl].view(torch.int16))
+                assert torch.equal(b.payload, b_all.payload[sl])
+                x, tr, _ = p.ida_batch(b, rc, reference=imgs[sl].contiguous())
+                assert torch.equal(x, x_all[sl])
+                assert torch.equal(tr, tr_all[sl])
+            x2, _, _ = p.ida_batch(b_all, rc, reference=imgs)
+            assert torch.equal(x2, x_all)
+        imgs = p.synth_images(p.SynthSpec(128, 128, 20, 5.0, 2), 0, 5)
+        cfgs = [p.SensingConfig(16, n, d, p.Algorithm.DD) for n, d in ((1, 10), (3, 10), (1, 2))]
+        outs = p.sense_decode_sweep(imgs, cfgs)
+        outs1 = p.sense_decode_sweep(imgs[3:4].contiguous(), cfgs)
+        for (ba, xa), (b1, x1) in zip(outs, outs1):
+            assert torch.equal(b1.payload, ba.payload[3:4]) and torch.equal(x1, xa[3:4])
+        field = (imgs[0].double() + 0.25).cpu().numpy()
+        d1 = p.denoise(p.DenoiserSpec("dct_threshold"), field, 17.0)
+        d2 = p.denoise(p.DenoiserSpec("dct_threshold"), field, 17.0)
+        assert np.array_equal(d1, d2)
+    finally:
+        os.environ.pop("ABCS_ALLOC_CLUSTER", None)

@@ -33,6 +33,11 @@ SIGNATURES = [
     "abcs::SensingConfig::validate() const",
     "abcs::make_grid(int, int, int)",
     "abcs::zigzag_order(int)",
+    "abcs::BlockDct::BlockDct(int)",
+    "abcs::BlockDct::forward(std::span<double const, 18446744073709551615ul>, std::span<double, 18446744073709551615ul>) const",
+    "abcs::BlockDct::inverse(std::span<double const, 18446744073709551615ul>, std::span<double, 18446744073709551615ul>) const",
+    "abcs::dct2(std::vector<double, std::allocator<double> > const&, int)",
+    "abcs::idct2(std::vector<double, std::allocator<double> > const&, int)",
     "abcs::ista_step(abcs::ReconState&, abcs::SensingOperator const&, std::span<double const, 18446744073709551615ul>, "
     "double)",
     "abcs::amp_step(abcs::ReconState&, abcs::SensingOperator const&, std::span<double const, 18446744073709551615ul>, "
