@@ -28,6 +28,8 @@ void* ctx_scratch(Ctx* ctx, size_t bytes, cudaStream_t stream, int* status) {
     cudaFree(ctx->scratch);
     ctx->scratch = nullptr;
     ctx->scratch_bytes = 0;
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);  // they point into the old scratch
+    ctx->graphs.clear();
   }
   const size_t want = bytes + bytes / 4 + (1u << 20);
   cudaError_t e = cudaMalloc(&ctx->scratch, want);
@@ -70,6 +72,7 @@ int abcs_ctx_create(int device, abcs_ctx** out) {
   auto* ctx = new Ctx;
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
+  if (const char* g = getenv("ABCS_NO_GRAPHS")) ctx->use_graphs = !(g[0] == '1');
   for (auto& st : ctx->pipe) {
     e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -99,6 +102,8 @@ int abcs_ctx_destroy(abcs_ctx* c) {
   for (auto& st : ctx->pipe)
     if (st) cudaStreamDestroy(st);
   for (auto& e : ctx->kpool) cudaEventDestroy(e);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  if (ctx->capture) cudaStreamDestroy(ctx->capture);
   delete ctx;
   return ABCS_OK;
 }
@@ -756,14 +761,62 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
   const size_t need = off_bytes + ida_scratch_bytes(rows, cols, block, y_stride, n, *cfg);
   char* scr = static_cast<char*>(ctx_scratch(ctx, need, s, &st));
   if (st) return st;
-  const int32_t* offsets = d_offsets;
-  if (!offsets) {
-    st = launch_offsets(ctx, rows * cols, n, block, d_counts, reinterpret_cast<int32_t*>(scr), nullptr, nullptr, s);
-    if (st) return st;
-    offsets = reinterpret_cast<int32_t*>(scr);
+  auto body = [&](cudaStream_t q) -> int {
+    const int32_t* offsets = d_offsets;
+    if (!offsets) {
+      const int r = launch_offsets(ctx, rows * cols, n, block, d_counts, reinterpret_cast<int32_t*>(scr), nullptr,
+                                   nullptr, q);
+      if (r) return r;
+      offsets = reinterpret_cast<int32_t*>(scr);
+    }
+    return launch_ida(ctx, rows, cols, block, d_counts, offsets, d_y, y_stride, n, *cfg, d_ref, ref_stride, ref_pitch,
+                      d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, q);
+  };
+  if (!ctx->use_graphs || ctx->timing) return body(s);
+  // one CUDA graph per distinct argument set (every pointer, size and setting of this call)
+  auto u = [](const void* p) { return (uint64_t)reinterpret_cast<uintptr_t>(p); };
+  uint64_t dbits, kbits;
+  memcpy(&dbits, &cfg->damping, 8);
+  memcpy(&kbits, &cfg->k, 8);
+  const std::vector<uint64_t> key = {(uint64_t)rows, (uint64_t)cols, (uint64_t)block, u(d_counts), u(d_offsets),
+                                     u(d_y), (uint64_t)y_stride, (uint64_t)n, (uint64_t)cfg->iterations,
+                                     (uint64_t)cfg->denoiser_block, dbits, kbits, u(d_ref), (uint64_t)ref_stride,
+                                     (uint64_t)ref_pitch, u(d_out), (uint64_t)out_stride, (uint64_t)out_pitch,
+                                     u(d_trace), u(d_diverged), u(scr)};
+  Ctx::GraphEntry* hit = nullptr;
+  for (auto& g : ctx->graphs)
+    if (g.key == key) hit = &g;
+  if (!hit) {
+    if (!ctx->capture && cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking) != cudaSuccess)
+      return body(s);
+    const int64_t l0 = ctx->launches;
+    if (cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return body(s);
+    const int r = body(ctx->capture);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->capture, &graph);
+    if (r) {
+      if (graph) cudaGraphDestroy(graph);
+      ctx->launches = l0;
+      return r;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = ce == cudaSuccess ? cudaGraphInstantiate(&exec, graph, 0) : ce;
+    if (graph) cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      ctx->launches = l0;
+      return body(s);  // capture unsupported here: plain launches
+    }
+    if (ctx->graphs.size() >= 16) {  // bounded cache: drop the oldest
+      cudaGraphExecDestroy(ctx->graphs.front().exec);
+      ctx->graphs.erase(ctx->graphs.begin());
+    }
+    ctx->graphs.push_back({key, exec, ctx->launches - l0});
+    ctx->launches = l0;
+    hit = &ctx->graphs.back();
   }
-  return launch_ida(ctx, rows, cols, block, d_counts, offsets, d_y, y_stride, n, *cfg, d_ref, ref_stride, ref_pitch,
-                    d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, s);
+  ctx->launches += hit->launches;
+  return cuda_status(cudaGraphLaunch(hit->exec, s), "ida graph launch");
 }
 
 // Shared argument checks and offsets for the explicit-state entry points.

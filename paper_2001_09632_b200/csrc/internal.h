@@ -53,6 +53,17 @@ struct Ctx {
   std::vector<KRec> krecs;
   std::vector<cudaEvent_t> kpool;
   size_t kpool_used = 0;
+  // abcs_ida_batch as a CUDA graph per distinct argument set (the init + per-iteration launches
+  // replayed with one cudaGraphLaunch; small batches are launch-bound): captured on a private
+  // stream, launched on the caller's
+  struct GraphEntry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t capture = nullptr;
+  bool use_graphs = true;
 };
 
 // Kernel timing brackets (no-ops unless timing is enabled on the ctx).

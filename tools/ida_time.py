@@ -13,10 +13,12 @@ import torch  # noqa: E402
 import paper_2001_09632_b200 as p  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "cfg4"
+nimg = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--n=")), "0"))
 if which == "cfg4":
     H, n, ell, sig, seed, algo, num, den, iters = 512, 64, 20, 5.0, 4, p.Algorithm.BBV, 3, 10, 10
 else:
     H, n, ell, sig, seed, algo, num, den, iters = 4096, 16, 200, 8.0, 5, p.Algorithm.DD, 1, 4, 5
+n = nimg or n
 imgs = p.synth_images(p.SynthSpec(H, H, ell, sig, seed), 0, n)
 b = p.sense_batch(imgs, p.SensingConfig(16, num, den, algo))
 rc = p.ReconConfig(p.ReconMethod.Ida, iterations=iters)
@@ -42,7 +44,14 @@ for k, (cnt, tot, _) in kt.items():
     avg = tot / cnt
     extra = f"  {per_iter / avg / 1e6:.0f} GB/s ({per_iter / avg / 1e6 / 6547:.3f} of HBM)" if k == "ida_step" else ""
     print(f"{k:14s} launches {cnt:4d}  avg {avg * 1e3:8.1f} us{extra}")
-print(f"batch {ms:.3f} ms  {n * iters / ms * 1e3:.0f} it/s")
+print(f"batch {ms:.3f} ms  {n * iters / ms * 1e3:.0f} it/s (kernel timing on: plain launches)")
+s.record()
+for _ in range(reps):
+    p.ida_batch(b, rc, out=out, trace=False, check=False)
+e.record()
+torch.cuda.synchronize()
+ms2 = s.elapsed_time(e) / reps
+print(f"batch {ms2:.3f} ms  {n * iters / ms2 * 1e3:.0f} it/s (default: CUDA graph unless ABCS_NO_GRAPHS=1)")
 if "--no-check" not in sys.argv:
     import oracle as o
     chk = o.best_available()
