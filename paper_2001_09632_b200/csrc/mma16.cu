@@ -16,6 +16,9 @@
 // a per-warp zigzag-ordered buffer: prefix writes to the payload are coalesced
 // and the inverse transform reads buf[rank] for rank < count (zeros above),
 // so no tile has to be cleared between blocks.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "mma_dct.cuh"
@@ -786,10 +789,45 @@ __device__ __forceinline__ int pick4(const int (&a)[kMaxSweep], int j) {
   return j == 0 ? a[0] : j == 1 ? a[1] : j == 2 ? a[2] : a[3];
 }
 
-__global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G, MultiArgs A) {
+// Decoded pixels of a block pair (16 x 32 fp32) leave through shared memory by one TMA tensor store
+// per plan (cp.async.bulk.tensor, 3-D map of that plan's decoded batch): the warp moves on while
+// the copy engine drains it, so bytes in flight no longer scale with the warps' own stores. The
+// 2-KB staging tile uses the 128-B swizzle (16-B chunk ^ row), which makes the fragment writes
+// bank-conflict free. Two tiles per warp alternate; a tile is rewritten only after its store has
+// finished reading it (wait_group.read).
+struct MultiMaps {
+  CUtensorMap m[kMaxSweep];
+};
+__device__ __forceinline__ void stage_dfrag_sw(unsigned char* tile, int col0, const Acc16& X) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = g + 8 * h, col = col0 + 8 * j + 2 * t;
+      const int off = row * 128 + (((col >> 2) ^ (row & 7)) << 4) + ((col & 3) << 2);
+      *reinterpret_cast<float2*>(tile + off) = make_float2(X.v[j][2 * h], X.v[j][2 * h + 1]);
+    }
+}
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* m, int x, int y, int z, const void* tile) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(m), "r"(x), "r"(y),
+      "r"(z), "r"((uint32_t)__cvta_generic_to_shared(tile))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+template <bool kBulk>
+__global__ void __launch_bounds__(kM16Threads, 2)
+sense16_multi_kernel(Grid16 G, MultiArgs A, const __grid_constant__ MultiMaps maps) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
   constexpr int kWbuf = 256;
   __shared__ float s_buf[kM16Warps][2][kWbuf];
+  extern __shared__ __align__(1024) unsigned char s_out_raw[];  // kBulk: [warp][2] 2-KB swizzled tiles
+  unsigned char* s_out = s_out_raw + ((1024 - ((uint32_t)__cvta_generic_to_shared(s_out_raw) & 1023)) & 1023);
+  int tile_sel = 0;
   Frag16 f;
   load_frag16(f);
   uint32_t rank_d[8];
@@ -867,13 +905,29 @@ __global__ void __launch_bounds__(kM16Threads, 2) sense16_multi_kernel(Grid16 G,
 #pragma unroll
           for (int s = 0; s < 8; ++s) Ym.v[s >> 2][s & 3] = (int)rank_d[s] < cq ? Y[q].v[s >> 2][s & 3] : 0.f;
           const Acc16 X = lo_j ? dct16_inv_from_yt_lo(f, Ym) : dct16_inv_from_yt(f, Ym);
-          store_dfrag(A.out[j] + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
-                      A.out_pitch, X);
+          if (kBulk) {
+            if (q == 0 && lane == 0) bulk_wait_read1();  // this tile's store from two rounds ago
+            if (q == 0) __syncwarp();
+            stage_dfrag_sw(s_out + (warp * 2 + tile_sel) * 2048, 16 * q, X);
+          } else {
+            store_dfrag(A.out[j] + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
+                        A.out_pitch, X);
+          }
+        }
+        if (kBulk) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // st.shared -> async proxy
+          __syncwarp();
+          if (lane == 0) {  // a lone last block: the map clips the pair's second half (past the image)
+            tma_store_tile(&maps.m[j], bc0 * 16, br * 16, (int)img, s_out + (warp * 2 + tile_sel) * 2048);
+            bulk_commit();
+          }
+          tile_sel ^= 1;
         }
       }
       __syncwarp();
     }
   }
+  if (kBulk && (threadIdx.x & 31) == 0) bulk_wait_all();  // smem must outlive the copies
 }
 
 int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
@@ -898,8 +952,40 @@ int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint
   }
   A.out_stride = out_stride;
   A.out_pitch = out_pitch;
+  bool bulk = (out_pitch % 4 == 0) && (out_stride % 4 == 0) && out_pitch >= cols * 16;  // 16-B aligned rows
+  for (int j = 0; j < np; ++j) bulk = bulk && ((uintptr_t)out[j] % 16 == 0);
+  if (const char* e = getenv("ABCS_MULTI_BULK")) bulk = bulk && e[0] != '0';
+  MultiMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (bulk) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                  &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        encode = nullptr;
+    }
+    for (int j = 0; j < np && bulk; ++j) {
+      const cuuint64_t dims[3] = {(cuuint64_t)cols * 16, (cuuint64_t)rows * 16, (cuuint64_t)n};
+      const cuuint64_t strides[2] = {(cuuint64_t)out_pitch * 4, (cuuint64_t)out_stride * 4};
+      const cuuint32_t box[3] = {32, 16, 1}, estr[3] = {1, 1, 1};
+      bulk = encode && encode(&maps.m[j], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out[j], dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
+  constexpr int kOutBytes = kM16Warps * 2 * 2048 + 1024;  // + alignment slack (swizzled tiles: 1024 B)
+  static bool attr = false;
+  if (bulk && !attr) {
+    cudaFuncSetAttribute(sense16_multi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOutBytes);
+    attr = true;
+  }
   const int kt = ktimer_begin(ctx, s, "sense16_gather_decode");
-  sense16_multi_kernel<<<grid_for(ctx, G.total_runs, 2), kM16Threads, 0, s>>>(G, A);
+  if (bulk)
+    sense16_multi_kernel<true><<<grid_for(ctx, G.total_runs, 2), kM16Threads, kOutBytes, s>>>(G, A, maps);
+  else
+    sense16_multi_kernel<false><<<grid_for(ctx, G.total_runs, 2), kM16Threads, 0, s>>>(G, A, maps);
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "sense16 multi launch");
