@@ -5,7 +5,7 @@ import sys
 
 tag = sys.argv[1]
 nblk = float(sys.argv[2]) if len(sys.argv) > 2 else 4096.0
-rows = list(csv.reader(open(f"gpurun_out/{tag}_raw.csv")))
+rows = list(csv.reader(open(f"{tag}_raw.csv")))
 d = dict(zip(rows[0], rows[2]))
 st = {k: float(v.replace(",", "")) for k, v in d.items() if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued")}
 tot = sum(st.values())
@@ -15,7 +15,7 @@ for k in ["gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustaine
           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
           "smsp__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]:
     print(k, d.get(k))
-rows = list(csv.reader(open(f"gpurun_out/{tag}_sass.csv")))
+rows = list(csv.reader(open(f"{tag}_sass.csv")))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 seq = [(r[ix["Address"]][-5:], r[ix["Source"]].strip(), int(r[ix["Instructions Executed"]] or 0),
