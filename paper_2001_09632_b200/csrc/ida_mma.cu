@@ -134,7 +134,8 @@ struct IdaF32Smem {
   double red[4][16];
   unsigned int bad[2];
   double mine[4];
-  uint64_t win_bar;  // TMA window load (one phase per CTA)
+  uint64_t win_bar;          // TMA window load (one phase per CTA)
+  unsigned short zrank[256];  // B = 16 zigzag rank of (u, v) at u * 16 + v (block phase)
 };
 static_assert(kFThreads / 32 * 512 <= kMIn * kRP, "staging buffers fit");
 static_assert(kMIn * kMP <= kMIn * kWP, "acc fits in the window");
@@ -411,7 +412,7 @@ __device__ __forceinline__ float fp16_range_scale(float (&v)[4]) {
 // are read where they lie (a block's prefix is one short run, so the column threads' rank-order
 // accesses stay in L1) and z is written back in place.
 constexpr int kTB = 336;  // per-block transpose tile: 16 rows x pitch 20 (+16: conflict-free between blocks)
-static_assert(16 * kTB <= kMIn * kWP, "transpose tiles fit in the window buffer");
+static_assert(16 * kTB <= kMIn * kRP, "transpose tiles fit in RS");
 
 // check_finite (recon.cpp:56-65) over a thread's 16 x values: the common case is one compare per
 // value; the first offending index (x-major, kind bit as in x_checks) only on the rare path.
@@ -472,18 +473,19 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     for (int c = 0; c < 16; ++c) xr[c] -= cb;
     abcs_gen::dct16_fwd(xr, T);
   }
-  __syncthreads();  // every x row is in registers: the window buffer takes the transposes
-  float* tb = s.in + b * kTB;
+  // Warp w owns blocks 2w and 2w + 1 through all stages, and each block's transpose tile lives in
+  // RS (free after the denoiser): the stages synchronise per warp, not per CTA.
+  float* tb = s.RS + b * kTB;
   if (valid) {
 #pragma unroll
     for (int v = 0; v < 16; ++v) tb[v * 20 + lr] = T[v];
   }
-  __syncthreads();
+  __syncwarp();
   // 2. columns: v = lr
   float Y[16];  // Y, then W = Y + z over the prefix
   if (valid) {
     const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];  // the block's prefix in y / z
-    const unsigned short* rk = zigzag_rank_dev<16>() + lr;
+    const unsigned short* rk = s.zrank + lr;
     {
       float Tc[16];
       load_row16(tb + lr * 20, Tc);
@@ -524,14 +526,14 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     if (lr == 0) S.cnt += cnt;
   }
   if (last) return;
-  __syncthreads();  // all column loads of tb done: it takes V
+  __syncwarp();  // all column loads of the warp's tiles done: they take V
   if (valid) {
     float V[16];
     abcs_gen::dct16_inv(Y, V);
 #pragma unroll
     for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
   }
-  __syncthreads();
+  __syncwarp();
   // 3. rows: pseudo = IDCT16 of row r of V
   if (valid) {
     float Vr[16], O[16];
@@ -551,11 +553,11 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
   const bool valid = t < 256 && cnt >= 0;
-  float* tb = s.in + b * kTB;  // acc (in the same buffer) is written only after the last tb read
+  float* tb = s.RS + b * kTB;  // per-block transpose tile; warp w owns blocks 2w, 2w + 1
   float cb = 0.f;
   if (valid) {
     const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];
-    const unsigned short* rk = zigzag_rank_dev<16>() + lr;
+    const unsigned short* rk = s.zrank + lr;
     float Wc[16], V[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -571,20 +573,19 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
     for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
   }
   cb = __shfl_sync(0xffffffffu, cb, threadIdx.x & 16);  // from the block's column-0 thread
-  __syncthreads();
+  __syncwarp();
   float O[16];
   if (valid) {
     float Vr[16];
     load_row16(tb + lr * 20, Vr);
     abcs_gen::dct16_inv(Vr, O);
   }
-  __syncthreads();
   if (valid) {
     float4* dst = reinterpret_cast<float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q] + cb, O[4 * q + 1] + cb, O[4 * q + 2] + cb, O[4 * q + 3] + cb);
   }
-  __syncthreads();
+  __syncwarp();  // the block phase reads each block's rows in the same warp
 }
 
 // ---- B = 8: two horizontally adjacent sensing blocks per warp step ------------------------
@@ -748,6 +749,7 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     tma_window(s.in, &win_map, C0 - 4, R0 - 4, img, &s.win_bar);
   const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
+  if (B == 16 && threadIdx.x < 256) s.zrank[threadIdx.x] = zigzag_rank_dev<16>()[threadIdx.x];
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
