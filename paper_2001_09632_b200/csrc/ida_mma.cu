@@ -135,7 +135,7 @@ struct IdaF32Smem {
   unsigned int bad[2];
   double mine[4];
   uint64_t win_bar;          // TMA window load (one phase per CTA)
-  unsigned short zrank[256];  // B = 16 zigzag rank of (u, v) at u * 16 + v (block phase)
+  unsigned short zidx[256];   // B = 16 zigzag order: flat u * 16 + v of rank k (block phase)
 };
 static_assert(kFThreads / 32 * 512 <= kMIn * kRP, "staging buffers fit");
 static_assert(kMIn * kMP <= kMIn * kWP, "acc fits in the window");
@@ -481,50 +481,69 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     for (int v = 0; v < 16; ++v) tb[v * 20 + lr] = T[v];
   }
   __syncwarp();
-  // 2. columns: v = lr
-  float Y[16];  // Y, then W = Y + z over the prefix
+  // 2. columns: v = lr. The column DCT lands in the tile as Y[u] at (row v, col u); the z update
+  // then walks the warp's two blocks' prefixes in zigzag order (they are consecutive in the
+  // payload: coalesced y / z loads, all in flight at once, and coalesced z stores), reading Y at
+  // each rank's (u, v) and leaving W = Y + z in its place; the column threads reload W.
+  float Y[16];
   if (valid) {
-    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];  // the block's prefix in y / z
-    const unsigned short* rk = s.zrank + lr;
-    {
-      float Tc[16];
-      load_row16(tb + lr * 20, Tc);
-      abcs_gen::dct16_fwd(Tc, Y);
-    }
+    float Tc[16];
+    load_row16(tb + lr * 20, Tc);
+    abcs_gen::dct16_fwd(Tc, Y);
+  }
+  __syncwarp();  // every lane holds its column: the tile takes Y
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(tb + lr * 20 + 4 * q) = make_float4(Y[4 * q], Y[4 * q + 1], Y[4 * q + 2], Y[4 * q + 3]);
+  }
+  __syncwarp();
+  const float cb0 = __shfl_sync(0xffffffffu, cb, 0), cb1 = __shfl_sync(0xffffffffu, cb, 16);  // the pair's centres
+  if (t < 256) {
+    const int lane = t & 31, b0 = b & ~1;
+    const int c0 = max(s.meta_cnt[b0], 0), c1 = max(s.meta_cnt[b0 + 1], 0), kw = c0 + c1;
+    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b0];  // the pair's run in y / z
     float zsq = 0.f, ysq = 0.f;
     unsigned int badz = ~0u;
+#pragma unroll 1
+    for (int e0 = 0; e0 < kw; e0 += 256) {  // up to 8 elements per lane in flight
+      float yv[8], zo[8];
 #pragma unroll
-    for (int h = 0; h < 16; h += 4) {  // 4 coefficients' prefix loads in flight at a time
-      int k[4];
-      float yv[4], zo[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        k[i] = rk[16 * (h + i)];
-        yv[i] = k[i] < cnt ? __ldg(P.y + pb + k[i]) : 0.f;
-        zo[i] = (k[i] < cnt && !P.is_init) ? P.z[pb + k[i]] : 0.f;
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + lane + 32 * i;
+        yv[i] = e < kw ? __ldg(P.y + pb + e) : 0.f;
+        zo[i] = (e < kw && !P.is_init) ? P.z[pb + e] : 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (k[i] < cnt) {
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + lane + 32 * i;
+        if (e < kw) {
+          const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0);
+          const int f = s.zidx[k];  // flat u * 16 + v
+          float* slot = s.RS + (b0 + q) * kTB + (f & 15) * 20 + (f >> 4);
+          const float yk = yv[i];
           // finish_step (recon.cpp:86-88); the centred transform's DC lacks 16 cb (exact)
-          const float ya = (h + i == 0 && lr == 0) ? yv[i] - 16.f * cb : yv[i];
-          const float zn = (ya - Y[h + i]) + ons * zo[i];
-          P.z[pb + k[i]] = zn;
+          const float ya = k == 0 ? yk - 16.f * (q ? cb1 : cb0) : yk;
+          const float yc = *slot;
+          const float zn = (ya - yc) + ons * zo[i];
+          P.z[pb + e] = zn;
+          *slot = yc + zn;  // W = Y + z
           zsq = fmaf(zn, zn, zsq);
-          ysq = fmaf(yv[i], yv[i], ysq);
+          ysq = fmaf(yk, yk, ysq);
           if (!isfinite(zn)) {
-            const unsigned int gi = (unsigned)(s.meta_off[b] + k[i]);
+            const unsigned int gi = (unsigned)(s.meta_off[b0] + e);
             badz = gi < badz ? gi : badz;
           }
-          Y[h + i] += zn;  // W = Y + z
         }
       }
     }
     S.z += (double)zsq;
     if (P.is_init) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
     S.badz = badz < S.badz ? badz : S.badz;
-    if (lr == 0) S.cnt += cnt;
+    if ((t & 15) == 0 && cnt >= 0) S.cnt += cnt;
   }
+  __syncwarp();
+  if (valid) load_row16(tb + lr * 20, Y);  // W of column lr
   if (last) return;
   __syncwarp();  // all column loads of the warp's tiles done: they take V
   if (valid) {
@@ -555,20 +574,35 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
   const bool valid = t < 256 && cnt >= 0;
   float* tb = s.RS + b * kTB;  // per-block transpose tile; warp w owns blocks 2w, 2w + 1
   float cb = 0.f;
-  if (valid) {
-    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b];
-    const unsigned short* rk = s.zrank + lr;
-    float Wc[16], V[16];
+  // embed each block's y prefix: zero the tile, then the warp scatters its two blocks' run (one
+  // coalesced read) to each rank's (u, v) slot (tile row v, column u)
+  if (t < 256) {
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int k = rk[16 * u];
-      Wc[u] = k < cnt ? __ldg(P.y + pb + k) : 0.f;
+    for (int q = 0; q < 4; ++q) *reinterpret_cast<float4*>(tb + lr * 20 + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncwarp();
+  if (t < 256) {
+    const int lane = t & 31, b0 = b & ~1;
+    const int c0 = max(s.meta_cnt[b0], 0), kw = c0 + max(s.meta_cnt[b0 + 1], 0);
+    const float* ysrc = P.y + (int64_t)img * P.y_stride + s.meta_off[b0];
+    for (int e = lane; e < kw; e += 32) {
+      const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0), f = s.zidx[k];
+      s.RS[(b0 + q) * kTB + (f & 15) * 20 + (f >> 4)] = __ldg(ysrc + e);
     }
+  }
+  __syncwarp();
+  float V[16];
+  if (valid) {
+    float Wc[16];
+    load_row16(tb + lr * 20, Wc);
     if (lr == 0) {  // centre on the block mean y00 / 16: out of the transform, added back after
       cb = Wc[0] * 0.0625f;
       Wc[0] = 0.f;
     }
     abcs_gen::dct16_inv(Wc, V);
+  }
+  __syncwarp();  // every column loaded: the tile takes V
+  if (valid) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) tb[r * 20 + lr] = V[r];
   }
@@ -749,7 +783,7 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     tma_window(s.in, &win_map, C0 - 4, R0 - 4, img, &s.win_bar);
   const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
-  if (B == 16 && threadIdx.x < 256) s.zrank[threadIdx.x] = zigzag_rank_dev<16>()[threadIdx.x];
+  if (B == 16 && threadIdx.x < 256) s.zidx[threadIdx.x] = zigzag_dev<16>()[threadIdx.x];
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
