@@ -60,10 +60,18 @@ static __device__ void finish_image(const IdaParams& P, int img, int region, con
   unsigned prev;
   asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(P.counters + img) : "memory");
   if (prev != (unsigned)P.regions_per_img - 1) return;
+  // the other CTAs' partials, visible after the acquire; plain loads (no volatile) so they are
+  // issued back to back instead of one round trip each, summed in region order (deterministic)
   double a[4] = {0.0, 0.0, 0.0, 0.0};
-  const volatile double* pp = P.partials + (int64_t)img * P.regions_per_img * 4;
-  for (int r = 0; r < P.regions_per_img; ++r)
-    for (int q = 0; q < 4; ++q) a[q] += pp[4 * r + q];
+  const double2* pp = reinterpret_cast<const double2*>(P.partials + (int64_t)img * P.regions_per_img * 4);
+#pragma unroll 8
+  for (int r = 0; r < P.regions_per_img; ++r) {
+    const double2 v0 = __ldcg(pp + 2 * r), v1 = __ldcg(pp + 2 * r + 1);  // L2, never a stale L1 line
+    a[0] += v0.x;
+    a[1] += v0.y;
+    a[2] += v1.x;
+    a[3] += v1.y;
+  }
   P.counters[img] = 0;  // ready for the next launch
   const double M = a[3];  // op.measurements() = sum of counts, re-summed every launch (exact in fp64)
   if (P.is_init && P.msize) P.msize[img] = M;
