@@ -518,6 +518,11 @@ size_t class_smem_bytes(int wmax, int n_blocks, int cs, bool arrays_in_smem) {
 
 // kSmemArrays: weights and allocations in shared memory; else weights in global scratch and
 // allocations in shared memory as u8 (kAv8, caps <= 255) or in global scratch as u16.
+// Weight ranges at least this wide take plain shared-memory atomics for the per-round histogram
+// (collisions are rare); narrower ones (DD: phase-1 counts, <= 256 classes) aggregate equal
+// weights in the warp first (__match_any_sync).
+constexpr int kAggregateBelow = 256;
+
 template <bool kSmemArrays, bool kAv8 = false>
 __global__ void __launch_bounds__(kClassThreads)
 alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64_t budget, int cap, int base,
@@ -647,15 +652,27 @@ alloc_class_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, int64
     for (int c = c0; c < c1; ++c) hist[c] = 0;
     __syncthreads();
     unsigned long long tw = 0, na = 0;
-    for (int k = 0; k < per_b; ++k) {  // warp-aggregated histogram (uniform trip count for match_any)
-      const int i = b0 + k, ph = k * kClassThreads + tid;
-      const bool act = i < b1 && (int)av[ph] < cap;
-      const int wi = act ? (int)wv[ph] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, wi);
-      if (act && (__ffs(peers) - 1) == lane) atomicAdd(&hist[wi], (unsigned)__popc(peers));
-      if (act) {
-        tw += (unsigned)wi;
-        na += 1;
+    if (wmax >= kAggregateBelow) {  // many distinct weights (BBV): plain shared atomics rarely collide
+      for (int k = 0; k < per_b; ++k) {
+        const int i = b0 + k, ph = k * kClassThreads + tid;
+        if (i < b1 && (int)av[ph] < cap) {
+          const int wi = (int)wv[ph];
+          atomicAdd(&hist[wi], 1u);
+          tw += (unsigned)wi;
+          na += 1;
+        }
+      }
+    } else {
+      for (int k = 0; k < per_b; ++k) {  // warp-aggregated histogram (uniform trip count for match_any)
+        const int i = b0 + k, ph = k * kClassThreads + tid;
+        const bool act = i < b1 && (int)av[ph] < cap;
+        const int wi = act ? (int)wv[ph] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, wi);
+        if (act && (__ffs(peers) - 1) == lane) atomicAdd(&hist[wi], (unsigned)__popc(peers));
+        if (act) {
+          tw += (unsigned)wi;
+          na += 1;
+        }
       }
     }
     const unsigned long long T0l = Reduce64(tmp.r).Sum(tw);
