@@ -564,32 +564,39 @@ sense8_kernel(Grid16 G, Sense16Args A) {
     const int32_t my_off = lane < nblk ? A.offsets[bidx_first + lane] : 0;
     int tot;
     const int my_pre = warp_excl_scan(my_cnt, tot);  // prefix of the run's counts (lane = block)
+    // the quad's image rows: lane -> pair L/8, row L%8 (16 bytes = blocks 2p, 2p+1 of the quad);
+    // the next quad's row is loaded while the current one is transformed (its latency hidden)
+    auto quad_row = [&](int qb) {
+      const int pp = lane >> 3, row = lane & 7;
+      const int b = qb + 2 * pp;  // run-relative block
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (b < nblk) {
+        const uint8_t* src = A.imgs + (int64_t)img * A.img_stride + (int64_t)(br * 8 + row) * A.pitch + (bcf + b) * 8;
+        const bool both = b + 1 < nblk;
+        if (A.aligned && both) {
+          v = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+          uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (q < 8 || both) w[q >> 2] |= (uint32_t)src[q] << (8 * (q & 3));
+          v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      return v;
+    };
+    uint4 vnext = make_uint4(0, 0, 0, 0);
+    if constexpr (kFromImage) vnext = quad_row(0);
     for (int qb = 0; qb < nblk; qb += 8) {
       const int pre0 = __shfl_sync(0xffffffffu, my_pre, qb);
       const int32_t off0 = __shfl_sync(0xffffffffu, my_off, qb);
       const int qend = min(qb + 8, nblk);
       const int qtot = (qend < 32 ? __shfl_sync(0xffffffffu, my_pre, qend & 31) : tot) - pre0;
       if constexpr (kFromImage) {
-        // stage the quad: lane -> pair L/8, row L%8 (16 bytes = blocks 2p, 2p+1 of the quad)
-        const int pp = lane >> 3, row = lane & 7;
-        const int b = qb + 2 * pp;  // run-relative block
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (b < nblk) {
-          const uint8_t* src = A.imgs + (int64_t)img * A.img_stride + (int64_t)(br * 8 + row) * A.pitch + (bcf + b) * 8;
-          const bool both = b + 1 < nblk;
-          if (A.aligned && both) {
-            v = __ldg(reinterpret_cast<const uint4*>(src));
-          } else {
-            uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (q < 8 || both) w[q >> 2] |= (uint32_t)src[q] << (8 * (q & 3));
-            v = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
         __syncwarp();
-        reinterpret_cast<uint4*>(st)[lane] = interleave_row16(v);
+        reinterpret_cast<uint4*>(st)[lane] = interleave_row16(vnext);
         __syncwarp();
+        if (qb + 8 < nblk) vnext = quad_row(qb + 8);
       } else {
         // the quad's prefixes (contiguous in the payload) -> smem, coalesced
         const float* src = A.payload + (int64_t)img * A.payload_stride + off0;
