@@ -166,7 +166,7 @@ __device__ __forceinline__ void run_pos(const Grid16& G, uint32_t r, uint32_t& i
   nblk = min(32, G.cols - bc_first);
 }
 
-template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false, bool kSweep = false>
+template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false, int kSweep = 0>
 __global__ void __launch_bounds__(kM16Threads, 3)
 sense16_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
@@ -191,13 +191,17 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       thr_lo[s] = in ? A.Tf - A.band : INFINITY;
     }
   }
-  uint32_t in_sw[kSweep ? kMaxSweep : 1];  // sweep: bit s set iff slot s is in plan j's prefix
-  if constexpr (kSweep) {
+  // sweep: plan j's phase-1 prefix and band, hoisted; P = the widest prefix
+  int sw_ph1[kSweep > 0 ? kSweep : 1];
+  float sw_hi[kSweep > 0 ? kSweep : 1], sw_lo[kSweep > 0 ? kSweep : 1];
+  int sw_P = 0;
+  if constexpr (kSweep > 0) {
 #pragma unroll
-    for (int j = 0; j < kMaxSweep; ++j) {
-      in_sw[j] = 0;
-#pragma unroll
-      for (int s = 0; s < 8; ++s) in_sw[j] |= (j < A.n_sw && (int)rank_d[s] < A.sw_phase1[j]) ? 1u << s : 0u;
+    for (int j = 0; j < kSweep; ++j) {
+      sw_ph1[j] = A.sw_phase1[j];
+      sw_hi[j] = A.sw_hi[j];
+      sw_lo[j] = A.sw_lo[j];
+      sw_P = max(sw_P, sw_ph1[j]);
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -243,53 +247,68 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       else if (lo_pair) dct16_fwd_exact_x2_lo(f, bx, Y);
       else dct16_fwd_exact_x2(f, bx, Y);
       const uint32_t bidx0 = bidx_first + 2 * p;
-      if constexpr (kSweep) {
-        // the same phase-1 test for each plan of the sweep (prefix phase1_j, band around T_j);
-        // the plans' warp counts travel packed (10 bits each) through one reduction and one vote
+      if constexpr (kSweep > 0) {
+        // DD phase 1 of kSweep plans by zigzag compaction: the pair's coefficients of rank < P go to
+        // the warp's rank-ordered buffer and lane L tests ranks (L & 15) + 16 i of block L >> 4
+        // against each plan (prefix phase1_j, band around T_j): 2P / 32 coefficients per lane
+        // instead of 8 slots per plan, most of them outside every prefix. A zigzag prefix of
+        // <= 136 entries lies in slots 0-5 (u + v <= 15), so slots 6-7 are stored only beyond.
+        __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (q == 1 && !two) break;
-          uint32_t packed = 0;
-          bool nr = false;
+        for (int q = 0; q < 2; ++q)
 #pragma unroll
-          for (int j = 0; j < kMaxSweep; ++j) {
-            if (j >= A.n_sw) break;
-            const float hi_t = A.sw_hi[j], lo_t = A.sw_lo[j];
-            const int smax = A.sw_phase1[j] <= 36 ? 2 : 8;  // a prefix of <= 36 lies in slots 0-1 (kLowCols)
-            uint32_t hb = 0, lb = 0;  // per slot: |Y| >= T + band, |Y| > T - band
+          for (int s = 0; s < 8; ++s)
+            if (s < 6 || sw_P > 136) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+        __syncwarp();
+        const int qb = lane >> 4, kl = lane & 15;
+        const float* zq = zb0 + kWbuf * qb;
+        uint32_t packed = 0;  // 8-bit count per plan (phase1 <= 128)
+        bool nr = false;
 #pragma unroll
-            for (int s = 0; s < 8; ++s) {
-              if (s >= smax) break;
-              const float a = fabsf(Y[q].v[s >> 2][s & 3]);
-              hb |= a >= hi_t ? 1u << s : 0u;
-              lb |= a > lo_t ? 1u << s : 0u;
-            }
-            hb &= in_sw[j];  // slots inside plan j's zigzag prefix
-            packed += (uint32_t)__popc(hb) << (10 * j);
-            nr |= (lb & ~hb & in_sw[j]) != 0u;
+        for (int i = 0; i < 8; ++i) {
+          if (16 * i >= sw_P) break;
+          const int k = kl + 16 * i;
+          const float a = fabsf(zq[k]);
+#pragma unroll
+          for (int j = 0; j < kSweep; ++j) {
+            const bool in = k < sw_ph1[j];
+            const bool hi = in && a >= sw_hi[j];
+            packed += hi ? 1u << (8 * j) : 0u;
+            nr |= in && !hi && a > sw_lo[j];
           }
-          const uint32_t sig = __reduce_add_sync(0xffffffffu, packed);
-          if (__any_sync(0xffffffffu, nr)) {  // rare: record each plan's near-threshold coefficients
+        }
+        if (qb == 1 && !two) {
+          packed = 0;
+          nr = false;
+        }
+        const uint32_t sig0 = __reduce_add_sync(0xffffffffu, qb == 0 ? packed : 0u);
+        const uint32_t sig1 = __reduce_add_sync(0xffffffffu, qb == 1 ? packed : 0u);
+        if (__any_sync(0xffffffffu, nr)) {  // rare: record each plan's near-threshold coefficients
+          if (nr) {
 #pragma unroll 1
-            for (int j = 0; j < A.n_sw; ++j) {
-              const int ph1 = A.sw_phase1[j];
-              const float hi_t = A.sw_hi[j], lo_t = A.sw_lo[j];
+            for (int j = 0; j < kSweep; ++j) {
               bool mine = false;
-              for (int s = 0; s < 8; ++s) {
-                const float a = fabsf(Y[q].v[s >> 2][s & 3]);
-                if ((int)rank_d[s] < ph1 && !(a >= hi_t) && a > lo_t) {
+#pragma unroll 1
+              for (int i = 0; 16 * i < sw_P; ++i) {
+                const int k = kl + 16 * i;
+                const float a = fabsf(zq[k]);
+                if (k < sw_ph1[j] && !(a >= sw_hi[j]) && a > sw_lo[j]) {
                   mine = true;
                   const uint32_t e = atomicAdd(A.sw_fix_count[j], 1u);
                   if (e < A.fix_cap) {
-                    A.sw_fix_list[j][2 * e] = bidx0 + q;
-                    A.sw_fix_list[j][2 * e + 1] = (uint32_t)(dslot_col(s) * 16 + dslot_row(s));
+                    A.sw_fix_list[j][2 * e] = bidx0 + qb;
+                    A.sw_fix_list[j][2 * e + 1] = zigzag_dev<16>()[k];  // flat u * 16 + v
                   }
                 }
               }
-              if (mine) A.sw_fix_flag[j][bidx0 + q] = 1;
+              if (mine) A.sw_fix_flag[j][bidx0 + qb] = 1;
             }
           }
-          if (lane < A.n_sw) A.sw_weights[lane][bidx0 + q] = (sig >> (10 * lane)) & 1023u;
+        }
+        if (lane < kSweep) {
+          uint32_t* w = A.sw_weights[lane];
+          w[bidx0] = (sig0 >> (8 * lane)) & 255u;
+          if (two) w[bidx0 + 1] = (sig1 >> (8 * lane)) & 255u;
         }
       } else if constexpr (kWeights) {
         // phase-1 test in registers: slot s is in the prefix iff rank_d[s] < phase1 (thresholds
@@ -1015,6 +1034,7 @@ int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const ui
   A.fix_cap = (uint32_t)(nbt * 2);
   A.n_sw = n_sw;
   for (int j = 0; j < n_sw; ++j) {
+    if (phase1[j] < 0 || phase1[j] > 128) return set_error(ABCS_ERR_LOGIC, "sense16 sweep: phase-1 prefix above 128");
     const float Tf = (float)T[j];
     const float band = (float)(1e-2 + fabs(T[j] - (double)Tf));  // as launch_sense16
     A.sw_phase1[j] = phase1[j];
@@ -1029,7 +1049,13 @@ int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const ui
     if (e != cudaSuccess) return cuda_status(e, "fixup reset");
   }
   int kt = ktimer_begin(ctx, s, "sense16_weights_sweep");
-  sense16_kernel<true, false, false, false, true><<<grid_for(ctx, G.total_runs), kM16Threads, 0, s>>>(G, A);
+  const unsigned grid = grid_for(ctx, G.total_runs);
+  switch (n_sw) {  // the plan count is a template argument: the per-coefficient tests fully unroll
+    case 1: sense16_kernel<true, false, false, false, 1><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    case 2: sense16_kernel<true, false, false, false, 2><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    case 3: sense16_kernel<true, false, false, false, 3><<<grid, kM16Threads, 0, s>>>(G, A); break;
+    default: sense16_kernel<true, false, false, false, 4><<<grid, kM16Threads, 0, s>>>(G, A); break;
+  }
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   cudaError_t e = cudaGetLastError();

@@ -710,6 +710,27 @@ def test_dd_guard_band_adversarial(p, torch, checker, num, den, T):
     assert_sense_equal(b, 0, checker.sense(img, 16, num, den, 2), 16)
 
 
+def test_dd_guard_band_adversarial_sweep(p, torch, checker):
+    """The cfg2 subrate sweep's shared DD phase 1 (one transform, three plans: phase1 12 / 38 / 64
+    at T = 60 / 30 / 15, zigzag-compacted tests) on a 512 x 512 image holding near-threshold
+    blocks for each plan: every plan's counts equal the reference's bit for bit."""
+    subrates = ((1, 10), (3, 10), (1, 2))
+    plans = [p.sense_plan(p.SensingConfig(16, n, d, p.Algorithm.DD), 512, 512) for n, d in subrates]
+    assert [pl.threshold for pl in plans] == [60.0, 30.0, 15.0]
+    img = synth(512, 512, seed=1234)[0]
+    i = 0
+    for pl in plans:
+        for blk in _dd_adversarial_blocks(pl.threshold, pl.dd_phase1, ("saturated", "checker", "gradient"), 96,
+                                          seed=int(pl.threshold) + 7):
+            img[(i // 32) * 16:(i // 32 + 1) * 16, (i % 32) * 16:(i % 32 + 1) * 16] = blk
+            i += 1
+    assert i >= 48, i
+    got = p.sense_decode_sweep(torch.from_numpy(img[None].copy()).cuda(),
+                               [p.SensingConfig(16, n, d, p.Algorithm.DD) for n, d in subrates])
+    for (b, _), (n, d) in zip(got, subrates):
+        assert_sense_equal(b, 0, checker.sense(img, 16, n, d, 2), 16)
+
+
 def test_empty_batch(p, torch):
     imgs = torch.empty((0, 64, 64), dtype=torch.uint8, device="cuda")
     b = p.sense_batch(imgs, p.SensingConfig(16, 1, 4, p.Algorithm.DD))
