@@ -67,12 +67,16 @@ __device__ __forceinline__ void unit_pos(const Grid16& G, uint32_t u, uint32_t& 
   bc0 = 2 * (int)(rem - r * G.pairs_per_row);
 }
 
-__device__ __forceinline__ uint4 load_row16(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch,
-                                            const Grid16& G, uint32_t img, int br, int bc0, bool aligned) {
-  const int lane = threadIdx.x & 31, b = lane >> 4, r = lane & 15;
+// Lane L reads row L % 16 of block L / 16 of a pair: the run's row pointer, advanced 32 B per pair.
+__device__ __forceinline__ const uint8_t* run_row_ptr(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch,
+                                                      uint32_t img, int br, int bcf) {
+  const int lane = threadIdx.x & 31;
+  return imgs + (int64_t)img * img_stride + (int64_t)(br * 16 + (lane & 15)) * pitch + (bcf + (lane >> 4)) * 16;
+}
+
+__device__ __forceinline__ uint4 load_row16_at(const uint8_t* p, bool valid, bool aligned) {
   uint4 v = make_uint4(0, 0, 0, 0);
-  if (bc0 + b < G.cols) {
-    const uint8_t* p = imgs + (int64_t)img * img_stride + (int64_t)(br * 16 + r) * pitch + (bc0 + b) * 16;
+  if (valid) {
     if (aligned) {
       v = __ldg(reinterpret_cast<const uint4*>(p));
     } else {
@@ -173,10 +177,26 @@ sense16_kernel(Grid16 G, Sense16Args A) {
   constexpr int kWbuf = 256;
   __shared__ float s_buf[kM16Warps][2][kWbuf];
   __shared__ uint2 s_btab[kWeights ? 8 * 32 : 1];  // stage-2 basis B pairs (fill_btab16), weights pass only
+  // sweep: per rank e = 16 i + kl each plan's band edge hi (s_thr[e]) and lo (s_thr[128 + e]), +inf
+  // where the rank lies outside that plan's phase-1 prefix (membership folded into the threshold)
+  __shared__ float4 s_thr[kSweep > 0 ? 8 * 16 * 2 : 1];
   Frag16 f;
   load_frag16(f);
   if constexpr (kWeights) {  // (measured: a win for the weights pass, a loss for the fused decode pass)
     if (threadIdx.x < 32) fill_btab16(f, s_btab);
+    if constexpr (kSweep > 0) {
+      for (int e = threadIdx.x; e < 8 * 16; e += blockDim.x) {
+        float h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool in = j < kSweep && e < A.sw_phase1[j];  // e = 16 i + kl = the rank
+          h[j] = in ? A.sw_hi[j] : INFINITY;
+          l[j] = in ? A.sw_lo[j] : INFINITY;
+        }
+        s_thr[e] = make_float4(h[0], h[1], h[2], h[3]);
+        s_thr[8 * 16 + e] = make_float4(l[0], l[1], l[2], l[3]);
+      }
+    }
     __syncthreads();
   }
   // The forward runs transposed (Y^T = C X^T C^T): D slot s holds Y[dslot_col(s)][dslot_row(s)].
@@ -222,14 +242,15 @@ sense16_kernel(Grid16 G, Sense16Args A) {
         if constexpr (kPayload) my_off = A.offsets[bidx_first + lane];
       }
     }
-    uint4 nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bcf, A.aligned);
+    const uint8_t* rowp = run_row_ptr(A.imgs, A.img_stride, A.pitch, img, br, bcf);
+    uint4 nxt = load_row16_at(rowp, (lane >> 4) < nblk, A.aligned);
     for (int p = 0; 2 * p < nblk; ++p) {
       const int bc0 = bcf + 2 * p;
       const bool two = 2 * p + 1 < nblk;
       __syncwarp();
       reinterpret_cast<uint4*>(st)[lane] = interleave_row16(nxt);
       __syncwarp();
-      if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
+      if (2 * p + 2 < nblk) nxt = load_row16_at(rowp + 32 * (p + 1), 2 * p + 2 + (lane >> 4) < nblk, A.aligned);
       uint32_t bx[2][2][2];
       u8_bfragT_il(st, bx[0]);
       u8_bfragT_il(st + 256, bx[1]);
@@ -262,21 +283,23 @@ sense16_kernel(Grid16 G, Sense16Args A) {
         __syncwarp();
         const int qb = lane >> 4, kl = lane & 15;
         const float* zq = zb0 + kWbuf * qb;
-        uint32_t packed = 0;  // 8-bit count per plan (phase1 <= 128)
-        bool nr = false;
+        // per plan j (byte j): coefficients at or above T_j + band (counted) and above T_j - band;
+        // the two words differ iff some coefficient is near T_j (inside the band)
+        uint32_t packed = 0, above_lo = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (16 * i >= sw_P) break;
-          const int k = kl + 16 * i;
-          const float a = fabsf(zq[k]);
+          const float a = fabsf(zq[kl + 16 * i]);
+          const float4 th = s_thr[16 * i + kl], tl = s_thr[8 * 16 + 16 * i + kl];  // conflict-free
+          const float hv[4] = {th.x, th.y, th.z, th.w}, lv[4] = {tl.x, tl.y, tl.z, tl.w};
 #pragma unroll
-          for (int j = 0; j < kSweep; ++j) {
-            const bool in = k < sw_ph1[j];
-            const bool hi = in && a >= sw_hi[j];
-            packed += hi ? 1u << (8 * j) : 0u;
-            nr |= in && !hi && a > sw_lo[j];
-          }
+          for (int j = 0; j < kSweep; ++j)
+            asm("{\n .reg .pred ph, pl;\n setp.ge.f32 ph, %2, %4;\n setp.gt.f32 pl, %2, %5;\n"
+                " @ph add.u32 %0, %0, %3;\n @pl add.u32 %1, %1, %3;\n}"
+                : "+r"(packed), "+r"(above_lo)
+                : "f"(a), "r"(1u << (8 * j)), "f"(hv[j]), "f"(lv[j]));
         }
+        bool nr = packed != above_lo;
         if (qb == 1 && !two) {
           packed = 0;
           nr = false;
@@ -878,14 +901,15 @@ sense16_multi_kernel(Grid16 G, MultiArgs A, const __grid_constant__ MultiMaps ma
         my_off[j] = A.offsets[j][bidx_first + lane];
       }
     }
-    uint4 nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bcf, A.aligned);
+    const uint8_t* rowp = run_row_ptr(A.imgs, A.img_stride, A.pitch, img, br, bcf);
+    uint4 nxt = load_row16_at(rowp, (lane >> 4) < nblk, A.aligned);
     for (int p = 0; 2 * p < nblk; ++p) {
       const int bc0 = bcf + 2 * p;
       const bool two = 2 * p + 1 < nblk;
       __syncwarp();
       reinterpret_cast<uint4*>(st)[lane] = interleave_row16(nxt);
       __syncwarp();
-      if (2 * p + 2 < nblk) nxt = load_row16(A.imgs, A.img_stride, A.pitch, G, img, br, bc0 + 2, A.aligned);
+      if (2 * p + 2 < nblk) nxt = load_row16_at(rowp + 32 * (p + 1), 2 * p + 2 + (lane >> 4) < nblk, A.aligned);
       uint32_t bx[2][2][2];
       u8_bfragT_il(st, bx[0]);
       u8_bfragT_il(st + 256, bx[1]);
