@@ -882,6 +882,12 @@ sense16_multi_kernel(Grid16 G, MultiArgs A, const __grid_constant__ MultiMaps ma
   uint32_t rank_d[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
+  uint32_t rk[2][2];  // the ranks of YtSplit's slot pairs {0,1}, {4,5} / {2,3}, {6,7} as fp16x2
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      rk[j][i] = h2u(__floats2half2_rn((float)rank_d[2 * j + 4 * i], (float)rank_d[2 * j + 4 * i + 1]));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* st = s_stage[warp];
   float* zb0 = &s_buf[warp][0][0];
@@ -930,39 +936,57 @@ sense16_multi_kernel(Grid16 G, MultiArgs A, const __grid_constant__ MultiMaps ma
 #pragma unroll
         for (int s = 0; s < 8; ++s)
           if (s < 2 || !lo_all) zb0[kWbuf * q + rank_d[s]] = Y[q].v[s >> 2][s & 3];
+      // each block's Y^T split once into fp16 hi/lo; every plan masks the split halves
+      YtSplit ys[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (lo_all) {
+          split2(Y[q].v[0][0], Y[q].v[0][1], ys[q].h[0][0], ys[q].l[0][0]);
+        } else {
+          ys[q] = split_yt(Y[q]);
+        }
+      }
       __syncwarp();
 #pragma unroll 1
       for (int j = 0; j < A.np; ++j) {
         // register arrays picked by a select chain: a dynamic index would put them in local memory
         const int32_t o0 = __shfl_sync(0xffffffffu, pick4(my_off, j), 2 * p);
         float* dst = A.payload[j] + (int64_t)img * A.payload_stride[j] + o0;
-        const int c0 = pick4(cnt0, j), c1 = pick4(cnt1, j), total = c0 + c1, skip = kWbuf - c0;
-#pragma unroll 1
-        for (int k = lane; k < total; k += 64) {
-          const int k2 = k + 32;
-          const float v0 = zb0[k < c0 ? k : k + skip];
-          float v1 = 0.f;
-          if (k2 < total) v1 = zb0[k2 < c0 ? k2 : k2 + skip];
-          dst[k] = v0;
-          if (k2 < total) dst[k2] = v1;
-        }
+        const int c0 = pick4(cnt0, j), c1 = pick4(cnt1, j);
+        // the pair's prefixes are adjacent in the payload: block 0's, then block 1's
+#pragma unroll 2
+        for (int k = lane; k < c0; k += 32) dst[k] = zb0[k];
+        float* dst1 = dst + c0;
+#pragma unroll 2
+        for (int k = lane; k < c1; k += 32) dst1[k] = zb0[kWbuf + k];
         const bool lo_j = c0 <= 36 && c1 <= 36;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (q == 1 && !two) break;
-          const int cq = q ? c1 : c0;
-          Acc16 Ym;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) Ym.v[s >> 2][s & 3] = (int)rank_d[s] < cq ? Y[q].v[s >> 2][s & 3] : 0.f;
-          const Acc16 X = lo_j ? dct16_inv_from_yt_lo(f, Ym) : dct16_inv_from_yt(f, Ym);
-          if (kBulk) {
-            if (q == 0 && lane == 0) bulk_wait_read1();  // this tile's store from two rounds ago
-            if (q == 0) __syncwarp();
-            stage_dfrag_sw(s_out + (warp * 2 + tile_sel) * 2048, 16 * q, X);
-          } else {
-            store_dfrag(A.out[j] + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + (bc0 + q) * 16,
-                        A.out_pitch, X);
-          }
+        // both blocks' inverses back to back (two independent MMA chains interleave); a lone last
+        // block's partner is a zero block, clipped by the tensor map or skipped below
+        const uint32_t ch0 = h2u(__floats2half2_rn((float)c0, (float)c0));
+        const uint32_t ch1 = h2u(__floats2half2_rn((float)c1, (float)c1));
+        Acc16 X[2];
+        if (lo_j) {
+          YtSplit m0, m1;
+          const uint32_t k0 = h2_lt_mask(rk[0][0], ch0), k1 = h2_lt_mask(rk[0][0], ch1);
+          m0.h[0][0] = ys[0].h[0][0] & k0;
+          m0.l[0][0] = ys[0].l[0][0] & k0;
+          m1.h[0][0] = ys[1].h[0][0] & k1;
+          m1.l[0][0] = ys[1].l[0][0] & k1;
+          X[0] = dct16_inv_from_split_lo(f, m0);
+          X[1] = dct16_inv_from_split_lo(f, m1);
+        } else {
+          X[0] = dct16_inv_from_split(f, mask_yt(ys[0], rk, ch0));
+          X[1] = dct16_inv_from_split(f, mask_yt(ys[1], rk, ch1));
+        }
+        if (kBulk) {
+          if (lane == 0) bulk_wait_read1();  // this tile's store from two rounds ago
+          __syncwarp();
+          stage_dfrag_sw(s_out + (warp * 2 + tile_sel) * 2048, 0, X[0]);
+          stage_dfrag_sw(s_out + (warp * 2 + tile_sel) * 2048, 16, X[1]);
+        } else {
+          float* o = A.out[j] + (int64_t)img * A.out_stride + (int64_t)(br * 16) * A.out_pitch + bc0 * 16;
+          store_dfrag(o, A.out_pitch, X[0]);
+          if (two) store_dfrag(o + 16, A.out_pitch, X[1]);
         }
         if (kBulk) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // st.shared -> async proxy

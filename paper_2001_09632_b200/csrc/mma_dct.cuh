@@ -382,6 +382,73 @@ __device__ __forceinline__ Acc16 dct16_inv_from_yt_lo(const Frag16& f, const Acc
   return R;
 }
 
+// Y^T split once into the stage-1 B operands of the inverse (dct16_inv_from_yt's pairs:
+// slots {0,1}, {4,5}, {2,3}, {6,7}); plans then mask the split halves instead of re-splitting.
+struct YtSplit {
+  uint32_t h[2][2], l[2][2];
+};
+__device__ __forceinline__ YtSplit split_yt(const Acc16& Yt) {
+  YtSplit r;
+  split2(Yt.v[0][0], Yt.v[0][1], r.h[0][0], r.l[0][0]);
+  split2(Yt.v[1][0], Yt.v[1][1], r.h[0][1], r.l[0][1]);
+  split2(Yt.v[0][2], Yt.v[0][3], r.h[1][0], r.l[1][0]);
+  split2(Yt.v[1][2], Yt.v[1][3], r.h[1][1], r.l[1][1]);
+  return r;
+}
+// per-half 0xffff where rank < count (ranks and count as exact fp16 pairs)
+__device__ __forceinline__ uint32_t h2_lt_mask(uint32_t ranks, uint32_t count) {
+  uint32_t m;
+  asm("set.lt.u32.f16x2 %0, %1, %2;" : "=r"(m) : "r"(ranks), "r"(count));
+  return m;
+}
+// The zigzag-prefix mask of a plan applied to the split halves: bit-identical to splitting the
+// masked Y^T (a masked value splits to +0 / +0). rk[j][i]: the slot pair's ranks as fp16x2.
+__device__ __forceinline__ YtSplit mask_yt(const YtSplit& S, const uint32_t (&rk)[2][2], uint32_t count_h2) {
+  YtSplit r;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t m = h2_lt_mask(rk[j][i], count_h2);
+      r.h[j][i] = S.h[j][i] & m;
+      r.l[j][i] = S.l[j][i] & m;
+    }
+  return r;
+}
+// dct16_inv_from_yt from pre-split (masked) operands
+__device__ __forceinline__ Acc16 dct16_inv_from_split(const Frag16& f, const YtSplit& S) {
+  Acc16 T;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    T.v[j][0] = T.v[j][1] = T.v[j][2] = T.v[j][3] = 0.f;
+    mma16816(T.v[j], f.th, S.l[j][0], S.l[j][1]);
+    mma16816(T.v[j], f.tl, S.h[j][0], S.h[j][1]);
+    mma16816(T.v[j], f.th, S.h[j][0], S.h[j][1]);
+  }
+  return stage2(T, f.tbh, f.tbl);
+}
+// dct16_inv_from_yt_lo from pre-split (masked) operands: only slots {0,1} (S.h/l[0][0])
+__device__ __forceinline__ Acc16 dct16_inv_from_split_lo(const Frag16& f, const YtSplit& S) {
+  Acc16 T;
+  T.v[0][0] = T.v[0][1] = T.v[0][2] = T.v[0][3] = 0.f;
+  mma16816(T.v[0], f.th, S.l[0][0], 0u);
+  mma16816(T.v[0], f.tl, S.h[0][0], 0u);
+  mma16816(T.v[0], f.th, S.h[0][0], 0u);
+  uint32_t ah[4], al[4];
+  split2(T.v[0][0], T.v[0][1], ah[0], al[0]);
+  split2(T.v[0][2], T.v[0][3], ah[1], al[1]);
+  ah[2] = al[2] = ah[3] = al[3] = 0u;
+  Acc16 R;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    R.v[j][0] = R.v[j][1] = R.v[j][2] = R.v[j][3] = 0.f;
+    mma16816(R.v[j], al, f.tbh[j][0], f.tbh[j][1]);
+    mma16816(R.v[j], ah, f.tbl[j][0], f.tbl[j][1]);
+    mma16816(R.v[j], ah, f.tbh[j][0], f.tbh[j][1]);
+  }
+  return R;
+}
+
 __device__ __forceinline__ uint4 interleave_row16(uint4 v) {
   return make_uint4(__byte_perm(v.x, v.z, 0x5410), __byte_perm(v.x, v.z, 0x7632), __byte_perm(v.y, v.w, 0x5410),
                     __byte_perm(v.y, v.w, 0x7632));
