@@ -381,29 +381,12 @@ static int sweep_impl(Ctx* ctx, const abcs_sense_plan* plans, int32_t np, const 
   };
   const char* multi_env = getenv("ABCS_SWEEP_MULTI");
   if (!(multi_env && multi_env[0] == '0') && p0.block == 16 && out_stride % 2 == 0 && out_pitch % 2 == 0) {
-    // every plan's allocation (the later plans' on the side stream, in parallel), then one
-    // payload pass that transforms each block once for all plans
-    cudaStream_t side = nullptr;
-    if (ctx->pipe_streams > 1) {
-      if (!ctx->side[lane]) {
-        cudaStreamCreateWithFlags(&ctx->side[lane], cudaStreamNonBlocking);
-        for (auto& e : ctx->ev_side[lane]) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      }
-      side = ctx->side[lane];
-      cudaError_t e = cudaEventRecord(ctx->ev_side[lane][0], s);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->ev_side[lane][0], 0);
-      if (e != cudaSuccess) return cuda_status(e, "sweep fork");
-    }
-    for (int j = 0; j < np; ++j) {
-      const abcs_sense_plan& q = plans[j];
-      st = launch_alloc_cta(ctx, q.rows, q.cols, n, weights[j], fa_of(j), (side && j > 0) ? side : s);
-      if (st) return st;
-    }
-    if (side) {
-      cudaError_t e = cudaEventRecord(ctx->ev_side[lane][1], side);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_side[lane][1], 0);
-      if (e != cudaSuccess) return cuda_status(e, "sweep join");
-    }
+    // every plan's allocation in one launch, then one payload pass that transforms each block
+    // once for all plans
+    FusedAlloc fas[4];
+    for (int j = 0; j < np; ++j) fas[j] = fa_of(j);
+    st = launch_alloc_cta_plans(ctx, np, p0.rows, p0.cols, n, weights, fas, s);
+    if (st) return st;
     const uint16_t* cnts[4];
     const int32_t* offc[4];
     float* pays[4];

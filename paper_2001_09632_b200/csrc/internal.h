@@ -167,6 +167,9 @@ struct FusedAlloc {
   int cap, base, wmax;
 };
 bool fused_alloc_supported(Ctx* ctx, int rows, int cols, int n, int wmax);
+// every plan's allocation of a DD sweep in one launch (plan = blockIdx.y)
+int launch_alloc_cta_plans(Ctx* ctx, int np, int rows, int cols, int n, uint32_t* const* weights,
+                           const FusedAlloc* fa, cudaStream_t s);
 // mode 1: DD weights; 2: payload; 3: payload + fused decode
 bool umma16_enabled();
 int launch_sense16_umma(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,

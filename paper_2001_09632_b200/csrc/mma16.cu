@@ -503,11 +503,24 @@ decode16_kernel(Grid16 G, uint32_t total_blocks, const uint16_t* __restrict__ co
 // the reference basis, |c| > T strict (sensing.cpp:354). Should the list overflow
 // (only adversarial inputs: capacity is 2 entries per block), every flagged block
 // is recounted in full in fp64 instead.
+struct FixPlans {  // plan j = blockIdx.y
+  int phase1[4];
+  double T[4];
+  const uint32_t* list[4];
+  const uint32_t* count[4];
+  const uint8_t* flags[4];
+  uint32_t* weights[4];
+};
 __global__ void __launch_bounds__(256)
-dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch, Grid16 G, int phase1, double T,
-                  const uint32_t* __restrict__ list, const uint32_t* __restrict__ count, uint32_t cap,
-                  const uint8_t* __restrict__ flags, uint32_t total_blocks, uint32_t* __restrict__ weights) {
-  const uint32_t n = *count;
+dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitch, Grid16 G, FixPlans F, uint32_t cap,
+                  uint32_t total_blocks) {
+  const int j = blockIdx.y;
+  const int phase1 = F.phase1[j];
+  const double T = F.T[j];
+  const uint32_t* __restrict__ list = F.list[j];
+  const uint8_t* __restrict__ flags = F.flags[j];
+  uint32_t* __restrict__ weights = F.weights[j];
+  const uint32_t n = *F.count[j];
   const double* C = basis_dev<16>();
   const int lane = threadIdx.x & 31, c = lane & 15;
   const unsigned half = 0xffffu << (lane & 16);
@@ -781,9 +794,17 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
       ktimer_end(ctx, s, kt);
       ctx->launches++;
       kt = ktimer_begin(ctx, s, "dd_fixup16");
-      dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1, T, A.fix_list,
-                                                               A.fix_count, A.fix_cap, A.fix_flag, G.nb * (uint32_t)n,
-                                                               weights);
+      {
+      FixPlans F{};
+      F.phase1[0] = phase1;
+      F.T[0] = T;
+      F.list[0] = A.fix_list;
+      F.count[0] = A.fix_count;
+      F.flags[0] = A.fix_flag;
+      F.weights[0] = weights;
+      dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, F, A.fix_cap,
+                                                               G.nb * (uint32_t)n);
+      }
       ktimer_end(ctx, s, kt);
       if (fa) {  // allocation: one CTA per image (cta_alloc.cuh)
         ctx->launches++;
@@ -1108,15 +1129,54 @@ int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const ui
   ctx->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_status(e, "sense16 sweep launch");
+  // every plan's fp64 fixup in one launch (plan j = blockIdx.y)
+  FixPlans F{};
   for (int j = 0; j < n_sw; ++j) {
-    kt = ktimer_begin(ctx, s, "dd_fixup16");
-    dd_fixup16_kernel<<<(unsigned)ctx->sm_count, 256, 0, s>>>(imgs, img_stride, pitch, G, phase1[j], T[j],
-                                                             A.sw_fix_list[j], A.sw_fix_count[j], A.fix_cap,
-                                                             A.sw_fix_flag[j], G.nb * (uint32_t)n, weights[j]);
-    ktimer_end(ctx, s, kt);
-    ctx->launches++;
+    F.phase1[j] = phase1[j];
+    F.T[j] = T[j];
+    F.list[j] = A.sw_fix_list[j];
+    F.count[j] = A.sw_fix_count[j];
+    F.flags[j] = A.sw_fix_flag[j];
+    F.weights[j] = weights[j];
   }
+  kt = ktimer_begin(ctx, s, "dd_fixup16");
+  dd_fixup16_kernel<<<dim3((unsigned)(ctx->sm_count + n_sw - 1) / n_sw, (unsigned)n_sw), 256, 0, s>>>(
+      imgs, img_stride, pitch, G, F, A.fix_cap, G.nb * (uint32_t)n);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
   return cuda_status(cudaGetLastError(), "dd fixup launch");
+}
+
+// Several plans' allocations in one launch (plan j = blockIdx.y, image = blockIdx.x).
+struct AllocPlans {
+  const uint32_t* weights[4];
+  FusedAlloc fa[4];
+};
+__global__ void __launch_bounds__(kCtaAllocThreads, 7)
+alloc_cta_plans_kernel(AllocPlans P, int nb) {
+  __shared__ CtaAllocSmem S;
+  const int img = blockIdx.x, j = blockIdx.y;
+  const FusedAlloc& fa = P.fa[j];
+  const int st = cta_allocate(S, P.weights[j] + (int64_t)img * nb, nb, fa.wmax, fa.budget, fa.cap, fa.base,
+                              fa.counts + (int64_t)img * nb, fa.offsets + (int64_t)img * nb);
+  if (threadIdx.x == 0 && fa.status) fa.status[img] = st;
+}
+
+int launch_alloc_cta_plans(Ctx* ctx, int np, int rows, int cols, int n, uint32_t* const* weights,
+                           const FusedAlloc* fa, cudaStream_t s) {
+  if (np < 1 || np > 4) return set_error(ABCS_ERR_LOGIC, "alloc plans: 1..4 plans");
+  const Grid16 G = make_grid16(rows, cols, n);
+  if (G.total_units == 0) return ABCS_OK;
+  AllocPlans P{};
+  for (int j = 0; j < np; ++j) {
+    P.weights[j] = weights[j];
+    P.fa[j] = fa[j];
+  }
+  const int kt = ktimer_begin(ctx, s, "alloc_cta");
+  alloc_cta_plans_kernel<<<dim3((unsigned)n, (unsigned)np), kCtaAllocThreads, 0, s>>>(P, (int)G.nb);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "alloc_cta launch");
 }
 
 // The per-image allocation of a DD plan (alloc_cta_kernel) from weights already computed.
