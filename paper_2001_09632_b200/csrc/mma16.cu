@@ -563,7 +563,6 @@ dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitc
   }
 }
 
-// largest_remainder_allocate with one warp per image (no CTA barriers).
 // Allocation for the fused DD path: one CTA per image (cta_alloc.cuh).
 __global__ void __launch_bounds__(kCtaAllocThreads, 7)
 alloc_cta_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, long long budget, int cap, int base,

@@ -24,7 +24,13 @@ timeout 300 python tools/prof_sweep.py > $O/sweep_plain.log 2>&1 && \
 timeout 900 ncu --clock-control none --import-source on --set full -k regex:sense16_multi -s 1 -c 1 \
   -o $O/multi -f python tools/prof_sweep.py > $O/multi_ncu.log 2>&1
 echo "multi ncu rc=$?"
-for k in ida multi; do
+timeout 900 ncu --clock-control none --import-source on --set full -k regex:sense16_kernel -s 1 -c 1 \
+  -o $O/weights -f python tools/prof_sweep.py > $O/weights_ncu.log 2>&1
+echo "weights ncu rc=$?"
+timeout 900 ncu --clock-control none --import-source on --set full -k regex:alloc_cta -s 1 -c 1 \
+  -o $O/alloc -f python tools/prof_sweep.py > $O/alloc_ncu.log 2>&1
+echo "alloc ncu rc=$?"
+for k in ida multi weights alloc; do
   ncu -i $O/$k.ncu-rep --page details --csv > $O/${k}_details.csv 2>/dev/null
   ncu -i $O/$k.ncu-rep --page raw --csv > $O/${k}_raw.csv 2>/dev/null
   ncu -i $O/$k.ncu-rep --page source --csv --print-source sass > $O/${k}_sass.csv 2>/dev/null
