@@ -18,6 +18,8 @@
 //   4. per-image reductions folded by the last CTA (finish_image).
 // fp32 operands are split into fp16 hi/lo pairs (mma_dct.cuh), ~fp32 accuracy.
 #include <cfloat>
+#include <cstring>
+#include <type_traits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -505,38 +507,46 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b0];  // the pair's run in y / z
     float zsq = 0.f, ysq = 0.f;
     unsigned int badz = ~0u;
+    // NS elements per lane in flight per round; NS from the pair's run length (warp-uniform), so
+    // short runs (cfg4: ~130) do not pay for 8 predicated slots per lane
+    auto rounds = [&](auto ns) {
+      constexpr int NS = decltype(ns)::value;
 #pragma unroll 1
-    for (int e0 = 0; e0 < kw; e0 += 256) {  // up to 8 elements per lane in flight
-      float yv[8], zo[8];
+      for (int e0 = 0; e0 < kw; e0 += 32 * NS) {
+        float yv[NS], zo[NS];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int e = e0 + lane + 32 * i;
-        yv[i] = e < kw ? __ldg(P.y + pb + e) : 0.f;
-        zo[i] = (e < kw && !P.is_init) ? P.z[pb + e] : 0.f;
-      }
+        for (int i = 0; i < NS; ++i) {
+          const int e = e0 + lane + 32 * i;
+          yv[i] = e < kw ? __ldg(P.y + pb + e) : 0.f;
+          zo[i] = (e < kw && !P.is_init) ? P.z[pb + e] : 0.f;
+        }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int e = e0 + lane + 32 * i;
-        if (e < kw) {
-          const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0);
-          const int f = s.zidx[k];  // flat u * 16 + v
-          float* slot = s.RS + (b0 + q) * kTB + (f & 15) * 20 + (f >> 4);
-          const float yk = yv[i];
-          // finish_step (recon.cpp:86-88); the centred transform's DC lacks 16 cb (exact)
-          const float ya = k == 0 ? yk - 16.f * (q ? cb1 : cb0) : yk;
-          const float yc = *slot;
-          const float zn = (ya - yc) + ons * zo[i];
-          P.z[pb + e] = zn;
-          *slot = yc + zn;  // W = Y + z
-          zsq = fmaf(zn, zn, zsq);
-          ysq = fmaf(yk, yk, ysq);
-          if (!isfinite(zn)) {
-            const unsigned int gi = (unsigned)(s.meta_off[b0] + e);
-            badz = gi < badz ? gi : badz;
+        for (int i = 0; i < NS; ++i) {
+          const int e = e0 + lane + 32 * i;
+          if (e < kw) {
+            const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0);
+            const int f = s.zidx[k];  // flat u * 16 + v
+            float* slot = s.RS + (b0 + q) * kTB + (f & 15) * 20 + (f >> 4);
+            const float yk = yv[i];
+            // finish_step (recon.cpp:86-88); the centred transform's DC lacks 16 cb (exact)
+            const float ya = k == 0 ? yk - 16.f * (q ? cb1 : cb0) : yk;
+            const float yc = *slot;
+            const float zn = (ya - yc) + ons * zo[i];
+            P.z[pb + e] = zn;
+            *slot = yc + zn;  // W = Y + z
+            zsq = fmaf(zn, zn, zsq);
+            ysq = fmaf(yk, yk, ysq);
+            if (!isfinite(zn)) {
+              const unsigned int gi = (unsigned)(s.meta_off[b0] + e);
+              badz = gi < badz ? gi : badz;
+            }
           }
         }
       }
-    }
+    };
+    if (kw <= 128) rounds(std::integral_constant<int, 4>{});
+    else if (kw <= 160) rounds(std::integral_constant<int, 5>{});
+    else rounds(std::integral_constant<int, 8>{});
     S.z += (double)zsq;
     if (P.is_init) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
     S.badz = badz < S.badz ? badz : S.badz;
@@ -567,7 +577,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
 // init, warm start: acc <- x0 = A* y (recon.cpp:119-131), the inverse of each block's y prefix
 // (columns then rows through the transpose tiles). Called before block_phase16_f32.
 template <class Sm>
-__device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s) {
+__device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s, float& ysq) {
   const int t = threadIdx.x;
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
@@ -581,13 +591,28 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
     for (int q = 0; q < 4; ++q) *reinterpret_cast<float4*>(tb + lr * 20 + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncwarp();
-  if (t < 256) {
+  if (t < 256) {  // the pair's payload run: up to 8 loads per lane in flight; z0 = 0 and ||y||^2 on the way
     const int lane = t & 31, b0 = b & ~1;
     const int c0 = max(s.meta_cnt[b0], 0), kw = c0 + max(s.meta_cnt[b0 + 1], 0);
-    const float* ysrc = P.y + (int64_t)img * P.y_stride + s.meta_off[b0];
-    for (int e = lane; e < kw; e += 32) {
-      const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0), f = s.zidx[k];
-      s.RS[(b0 + q) * kTB + (f & 15) * 20 + (f >> 4)] = __ldg(ysrc + e);
+    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b0];
+#pragma unroll 1
+    for (int e0 = 0; e0 < kw; e0 += 256) {
+      float yv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + lane + 32 * i;
+        yv[i] = e < kw ? __ldg(P.y + pb + e) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + lane + 32 * i;
+        if (e < kw) {
+          const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0), f = s.zidx[k];
+          s.RS[(b0 + q) * kTB + (f & 15) * 20 + (f >> 4)] = yv[i];
+          P.z[pb + e] = 0.f;
+          ysq = fmaf(yv[i], yv[i], ysq);
+        }
+      }
     }
   }
   __syncwarp();
@@ -627,7 +652,7 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s)
 // so pseudo0 = x0 + A* z0 = x0 and the block phase's transforms are skipped. sigma0 = ||y|| / sqrt(M)
 // needs ||y||^2, summed over each warp's payload run; the trace's PSNR of x0 needs the SSE.
 template <class Sm>
-__device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S) {
+__device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S, float ysq) {
   const int t = threadIdx.x;
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
@@ -636,22 +661,17 @@ __device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s
     load_row16(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc, xr);
     const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;
     row_checks(P, img, gr, gc, xr, S);
+    if (P.pseudo_out) {  // pseudo0 = x0 (internal buffer: Wc % 16 == 0, 16-B aligned rows)
+      float4* dst = reinterpret_cast<float4*>(P.pseudo_out + (int64_t)img * P.Hc * P.Wc + (int64_t)gr * P.Wc + gc);
 #pragma unroll
-    for (int c = 0; c < 16; c += 2) store_out(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), make_float2(0.f, 0.f));
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(xr[4 * q], xr[4 * q + 1], xr[4 * q + 2], xr[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) store_out(P, img, gr, gc + c, make_float2(xr[c], xr[c + 1]), make_float2(0.f, 0.f));
+    }
     if (lr == 0) S.cnt += cnt;
   }
-  if (t < 256) {
-    const int lane = t & 31, b0 = b & ~1;
-    const int kw = max(s.meta_cnt[b0], 0) + max(s.meta_cnt[b0 + 1], 0);
-    const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b0];
-    float ysq = 0.f;
-    for (int e = lane; e < kw; e += 32) {  // the warp over its pair's payload run
-      const float yv = __ldg(P.y + pb + e);
-      ysq = fmaf(yv, yv, ysq);
-      P.z[pb + e] = 0.f;
-    }
-    S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
-  }
+  if (t < 256) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128), summed while init_x16_f32 embedded y
 }
 
 // ---- B = 8: two horizontally adjacent sensing blocks per warp step ------------------------
@@ -817,12 +837,13 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
   if (B == 16 && threadIdx.x < 256) s.zidx[threadIdx.x] = zigzag_dev<16>()[threadIdx.x];
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
+  float ysq16 = 0.f;
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
       for (int i = threadIdx.x; i < kMIn * kMP / 4; i += blockDim.x)
         reinterpret_cast<float4*>(s.acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (B == 16) {
-      init_x16_f32(P, img, R0, C0, s);
+      init_x16_f32(P, img, R0, C0, s, ysq16);
     } else {
       init_x8(P, img, R0, C0, s);
     }
@@ -843,11 +864,13 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
-  if (B == 16 && P.is_init && P.warm) init_finish16(P, img, R0, C0, s, S);
+  if (B == 16 && P.is_init && P.warm) init_finish16(P, img, R0, C0, s, S, ysq16);
   else if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
   else block_phase8(P, img, R0, C0, s, S);
   reduce_and_finish(P, img, region, s, S);
 }
+
+#include "ida_tc.cuh"
 
 // Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109): the IDA step's fp32
 // denoiser (denoise_region_f32) over 64 x 64 regions, the window by cp.async (any field stride).
@@ -919,6 +942,55 @@ static int encode_window_map(CUtensorMap* tm, const float* field, int Wc, int Hc
   return r == CUDA_SUCCESS ? ABCS_OK : set_error(ABCS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
+// The tensor-core step (ida_tc.cuh) is opt-in (ABCS_IDA_TC=1) for plain IDA steps with B = 16:
+// parity-green, but slower than the fp32 CUDA-core denoiser of ida_mma_kernel.
+bool ida_tc_enabled() {
+  const char* e = getenv("ABCS_IDA_TC");
+  return e && e[0] == '1';
+}
+
+// The tensor-core step's basis operands (ida_tc.cuh tc_load_bases) from the reference basis
+// (dct.cpp:9-21): C[u][r] C[v][c] in fp64, split into fp16 hi + lo, laid out as the MMAs' B
+// operands. Called once per context (a synchronous copy: outside any stream capture).
+int ida_tc_upload_bases() {
+  static unsigned char host[32768];
+  const double* C = abcs_gen::kBasis8;
+  auto put = [&](int base, int off, double val) {
+    const __half h = __double2half(val), l = __double2half(val - (double)__half2float(h));
+    memcpy(host + base + off, &h, 2);
+    memcpy(host + base + (base < 16384 ? 2048 : 512) + off, &l, 2);
+  };
+  for (int j = 0; j < 4; ++j)  // F_j[p][k]: n = k = 8u + v (coefficient), K = p (pixel of quad (dy, dx))
+    for (int n = 0; n < 64; ++n)
+      for (int p = 0; p < 16; ++p) {
+        const int u = n >> 3, v = n & 7, r = 4 * (j >> 1) + (p >> 2), c = 4 * (j & 1) + (p & 3);
+        put((2 * j) * 2048, (n & 7) * 16 + (n >> 3) * 256 + (p >> 3) * 128 + (p & 7) * 2, C[u * 8 + r] * C[v * 8 + c]);
+      }
+  for (int c4 = 0; c4 < 4; ++c4)  // G_{c,j}[k][p]: n = p (pixel of quad (a, b)), K = k - 16 c
+    for (int j = 0; j < 4; ++j)
+      for (int p = 0; p < 16; ++p)
+        for (int kk = 0; kk < 16; ++kk) {
+          const int k = 16 * c4 + kk, u = k >> 3, v = k & 7, r = 4 * (j >> 1) + (p >> 2), c = 4 * (j & 1) + (p & 3);
+          put(16384 + ((c4 * 4 + j) * 2) * 512, (p & 7) * 16 + (p >> 3) * 256 + (kk >> 3) * 128 + (kk & 7) * 2,
+              C[u * 8 + r] * C[v * 8 + c]);
+        }
+  return cuda_status(cudaMemcpyToSymbol(g_tc_bases, host, sizeof(host)), "tensor-core IDA bases");
+}
+
+static void launch_ida_tc(const IdaParams& P, const CUtensorMap& tm, cudaStream_t s) {
+  static int grid_cap = 0;
+  const int bytes = (int)sizeof(IdaTcSmem) + 128;
+  if (!grid_cap) {
+    cudaFuncSetAttribute(ida_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_cap = std::max(1, sms) * IDA_TC_MINB;  // 2 CTAs x 256 TMEM columns per SM
+  }
+  const int total = P.n * P.regions_per_img;
+  ida_tc_kernel<<<std::min(total, grid_cap), kTcThreads, bytes, s>>>(P, tm);
+}
+
 template <int B>
 static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   static bool attr = false;  // > 48 KB of dynamic shared memory: opt in once per instantiation
@@ -930,6 +1002,10 @@ static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   if (!P.is_init && !P.x_in && P.pseudo_in && encode_window_map(&tm, P.pseudo_in, P.Wc, P.Hc, P.n) != ABCS_OK) return;
+  if (B == 16 && !P.is_init && !P.x_in && ida_tc_enabled()) {
+    launch_ida_tc(P, tm, s);
+    return;
+  }
   ida_mma_kernel<B><<<grid, kFThreads, bytes, s>>>(P, tm);
 }
 
