@@ -80,10 +80,6 @@ int abcs_ctx_create(int device, abcs_ctx** out) {
       return cuda_status(e, "stream create");
     }
   }
-  if (int st = ida_tc_upload_bases()) {
-    delete ctx;
-    return st;
-  }
   *out = reinterpret_cast<abcs_ctx*>(ctx);
   return ABCS_OK;
 }
@@ -769,7 +765,7 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
                                      u(d_y), (uint64_t)y_stride, (uint64_t)n, (uint64_t)cfg->iterations,
                                      (uint64_t)cfg->denoiser_block, dbits, kbits, u(d_ref), (uint64_t)ref_stride,
                                      (uint64_t)ref_pitch, u(d_out), (uint64_t)out_stride, (uint64_t)out_pitch,
-                                     u(d_trace), u(d_diverged), u(scr), (uint64_t)ida_tc_enabled()};
+                                     u(d_trace), u(d_diverged), u(scr)};
   Ctx::GraphEntry* hit = nullptr;
   for (auto& g : ctx->graphs)
     if (g.key == key) hit = &g;

@@ -870,8 +870,6 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
   reduce_and_finish(P, img, region, s, S);
 }
 
-#include "ida_tc.cuh"
-
 // Standalone denoise(dct_threshold) on f32 fields (denoise.cpp:96-109): the IDA step's fp32
 // denoiser (denoise_region_f32) over 64 x 64 regions, the window by cp.async (any field stride).
 template <bool kVec>
@@ -942,55 +940,6 @@ static int encode_window_map(CUtensorMap* tm, const float* field, int Wc, int Hc
   return r == CUDA_SUCCESS ? ABCS_OK : set_error(ABCS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
-// The tensor-core step (ida_tc.cuh) is opt-in (ABCS_IDA_TC=1) for plain IDA steps with B = 16:
-// parity-green, but slower than the fp32 CUDA-core denoiser of ida_mma_kernel.
-bool ida_tc_enabled() {
-  const char* e = getenv("ABCS_IDA_TC");
-  return e && e[0] == '1';
-}
-
-// The tensor-core step's basis operands (ida_tc.cuh tc_load_bases) from the reference basis
-// (dct.cpp:9-21): C[u][r] C[v][c] in fp64, split into fp16 hi + lo, laid out as the MMAs' B
-// operands. Called once per context (a synchronous copy: outside any stream capture).
-int ida_tc_upload_bases() {
-  static unsigned char host[32768];
-  const double* C = abcs_gen::kBasis8;
-  auto put = [&](int base, int off, double val) {
-    const __half h = __double2half(val), l = __double2half(val - (double)__half2float(h));
-    memcpy(host + base + off, &h, 2);
-    memcpy(host + base + (base < 16384 ? 2048 : 512) + off, &l, 2);
-  };
-  for (int j = 0; j < 4; ++j)  // F_j[p][k]: n = k = 8u + v (coefficient), K = p (pixel of quad (dy, dx))
-    for (int n = 0; n < 64; ++n)
-      for (int p = 0; p < 16; ++p) {
-        const int u = n >> 3, v = n & 7, r = 4 * (j >> 1) + (p >> 2), c = 4 * (j & 1) + (p & 3);
-        put((2 * j) * 2048, (n & 7) * 16 + (n >> 3) * 256 + (p >> 3) * 128 + (p & 7) * 2, C[u * 8 + r] * C[v * 8 + c]);
-      }
-  for (int c4 = 0; c4 < 4; ++c4)  // G_{c,j}[k][p]: n = p (pixel of quad (a, b)), K = k - 16 c
-    for (int j = 0; j < 4; ++j)
-      for (int p = 0; p < 16; ++p)
-        for (int kk = 0; kk < 16; ++kk) {
-          const int k = 16 * c4 + kk, u = k >> 3, v = k & 7, r = 4 * (j >> 1) + (p >> 2), c = 4 * (j & 1) + (p & 3);
-          put(16384 + ((c4 * 4 + j) * 2) * 512, (p & 7) * 16 + (p >> 3) * 256 + (kk >> 3) * 128 + (kk & 7) * 2,
-              C[u * 8 + r] * C[v * 8 + c]);
-        }
-  return cuda_status(cudaMemcpyToSymbol(g_tc_bases, host, sizeof(host)), "tensor-core IDA bases");
-}
-
-static void launch_ida_tc(const IdaParams& P, const CUtensorMap& tm, cudaStream_t s) {
-  static int grid_cap = 0;
-  const int bytes = (int)sizeof(IdaTcSmem) + 128;
-  if (!grid_cap) {
-    cudaFuncSetAttribute(ida_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap = std::max(1, sms) * IDA_TC_MINB;  // 2 CTAs x 256 TMEM columns per SM
-  }
-  const int total = P.n * P.regions_per_img;
-  ida_tc_kernel<<<std::min(total, grid_cap), kTcThreads, bytes, s>>>(P, tm);
-}
-
 template <int B>
 static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   static bool attr = false;  // > 48 KB of dynamic shared memory: opt in once per instantiation
@@ -1002,10 +951,6 @@ static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   if (!P.is_init && !P.x_in && P.pseudo_in && encode_window_map(&tm, P.pseudo_in, P.Wc, P.Hc, P.n) != ABCS_OK) return;
-  if (B == 16 && !P.is_init && !P.x_in && ida_tc_enabled()) {
-    launch_ida_tc(P, tm, s);
-    return;
-  }
   ida_mma_kernel<B><<<grid, kFThreads, bytes, s>>>(P, tm);
 }
 

@@ -109,8 +109,6 @@ int launch_ida(Ctx* ctx, int32_t rows, int32_t cols, int32_t block, const uint16
                void* scratch, cudaStream_t s);
 struct IdaParams;
 int ida_mma_region();
-int ida_tc_upload_bases();  // once per context (ida_mma.cu)
-bool ida_tc_enabled();      // ABCS_IDA_TC=1: the tensor-core IDA step (ida_tc.cuh)
 void launch_ida_mma_kernel(int block, const IdaParams& P, dim3 grid, cudaStream_t s);
 int launch_psnr(Ctx* ctx, const uint8_t* ref, int64_t ref_stride, int ref_pitch, const float* img, int64_t img_stride,
                 int img_pitch, int h, int w, int n, double* psnr, cudaStream_t s, double* mse = nullptr,

@@ -809,53 +809,6 @@ def test_race_free_batch_independence(p, torch, cs):
         os.environ.pop("ABCS_ALLOC_CLUSTER", None)
 
 
-@pytest.mark.parametrize("case", [c for c in IDA_CASES if c[2] == 16] + [(200, 328, 16, 1, 4, 1, 4)])
-def test_ida_tensor_core_path_parity(p, torch, checker, case):
-    """The opt-in tcgen05 IDA step (ABCS_IDA_TC=1, ida_tc.cuh: Kronecker-form 8x8 denoiser with the
-    overlap-add folded into the inverse GEMM) against the reference, at the bars of test_ida_parity."""
-    H, W, B, num, den, algo, iters = case
-    imgs = synth(H, W, n=2, seed=H * W + iters + 7)
-    b = sense_dev(p, torch, imgs, B, num, den, algo)
-    ref_t = torch.from_numpy(imgs).cuda()
-    rc = p.ReconConfig(p.ReconMethod.Ida, iterations=iters)
-    base, _, _ = p.ida_batch(b, rc, reference=ref_t)
-    try:
-        os.environ["ABCS_IDA_TC"] = "1"
-        out, tr, _ = p.ida_batch(b, rc, reference=ref_t)
-        torch.cuda.synchronize()
-    finally:
-        os.environ.pop("ABCS_IDA_TC", None)
-    assert float((out - base).abs().max()) <= 2 * PIXEL_TOL  # each within PIXEL_TOL of the reference
-    out, tr = out.cpu().numpy(), tr.cpu().numpy()
-    for i in range(2):
-        want = checker.sense(imgs[i], B, num, den, algo)
-        x, trace = checker.reconstruct_ida(b.plan.rows, b.plan.cols, B, want["counts"], want["coeffs"], iters,
-                                           ref=imgs[i])
-        assert np.max(np.abs(out[i] - x)) <= PIXEL_TOL, (i, np.max(np.abs(out[i] - x)))
-        assert np.max(np.abs(tr[i, :, 3] - trace[:, 3])) <= PSNR_TOL
-        assert np.allclose(tr[i, :, 2], trace[:, 2], rtol=1e-4)
-
-
-def test_ida_tensor_core_path_rescale(p, checker):
-    """x1000 field on the tcgen05 IDA step: the power-of-two operand rescale keeps the fp16 halves
-    finite (no spurious divergence) and the result follows the reference."""
-    H, W, iters = 96, 128, 3
-    img = synth(H, W, n=1, seed=517)[0]
-    want = checker.sense(img, 16, 1, 4, 1)
-    coeffs = (want["coeffs"] * 1000.0).astype(np.float32)
-    ms = p.MeasurementSet(H, W, 16, p.Algorithm.BBV, 1, 4, want["threshold"], want["counts"], coeffs)
-    try:
-        os.environ["ABCS_IDA_TC"] = "1"
-        res = p.reconstruct(ms, p.ReconConfig(p.ReconMethod.Ida, iterations=iters), reference=img)
-    finally:
-        os.environ.pop("ABCS_IDA_TC", None)
-    x_ref, trace = checker.reconstruct_ida(want["rows"], want["cols"], 16, want["counts"], coeffs.astype(np.float64),
-                                           iters, ref=img)
-    assert np.max(np.abs(res.image - x_ref)) <= PIXEL_TOL * 1000.0
-    tr = np.array([[r.iteration, r.residual_norm, r.sigma, r.psnr_db] for r in res.trace])
-    assert np.allclose(tr[:, 2], trace[:, 2], rtol=1e-4)
-
-
 @pytest.mark.parametrize("B", [8, 16, 32])
 def test_ida_large_dynamic_range(p, checker, B):
     """IDA on a measurement set scaled x1000 (fields ~2.5e5, beyond fp16's range): the B = 16 path
