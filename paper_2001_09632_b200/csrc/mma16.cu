@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "mma_dct.cuh"
+#include "zz_banks.cuh"
 #include "cta_alloc.cuh"
 
 namespace abcs_b200 {
@@ -174,7 +175,7 @@ template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false, int
 __global__ void __launch_bounds__(kM16Threads, 3)
 sense16_kernel(Grid16 G, Sense16Args A) {
   __shared__ __align__(16) uint8_t s_stage[kM16Warps][512];
-  constexpr int kWbuf = 256;
+  constexpr int kWbuf = kSweep > 0 ? 272 : 256;  // sweep: the second block's buffer 16 banks over
   __shared__ float s_buf[kM16Warps][2][kWbuf];
   __shared__ uint2 s_btab[kWeights ? 8 * 32 : 1];  // stage-2 basis B pairs (fill_btab16), weights pass only
   // sweep: per rank e = 16 i + kl each plan's band edge hi (s_thr[e]) and lo (s_thr[128 + e]), +inf
@@ -205,6 +206,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     rank_d[s] = zigzag_rank_dev<16>()[dslot_col(s) * 16 + dslot_row(s)];
+    if constexpr (kSweep > 0) rank_d[s] = (rank_d[s] & ~31u) | kZzBank16[rank_d[s]];  // store address
     if constexpr (kWeights && !kSweep) {
       const bool in = (int)rank_d[s] < A.phase1;
       thr_hi[s] = in ? A.Tf + A.band : INFINITY;
@@ -215,6 +217,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
   int sw_ph1[kSweep > 0 ? kSweep : 1];
   float sw_hi[kSweep > 0 ? kSweep : 1], sw_lo[kSweep > 0 ? kSweep : 1];
   int sw_P = 0;
+  uint32_t sw_addr[2] = {0u, 0u};  // read address of test group i (8 bits each): rank 16 i + kl
   if constexpr (kSweep > 0) {
 #pragma unroll
     for (int j = 0; j < kSweep; ++j) {
@@ -222,6 +225,12 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       sw_hi[j] = A.sw_hi[j];
       sw_lo[j] = A.sw_lo[j];
       sw_P = max(sw_P, sw_ph1[j]);
+    }
+    const int kl = threadIdx.x & 15;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = 16 * i + kl;
+      sw_addr[i >> 2] |= ((uint32_t)(k & ~31) | kZzBank16[k]) << (8 * (i & 3));
     }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,10 +279,12 @@ sense16_kernel(Grid16 G, Sense16Args A) {
       const uint32_t bidx0 = bidx_first + 2 * p;
       if constexpr (kSweep > 0) {
         // DD phase 1 of kSweep plans by zigzag compaction: the pair's coefficients of rank < P go to
-        // the warp's rank-ordered buffer and lane L tests ranks (L & 15) + 16 i of block L >> 4
-        // against each plan (prefix phase1_j, band around T_j): 2P / 32 coefficients per lane
-        // instead of 8 slots per plan, most of them outside every prefix. A zigzag prefix of
-        // <= 136 entries lies in slots 0-5 (u + v <= 15), so slots 6-7 are stored only beyond.
+        // the warp's rank-ordered buffer and lane L tests ranks (L & 15) + 16 i of
+        // block L >> 4 against each plan (prefix phase1_j, band around T_j): 2P / 32 coefficients
+        // per lane instead of 8 slots per plan, most of them outside every prefix. A zigzag prefix
+        // of <= 136 entries lies in slots 0-5 (u + v <= 15), so slots 6-7 are stored only beyond.
+        // Bank-permuted rows (kZzBank16) with the second block 16 banks over: every store slot and
+        // every test read is one wavefront.
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 2; ++q)
@@ -289,7 +300,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (16 * i >= sw_P) break;
-          const float a = fabsf(zq[kl + 16 * i]);
+          const float a = fabsf(zq[(sw_addr[i >> 2] >> (8 * (i & 3))) & 255u]);
           const float4 th = s_thr[16 * i + kl], tl = s_thr[8 * 16 + 16 * i + kl];  // conflict-free
           const float hv[4] = {th.x, th.y, th.z, th.w}, lv[4] = {tl.x, tl.y, tl.z, tl.w};
 #pragma unroll
@@ -314,7 +325,7 @@ sense16_kernel(Grid16 G, Sense16Args A) {
 #pragma unroll 1
               for (int i = 0; 16 * i < sw_P; ++i) {
                 const int k = kl + 16 * i;
-                const float a = fabsf(zq[k]);
+                const float a = fabsf(zq[(k & ~31) | kZzBank16[k]]);
                 if (k < sw_ph1[j] && !(a >= sw_hi[j]) && a > sw_lo[j]) {
                   mine = true;
                   const uint32_t e = atomicAdd(A.sw_fix_count[j], 1u);
