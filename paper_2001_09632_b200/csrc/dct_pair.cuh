@@ -60,4 +60,16 @@ __device__ __forceinline__ float2 p_soft(float2 c, float t0, float t1) {
   return p_sub(c, k);
 }
 
+// clamp(c, -t, t) for t >= 0 in ONE instruction per lane: min.xorsign.abs gives min(|c|, |t|) with
+// the sign of c (t's sign bit is clear), SASS FMNMX.XORSIGN. c - clamp(c, -t, t) is the soft
+// threshold above, so the IDA denoiser can sum clamps instead (linearity, see ida_mma.cu).
+__device__ __forceinline__ float clamp_abs(float c, float t) {
+  float r;
+  asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(r) : "f"(c), "f"(t));
+  return r;
+}
+__device__ __forceinline__ float2 p_clamp(float2 c, float t0, float t1) {
+  return make_float2(clamp_abs(c.x, t0), clamp_abs(c.y, t1));
+}
+
 }  // namespace abcs_b200

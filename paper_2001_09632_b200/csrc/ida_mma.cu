@@ -33,9 +33,6 @@ namespace abcs_b200 {
 
 constexpr int kMR = 64;          // output region side
 constexpr int kMIn = kMR + 8;    // 72: region + 4-px halo each side
-constexpr int kMP = 72;          // smem row pitch (floats): 72 = 8 mod 32 -> conflict-free float2 fragments
-
-constexpr int kMOff = 4 * kMP + 4;  // region pixel (0, 0) inside acc
 constexpr int kWinBytes = 76 * kMIn * 4;  // the fused kernel's TMA window box (kWP x kMIn floats)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -73,7 +70,7 @@ __device__ __forceinline__ void tma_window_wait(uint64_t* bar) {
 
 // field[R0-4 .. R0+68) x [C0-4 .. C0+68) -> s.in (zeros outside the image). The vector path
 // only issues async copies; the caller waits (cp_async_wait_all + barrier) before reading.
-template <bool kVec, int WP = kMP>
+template <bool kVec, int WP>
 __device__ __forceinline__ void load_window(const float* __restrict__ f, int64_t pitch, int R0, int C0, int H, int W,
                                             float* in) {
   if (kVec) {  // W % 4 == 0, 16-byte aligned rows: every float4 is wholly inside or outside
@@ -122,10 +119,14 @@ constexpr int kRP = kTP * 16 + 4;  // R / S row pitch: [tp][v][2] + 4 (148 = 20 
 #endif
 constexpr int kFThreads = 32 * kTP;  // fused kernel: warp w owns segment pair tp = w through stages A-C
 
+// The denoiser's output x replaces the window in place (same layout), so acc is the window: region
+// pixel (0, 0) at kAOff, pitch kWP (76 = 12 mod 32: the block phase's float4 row loads are
+// conflict-free per quarter warp).
+constexpr int kAOff = 4 * kWP + 4;
 struct IdaF32Smem {
   union {
     float in[kMIn * kWP];   // field window (pitch kWP), the TMA destination (128-B aligned)
-    float acc[kMIn * kMP];  // then x over the region (at kMOff, pitch kMP) for the block phase
+    float acc[kMIn * kWP];  // then x over the region (at kAOff, pitch kWP) for the block phase
   };
   union {
     float RS[kMIn * kRP];     // stage A output R[y][tp][v][tj parity], overwritten in place by stage B's S
@@ -137,10 +138,9 @@ struct IdaF32Smem {
   unsigned int bad[2];
   double mine[4];
   uint64_t win_bar;          // TMA window load (one phase per CTA)
-  unsigned short zidx[256];   // B = 16 zigzag order: flat u * 16 + v of rank k (block phase)
+  unsigned short zslot[256];  // B = 16: rank k's slot in a block's transpose tile, (v, u) -> v * 20 + u
 };
 static_assert(kFThreads / 32 * 512 <= kMIn * kRP, "staging buffers fit");
-static_assert(kMIn * kMP <= kMIn * kWP, "acc fits in the window");
 
 __device__ __forceinline__ bool tile_on_grid(int R0, int C0, int H, int W, int ti, int tj) {
   return tj <= 16 && (unsigned)(R0 - 4 + 4 * ti) <= (unsigned)(H - 8) && (unsigned)(C0 - 4 + 4 * tj) <= (unsigned)(W - 8);
@@ -158,7 +158,7 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
   return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-// dct_soft_threshold of the window s.in into s.acc (the 64 x 64 region, pitch kMP at kMOff;
+// dct_soft_threshold of the window s.in into s.acc (the 64 x 64 region, pitch kWP at kAOff;
 // acc aliases the window, which is dead once every warp is past stage A).
 // Warp w owns segment pair tp = w (tj = 2w, 2w + 1) through stages A-C, so the stages are
 // ordered by __syncwarp; only stage C's quads shared with the neighbouring pair need the CTA.
@@ -185,12 +185,23 @@ __device__ __forceinline__ void l1_prefetch_region_yz(const IdaParams& P, int im
     asm volatile("prefetch.global.L1 [%0];\n" ::"l"(base + o));
 }
 
+// Linearity form of the soft threshold: soft(Y) = Y - clamp(Y, -t, t) (t = 0 at the DC, which
+// passes, and for tiles off the image's tile grid, which weigh nothing), and the on-grid tiles
+// covering a pixel sum to w p, so
+//   dct_soft_threshold(p) = (sum_tiles IDCT(soft(Y))) / w = p - (sum_tiles IDCT(clamp(Y))) / w.
+// The clamp is one FMNMX.XORSIGN per coefficient (the soft threshold took two FMNMX and half an
+// FADD2), and the transformed corrections are bounded by the threshold, not by the field.
+__device__ __forceinline__ float quad_scale(int br, int bc, int H, int W) {
+  const int w = ((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0));
+  return w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
+}
+
 __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
   const int lane = threadIdx.x & 31, tp = threadIdx.x >> 5;
-  // The field is centred on a per-region constant cen before the transforms and cen is added back
-  // to the output: D(p - cen) = D(p) - cen exactly (the DC passes the threshold and the weights
-  // sum to one), and the smaller magnitudes cut the fp32 rounding of every butterfly stage (DAMP's
-  // Monte-Carlo divergence differences two denoiser calls and feels that rounding).
+  // The forward transforms run on the field centred on a per-region constant cen (the AC
+  // coefficients are those of p; the DC is never used, its clamp is 0): smaller magnitudes, less
+  // fp32 rounding in every butterfly stage (DAMP's Monte-Carlo divergence differences two
+  // denoiser calls and feels that rounding).
   const float cen = 0.25f * (s.in[35 * kWP + 35] + s.in[35 * kWP + 36] + s.in[36 * kWP + 35] + s.in[36 * kWP + 36]);
   const float2 mc = make_float2(-cen, -cen);
   // A: row DCTs of the window rows y = lane + 32 j (lanes along rows: conflict-free)
@@ -210,49 +221,65 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
     for (int q = 0; q < 4; ++q) d[q] = make_float4(Y[2 * q].x, Y[2 * q].y, Y[2 * q + 1].x, Y[2 * q + 1].y);
   }
   __syncwarp();
-  // B: lanes = (coefficient column v, tile tq of a group of 4 consecutive tile rows); per tile:
-  // column DCT, soft threshold, inverse column DCT. A tile's top half (4 rows) plus the bottom
-  // half of the tile above (the lane 8 below, or the carry from the previous group) completes
-  // those S rows, written in place over R (every R row they replace was loaded by both of its
-  // tiles before the warp's first store to it: the loads of a group precede its stores).
+  // B: lanes = (coefficient column v, run tq). Run tq walks the tile rows [first, end) = 0..4, 5..8,
+  // 9..12, 13..16 top to bottom; per tile: column DCT, clamp, inverse column DCT. The window of 8
+  // rows slides by 4 in registers (4 new rows per tile), and a tile's top half plus the bottom half
+  // of the tile above (carried in registers) completes those S rows, written in place over R: the
+  // rows a store replaces were last read by the same lane. A run's first tile keeps its top half
+  // until every run is done: the previous run's last tile still reads those R rows.
   {
-    const float kInf = __int_as_float(0x7f800000);
     const int v = lane & 7, tq = lane >> 3;
     const bool gc0 = (unsigned)(C0 - 4 + 8 * tp) <= (unsigned)(W - 8);
     const bool gc1 = tp < 8 && (unsigned)(C0 + 8 * tp) <= (unsigned)(W - 8);
-    float2 carry[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll 1
-    for (int g = 0; g < 5; ++g) {
-      const int ti = min(4 * g + tq, 16);  // group 4: tiles 17..19 are repeats of 16, never stored
-      const bool act = 4 * g + tq <= 16;
-      float* col = s.RS + 4 * ti * kRP + 16 * tp + 2 * v;
-      float2 x[8], Y[8], X[8];
+    const int t_first = tq == 0 ? 0 : 4 * tq + 1, t_end = 4 * tq + 5;
+    float* col = s.RS + 16 * tp + 2 * v;
+    float2 x[8], first[4], carry[4];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) x[r] = lds2(col + r * kRP);
-      __syncwarp();
+    for (int r = 0; r < 8; ++r) x[r] = lds2(col + (4 * t_first + r) * kRP);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int ti = t_first + i;
+      const bool act = ti < t_end;  // warp-uniform except the 5th tile (run 0 only)
+      if (i > 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) x[r] = x[4 + r];
+        if (act) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) x[4 + r] = lds2(col + (4 * ti + 4 + r) * kRP);
+        }
+      }
+      float2 Y[8], X[8];
       dct8_fwd_pair(x, Y);
       const bool gr = (unsigned)(R0 - 4 + 4 * ti) <= (unsigned)(H - 8);
-      const bool g0 = gr && gc0, g1 = gr && gc1;
-      const float t0 = g0 ? thr : kInf, t1 = g1 ? thr : kInf;
-      // the DC (u = 0, v = 0) passes through (denoise.cpp:76)
-      Y[0] = p_soft(Y[0], v == 0 ? (g0 ? 0.f : kInf) : t0, v == 0 ? (g1 ? 0.f : kInf) : t1);
+      const float t0 = gr && gc0 ? thr : 0.f, t1 = gr && gc1 ? thr : 0.f;
+      Y[0] = p_clamp(Y[0], v == 0 ? 0.f : t0, v == 0 ? 0.f : t1);  // the DC passes (denoise.cpp:76)
 #pragma unroll
-      for (int u = 1; u < 8; ++u) Y[u] = p_soft(Y[u], t0, t1);
+      for (int u = 1; u < 8; ++u) Y[u] = p_clamp(Y[u], t0, t1);
       dct8_inv_pair(Y, X);
+      if (i == 0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        // lane L takes lane L - 8 (mod 32): the tile above, or (tq = 0) the previous group's last tile
-        const float2 above = shfl2(tq == 3 ? carry[r] : X[4 + r], (lane + 24) & 31);
-        if (act) sts2(col + r * kRP, p_add(X[r], above));
-        carry[r] = X[4 + r];
+        for (int r = 0; r < 4; ++r) first[r] = X[r];
+      } else if (act) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) sts2(col + (4 * ti + r) * kRP, p_add(X[r], carry[r]));
+      }
+      if (act) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) carry[r] = X[4 + r];
       }
     }
+    __syncwarp();  // every run past its loads
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 above = shfl2(carry[r], (lane + 24) & 31);  // the previous run's last tile
+      if (tq > 0) sts2(col + (4 * t_first + r) * kRP, p_add(first[r], above));
+    }
   }
-  __syncthreads();  // acc (stage C's output) aliases the window; S rows of every pair are complete
-  // C: inverse row DCTs of S over the region rows yr = lane + 32 j.
-  // Output quads (window cols): Q0 = 8tp..+3 (tj0 only), Q1 = 8tp+4..+7 (tj0 + tj1, complete),
-  // Q2 = 8tp+8..+11 (tj1 only). Q0 of pair tp+1 and Q2 of pair tp are the same quad: Q0 is
-  // stored first, Q2 added after a barrier (a fixed order), then scaled by 1 / weight.
+  __syncthreads();  // stage C writes window quads the neighbouring pairs' stage A read
+  // C: inverse row DCTs of S over the region rows yr = lane + 32 j, and x = p - correction / w in
+  // place over the window. Output quads (window cols): Q0 = 8tp..+3 (tj0 only), Q1 = 8tp+4..+7
+  // (tj0 + tj1, complete), Q2 = 8tp+8..+11 (tj1 only). Q0 of pair tp+1 and Q2 of pair tp are the
+  // same quad: Q0 is applied first, Q2 after a barrier (a fixed order).
   float4 q2[2];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -266,15 +293,20 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
       y[2 * q + 1] = make_float2(v.z, v.w);
     }
     dct8_inv_pair(y, X);
-    float* row = s.acc + kMOff + yr * kMP - 4;  // indexed by window column
-    if (tp >= 1) *reinterpret_cast<float4*>(row + 8 * tp) = make_float4(X[0].x, X[1].x, X[2].x, X[3].x);
+    float* row = s.in + (yr + 4) * kWP;  // indexed by window column
+    const int br = (R0 + yr) & ~3;       // weights: on-grid tile origins per axis (1 or 2)
+    if (tp >= 1) {
+      const float sc = quad_scale(br, C0 + 8 * tp - 4, H, W);
+      float4* d = reinterpret_cast<float4*>(row + 8 * tp);
+      const float4 p = *d;
+      *d = make_float4(fmaf(-X[0].x, sc, p.x), fmaf(-X[1].x, sc, p.y), fmaf(-X[2].x, sc, p.z), fmaf(-X[3].x, sc, p.w));
+    }
     if (tp <= 7) {
-      const int br = (R0 + yr) & ~3, bc = C0 + 8 * tp;  // weights: tile origins per axis (1 or 2)
-      const int w = max(((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0)), 1);
-      const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
-      *reinterpret_cast<float4*>(row + 8 * tp + 4) =
-          make_float4(fmaf(X[4].x + X[0].y, sc, cen), fmaf(X[5].x + X[1].y, sc, cen), fmaf(X[6].x + X[2].y, sc, cen),
-                      fmaf(X[7].x + X[3].y, sc, cen));
+      const float sc = quad_scale(br, C0 + 8 * tp, H, W);
+      float4* d = reinterpret_cast<float4*>(row + 8 * tp + 4);
+      const float4 p = *d;
+      *d = make_float4(fmaf(-(X[4].x + X[0].y), sc, p.x), fmaf(-(X[5].x + X[1].y), sc, p.y),
+                       fmaf(-(X[6].x + X[2].y), sc, p.z), fmaf(-(X[7].x + X[3].y), sc, p.w));
     }
     q2[j] = make_float4(X[4].y, X[5].y, X[6].y, X[7].y);
   }
@@ -283,13 +315,11 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int yr = lane + 32 * j;
-      const int br = (R0 + yr) & ~3, bc = C0 + 8 * tp + 4;
-      const int w = max(((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0)), 1);
-      const float sc = w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
-      float4* d = reinterpret_cast<float4*>(s.acc + kMOff + yr * kMP + 8 * tp + 4);
+      const float sc = quad_scale((R0 + yr) & ~3, C0 + 8 * tp + 4, H, W);
+      float4* d = reinterpret_cast<float4*>(s.in + (yr + 4) * kWP + 8 * tp + 8);
       const float4 a = *d;
-      *d = make_float4(fmaf(a.x + q2[j].x, sc, cen), fmaf(a.y + q2[j].y, sc, cen), fmaf(a.z + q2[j].z, sc, cen),
-                       fmaf(a.w + q2[j].w, sc, cen));
+      *d = make_float4(fmaf(-q2[j].x, sc, a.x), fmaf(-q2[j].y, sc, a.y), fmaf(-q2[j].z, sc, a.z),
+                       fmaf(-q2[j].w, sc, a.w));
     }
   }
   __syncthreads();
@@ -464,8 +494,8 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
   float T[16], cb = 0.f;
   if (valid) {
     float xr[16];
-    load_row16(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc, xr);
-    cb = s.acc[kMOff + (16 * br + 8) * kMP + 16 * bc + 8];
+    load_row16(s.acc + kAOff + (16 * br + lr) * kWP + 16 * bc, xr);
+    cb = s.acc[kAOff + (16 * br + 8) * kWP + 16 * bc + 8];
     row_checks(P, img, gr, gc, xr, S);
     if (last) {  // the estimate itself (recon.cpp:255-257 clamp on reconstruct's final step)
 #pragma unroll
@@ -492,6 +522,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     float Tc[16];
     load_row16(tb + lr * 20, Tc);
     abcs_gen::dct16_fwd(Tc, Y);
+    if (lr == 0) Y[0] += 16.f * cb;  // the tile holds the true DC: the centred one lacks 16 cb (exact)
   }
   __syncwarp();  // every lane holds its column: the tile takes Y
   if (valid) {
@@ -500,46 +531,41 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
       *reinterpret_cast<float4*>(tb + lr * 20 + 4 * q) = make_float4(Y[4 * q], Y[4 * q + 1], Y[4 * q + 2], Y[4 * q + 3]);
   }
   __syncwarp();
-  const float cb0 = __shfl_sync(0xffffffffu, cb, 0), cb1 = __shfl_sync(0xffffffffu, cb, 16);  // the pair's centres
   if (t < 256) {
     const int lane = t & 31, b0 = b & ~1;
     const int c0 = max(s.meta_cnt[b0], 0), c1 = max(s.meta_cnt[b0 + 1], 0), kw = c0 + c1;
     const int64_t pb = (int64_t)img * P.y_stride + s.meta_off[b0];  // the pair's run in y / z
+    const float* yrun = P.y + pb;
+    float* zrun = P.z + pb;
+    float* tile0 = s.RS + b0 * kTB;
     float zsq = 0.f, ysq = 0.f;
-    unsigned int badz = ~0u;
+    bool bad = false;
     // NS elements per lane in flight per round; NS from the pair's run length (warp-uniform), so
     // short runs (cfg4: ~130) do not pay for 8 predicated slots per lane
     auto rounds = [&](auto ns) {
       constexpr int NS = decltype(ns)::value;
 #pragma unroll 1
-      for (int e0 = 0; e0 < kw; e0 += 32 * NS) {
+      for (int e0 = lane; e0 < kw; e0 += 32 * NS) {
         float yv[NS], zo[NS];
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
-          const int e = e0 + lane + 32 * i;
-          yv[i] = e < kw ? __ldg(P.y + pb + e) : 0.f;
-          zo[i] = (e < kw && !P.is_init) ? P.z[pb + e] : 0.f;
+          const int e = e0 + 32 * i;
+          yv[i] = e < kw ? __ldg(yrun + e) : 0.f;
+          zo[i] = (e < kw && !P.is_init) ? zrun[e] : 0.f;
         }
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
-          const int e = e0 + lane + 32 * i;
+          const int e = e0 + 32 * i;
           if (e < kw) {
-            const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0);
-            const int f = s.zidx[k];  // flat u * 16 + v
-            float* slot = s.RS + (b0 + q) * kTB + (f & 15) * 20 + (f >> 4);
-            const float yk = yv[i];
-            // finish_step (recon.cpp:86-88); the centred transform's DC lacks 16 cb (exact)
-            const float ya = k == 0 ? yk - 16.f * (q ? cb1 : cb0) : yk;
+            const bool q = e >= c0;
+            float* slot = tile0 + (q ? kTB : 0) + s.zslot[q ? e - c0 : e];
             const float yc = *slot;
-            const float zn = (ya - yc) + ons * zo[i];
-            P.z[pb + e] = zn;
+            const float zn = (yv[i] - yc) + ons * zo[i];  // finish_step (recon.cpp:86-88)
+            zrun[e] = zn;
             *slot = yc + zn;  // W = Y + z
             zsq = fmaf(zn, zn, zsq);
-            ysq = fmaf(yk, yk, ysq);
-            if (!isfinite(zn)) {
-              const unsigned int gi = (unsigned)(s.meta_off[b0] + e);
-              badz = gi < badz ? gi : badz;
-            }
+            ysq = fmaf(yv[i], yv[i], ysq);
+            bad |= !(fabsf(zn) <= FLT_MAX);
           }
         }
       }
@@ -549,11 +575,21 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
     else rounds(std::integral_constant<int, 8>{});
     S.z += (double)zsq;
     if (P.is_init) S.y += (double)ysq;  // ||y||^2 (recon.cpp:128)
-    S.badz = badz < S.badz ? badz : S.badz;
+    if (bad) {  // rare: the first non-finite residual of this lane's elements (its own stores)
+      for (int e = lane; e < kw; e += 32)
+        if (!isfinite(zrun[e])) {
+          const unsigned int gi = (unsigned)(s.meta_off[b0] + e);
+          S.badz = gi < S.badz ? gi : S.badz;
+          break;
+        }
+    }
     if ((t & 15) == 0 && cnt >= 0) S.cnt += cnt;
   }
   __syncwarp();
-  if (valid) load_row16(tb + lr * 20, Y);  // W of column lr
+  if (valid) {
+    load_row16(tb + lr * 20, Y);  // W of column lr
+    if (lr == 0) Y[0] -= 16.f * cb;  // centred again for the inverse
+  }
   if (last) return;
   __syncwarp();  // all column loads of the warp's tiles done: they take V
   if (valid) {
@@ -607,8 +643,8 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s,
       for (int i = 0; i < 8; ++i) {
         const int e = e0 + lane + 32 * i;
         if (e < kw) {
-          const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0), f = s.zidx[k];
-          s.RS[(b0 + q) * kTB + (f & 15) * 20 + (f >> 4)] = yv[i];
+          const int q = e < c0 ? 0 : 1, k = e - (q ? c0 : 0);
+          s.RS[(b0 + q) * kTB + s.zslot[k]] = yv[i];
           P.z[pb + e] = 0.f;
           ysq = fmaf(yv[i], yv[i], ysq);
         }
@@ -640,7 +676,7 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s,
     abcs_gen::dct16_inv(Vr, O);
   }
   if (valid) {
-    float4* dst = reinterpret_cast<float4*>(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc);
+    float4* dst = reinterpret_cast<float4*>(s.acc + kAOff + (16 * br + lr) * kWP + 16 * bc);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q] + cb, O[4 * q + 1] + cb, O[4 * q + 2] + cb, O[4 * q + 3] + cb);
   }
@@ -658,7 +694,7 @@ __device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s
   const int cnt = s.meta_cnt[b];
   if (t < 256 && cnt >= 0) {
     float xr[16];
-    load_row16(s.acc + kMOff + (16 * br + lr) * kMP + 16 * bc, xr);
+    load_row16(s.acc + kAOff + (16 * br + lr) * kWP + 16 * bc, xr);
     const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;
     row_checks(P, img, gr, gc, xr, S);
     if (P.pseudo_out) {  // pseudo0 = x0 (internal buffer: Wc % 16 == 0, 16-B aligned rows)
@@ -713,8 +749,8 @@ __device__ void init_x8(const IdaParams& P, int img, int R0, int C0, Sm& s) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) X[i] *= ysc;
     const int lr = 8 * br + g, lc = 8 * bc + 2 * t;
-    *reinterpret_cast<float2*>(s.acc + kMOff + lr * kMP + lc) = make_float2(X[0], X[1]);
-    *reinterpret_cast<float2*>(s.acc + kMOff + lr * kMP + lc + 8) = make_float2(X[2], X[3]);
+    *reinterpret_cast<float2*>(s.acc + kAOff + lr * kWP + lc) = make_float2(X[0], X[1]);
+    *reinterpret_cast<float2*>(s.acc + kAOff + lr * kWP + lc + 8) = make_float2(X[2], X[3]);
     __syncwarp();
   }
 }
@@ -743,8 +779,8 @@ __device__ void block_phase8(const IdaParams& P, int img, int R0, int C0, Sm& s,
     stage_yz_async(P, ibase + boff[1], cnt[1], yb + 64, zb + 64, !P.is_init);
     if (lane == 0) S.cnt += cnt[0] + cnt[1];
     const int lr = 8 * br + g, lc = 8 * bc + 2 * t;
-    const float2 x0 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc);
-    const float2 x1 = *reinterpret_cast<const float2*>(s.acc + kMOff + lr * kMP + lc + 8);
+    const float2 x0 = *reinterpret_cast<const float2*>(s.acc + kAOff + lr * kWP + lc);
+    const float2 x1 = *reinterpret_cast<const float2*>(s.acc + kAOff + lr * kWP + lc + 8);
     float Yt[4], xs[4] = {x0.x, x0.y, x1.x, x1.y};
     const float xsc = fp16_range_scale(xs);
     dct8x2_fwdT(f, make_float2(xs[0], xs[1]), make_float2(xs[2], xs[3]), Yt);
@@ -835,12 +871,15 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     tma_window(s.in, &win_map, C0 - 4, R0 - 4, img, &s.win_bar);
   const double sigma = denoise ? P.sigma_in[img] : 0.0;
   fetch_meta<B>(P, img, R0, C0, s);  // visible to the block phase after the next barrier
-  if (B == 16 && threadIdx.x < 256) s.zidx[threadIdx.x] = zigzag_dev<16>()[threadIdx.x];
+  if (B == 16 && threadIdx.x < 256) {  // rank k's (u, v) = f / 16, f % 16 -> tile slot v * 20 + u
+    const int f = zigzag_dev<16>()[threadIdx.x];
+    s.zslot[threadIdx.x] = (unsigned short)((f & 15) * 20 + (f >> 4));
+  }
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
   float ysq16 = 0.f;
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
-      for (int i = threadIdx.x; i < kMIn * kMP / 4; i += blockDim.x)
+      for (int i = threadIdx.x; i < kMIn * kWP / 4; i += blockDim.x)
         reinterpret_cast<float4*>(s.acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else if (B == 16) {
       init_x16_f32(P, img, R0, C0, s, ysq16);
@@ -854,7 +893,7 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
       const int r = i / (kMR / 4), c = 4 * (i % (kMR / 4));
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (R0 + r < P.Hc && C0 + c < P.Wc) v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)(R0 + r) * P.Wc + C0 + c));
-      *reinterpret_cast<float4*>(s.acc + kMOff + r * kMP + c) = v;
+      *reinterpret_cast<float4*>(s.acc + kAOff + r * kWP + c) = v;
     }
     __syncthreads();
   } else {
@@ -886,7 +925,7 @@ denoise_f32_kernel(const float* __restrict__ field, int H, int W, int64_t stride
   denoise_region_f32(s, R0, C0, H, W, (float)thr[img]);
   for (int i = threadIdx.x; i < kMR * kMR; i += blockDim.x) {
     const int r = i / kMR, c = i % kMR;
-    if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s.acc[kMOff + r * kMP + c];
+    if (R0 + r < H && C0 + c < W) out[(int64_t)img * stride + (int64_t)(R0 + r) * W + C0 + c] = s.acc[kAOff + r * kWP + c];
   }
 }
 
