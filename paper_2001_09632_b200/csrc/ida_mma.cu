@@ -613,7 +613,7 @@ __device__ void block_phase16_f32(const IdaParams& P, int img, int R0, int C0, S
 // init, warm start: acc <- x0 = A* y (recon.cpp:119-131), the inverse of each block's y prefix
 // (columns then rows through the transpose tiles). Called before block_phase16_f32.
 template <class Sm>
-__device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s, float& ysq) {
+__device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s, float& ysq, float (&xo)[16]) {
   const int t = threadIdx.x;
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
@@ -675,12 +675,8 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s,
     load_row16(tb + lr * 20, Vr);
     abcs_gen::dct16_inv(Vr, O);
   }
-  if (valid) {
-    float4* dst = reinterpret_cast<float4*>(s.acc + kAOff + (16 * br + lr) * kWP + 16 * bc);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst[q] = make_float4(O[4 * q] + cb, O[4 * q + 1] + cb, O[4 * q + 2] + cb, O[4 * q + 3] + cb);
-  }
-  __syncwarp();  // the block phase reads each block's rows in the same warp
+  for (int c = 0; c < 16; ++c) xo[c] = O[c] + cb;  // row lr of block b: the thread that checks / stores it
 }
 
 // Warm start, the rest of init_state (recon.cpp:119-131): x0 = A* y is in acc; z0 = y - A x0 is 0
@@ -688,13 +684,12 @@ __device__ void init_x16_f32(const IdaParams& P, int img, int R0, int C0, Sm& s,
 // so pseudo0 = x0 + A* z0 = x0 and the block phase's transforms are skipped. sigma0 = ||y|| / sqrt(M)
 // needs ||y||^2, summed over each warp's payload run; the trace's PSNR of x0 needs the SSE.
 template <class Sm>
-__device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S, float ysq) {
+__device__ void init_finish16(const IdaParams& P, int img, int R0, int C0, Sm& s, IdaLaneSums& S, float ysq,
+                              const float (&xr)[16]) {
   const int t = threadIdx.x;
   const int b = (t >> 4) & 15, lr = t & 15, br = b >> 2, bc = b & 3;
   const int cnt = s.meta_cnt[b];
   if (t < 256 && cnt >= 0) {
-    float xr[16];
-    load_row16(s.acc + kAOff + (16 * br + lr) * kWP + 16 * bc, xr);
     const int gr = R0 + 16 * br + lr, gc = C0 + 16 * bc;
     row_checks(P, img, gr, gc, xr, S);
     if (P.pseudo_out) {  // pseudo0 = x0 (internal buffer: Wc % 16 == 0, 16-B aligned rows)
@@ -876,14 +871,11 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     s.zslot[threadIdx.x] = (unsigned short)((f & 15) * 20 + (f >> 4));
   }
   if (P.is_init && P.warm) __syncthreads();  // the warm start reads the region's metadata right away
-  float ysq16 = 0.f;
   if (P.is_init) {
     if (!P.warm) {  // cold start: x0 = 0, so z0 = y (recon.cpp:119-131)
       for (int i = threadIdx.x; i < kMIn * kWP / 4; i += blockDim.x)
         reinterpret_cast<float4*>(s.acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else if (B == 16) {
-      init_x16_f32(P, img, R0, C0, s, ysq16);
-    } else {
+    } else {  // B = 16 warm starts run ida_init16_kernel
       init_x8(P, img, R0, C0, s);
     }
     __syncthreads();
@@ -903,9 +895,38 @@ __global__ void __launch_bounds__(kFThreads, IDA_MINB) ida_mma_kernel(IdaParams 
     denoise_region_f32(s, R0, C0, P.Hc, P.Wc, (float)(P.k * sigma));
   }
   IdaLaneSums S;
-  if (B == 16 && P.is_init && P.warm) init_finish16(P, img, R0, C0, s, S, ysq16);
-  else if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
+  if (B == 16) block_phase16_f32(P, img, R0, C0, s, S);
   else block_phase8(P, img, R0, C0, s, S);
+  reduce_and_finish(P, img, region, s, S);
+}
+
+// Warm-start init for B = 16 (init_state, recon.cpp:119-131): x0 = A* y per sensing block, straight
+// from the transpose tiles to pseudo0 (or x) in registers. No window and no denoiser, so only the
+// tiles and the metadata live in shared memory: 8 warps and ~24 KB per CTA, several CTAs per SM.
+struct IdaInitSmem {
+  float RS[16 * kTB];  // the region's 16 per-block transpose tiles
+  int meta_cnt[64];
+  int meta_off[64];
+  double red[4][16];
+  unsigned int bad[2];
+  double mine[4];
+  unsigned short zslot[256];
+};
+
+__global__ void __launch_bounds__(256, 4) ida_init16_kernel(IdaParams P) {
+  __shared__ __align__(16) IdaInitSmem s;
+  const int img = blockIdx.y, region = blockIdx.x;
+  const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
+  fetch_meta<16>(P, img, R0, C0, s);
+  {
+    const int f = zigzag_dev<16>()[threadIdx.x];
+    s.zslot[threadIdx.x] = (unsigned short)((f & 15) * 20 + (f >> 4));
+  }
+  __syncthreads();
+  float ysq = 0.f, xr[16];
+  init_x16_f32(P, img, R0, C0, s, ysq, xr);
+  IdaLaneSums S;
+  init_finish16(P, img, R0, C0, s, S, ysq, xr);
   reduce_and_finish(P, img, region, s, S);
 }
 
@@ -989,6 +1010,10 @@ static void launch_ida_b(const IdaParams& P, dim3 grid, cudaStream_t s) {
   }
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
+  if (B == 16 && P.is_init && P.warm) {
+    ida_init16_kernel<<<grid, 256, 0, s>>>(P);
+    return;
+  }
   if (!P.is_init && !P.x_in && P.pseudo_in && encode_window_map(&tm, P.pseudo_in, P.Wc, P.Hc, P.n) != ABCS_OK) return;
   ida_mma_kernel<B><<<grid, kFThreads, bytes, s>>>(P, tm);
 }
