@@ -24,6 +24,7 @@
 #include "mma_dct.cuh"
 #include "zz_banks.cuh"
 #include "cta_alloc.cuh"
+#include "warp_alloc.cuh"
 
 namespace abcs_b200 {
 
@@ -574,6 +575,32 @@ dd_fixup16_kernel(const uint8_t* __restrict__ imgs, int64_t img_stride, int pitc
   }
 }
 
+// Allocation of DD plans from computed weights: one warp per image (warp_alloc.cuh), four
+// images per CTA; ABCS_ALLOC_CTA=1 selects the 256-thread CTA allocator (cta_alloc.cuh).
+constexpr int kWarpAllocWarps = 4;
+static bool alloc_use_cta() {
+  static const int v = [] {
+    const char* e = getenv("ABCS_ALLOC_CTA");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return v != 0;
+}
+static int warp_alloc_smem(int nb) { return kWarpAllocWarps * warp_alloc_bytes(nb); }
+static void warp_alloc_attr(const void* k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, warp_alloc_smem(kCtaAllocMaxBlocks));
+}
+
+__global__ void __launch_bounds__(32 * kWarpAllocWarps)
+alloc_warp_kernel(const uint32_t* __restrict__ weights, int nb, int n, int wmax, long long budget, int cap, int base,
+                  uint16_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const int warp = threadIdx.x >> 5, img = blockIdx.x * kWarpAllocWarps + warp;
+  if (img >= n) return;
+  const int st = warp_allocate(wsm + warp * warp_alloc_bytes(nb), weights + (int64_t)img * nb, nb, wmax, budget, cap,
+                               base, counts + (int64_t)img * nb, offsets + (int64_t)img * nb);
+  if ((threadIdx.x & 31) == 0 && status) status[img] = st;
+}
+
 // Allocation for the fused DD path: one CTA per image (cta_alloc.cuh).
 __global__ void __launch_bounds__(kCtaAllocThreads, 7)
 alloc_cta_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, long long budget, int cap, int base,
@@ -819,8 +846,19 @@ int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t*
       if (fa) {  // allocation: one CTA per image (cta_alloc.cuh)
         ctx->launches++;
         kt = ktimer_begin(ctx, s, "alloc_cta");
-        alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa->wmax, fa->budget, fa->cap,
-                                                                   fa->base, fa->counts, fa->offsets, fa->status);
+        if (alloc_use_cta()) {
+          alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa->wmax, fa->budget, fa->cap,
+                                                                     fa->base, fa->counts, fa->offsets, fa->status);
+        } else {
+          static bool attr = false;
+          if (!attr) {
+            warp_alloc_attr((const void*)alloc_warp_kernel);
+            attr = true;
+          }
+          alloc_warp_kernel<<<(unsigned)((n + kWarpAllocWarps - 1) / kWarpAllocWarps), 32 * kWarpAllocWarps,
+                              warp_alloc_smem((int)G.nb), s>>>(weights, (int)G.nb, n, fa->wmax, fa->budget, fa->cap,
+                                                               fa->base, fa->counts, fa->offsets, fa->status);
+        }
         ktimer_end(ctx, s, kt);
       }
       break;
@@ -1172,6 +1210,17 @@ alloc_cta_plans_kernel(AllocPlans P, int nb) {
   if (threadIdx.x == 0 && fa.status) fa.status[img] = st;
 }
 
+__global__ void __launch_bounds__(32 * kWarpAllocWarps)
+alloc_warp_plans_kernel(AllocPlans P, int nb, int n) {
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const int warp = threadIdx.x >> 5, img = blockIdx.x * kWarpAllocWarps + warp, j = blockIdx.y;
+  if (img >= n) return;
+  const FusedAlloc& fa = P.fa[j];
+  const int st = warp_allocate(wsm + warp * warp_alloc_bytes(nb), P.weights[j] + (int64_t)img * nb, nb, fa.wmax,
+                               fa.budget, fa.cap, fa.base, fa.counts + (int64_t)img * nb, fa.offsets + (int64_t)img * nb);
+  if ((threadIdx.x & 31) == 0 && fa.status) fa.status[img] = st;
+}
+
 int launch_alloc_cta_plans(Ctx* ctx, int np, int rows, int cols, int n, uint32_t* const* weights,
                            const FusedAlloc* fa, cudaStream_t s) {
   if (np < 1 || np > 4) return set_error(ABCS_ERR_LOGIC, "alloc plans: 1..4 plans");
@@ -1183,7 +1232,17 @@ int launch_alloc_cta_plans(Ctx* ctx, int np, int rows, int cols, int n, uint32_t
     P.fa[j] = fa[j];
   }
   const int kt = ktimer_begin(ctx, s, "alloc_cta");
-  alloc_cta_plans_kernel<<<dim3((unsigned)n, (unsigned)np), kCtaAllocThreads, 0, s>>>(P, (int)G.nb);
+  if (alloc_use_cta()) {
+    alloc_cta_plans_kernel<<<dim3((unsigned)n, (unsigned)np), kCtaAllocThreads, 0, s>>>(P, (int)G.nb);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      warp_alloc_attr((const void*)alloc_warp_plans_kernel);
+      attr = true;
+    }
+    alloc_warp_plans_kernel<<<dim3((unsigned)((n + kWarpAllocWarps - 1) / kWarpAllocWarps), (unsigned)np),
+                              32 * kWarpAllocWarps, warp_alloc_smem((int)G.nb), s>>>(P, (int)G.nb, n);
+  }
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "alloc_cta launch");
@@ -1195,8 +1254,19 @@ int launch_alloc_cta(Ctx* ctx, int rows, int cols, int n, const uint32_t* weight
   const Grid16 G = make_grid16(rows, cols, n);
   if (G.total_units == 0) return ABCS_OK;
   const int kt = ktimer_begin(ctx, s, "alloc_cta");
-  alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa.wmax, fa.budget, fa.cap, fa.base,
-                                                             fa.counts, fa.offsets, fa.status);
+  if (alloc_use_cta()) {
+    alloc_cta_kernel<<<(unsigned)n, kCtaAllocThreads, 0, s>>>(weights, (int)G.nb, fa.wmax, fa.budget, fa.cap, fa.base,
+                                                               fa.counts, fa.offsets, fa.status);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      warp_alloc_attr((const void*)alloc_warp_kernel);
+      attr = true;
+    }
+    alloc_warp_kernel<<<(unsigned)((n + kWarpAllocWarps - 1) / kWarpAllocWarps), 32 * kWarpAllocWarps,
+                        warp_alloc_smem((int)G.nb), s>>>(weights, (int)G.nb, n, fa.wmax, fa.budget, fa.cap, fa.base,
+                                                         fa.counts, fa.offsets, fa.status);
+  }
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "alloc_cta launch");
