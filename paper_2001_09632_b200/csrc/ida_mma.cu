@@ -191,9 +191,10 @@ __device__ __forceinline__ void l1_prefetch_region_yz(const IdaParams& P, int im
 //   dct_soft_threshold(p) = (sum_tiles IDCT(soft(Y))) / w = p - (sum_tiles IDCT(clamp(Y))) / w.
 // The clamp is one FMNMX.XORSIGN per coefficient (the soft threshold took two FMNMX and half an
 // FADD2), and the transformed corrections are bounded by the threshold, not by the field.
-__device__ __forceinline__ float quad_scale(int br, int bc, int H, int W) {
-  const int w = ((br >= 4 ? 1 : 0) + (br <= H - 8 ? 1 : 0)) * ((bc >= 4 ? 1 : 0) + (bc <= W - 8 ? 1 : 0));
-  return w == 4 ? 0.25f : (w == 2 ? 0.5f : 1.f);
+// 1 / (on-grid tile origins covering the 4-px band starting at b) along one axis: 1 or 1/2 (the
+// weight is separable, w = w_row w_col, so 1 / w is the product of the two axis factors)
+__device__ __forceinline__ float axis_scale(int b, int extent) {
+  return (b >= 4 && b <= extent - 8) ? 0.5f : 1.f;
 }
 
 __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, float thr) {
@@ -281,6 +282,7 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
   // (tj0 + tj1, complete), Q2 = 8tp+8..+11 (tj1 only). Q0 of pair tp+1 and Q2 of pair tp are the
   // same quad: Q0 is applied first, Q2 after a barrier (a fixed order).
   float4 q2[2];
+  const float fc0 = axis_scale(C0 + 8 * tp - 4, W), fc1 = axis_scale(C0 + 8 * tp, W);
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int yr = lane + 32 * j;
@@ -294,15 +296,15 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
     }
     dct8_inv_pair(y, X);
     float* row = s.in + (yr + 4) * kWP;  // indexed by window column
-    const int br = (R0 + yr) & ~3;       // weights: on-grid tile origins per axis (1 or 2)
+    const float fr = axis_scale((R0 + yr) & ~3, H);  // weights: on-grid tile origins per axis (1 or 2)
     if (tp >= 1) {
-      const float sc = quad_scale(br, C0 + 8 * tp - 4, H, W);
+      const float sc = fr * fc0;
       float4* d = reinterpret_cast<float4*>(row + 8 * tp);
       const float4 p = *d;
       *d = make_float4(fmaf(-X[0].x, sc, p.x), fmaf(-X[1].x, sc, p.y), fmaf(-X[2].x, sc, p.z), fmaf(-X[3].x, sc, p.w));
     }
     if (tp <= 7) {
-      const float sc = quad_scale(br, C0 + 8 * tp, H, W);
+      const float sc = fr * fc1;
       float4* d = reinterpret_cast<float4*>(row + 8 * tp + 4);
       const float4 p = *d;
       *d = make_float4(fmaf(-(X[4].x + X[0].y), sc, p.x), fmaf(-(X[5].x + X[1].y), sc, p.y),
@@ -312,10 +314,11 @@ __device__ void denoise_region_f32(IdaF32Smem& s, int R0, int C0, int H, int W, 
   }
   __syncthreads();
   if (tp <= 7) {
+    const float fc2 = axis_scale(C0 + 8 * tp + 4, W);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int yr = lane + 32 * j;
-      const float sc = quad_scale((R0 + yr) & ~3, C0 + 8 * tp + 4, H, W);
+      const float sc = axis_scale((R0 + yr) & ~3, H) * fc2;
       float4* d = reinterpret_cast<float4*>(s.in + (yr + 4) * kWP + 8 * tp + 8);
       const float4 a = *d;
       *d = make_float4(fmaf(-q2[j].x, sc, a.x), fmaf(-q2[j].y, sc, a.y), fmaf(-q2[j].z, sc, a.z),
@@ -826,11 +829,12 @@ __device__ void reduce_and_finish(const IdaParams& P, int img, int region, Sm& s
     s.bad[0] = ~0u;
     s.bad[1] = ~0u;
   }
+  const bool has_sse = P.ref != nullptr, has_y = P.is_init != 0;  // otherwise those sums are 0
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     S.z += __shfl_xor_sync(0xffffffffu, S.z, o);
-    S.sse += __shfl_xor_sync(0xffffffffu, S.sse, o);
-    S.y += __shfl_xor_sync(0xffffffffu, S.y, o);
+    if (has_sse) S.sse += __shfl_xor_sync(0xffffffffu, S.sse, o);
+    if (has_y) S.y += __shfl_xor_sync(0xffffffffu, S.y, o);
     S.cnt += __shfl_xor_sync(0xffffffffu, S.cnt, o);
   }
   __syncthreads();
