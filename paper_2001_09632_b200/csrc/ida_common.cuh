@@ -49,28 +49,45 @@ struct IdaParams {
 
 // Last CTA of an image folds the region partials (fixed order, so the result
 // is deterministic) into sigma, the trace row and the divergence record.
-// Called by every thread with `mine` written by thread 0 (the only thread that
-// continues): the partial is published with a release RMW on the image's counter,
-// and the CTA whose RMW completes the count acquires every other CTA's partial.
-// No CTA barrier and no sequentially consistent fence: the other threads leave.
+// Called by every thread with `mine` written by thread 0: the partial is published with a
+// release RMW on the image's counter, and the CTA whose RMW completes the count acquires every
+// other CTA's partial and folds them with all its threads. No sequentially consistent fence.
 static __device__ void finish_image(const IdaParams& P, int img, int region, const double* mine) {
-  if (threadIdx.x != 0) return;
-  double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
-  for (int q = 0; q < 4; ++q) part[q] = mine[q];
-  unsigned prev;
-  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(P.counters + img) : "memory");
-  if (prev != (unsigned)P.regions_per_img - 1) return;
-  // the other CTAs' partials, visible after the acquire; plain loads (no volatile) so they are
-  // issued back to back instead of one round trip each, summed in region order (deterministic)
+  __shared__ unsigned int s_last;
+  __shared__ double s_fold[32][4];
+  if (threadIdx.x == 0) {
+    double* part = P.partials + ((int64_t)img * P.regions_per_img + region) * 4;
+    for (int q = 0; q < 4; ++q) part[q] = mine[q];
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(P.counters + img) : "memory");
+    s_last = prev == (unsigned)P.regions_per_img - 1 ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // The last CTA of the image folds every region's partial with all its threads (a 4096-region
+  // image is 4096 L2 round trips for one thread): thread t sums regions t, t + nt, ... in order,
+  // then a fixed shuffle tree and the warps in order -- deterministic for a given block size.
+  __threadfence();  // the other threads' side of thread 0's acquire
   double a[4] = {0.0, 0.0, 0.0, 0.0};
   const double2* pp = reinterpret_cast<const double2*>(P.partials + (int64_t)img * P.regions_per_img * 4);
-#pragma unroll 8
-  for (int r = 0; r < P.regions_per_img; ++r) {
+  for (int r = threadIdx.x; r < P.regions_per_img; r += blockDim.x) {
     const double2 v0 = __ldcg(pp + 2 * r), v1 = __ldcg(pp + 2 * r + 1);  // L2, never a stale L1 line
     a[0] += v0.x;
     a[1] += v0.y;
     a[2] += v1.x;
     a[3] += v1.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+  if ((threadIdx.x & 31) == 0)
+    for (int q = 0; q < 4; ++q) s_fold[threadIdx.x >> 5][q] = a[q];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < 4; ++q) {
+    a[q] = 0.0;
+    for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) a[q] += s_fold[w][q];
   }
   P.counters[img] = 0;  // ready for the next launch
   const double M = a[3];  // op.measurements() = sum of counts, re-summed every launch (exact in fp64)
