@@ -917,7 +917,7 @@ struct IdaInitSmem {
   unsigned short zslot[256];
 };
 
-__global__ void __launch_bounds__(256, 4) ida_init16_kernel(IdaParams P) {
+__global__ void __launch_bounds__(256, 6) ida_init16_kernel(IdaParams P) {
   __shared__ __align__(16) IdaInitSmem s;
   const int img = blockIdx.y, region = blockIdx.x;
   const int R0 = (region / P.regions_x) * kMR, C0 = (region % P.regions_x) * kMR;
