@@ -304,6 +304,9 @@ alloc_kernel(const uint32_t* __restrict__ weights, int nb, int64_t budget, const
 constexpr int kClassThreads = 1024;
 using Reduce64C = cub::BlockReduce<unsigned long long, kClassThreads>;
 using ScanIC = cub::BlockScan<int, kClassThreads>;
+constexpr int kBucketBits = 11;  // threshold search: classes bucketed by their key's top 11 bits
+constexpr int kBuckets = 1 << kBucketBits;
+constexpr int kMaxCand = 256;    // classes sharing the threshold's bucket ranked pairwise
 struct ClassShared {
   union {
     typename Reduce64C::TempStorage r;
@@ -312,6 +315,9 @@ struct ClassShared {
   unsigned int hist8[256];
   long long sh_ll[4];
   int sh_int[4];
+  unsigned int bucket[kBuckets];  // weighted (blocks per class) histogram of the key's top bits
+  int cand[kMaxCand];
+  int ncand;
 };
 struct ClassSel {  // the round's selection: units by class rank, exact ties by block index
   long long need;  // tie-group units still to hand out (to the lowest indices)
@@ -364,7 +370,85 @@ __device__ ClassSel class_round_select(ClassShared& sm, uint32_t* gh, int c0, in
   bool rank_mode = false;
   uint64_t thr_key = 0;
   int thr_flag = 0;
-  if (!sel_all && !none && ncls <= 512) {
+  bool bucketed = false;
+  if (!sel_all && !none && ncls > 64) {  // (a few dozen classes: the pairwise ranking below is cheaper)
+    // threshold by bucket: a weighted histogram of the keys' top kBucketBits bits, a descending
+    // scan for the bucket where the count of blocks ranking above first reaches `need`, then the
+    // classes inside that bucket (usually one or two) ranked pairwise by (key, flag)
+    for (int b = tid; b < kBuckets; b += kClassThreads) sm.bucket[b] = 0;
+    if (tid == 0) sm.ncand = 0;
+    __syncthreads();
+    for (int k = tid; k < ncls; k += kClassThreads)
+      atomicAdd(&sm.bucket[(unsigned)(ckey[k] >> (64 - kBucketBits))], ccnt[k]);
+    __syncthreads();
+    constexpr int kPer = kBuckets / kClassThreads;  // buckets per thread, descending
+    unsigned int loc = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) loc += sm.bucket[kBuckets - 1 - (tid * kPer + i)];
+    unsigned int before, total_b;
+    {
+      int ex, tot;
+      ScanI(sm.tmp.s).ExclusiveSum((int)loc, ex, tot);
+      before = (unsigned)ex;
+      total_b = (unsigned)tot;
+    }
+    (void)total_b;
+    if ((long long)before < need && need <= (long long)before + loc) {
+      unsigned int cum = before;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int b = kBuckets - 1 - (tid * kPer + i);
+        const unsigned int h = sm.bucket[b];
+        if ((long long)cum < need && need <= (long long)cum + h) {
+          sm.sh_int[0] = b;
+          sm.sh_ll[0] = (long long)cum;  // blocks in higher buckets
+        }
+        cum += h;
+      }
+    }
+    __syncthreads();
+    const int bstar = sm.sh_int[0];
+    const long long above_b = sm.sh_ll[0];
+    for (int k = tid; k < ncls; k += kClassThreads)
+      if ((int)(ckey[k] >> (64 - kBucketBits)) == bstar) {
+        const int slot = atomicAdd(&sm.ncand, 1);
+        if (slot < kMaxCand) sm.cand[slot] = k;
+      }
+    __syncthreads();
+    const int m = sm.ncand;
+    if (m <= kMaxCand) {
+      bucketed = true;
+      rank_mode = true;
+      if (tid < m) {
+        const int c = sm.cand[tid];
+        const uint64_t kk = ckey[c];
+        const int fk = cflag[c];
+        long long above = above_b, eqc = 0;
+        for (int j = 0; j < m; ++j) {
+          const int d = sm.cand[j];
+          const uint64_t kd = ckey[d];
+          const int fd = cflag[d];
+          const long long cd = ccnt[d];
+          above += (kd > kk || (kd == kk && fd > fk)) ? cd : 0;
+          eqc += (kd == kk && fd == fk) ? cd : 0;
+        }
+        if (above < need && need <= above + eqc) {  // the threshold tie group (tied classes agree)
+          sm.sh_ll[3] = above;
+          sm.sh_int[2] = (int)eqc;
+          sm.sh_int[1] = fk;
+          sm.sh_ll[2] = (long long)kk;
+        }
+      }
+      __syncthreads();
+      need -= sm.sh_ll[3];
+      all_equal_taken = need == (long long)sm.sh_int[2];
+      thr_key = (uint64_t)sm.sh_ll[2];
+      thr_flag = sm.sh_int[1];
+      __syncthreads();
+    }
+  }
+  if (bucketed) {
+  } else if (!sel_all && !none && ncls <= 512) {
     // few classes: each class counts the blocks ranking strictly above it and tied with it
     // (a power-of-two group of tpc threads per class splits the scan; shuffle-reduced)
     rank_mode = true;
@@ -1065,7 +1149,8 @@ int launch_alloc_shard(Ctx* ctx, int phase, const uint32_t* weights, int32_t n_b
   A.counts = counts;
   A.offsets = offsets;
   const size_t dyn = phase == 1 ? nc * 4 : 0;
-  if (dyn > 48 * 1024) cudaFuncSetAttribute(alloc_shard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  // the opt-in covers static + dynamic shared memory above 48 KB (ClassShared is ~14 KB static)
+  if (dyn > 16 * 1024) cudaFuncSetAttribute(alloc_shard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   const int kt = ktimer_begin(ctx, s, "alloc_shard");
   alloc_shard_kernel<<<1, kClassThreads, dyn, s>>>(phase, A);
   ktimer_end(ctx, s, kt);

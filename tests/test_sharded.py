@@ -357,3 +357,35 @@ def test_sharded_ida_matches_whole_image(H, W, k, checker):
     assert float(np.max(np.abs(got.cpu().numpy() - xr))) <= 1e-3
     psnr_ref = 10 * np.log10(255 ** 2 / np.mean((xr - host.astype(np.float64)) ** 2))
     assert abs(10 * np.log10(255 ** 2 / mse(got)) - psnr_ref) <= 0.01
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 2])
+def test_device_shard_allocation_crowded_buckets(k, checker):
+    """The round threshold search by key buckets (> 64 weight classes, alloc.cu
+    class_round_select): shares far below one unit put every class's key in the lowest buckets
+    (65-256 classes ranked pairwise inside one bucket, or > 256 -> the radix fallback), and capped
+    multi-round vectors, against the reference allocator (sensing.cpp:110-177)."""
+    import torch
+
+    from paper_2001_09632_b200.sharded import DeviceShard, ShardComm, allocate_sharded
+    rng = np.random.default_rng(77 + k)
+    cases = [(np.repeat(np.arange(1, 1001), 4), 1000, 255, 1),      # > 256 classes in bucket 0
+             (np.repeat(np.arange(1, 1001), 4), 1000, 255, 5),      # ~170 classes per bucket
+             (np.repeat(np.arange(1, 1001), 4), 1000, 255, 50),
+             (np.repeat(np.arange(1, 201), 3), 200, 255, 7),
+             (rng.integers(65, 4000, 4096), 4000, 120, 4096 * 40),  # capped rounds
+             ((np.arange(600) % 150 + 1) * 64, 150 * 64, 200, 12345)]  # shares with equal fractions
+    for w, wmax, cap, budget in cases:
+        w = np.asarray(w, dtype=np.int64)
+        n = w.size
+        comm = ShardComm(k)
+        cuts = [n * j // k for j in range(k + 1)]
+        wt = torch.from_numpy(w.astype(np.int32)).cuda()
+        shards = [DeviceShard(wt[cuts[j]:cuts[j + 1]], wmax, cap, 0) for j in range(k)]
+        counts = [torch.empty(s.nb, dtype=torch.uint16, device="cuda") for s in shards]
+        offs = [torch.empty(s.nb, dtype=torch.int32, device="cuda") for s in shards]
+        allocate_sharded(shards, comm, budget, counts, offs)
+        got = np.concatenate([c.cpu().numpy().view(np.uint16).astype(np.int64) for c in counts])
+        want = checker.allocate(w.astype(np.float64), budget, np.full(n, cap, np.int32))
+        assert np.array_equal(got, np.asarray(want, dtype=np.int64)), (n, budget, k)
