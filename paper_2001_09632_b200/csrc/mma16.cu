@@ -37,7 +37,8 @@ struct Grid16 {
   uint32_t pairs_per_row;     // ceil(cols / 2)
   uint32_t units_per_img;     // rows * pairs_per_row
   uint32_t total_units;
-  uint32_t runs_per_row;      // ceil(cols / 32): a run = up to 32 consecutive blocks of a block-row
+  int run_len;                // blocks per warp run: 32, or 16 / 8 when a small batch would underfill the GPU
+  uint32_t runs_per_row;      // ceil(cols / run_len): a run = up to run_len consecutive blocks of a block-row
   uint32_t total_runs;
   FastDiv div_units, div_pairs, div_nb, div_cols, div_runs_img, div_runs_row;
 };
@@ -50,7 +51,11 @@ static Grid16 make_grid16(int rows, int cols, int n) {
   g.pairs_per_row = (uint32_t)(cols + 1) / 2;
   g.units_per_img = (uint32_t)rows * g.pairs_per_row;
   g.total_units = g.units_per_img * (uint32_t)n;
-  g.runs_per_row = (uint32_t)(cols + 31) / 32;
+  // one warp per run: shorter runs for small batches (cfg1, cfg4) so the warps still fill the
+  // 148 SMs (>= 1024 runs; cfg4 measured slower at 16), 32-block runs otherwise (fewer per-run set-ups)
+  g.run_len = 32;
+  while (g.run_len > 8 && (uint64_t)((cols + g.run_len - 1) / g.run_len) * rows * n < 1024) g.run_len /= 2;
+  g.runs_per_row = (uint32_t)((cols + g.run_len - 1) / g.run_len);
   g.total_runs = g.runs_per_row * (uint32_t)rows * (uint32_t)n;
   g.div_runs_img = FastDiv(g.runs_per_row * (uint32_t)rows);
   g.div_runs_row = FastDiv(g.runs_per_row);
@@ -168,8 +173,8 @@ __device__ __forceinline__ void run_pos(const Grid16& G, uint32_t r, uint32_t& i
   const uint32_t rem = r - img * (G.runs_per_row * (uint32_t)G.rows);
   const uint32_t row = G.div_runs_row.div(rem);
   br = (int)row;
-  bc_first = 32 * (int)(rem - row * G.runs_per_row);
-  nblk = min(32, G.cols - bc_first);
+  bc_first = G.run_len * (int)(rem - row * G.runs_per_row);
+  nblk = min(G.run_len, G.cols - bc_first);
 }
 
 template <bool kWeights, bool kPayload, bool kDecode, bool kLowCols = false, int kSweep = 0>
