@@ -27,7 +27,7 @@ echo "multi ncu rc=$?"
 timeout 900 ncu --clock-control none --import-source on --set full -k regex:sense16_kernel -s 1 -c 1 \
   -o $O/weights -f python tools/prof_sweep.py > $O/weights_ncu.log 2>&1
 echo "weights ncu rc=$?"
-timeout 900 ncu --clock-control none --import-source on --set full -k regex:alloc_cta -s 1 -c 1 \
+timeout 900 ncu --clock-control none --import-source on --set full -k regex:alloc_warp -s 1 -c 1 \
   -o $O/alloc -f python tools/prof_sweep.py > $O/alloc_ncu.log 2>&1
 echo "alloc ncu rc=$?"
 for k in ida multi weights alloc; do
