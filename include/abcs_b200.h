@@ -274,6 +274,16 @@ int abcs_allocate_batch(abcs_ctx* ctx, const uint32_t* d_weights, int32_t n_bloc
                         int32_t base, uint16_t* d_counts, int32_t* d_offsets, int32_t* d_status,
                         void* stream);
 
+/* largest_remainder_allocate (sensing.cpp:110-177) for n independent vectors of small integer
+ * weights (0 <= w <= wmax <= 127, n_blocks <= 4096, uniform cap): the DD phase-2 allocation,
+ * one warp per vector (csrc/warp_alloc.cuh), bit-exact. counts = base + allocation (u16),
+ * offsets = exclusive scan (required). d_status[i] (nullable) receives ABCS_OK, or
+ * ABCS_ERR_LOGIC for a weight above wmax, a negative budget or budget > cap * n_blocks. */
+int abcs_allocate_small_batch(abcs_ctx* ctx, const uint32_t* d_weights, int32_t n_blocks,
+                              int32_t n_vectors, int64_t budget, int32_t cap, int32_t base,
+                              int32_t wmax, uint16_t* d_counts, int32_t* d_offsets,
+                              int32_t* d_status, void* stream);
+
 /* decode_idct (recon.cpp:109-117) = SensingOperator::adjoint (operators.cpp:50-76):
  * out image i (cropped rows*B x cols*B, f32, `out_pitch` floats per row) from
  * counts/payload. offsets nullable (computed). d_format_error (nullable, per

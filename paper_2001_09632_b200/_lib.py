@@ -106,6 +106,7 @@ SIGNATURES = {
                                                 I32, P]),
     "abcs_sense_weights_batch": (C.c_int, [P, C.POINTER(SensePlanC), P, I64, I32, I32, P, P, P]),
     "abcs_allocate_batch": (C.c_int, [P, P, I32, I32, I64, P, I32, I32, P, P, P, P]),
+    "abcs_allocate_small_batch": (C.c_int, [P, P, I32, I32, I64, I32, I32, I32, P, P, P, P]),
     "abcs_decode_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, P, I64, I32, P, P, P]),
     "abcs_forward_batch": (C.c_int, [P, I32, I32, I32, P, P, P, I64, I32, I32, P, I64, P]),
     "abcs_block_dct_f64": (C.c_int, [P, I32, I32, P, P, I64, P]),

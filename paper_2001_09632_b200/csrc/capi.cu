@@ -567,6 +567,28 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
   return ABCS_OK;
 }
 
+int abcs_allocate_small_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors,
+                              int64_t budget, int32_t cap, int32_t base, int32_t wmax, uint16_t* d_counts,
+                              int32_t* d_offsets, int32_t* d_status, void* stream) {
+  ABCS_NVTX("abcs_allocate_small_batch");
+  CHECK_CTX(c);
+  if (n_blocks < 0 || n_vectors < 0 || n_blocks > 4096 || wmax < 0 || wmax > 127 || cap < 0 || cap > 65535 ||
+      (n_blocks * (int64_t)n_vectors > 0 && (!d_weights || !d_counts || !d_offsets)))
+    return set_error(ABCS_ERR_INVALID_ARGUMENT, "bad arguments (n_blocks <= 4096, 0 <= wmax <= 127)");
+  if (n_blocks == 0 || n_vectors == 0) return ABCS_OK;
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  cudaSetDevice(ctx->device);
+  FusedAlloc fa{};
+  fa.status = d_status;
+  fa.counts = d_counts;
+  fa.offsets = d_offsets;
+  fa.budget = budget;
+  fa.cap = cap;
+  fa.base = base;
+  fa.wmax = wmax;
+  return launch_alloc_small(ctx, n_blocks, n_vectors, d_weights, fa, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int abcs_allocate_batch(abcs_ctx* c, const uint32_t* d_weights, int32_t n_blocks, int32_t n_vectors, int64_t budget,
                         const int32_t* d_caps, int32_t cap, int32_t base, uint16_t* d_counts, int32_t* d_offsets,
                         int32_t* d_status, void* stream) {

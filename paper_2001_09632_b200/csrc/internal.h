@@ -182,6 +182,8 @@ int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint
 int launch_sense16_sweep(Ctx* ctx, int n_sw, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
                          int pitch, const int* phase1, const double* T, uint32_t* const* weights,
                          uint32_t* const* fix_scratch, cudaStream_t s);
+// one warp per vector of n_blocks (<= 4096) weights in [0, fa.wmax <= 127] (warp_alloc.cuh)
+int launch_alloc_small(Ctx* ctx, int n_blocks, int n, const uint32_t* weights, const FusedAlloc& fa, cudaStream_t s);
 int launch_alloc_cta(Ctx* ctx, int rows, int cols, int n, const uint32_t* weights, const FusedAlloc& fa,
                      cudaStream_t s);
 int launch_sense16(Ctx* ctx, int mode, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride, int pitch,

@@ -1253,6 +1253,21 @@ int launch_alloc_cta_plans(Ctx* ctx, int np, int rows, int cols, int n, uint32_t
   return cuda_status(cudaGetLastError(), "alloc_cta launch");
 }
 
+int launch_alloc_small(Ctx* ctx, int n_blocks, int n, const uint32_t* weights, const FusedAlloc& fa, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    warp_alloc_attr((const void*)alloc_warp_kernel);
+    attr = true;
+  }
+  const int kt = ktimer_begin(ctx, s, "alloc_small");
+  alloc_warp_kernel<<<(unsigned)((n + kWarpAllocWarps - 1) / kWarpAllocWarps), 32 * kWarpAllocWarps,
+                      warp_alloc_smem(n_blocks), s>>>(weights, n_blocks, n, fa.wmax, fa.budget, fa.cap, fa.base,
+                                                      fa.counts, fa.offsets, fa.status);
+  ktimer_end(ctx, s, kt);
+  ctx->launches++;
+  return cuda_status(cudaGetLastError(), "alloc_small launch");
+}
+
 // The per-image allocation of a DD plan (alloc_cta_kernel) from weights already computed.
 int launch_alloc_cta(Ctx* ctx, int rows, int cols, int n, const uint32_t* weights, const FusedAlloc& fa,
                      cudaStream_t s) {

@@ -20,6 +20,8 @@ struct WarpAllocTables {
   uint32_t hist[kCtaAllocMaxW + 1];
   uint32_t give[kCtaAllocMaxW + 1];  // whole (+1 above the threshold); bit 31: the exact-tie group
   uint8_t flag[kCtaAllocMaxW + 1];
+  uint32_t bucket[256];  // the round's weighted histogram of the keys' top 8 bits
+  uint8_t cand[32];      // classes in the threshold's bucket
 };
 
 // bytes of one warp's shared state for nb blocks (tables, u8 weights, u16 allocations)
@@ -124,6 +126,80 @@ __device__ int warp_allocate(unsigned char* sm, const uint32_t* __restrict__ wei
       int thr_above = -1, thr_eq = 0;
       uint64_t thr_key = 0;
       int thr_flag = 0;
+      // 1. the bucket (top 8 key bits) where the blocks ranking above first reach `need`: a
+      //    weighted 256-bucket histogram scanned from the top, lane L owning buckets 255-8L..-7
+      for (int b = lane; b < 256; b += 32) S.bucket[b] = 0;
+      __syncwarp();
+      for (int c = lane; c <= wmax; c += 32)
+        if (S.hist[c]) atomicAdd(&S.bucket[(unsigned)(S.key[c] >> 56)], S.hist[c]);
+      __syncwarp();
+      int bk[8], loc = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        bk[i] = (int)S.bucket[255 - (8 * lane + i)];
+        loc += bk[i];
+      }
+      int incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int bstar = -1, above_b = 0;
+      {
+        int cum = incl - loc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (bstar < 0 && cum < need && need <= cum + bk[i]) {
+            bstar = 255 - (8 * lane + i);
+            above_b = cum;
+          }
+          cum += bk[i];
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, bstar >= 0);
+        const int src = ball ? __ffs(ball) - 1 : 0;
+        bstar = __shfl_sync(0xffffffffu, bstar, src);
+        above_b = __shfl_sync(0xffffffffu, above_b, src);
+      }
+      // 2. the classes in that bucket: compacted into the warp's candidate list (class order)
+      int m = 0;
+      for (int c0 = 0; c0 <= wmax; c0 += 32) {
+        const int c = c0 + lane;
+        const bool in = c <= wmax && S.hist[c] && (int)(S.key[c] >> 56) == bstar;
+        const unsigned ball = __ballot_sync(0xffffffffu, in);
+        if (in && m + __popc(ball & ((1u << lane) - 1)) < 32) S.cand[m + __popc(ball & ((1u << lane) - 1))] = (uint8_t)c;
+        m += __popc(ball);
+      }
+      __syncwarp();
+      if (bstar >= 0 && m <= 32) {
+        // 3. lane j ranks candidate j among the candidates (blocks above it = higher buckets plus
+        //    the candidates ranking above it)
+        int above = above_b, eqc = 0;
+        uint64_t kk = 0;
+        int fk = 0;
+        if (lane < m) {
+          const int c = S.cand[lane];
+          kk = S.key[c];
+          fk = S.flag[c];
+          for (int j = 0; j < m; ++j) {
+            const int d = S.cand[j];
+            const uint64_t kd = S.key[d];
+            const int fd = S.flag[d];
+            const int hd = (int)S.hist[d];
+            above += (kd > kk || (kd == kk && fd > fk)) ? hd : 0;
+            eqc += (kd == kk && fd == fk) ? hd : 0;
+          }
+        }
+        const bool hit = lane < m && above < need && need <= above + eqc;  // tied classes agree
+        const unsigned ball = __ballot_sync(0xffffffffu, hit);
+        if (ball) {
+          const int src = __ffs(ball) - 1;
+          thr_above = __shfl_sync(0xffffffffu, above, src);
+          thr_eq = __shfl_sync(0xffffffffu, eqc, src);
+          thr_key = __shfl_sync(0xffffffffu, kk, src);
+          thr_flag = __shfl_sync(0xffffffffu, fk, src);
+        }
+      } else {  // crowded bucket (tiny shares): every class ranks against every class
       for (int c0 = 0; c0 <= wmax; c0 += 32) {
         const int c = c0 + lane;
         const uint32_t h = c <= wmax ? S.hist[c] : 0u;
@@ -153,6 +229,7 @@ __device__ int warp_allocate(unsigned char* sm, const uint32_t* __restrict__ wei
           thr_flag = __shfl_sync(0xffffffffu, fk, src);
         }
       }
+      }
       if (thr_above < 0) return ABCS_ERR_LOGIC;
       need -= thr_above;
       all_taken = need == thr_eq;
@@ -170,9 +247,16 @@ __device__ int warp_allocate(unsigned char* sm, const uint32_t* __restrict__ wei
     int tie_base = 0;
     if (any_tie) {  // the tied blocks in index order: lane order, then position within the lane
       int ties = 0;
-      for (int k = 0; k < nmine; ++k) {
-        const int ph = k * 32 + lane;
-        ties += ((int)av[ph] < cap && (S.give[wv[ph]] >> 31)) ? 1 : 0;
+      for (int k0 = 0; k0 < nmine; k0 += 8) {  // 8 blocks' loads in flight per batch
+        int a[8], c[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const bool in = k0 + e < nmine;
+          a[e] = in ? (int)av[(k0 + e) * 32 + lane] : cap;
+          c[e] = in ? (int)wv[(k0 + e) * 32 + lane] : 0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ties += (a[e] < cap && (S.give[c[e]] >> 31)) ? 1 : 0;
       }
       int incl = ties;
 #pragma unroll
@@ -183,22 +267,31 @@ __device__ int warp_allocate(unsigned char* sm, const uint32_t* __restrict__ wei
       tie_base = incl - ties;
     }
     int taken_sum = 0, dtw = 0, dna = 0;
-    for (int k = 0; k < nmine; ++k) {
-      const int ph = k * 32 + lane;
-      const int a = (int)av[ph];
-      if (a >= cap) continue;
-      const int c = wv[ph];
-      const uint32_t g = S.give[c];
-      int give = (int)(g & 0x7fffffffu);
-      if (g >> 31) give += (tie_base++ < need) ? 1 : 0;
-      const int room = cap - a;
-      const int taken = give < room ? give : room;  // sensing.cpp:162-171
-      av[ph] = (uint16_t)(a + taken);
-      taken_sum += taken;
-      if (a + taken >= cap) {  // capped: the block leaves the active pool
-        atomicSub(&S.hist[c], 1u);
-        dtw += c;
-        dna += 1;
+    for (int k0 = 0; k0 < nmine; k0 += 8) {  // 8 blocks per batch: loads first, then the updates
+      int a[8], c[8];
+      uint32_t g[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool in = k0 + e < nmine;
+        a[e] = in ? (int)av[(k0 + e) * 32 + lane] : cap;
+        c[e] = in ? (int)wv[(k0 + e) * 32 + lane] : 0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] = S.give[c[e]];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (a[e] >= cap) continue;  // capped (or past the lane's range)
+        int give = (int)(g[e] & 0x7fffffffu);
+        if (g[e] >> 31) give += (tie_base++ < need) ? 1 : 0;
+        const int room = cap - a[e];
+        const int taken = give < room ? give : room;  // sensing.cpp:162-171
+        av[(k0 + e) * 32 + lane] = (uint16_t)(a[e] + taken);
+        taken_sum += taken;
+        if (a[e] + taken >= cap) {  // capped: the block leaves the active pool
+          atomicSub(&S.hist[c[e]], 1u);
+          dtw += c[e];
+          dna += 1;
+        }
       }
     }
     taken_sum = warp_sum_i(taken_sum);

@@ -215,6 +215,55 @@ def test_allocator_adversarial_and_large(p, checker, rng):
         p.largest_remainder_allocate([1, 2], 10, [1, 1])
 
 
+def test_small_alphabet_allocator_adversarial(p, torch, checker, rng):
+    """The one-warp-per-vector allocator of DD plans (csrc/warp_alloc.cuh, abcs_allocate_small_batch):
+    bucketed thresholds, crowded buckets (tiny shares -> pairwise fallback), exact-tie groups
+    split at the lower indices, capped multi-round vectors and uniform (all-zero) weights, against
+    the reference allocator (sensing.cpp:110-177)."""
+    from paper_2001_09632_b200 import _lib
+    cases = []
+    for i in range(120):
+        nb = int(rng.integers(1, 4097))
+        wmax = int(rng.integers(0, 128))
+        kind = i % 4
+        if kind == 0:
+            w = rng.integers(0, wmax + 1, nb)
+        elif kind == 1:  # few distinct values: large exact-tie groups
+            w = rng.choice(rng.integers(0, wmax + 1, 3), nb)
+        elif kind == 2:  # DD-like: mostly small counts, a tail at the prefix length
+            w = np.minimum(rng.geometric(0.2, nb) - 1, wmax)
+        else:
+            w = np.zeros(nb, dtype=np.int64)
+        cap = int(rng.integers(1, 256))
+        budget = int(rng.integers(0, cap * nb + 1)) if i % 3 else int(rng.integers(0, max(1, nb // 8)))
+        cases.append((w.astype(np.int64), wmax, cap, budget))
+    lib = _lib.load()
+    ctx = p.Context.get()
+    for i, (w, wmax, cap, budget) in enumerate(cases):
+        nb = w.size
+        wt = torch.from_numpy(w.astype(np.int32)).cuda()
+        counts = torch.empty(nb, dtype=torch.int16, device="cuda")
+        offs = torch.empty(nb, dtype=torch.int32, device="cuda")
+        st = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+        assert lib.abcs_allocate_small_batch(ctx.handle, wt.data_ptr(), nb, 1, budget, cap, 0, wmax,
+                                             counts.data_ptr(), offs.data_ptr(), st.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0, i
+        got = counts.cpu().numpy().view(np.uint16).astype(np.int64)
+        want = np.asarray(checker.allocate(w.astype(np.float64), budget, np.full(nb, cap, np.int32)), dtype=np.int64)
+        assert np.array_equal(got, want), (i, nb, wmax, cap, budget)
+        assert np.array_equal(offs.cpu().numpy(), np.cumsum(got) - got), i
+    # a weight above the declared bound is reported, not allocated
+    wt = torch.tensor([1, 200], dtype=torch.int32, device="cuda")
+    counts = torch.empty(2, dtype=torch.int16, device="cuda")
+    offs = torch.empty(2, dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.abcs_allocate_small_batch(ctx.handle, wt.data_ptr(), 2, 1, 3, 10, 0, 127, counts.data_ptr(), offs.data_ptr(),
+                                  st.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert int(st.item()) == _lib.LOGIC
+
+
 @pytest.mark.parametrize("H,W,B,num,den,algo", [(1536, 1536, 16, 3, 10, 2), (1000, 1480, 16, 1, 4, 1),
                                                   (1080, 1920, 8, 1, 5, 1)])
 def test_class_allocator_cluster_sizes(p, torch, checker, H, W, B, num, den, algo):
