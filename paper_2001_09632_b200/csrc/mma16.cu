@@ -621,7 +621,12 @@ alloc_cta_kernel(const uint32_t* __restrict__ weights, int nb, int wmax, long lo
 // Grid-stride CTAs: two full waves of `per_sm` resident CTAs per SM (equal work per CTA).
 static unsigned grid_for(Ctx* ctx, uint32_t warps_needed, uint32_t per_sm = 3) {
   const uint32_t ctas = (warps_needed + kM16Warps - 1) / kM16Warps;
-  const uint32_t cap = (uint32_t)ctx->sm_count * per_sm * 2;
+  static const uint32_t waves = [] {
+    const char* e = getenv("ABCS_GRID_WAVES");  // 0 = one run per warp (no grid-stride)
+    return e ? (uint32_t)atoi(e) : 2u;
+  }();
+  if (waves == 0) return ctas ? ctas : 1;
+  const uint32_t cap = (uint32_t)ctx->sm_count * per_sm * waves;
   return ctas < cap ? (ctas ? ctas : 1) : cap;
 }
 
@@ -1078,6 +1083,19 @@ sense16_multi_kernel(Grid16 G, MultiArgs A, const __grid_constant__ MultiMaps ma
   if (kBulk && (threadIdx.x & 31) == 0) bulk_wait_all();  // smem must outlive the copies
 }
 
+// The payload pass's grid: one warp per run when ABCS_MULTI_WAVES=0 (no grid-stride tail),
+// else grid_for's cap of `waves` rounds of 2 resident CTAs per SM.
+static unsigned multi_grid(Ctx* ctx, uint32_t runs) {
+  static const int waves = [] {
+    const char* e = getenv("ABCS_MULTI_WAVES");
+    return e ? atoi(e) : 3;  // the 3-chunk pipelined cfg2 step: 1.325 ms at 3, 1.341 at 2, 1.334 at 0
+  }();
+  const uint32_t ctas = (runs + kM16Warps - 1) / kM16Warps;
+  if (waves <= 0) return ctas ? ctas : 1;
+  const uint32_t cap = (uint32_t)ctx->sm_count * 2u * (uint32_t)waves;
+  return ctas < cap ? (ctas ? ctas : 1) : cap;
+}
+
 int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint8_t* imgs, int64_t img_stride,
                          int pitch, const uint16_t* const* counts, const int32_t* const* offsets,
                          float* const* payload, const int64_t* payload_stride, float* const* out, int64_t out_stride,
@@ -1131,9 +1149,9 @@ int launch_sense16_multi(Ctx* ctx, int np, int rows, int cols, int n, const uint
   }
   const int kt = ktimer_begin(ctx, s, "sense16_gather_decode");
   if (bulk)
-    sense16_multi_kernel<true><<<grid_for(ctx, G.total_runs, 2), kM16Threads, kOutBytes, s>>>(G, A, maps);
+    sense16_multi_kernel<true><<<multi_grid(ctx, G.total_runs), kM16Threads, kOutBytes, s>>>(G, A, maps);
   else
-    sense16_multi_kernel<false><<<grid_for(ctx, G.total_runs, 2), kM16Threads, 0, s>>>(G, A, maps);
+    sense16_multi_kernel<false><<<multi_grid(ctx, G.total_runs), kM16Threads, 0, s>>>(G, A, maps);
   ktimer_end(ctx, s, kt);
   ctx->launches++;
   return cuda_status(cudaGetLastError(), "sense16 multi launch");
