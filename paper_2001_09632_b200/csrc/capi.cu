@@ -537,8 +537,13 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
     }
     return ABCS_OK;
   }
-  // chunks of the batch on the pipe streams, as sense_chunked
-  const int nchunks = std::max(1, std::min<int>(ctx->pipe_streams, n / 64));
+  // chunks of the batch round-robin on the pipe streams, as sense_chunked
+  static const int chunks_env = [] {
+    const char* e = getenv("ABCS_SWEEP_CHUNKS");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const int want_chunks = chunks_env ? chunks_env : ctx->pipe_streams;
+  const int nchunks = ctx->pipe_streams <= 1 ? 1 : std::max(1, std::min<int>(want_chunks, n / 64));
   const int chunk = (n + nchunks - 1) / nchunks;
   const size_t per = align_up(sweep_scratch_bytes(plans, n_plans, chunk, d_offsets), 256);
   int st;
@@ -555,13 +560,15 @@ int abcs_sense_decode_sweep_batch(abcs_ctx* c, const abcs_sense_plan* plans, int
   if (e != cudaSuccess) return cuda_status(e, "fork");
   for (int k = 0; k < nchunks; ++k) {
     const int first = k * chunk, cnt = std::min(chunk, n - first);
-    cudaStream_t cs = ctx->pipe[k];
+    if (cnt <= 0) break;
+    const int lane = k % ctx->pipe_streams;
+    cudaStream_t cs = ctx->pipe[lane];
     cudaStreamWaitEvent(cs, ctx->ev_fork, 0);
     st = sweep_impl(ctx, plans, n_plans, d_images, image_stride, pitch, cnt, first, d_counts, d_offsets, d_payload,
-                    d_out, out_stride, out_pitch, scr + per * k, cs, k);
+                    d_out, out_stride, out_pitch, scr + per * k, cs, lane);
     if (st) return st;
-    e = cudaEventRecord(ctx->ev_join[k], cs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_join[k], 0);
+    e = cudaEventRecord(ctx->ev_join[lane], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->ev_join[lane], 0);
     if (e != cudaSuccess) return cuda_status(e, "join");
   }
   return ABCS_OK;
