@@ -104,7 +104,8 @@ int abcs_ctx_destroy(abcs_ctx* c) {
   for (auto& e : ctx->kpool) cudaEventDestroy(e);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   if (ctx->capture) cudaStreamDestroy(ctx->capture);
-  if (ctx->ida_side) cudaStreamDestroy(ctx->ida_side);
+  for (auto& q : ctx->ida_side)
+    if (q) cudaStreamDestroy(q);
   for (auto& e : ctx->ida_ev)
     if (e) cudaEventDestroy(e);
   delete ctx;
@@ -774,26 +775,30 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
   int st;
   const size_t off_bytes = d_offsets ? 0 : align_up((size_t)n * rows * cols * 4, 256);
   // Images are independent through every iteration (sigma and the halos are per image), so a batch
-  // runs as two half-batch chains on two streams: each step's last, partial wave of CTAs overlaps
-  // the other chain's step instead of idling SMs (ABCS_IDA_SPLIT=0 keeps one chain).
-  static const int split_env = [] {
+  // runs as `chains` sub-batch chains on their own streams: each step's last, partial wave of CTAs
+  // overlaps another chain's step instead of idling SMs (ABCS_IDA_SPLIT=1 keeps one chain; one chain
+  // while the ctx times kernels, so per-launch durations stay those of one step).
+  static const int split_env = [] {  // chains per batch (1..4)
     const char* e = getenv("ABCS_IDA_SPLIT");
-    return e ? atoi(e) : 1;
+    return e ? std::max(1, std::min(4, atoi(e))) : 2;
   }();
-  // (one chain while the ctx times kernels: per-launch durations stay those of one step)
-  const int nA = (split_env && !ctx->timing && n >= 16 && (block == 8 || block == 16)) ? n / 2 : n, nB = n - nA;
-  const size_t scrA = align_up(ida_scratch_bytes(rows, cols, block, y_stride, nA, *cfg), 256);
-  const size_t scrB = nB ? align_up(ida_scratch_bytes(rows, cols, block, y_stride, nB, *cfg), 256) : 0;
-  const size_t need = off_bytes + scrA + scrB;
+  const int chains = (!ctx->timing && n >= 8 * split_env && (block == 8 || block == 16)) ? split_env : 1;
+  int first[5];
+  size_t soff[5];
+  soff[0] = 0;
+  for (int k = 0; k <= chains; ++k) first[k] = (int)((int64_t)n * k / chains);
+  for (int k = 0; k < chains; ++k)
+    soff[k + 1] = soff[k] + align_up(ida_scratch_bytes(rows, cols, block, y_stride, first[k + 1] - first[k], *cfg), 256);
+  const size_t need = off_bytes + soff[chains];
   char* scr = static_cast<char*>(ctx_scratch(ctx, need, s, &st));
   if (st) return st;
-  if (nB) {
-    if (!ctx->ida_side && cudaStreamCreateWithFlags(&ctx->ida_side, cudaStreamNonBlocking) != cudaSuccess)
+  for (int k = 1; k < chains; ++k)
+    if (!ctx->ida_side[k - 1] && cudaStreamCreateWithFlags(&ctx->ida_side[k - 1], cudaStreamNonBlocking) != cudaSuccess)
       return set_error(ABCS_ERR_CUDA, "ida stream");
+  if (chains > 1)
     for (auto& e : ctx->ida_ev)
       if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
         return set_error(ABCS_ERR_CUDA, "ida event");
-  }
   auto body = [&](cudaStream_t q) -> int {
     const int32_t* offsets = d_offsets;
     if (!offsets) {
@@ -802,25 +807,28 @@ int abcs_ida_batch(abcs_ctx* c, int32_t rows, int32_t cols, int32_t block, const
       if (r) return r;
       offsets = reinterpret_cast<int32_t*>(scr);
     }
-    if (!nB)
-      return launch_ida(ctx, rows, cols, block, d_counts, offsets, d_y, y_stride, n, *cfg, d_ref, ref_stride,
-                        ref_pitch, d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, q);
-    cudaStream_t q2 = ctx->ida_side;
-    cudaError_t e = cudaEventRecord(ctx->ida_ev[0], q);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(q2, ctx->ida_ev[0], 0);
-    if (e != cudaSuccess) return cuda_status(e, "ida fork");
+    if (chains > 1) {
+      cudaError_t e = cudaEventRecord(ctx->ida_ev[0], q);
+      for (int k = 1; k < chains && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ctx->ida_side[k - 1], ctx->ida_ev[0], 0);
+      if (e != cudaSuccess) return cuda_status(e, "ida fork");
+    }
     const int64_t nbk = (int64_t)rows * cols;
-    int r = launch_ida(ctx, rows, cols, block, d_counts, offsets, d_y, y_stride, nA, *cfg, d_ref, ref_stride,
-                       ref_pitch, d_out, out_stride, out_pitch, d_trace, d_diverged, scr + off_bytes, q);
-    if (r) return r;
-    r = launch_ida(ctx, rows, cols, block, d_counts + nA * nbk, offsets + nA * nbk, d_y + nA * y_stride, y_stride, nB,
-                   *cfg, d_ref ? d_ref + nA * ref_stride : nullptr, ref_stride, ref_pitch, d_out + nA * out_stride,
-                   out_stride, out_pitch, d_trace ? d_trace + (int64_t)nA * (cfg->iterations + 1) * 4 : nullptr,
-                   d_diverged ? d_diverged + 2 * (int64_t)nA : nullptr, scr + off_bytes + scrA, q2);
-    if (r) return r;
-    e = cudaEventRecord(ctx->ida_ev[1], q2);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(q, ctx->ida_ev[1], 0);
-    return e == cudaSuccess ? ABCS_OK : cuda_status(e, "ida join");
+    for (int k = 0; k < chains; ++k) {
+      const int f0 = first[k], cnt = first[k + 1] - first[k];
+      cudaStream_t qk = k ? ctx->ida_side[k - 1] : q;
+      const int r = launch_ida(ctx, rows, cols, block, d_counts + f0 * nbk, offsets + f0 * nbk, d_y + f0 * y_stride,
+                               y_stride, cnt, *cfg, d_ref ? d_ref + f0 * ref_stride : nullptr, ref_stride, ref_pitch,
+                               d_out + f0 * out_stride, out_stride, out_pitch,
+                               d_trace ? d_trace + (int64_t)f0 * (cfg->iterations + 1) * 4 : nullptr,
+                               d_diverged ? d_diverged + 2 * (int64_t)f0 : nullptr, scr + off_bytes + soff[k], qk);
+      if (r) return r;
+    }
+    for (int k = 1; k < chains; ++k) {
+      cudaError_t e = cudaEventRecord(ctx->ida_ev[k], ctx->ida_side[k - 1]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(q, ctx->ida_ev[k], 0);
+      if (e != cudaSuccess) return cuda_status(e, "ida join");
+    }
+    return ABCS_OK;
   };
   if (!ctx->use_graphs || ctx->timing) return body(s);
   // one CUDA graph per distinct argument set (every pointer, size and setting of this call)

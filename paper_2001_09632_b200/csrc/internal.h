@@ -40,8 +40,8 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   // sweep: per pipe lane, a side stream for the allocations of the later plans
   cudaStream_t side[3] = {nullptr, nullptr, nullptr};
-  cudaStream_t ida_side = nullptr;                   // abcs_ida_batch: the second half of a split batch
-  cudaEvent_t ida_ev[2] = {nullptr, nullptr};        // its fork / join
+  cudaStream_t ida_side[3] = {};                     // abcs_ida_batch: the chains after the first of a split batch
+  cudaEvent_t ida_ev[4] = {};                         // fork, and one join per side chain
   cudaEvent_t ev_side[3][5] = {};
   size_t pipe_bytes = 0;
   // opt-in per-kernel CUDA-event timing (abcs_ctx_kernel_timing): events recorded on the
